@@ -1,0 +1,224 @@
+"""workloads -- seeded synthetic inputs shared by the oracle tests and the CUDA path.
+
+This module holds NONE of the method's arithmetic (no QoE, gain, priority,
+knapsack or bound computation): it only draws request populations, delivery
+timestamps and the synthetic latency table, following the recipe in DESIGN.md
+("Input recipe"), which restates SURVEY.md section 8(d):
+
+* lengths: lognormal fits to Table 2, clamped;
+* TTFT target max(input/5000, 1) s; speeds 4.8 / 3.3 tok/s;
+* arrivals: cyclic burst, intensity 2, duration 35%, or Poisson;
+* latency table tau(B) = 20000 + 800 B microseconds -- synthetic ("OPT-13B-like"
+  in BASELINE.json has no PAPER.md counterpart; labelled synthetic);
+* KV capacity M = 163,840 tokens; Delta t = 2 s.
+
+All times are integer microseconds; delivery timestamps are microseconds since
+the request's arrival (u32), packed per request in request order.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+UINT32_MAX = 0xFFFFFFFF
+
+# Table 2 lognormal fits: (input mu, sigma, output mu, sigma)
+LENGTH_FITS = {
+    "sharegpt": (7.0696, 1.4087, 5.7160, 0.6888),
+    "arxiv": (9.6191, 0.5848, 6.3742, 0.2490),
+    "coding": (5.5955, 1.3559, 7.1993, 1.6728),
+}
+READ_PERIOD_US = 208_333    # 4.8 tok/s, round(1e6/4.8)
+LISTEN_PERIOD_US = 303_030  # 3.3 tok/s, round(1e6/3.3)
+KV_CAPACITY = 163_840
+HORIZON_US = 2_000_000
+B_CAP = 256
+
+
+def tau_table(B_cap: int = B_CAP, base_us: int = 20_000, per_B_us: int = 800) -> np.ndarray:
+    """Synthetic decode latency tau(B) = base + per_B * B (microseconds), index B-1."""
+    B = np.arange(1, B_cap + 1, dtype=np.int64)
+    return (base_us + per_B_us * B).astype(np.uint32)
+
+
+@dataclass
+class Snapshot:
+    """SoA request table + decision parameters (the C-ABI's AndesRequests/AndesSchedParams)."""
+    arrival_us: np.ndarray
+    ttft_us: np.ndarray
+    period_us: np.ndarray
+    ctx_len: np.ndarray
+    n_deliv: np.ndarray
+    max_total: np.ndarray
+    start_off_us: np.ndarray
+    rank: np.ndarray
+    running: np.ndarray
+    tl_base: np.ndarray
+    tl_pool: np.ndarray
+    now_us: int = 0
+    horizon_us: int = HORIZON_US
+    tau_us: np.ndarray = field(default_factory=tau_table)
+    kv_capacity: int = KV_CAPACITY
+    preempt_cap: int = UINT32_MAX
+    cur_latency_us: int = 0
+    name: str = ""
+
+    @property
+    def n(self) -> int:
+        return int(self.arrival_us.shape[0])
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.tl_pool.shape[0])
+
+    def subset(self, idx) -> "Snapshot":
+        """Requests idx (re-packed pool), same parameters."""
+        idx = np.asarray(idx, dtype=np.int64)
+        g = self.n_deliv[idx]
+        parts = [self.tl_pool[int(self.tl_base[i]):int(self.tl_base[i]) + int(self.n_deliv[i])] for i in idx]
+        pool = np.concatenate(parts).astype(np.uint32) if len(parts) else np.zeros(0, np.uint32)
+        base = np.zeros(len(idx), np.uint64)
+        if len(idx):
+            base[1:] = np.cumsum(g[:-1].astype(np.uint64))
+        return replace(self, arrival_us=self.arrival_us[idx].copy(), ttft_us=self.ttft_us[idx].copy(),
+                       period_us=self.period_us[idx].copy(), ctx_len=self.ctx_len[idx].copy(),
+                       n_deliv=g.copy(), max_total=self.max_total[idx].copy(),
+                       start_off_us=self.start_off_us[idx].copy(), rank=self.rank[idx].copy(),
+                       running=self.running[idx].copy(), tl_base=base, tl_pool=pool)
+
+
+def _pack(timelines):
+    g = np.array([len(t) for t in timelines], dtype=np.uint32)
+    base = np.zeros(len(timelines), np.uint64)
+    if len(timelines):
+        base[1:] = np.cumsum(g[:-1].astype(np.uint64))
+    pool = np.concatenate([np.asarray(t, np.uint32) for t in timelines]) if int(g.sum()) else np.zeros(0, np.uint32)
+    return g, base, pool
+
+
+def sample_lengths(rng, n, dataset="sharegpt", in_clamp=(1, 32768), out_clamp=(1, 8192)):
+    mi, si, mo, so = LENGTH_FITS[dataset]
+    inp = np.clip(np.rint(rng.lognormal(mi, si, n)), *in_clamp).astype(np.int64)
+    out = np.clip(np.rint(rng.lognormal(mo, so, n)), *out_clamp).astype(np.int64)
+    return inp, out
+
+
+def cyclic_burst_arrivals(rng, n, mean_rate_per_s, cycle_s=1200.0, burst_frac=0.35, intensity=2.0):
+    """Cyclic burst: each cycle a burst phase at intensity x mean for
+    burst_frac of the cycle, then a base phase whose rate keeps the cycle mean.
+    Returns n arrival times (seconds, ascending) from t=0."""
+    r_b = intensity * mean_rate_per_s
+    r_0 = (1.0 - intensity * burst_frac) / (1.0 - burst_frac) * mean_rate_per_s
+    out = []
+    t = 0.0
+    while len(out) < n:
+        phase = (t % cycle_s) / cycle_s
+        rate = r_b if phase < burst_frac else r_0
+        t += rng.exponential(1.0 / rate)
+        out.append(t)
+    return np.array(out[:n])
+
+
+def snapshot(n, seed=1, dataset="sharegpt", listen_frac=0.0, window_s=1200.0, arrivals="burst",
+             tau_gap_B=B_CAP, kv_capacity=KV_CAPACITY, preempt_cap=UINT32_MAX, B_cap=B_CAP,
+             horizon_us=HORIZON_US, name="") -> Snapshot:
+    """Live-population snapshot at `now` (recipe: DESIGN.md "Input recipe").
+
+    Classes: 30% running/recently served (g ~ U[1, out-1]); 40% preempted mid-stream
+    (same, with one pause U[0.5, 5] s at a uniform index); 30% queued (g = 0).
+    First token at a + Exp(2 s) + input/5000 s; later tokens spaced tau(tau_gap_B)
+    +-10% jitter; everything truncated at `now`. Running flag: class-0 requests in
+    arrival order while their context lengths fit in M.
+    """
+    rng = np.random.default_rng(seed)
+    tau = tau_table(B_cap)
+    inp, out = sample_lengths(rng, n, dataset)
+    if arrivals == "burst":
+        arr_s = cyclic_burst_arrivals(rng, n, n / window_s)
+    else:  # Poisson
+        arr_s = np.cumsum(rng.exponential(window_s / n, n))
+    now_s = float(arr_s[-1]) + 0.05
+    arr_us = np.rint(arr_s * 1e6).astype(np.int64)
+    now_us = int(np.rint(now_s * 1e6))
+    age_us = now_us - arr_us
+    cls = rng.choice(3, size=n, p=[0.3, 0.4, 0.3])
+    ttft = np.maximum(200 * inp, 1_000_000).astype(np.uint32)          # max(len/5000, 1) s
+    period = np.where(rng.random(n) < listen_frac, LISTEN_PERIOD_US, READ_PERIOD_US).astype(np.uint32)
+    gap = float(tau[min(tau_gap_B, B_cap) - 1])
+    timelines = []
+    for i in range(n):
+        if cls[i] == 2 or out[i] <= 1:
+            timelines.append(np.zeros(0, np.uint32))
+            continue
+        g = int(rng.integers(1, out[i]))
+        first = rng.exponential(2e6) + inp[i] * 200.0
+        gaps = gap * (1.0 + rng.uniform(-0.1, 0.1, g - 1))
+        ts = first + np.concatenate([[0.0], np.cumsum(gaps)])
+        if cls[i] == 1 and g > 1:
+            k = int(rng.integers(1, g))
+            ts[k:] += rng.uniform(0.5e6, 5e6)
+        ts = np.floor(ts)
+        ts = ts[ts <= age_us[i]]
+        timelines.append(ts.astype(np.uint32))
+    g, base, pool = _pack(timelines)
+    ctx = (inp + g).astype(np.uint32)
+    running = np.zeros(n, np.uint8)
+    W = 0
+    for i in range(n):
+        if cls[i] == 0 and g[i] > 0 and W + int(ctx[i]) <= kv_capacity:
+            running[i] = 1
+            W += int(ctx[i])
+    return Snapshot(arrival_us=arr_us, ttft_us=ttft, period_us=period, ctx_len=ctx, n_deliv=g,
+                    max_total=np.full(n, UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                    rank=np.arange(n, dtype=np.uint32), running=running, tl_base=base, tl_pool=pool,
+                    now_us=now_us, horizon_us=horizon_us, tau_us=tau, kv_capacity=kv_capacity,
+                    preempt_cap=preempt_cap, name=name or f"{dataset}-{n}-s{seed}")
+
+
+def config2(seed=1) -> Snapshot:
+    """BASELINE config 2: 4K ShareGPT-shaped snapshot, all readers, B=1..256, P_cap off."""
+    return snapshot(4096, seed=seed, listen_frac=0.0, window_s=300.0, name=f"cfg2-4k-s{seed}")
+
+
+def config3(seed=1, n=65536) -> Snapshot:
+    """BASELINE config 3: burst at 2x capacity, 64K live, 50/50 reading/listening, P_cap = 16."""
+    return snapshot(n, seed=seed, listen_frac=0.5, window_s=1200.0, preempt_cap=16,
+                    name=f"cfg3-{n // 1024}k-s{seed}")
+
+
+def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True) -> Snapshot:
+    """Small adversarial instances for parity: arbitrary periods, ttft, offsets,
+    max_total caps, deliveries ahead of / behind schedule, pauses, ties."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 12)) if n is None else n
+    now = int(rng.integers(2_000_000, 20_000_000))
+    arr = now - rng.integers(0, 15_000_000, n)
+    # periods >= 50 ms keep m (tokens due by now + dt) below ~500 for the literal walk
+    period = rng.choice([50_000, 100_000, 208_333, 303_030, 999_983], n).astype(np.uint32)
+    ttft = rng.choice([0, 1, 500_000, 1_000_000, 1_300_000, 3_000_000], n).astype(np.uint32)
+    timelines = []
+    for i in range(n):
+        g = int(rng.integers(0, max_tokens + 1)) if rng.random() < 0.8 else 0
+        if g == 0:
+            timelines.append(np.zeros(0, np.uint32))
+            continue
+        age = int(now - arr[i])
+        ts = np.sort(rng.integers(0, max(age, 1) + 1, g))
+        if edge and rng.random() < 0.3:
+            ts = np.minimum(ts, ttft[i] + np.arange(g) * int(period[i]))  # on/ahead of schedule
+            ts = np.sort(np.minimum(ts, age))
+        timelines.append(ts.astype(np.uint32))
+    g, base, pool = _pack(timelines)
+    ctx = rng.integers(1, 60, n).astype(np.uint32)
+    mt = np.where(rng.random(n) < 0.2, g + rng.integers(0, 5, n), UINT32_MAX).astype(np.uint32)
+    off = np.where(rng.random(n) < 0.3, rng.integers(0, 3_000_000, n), 0).astype(np.uint32)
+    rank = rng.permutation(n).astype(np.uint32)
+    running = (rng.random(n) < 0.5).astype(np.uint8)
+    tau = np.sort(rng.integers(1, 400_000, B_cap)).astype(np.uint32)
+    horizon = int(rng.choice([1, 250_000, 2_000_000, 5_000_000]))
+    M = int(max(int(ctx.max()), int(rng.integers(20, 300))))
+    return Snapshot(arrival_us=arr.astype(np.int64), ttft_us=ttft, period_us=period, ctx_len=ctx, n_deliv=g,
+                    max_total=mt, start_off_us=off, rank=rank, running=running, tl_base=base, tl_pool=pool,
+                    now_us=now, horizon_us=horizon, tau_us=tau, kv_capacity=M,
+                    preempt_cap=int(rng.choice([UINT32_MAX, 0, 1, 2])), name=f"rand-s{seed}")
