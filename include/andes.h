@@ -1,0 +1,187 @@
+/*
+ * andes.h -- C ABI of the B200-native Andes scheduling-decision library (libandes.so).
+ *
+ * The library computes, on one B200 (sm_100a), the per-iteration QoE-aware
+ * scheduling decision of Andes (arXiv 2404.16283, "PAPER"):
+ *   S1  QoE of every live request's delivered-token timeline   (Eq. 1-3)
+ *   S3  QoE gain of serving vs waiting over Delta t, for every
+ *       candidate batch size B                                 (Eq. 4)
+ *   S4  priority = gain / context length and Algorithm 1's
+ *       greedy packing for every B                             (Eq. 6)
+ *   S5  best B
+ *   S0/S2 selective triggering and batch-size range
+ *   S6  preemption cap                                         (reading R18)
+ * "P:Lnnn" = line nnn of the paper's text; "Rnn" = the numbered
+ * readings of silent/ambiguous passages listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every array pointer is DEVICE memory owned by the caller, unless the
+ *    entry point's name ends in _host.  The library never frees caller memory.
+ *  - Times are integer microseconds. Absolute times are int64; times relative
+ *    to a request's arrival are uint32 (must be < 2^32 us, ~71.6 min).
+ *  - `stream` is a cudaStream_t passed as void*. Device entry points are
+ *    ASYNCHRONOUS on that stream: they validate host-side arguments, enqueue
+ *    kernels and return; results are valid after the stream is synchronised.
+ *  - Host-side validation errors return a negative AndesStatus before any launch.
+ *  - The library never allocates, frees or synchronises inside a device entry
+ *    point; its workspace is sized by andes_create's limits.
+ *  - One context per stream; contexts are not thread-safe.
+ *  - Data preconditions (timestamps nondecreasing, 1 <= l_i <= M, ranks unique,
+ *    tl_base nondecreasing) are checked on the device only when
+ *    ANDES_DEBUG_CHECKS is set; a violation sets the context's device error word
+ *    and the NEXT call on that context returns ANDES_E_RANGE.
+ */
+#ifndef ANDES_H
+#define ANDES_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct AndesCtx AndesCtx; /* opaque; owns a device workspace sized at create */
+
+typedef enum {
+    ANDES_OK = 0,
+    ANDES_E_INVAL = -1,    /* bad argument (null pointer, zero period, B out of range, ...) */
+    ANDES_E_RANGE = -2,    /* a device-side data precondition failed (debug checks)        */
+    ANDES_E_CUDA = -3,     /* a CUDA runtime error; see andes_last_error                   */
+    ANDES_E_NCCL = -4,     /* reserved for the multi-GPU entry points                      */
+    ANDES_E_CAPACITY = -5, /* n, B_cap, token count or running-set size above the limits   */
+    ANDES_NOT_TRIGGERED = 1 /* _host entry points only: the trigger did not fire           */
+} AndesStatus;
+
+/* Workspace limits, fixed at create. */
+typedef struct {
+    uint32_t max_requests; /* largest n of any call                                     */
+    uint32_t max_B;        /* largest B_cap (<= 1024)                                   */
+    uint64_t max_tokens;   /* largest timestamp-pool span (tl_base[n-1] + n_deliv[n-1]) */
+    uint32_t max_running;  /* largest number of running requests (victim sort; <= 8192) */
+    int32_t device;        /* CUDA device ordinal                                       */
+} AndesLimits;
+
+/* Request table (the paper's Request Tracker state), structure of arrays,
+ * length n.  Storing requests in rank order is recommended (coalesced tie scans). */
+typedef struct {
+    uint32_t n;
+    const int64_t *arrival_us;    /* a_i: arrival time (absolute)                                   */
+    const uint32_t *ttft_us;      /* TTFT target (reading R1: I_1 = a + ttft)                */
+    const uint32_t *period_us;    /* P_i = 1/consumption speed, >= 1 (I_j = I_1+(j-1)P) */
+    const uint32_t *ctx_len;      /* l_i = prompt + generated tokens, 1 <= l_i <= M (Eq. 5)  */
+    const uint32_t *n_deliv;      /* g_i: tokens delivered so far                                    */
+    const uint32_t *max_total;    /* total-token cap; UINT32_MAX = unknown (reading R7)      */
+    const uint32_t *start_off_us; /* o_i: delay before the first new token if served; NULL = all 0
+                                     (P:L355 excludes preemption overhead; reading R6)               */
+    const uint32_t *rank;         /* unique tie-break; smaller = earlier arrival = wins (reading R10) */
+    const uint8_t *running;       /* 1 if in the current batch                                       */
+    const uint64_t *tl_base;      /* element offset of request i's timestamps in tl_pool; must be
+                                     nondecreasing in i with tl_base[i+1] >= tl_base[i] + n_deliv[i] */
+    const uint32_t *tl_pool;      /* delivery timestamps, us since arrival, nondecreasing per request,
+                                     each <= now - arrival; 16-byte aligned                           */
+} AndesRequests;
+
+/* andes_qoe_eval modes */
+#define ANDES_EVAL_INFLIGHT 0u /* QoE at eval time t: tokens due by t, clamp at t (reading R3) */
+#define ANDES_EVAL_FINAL 1u    /* whole delivered timeline, no clamp (reading R19)                     */
+
+/* andes_schedule flags */
+#define ANDES_FORCE 1u        /* run the solver even if the trigger does not fire            */
+#define ANDES_PRUNE 2u        /* restrict B to [B_min, B_max]; default [1, B_max] */
+#define ANDES_DEBUG_CHECKS 4u /* device-side data precondition checks                         */
+
+/* Decision-time parameters. */
+typedef struct {
+    int64_t now_us;          /* decision time                                                  */
+    uint32_t horizon_us;     /* Delta t (reading R8), >= 1                             */
+    uint32_t B_cap;          /* candidate batch sizes are 1..B_cap, 1 <= B_cap <= max_B         */
+    const uint32_t *tau_us;  /* DEVICE u32[B_cap]: token latency tau(B) at index B-1 (App. B)   */
+    uint64_t kv_capacity;    /* M: KV-cache capacity in tokens (Eq. 5)                          */
+    uint32_t preempt_cap;    /* max preemptions per decision; UINT32_MAX = off (reading R18)    */
+    uint32_t cur_latency_us; /* current iteration latency (trigger)                     */
+    uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS                  */
+} AndesSchedParams;
+
+/* scalars[] layout of AndesDecision */
+#define ANDES_SC_B_STAR 0   /* chosen batch size B* (0 = empty decision / not triggered)   */
+#define ANDES_SC_REALIZED 1 /* number of requests served after the cap                      */
+#define ANDES_SC_N_ADMIT 2
+#define ANDES_SC_N_PREEMPT 3
+#define ANDES_SC_B_LO 4
+#define ANDES_SC_B_HI 5
+#define ANDES_SC_FLAGS 6  /* ANDES_F_* below                                                 */
+#define ANDES_SC_K_STAR 7 /* Algorithm 1 prefix length at B* (before the cap)                */
+#define ANDES_SC_COUNT 8
+#define ANDES_F_TRIGGERED 1u
+#define ANDES_F_CAP_HIT 2u
+#define ANDES_F_CAP_OVERRIDDEN 4u
+#define ANDES_F_SLOW_PATH 8u /* informational: a capacity fallback path ran */
+
+/* Decision outputs (DEVICE memory owned by the caller). */
+typedef struct {
+    uint8_t *serve_mask;   /* [n]  final serve set x (Alg. 1 output P:L512, after the cap)     */
+    uint32_t *admit_idx;   /* [B_cap] admitted/resumed requests, greedy order                  */
+    uint32_t *preempt_idx; /* [n]  preempted requests, victim order (reading R18)              */
+    uint32_t *scalars;     /* [ANDES_SC_COUNT]                                                 */
+    int64_t *V;            /* [B_cap] V(B) = sum of llrint(gain*2^32) over S_B; INT64_MIN if B
+                              was not a candidate (reading R9)                                   */
+    uint32_t *kstar;       /* [B_cap] Algorithm 1 prefix length per B; 0 if not a candidate    */
+} AndesDecision;
+
+/* QoE outputs of andes_qoe_eval (DEVICE memory; any pointer may be NULL). */
+typedef struct {
+    float *q;         /* [n] QoE (Eq. 3) rounded to fp32                        */
+    double *q64;      /* [n] QoE in fp64 (1 - S_delay/S_whole, RN; R4: 1 if S_whole = 0) */
+    int64_t *s_delay; /* [n] S_delay in us (Eq. 1), exact                        */
+    int64_t *s_whole; /* [n] S_whole in us (Eq. 2), exact                        */
+    uint32_t *m;      /* [n] number of tokens evaluated                           */
+} AndesQoeOut;
+
+/* Create/destroy a context on limits->device. Allocates the device workspace. */
+int andes_create(AndesCtx **ctx, const AndesLimits *limits);
+int andes_destroy(AndesCtx *ctx);
+
+/* Human-readable description of the last error on ctx (never NULL). */
+const char *andes_last_error(const AndesCtx *ctx);
+
+/* S1: QoE of every request (Eq. 1-3).  INFLIGHT: at relative time
+ * t_i = eval_time_us - a_i over the m_i = min(#{j: I_j <= t_i}, max_total) due
+ * tokens, actual consumption clamped at t_i, undelivered due tokens at t_i
+ * (readings R1-R5).  FINAL: over all n_deliv tokens without clamp (R19).
+ * Errors: ANDES_E_INVAL (null req/out/arrays, mode), ANDES_E_CAPACITY (n or token
+ * span above limits), ANDES_E_CUDA. */
+int andes_qoe_eval(AndesCtx *ctx, const AndesRequests *req, int64_t eval_time_us, uint32_t mode,
+                   const AndesQoeOut *out, void *stream);
+
+/* S3 materialised for an explicit list of B (parity and inspection):
+ * gain_out f64[nB*n] = Q_serve,i(B) - Q_wait,i (Eq. 4), key_out f32[nB*n] =
+ * float(gain / l_i) with -0 -> +0 (Eq. 6, reading R9); row b is B = B_list_host[b]
+ * (HOST array, 1 <= B <= B_cap).  qwait_out f64[n] optional.  Q_serve uses one new
+ * token every tau(B) starting at now + o_i (reading R6).  Either output may be NULL.
+ * Errors: ANDES_E_INVAL, ANDES_E_CAPACITY (nB > max_B), ANDES_E_CUDA. */
+int andes_gain_estimate(AndesCtx *ctx, const AndesRequests *req, int64_t now_us, uint32_t horizon_us,
+                        const uint32_t *tau_us, uint32_t B_cap, const uint32_t *B_list_host, uint32_t nB,
+                        double *gain_out, float *key_out, double *qwait_out, void *stream);
+
+/* S0-S6: one full scheduling decision.  Asynchronous: the trigger outcome is
+ * reported in scalars[ANDES_SC_FLAGS] & ANDES_F_TRIGGERED; when it does not fire
+ * serve_mask = running and every other output is zero.  Errors: ANDES_E_INVAL,
+ * ANDES_E_CAPACITY, ANDES_E_RANGE (previous call's debug check failed), ANDES_E_CUDA. */
+int andes_schedule(AndesCtx *ctx, const AndesRequests *req, const AndesSchedParams *p, AndesDecision *out,
+                   void *stream);
+
+/* Same decision with every pointer in req, p->tau_us and out in HOST memory:
+ * copies the inputs host->device into the context workspace, runs the decision,
+ * copies the outputs back and synchronises `stream`.  Returns ANDES_NOT_TRIGGERED
+ * when the trigger did not fire (outputs still written).  Requires the context
+ * to have been created with max_tokens covering the pool. */
+int andes_schedule_host(AndesCtx *ctx, const AndesRequests *req_host, const AndesSchedParams *p_host,
+                        AndesDecision *out_host, void *stream);
+
+/* Library version string, e.g. "andes-b200 0.1 sm_100a". */
+const char *andes_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANDES_H */

@@ -1,0 +1,262 @@
+"""paper_2404_16283_b200 -- B200-native Andes scheduling decision (arXiv 2404.16283).
+
+Thin ctypes binding over ``libandes.so`` (include/andes.h).  Argument marshalling
+only: every step of the decision runs in the library's sm_100a kernels.  PyTorch
+is used for device memory and streams.  There is no CPU fallback: if the shared
+library is missing or no CUDA device is present the calls raise.
+
+Entry points (same names as the C ABI):
+    Context.qoe_eval        -> andes_qoe_eval
+    Context.gain_estimate   -> andes_gain_estimate
+    Context.schedule        -> andes_schedule
+    Context.schedule_host   -> andes_schedule_host
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libandes.so")
+
+ANDES_OK = 0
+ANDES_NOT_TRIGGERED = 1
+ANDES_EVAL_INFLIGHT = 0
+ANDES_EVAL_FINAL = 1
+ANDES_FORCE = 1
+ANDES_PRUNE = 2
+ANDES_DEBUG_CHECKS = 4
+ANDES_F_TRIGGERED = 1
+ANDES_F_CAP_HIT = 2
+ANDES_F_CAP_OVERRIDDEN = 4
+ANDES_F_SLOW_PATH = 8
+UINT32_MAX = 0xFFFFFFFF
+SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags", "k_star"]
+
+EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
+           "andes_schedule", "andes_schedule_host", "andes_version"]
+
+
+class AndesError(RuntimeError):
+    pass
+
+
+class Limits(C.Structure):
+    _fields_ = [("max_requests", C.c_uint32), ("max_B", C.c_uint32), ("max_tokens", C.c_uint64),
+                ("max_running", C.c_uint32), ("device", C.c_int32)]
+
+
+class Requests(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("arrival_us", C.c_void_p), ("ttft_us", C.c_void_p),
+                ("period_us", C.c_void_p), ("ctx_len", C.c_void_p), ("n_deliv", C.c_void_p),
+                ("max_total", C.c_void_p), ("start_off_us", C.c_void_p), ("rank", C.c_void_p),
+                ("running", C.c_void_p), ("tl_base", C.c_void_p), ("tl_pool", C.c_void_p)]
+
+
+class SchedParams(C.Structure):
+    _fields_ = [("now_us", C.c_int64), ("horizon_us", C.c_uint32), ("B_cap", C.c_uint32),
+                ("tau_us", C.c_void_p), ("kv_capacity", C.c_uint64), ("preempt_cap", C.c_uint32),
+                ("cur_latency_us", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class DecisionPtrs(C.Structure):
+    _fields_ = [("serve_mask", C.c_void_p), ("admit_idx", C.c_void_p), ("preempt_idx", C.c_void_p),
+                ("scalars", C.c_void_p), ("V", C.c_void_p), ("kstar", C.c_void_p)]
+
+
+class QoeOut(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("q64", C.c_void_p), ("s_delay", C.c_void_p), ("s_whole", C.c_void_p),
+                ("m", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libandes.so (raises if it has not been built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; build it with `python paper_2404_16283_b200/build.py` "
+                              "(or __graft_entry__.build()). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        L.andes_create.argtypes = [C.POINTER(C.c_void_p), C.POINTER(Limits)]
+        L.andes_destroy.argtypes = [C.c_void_p]
+        L.andes_last_error.argtypes = [C.c_void_p]
+        L.andes_last_error.restype = C.c_char_p
+        L.andes_version.restype = C.c_char_p
+        L.andes_qoe_eval.argtypes = [C.c_void_p, C.POINTER(Requests), C.c_int64, C.c_uint32, C.POINTER(QoeOut),
+                                     C.c_void_p]
+        L.andes_gain_estimate.argtypes = [C.c_void_p, C.POINTER(Requests), C.c_int64, C.c_uint32, C.c_void_p,
+                                          C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
+        L.andes_schedule.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
+                                     C.POINTER(DecisionPtrs), C.c_void_p]
+        L.andes_schedule_host.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
+                                          C.POINTER(DecisionPtrs), C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().andes_version().decode()
+
+
+_FIELDS = [("arrival_us", "int64"), ("ttft_us", "int32"), ("period_us", "int32"), ("ctx_len", "int32"),
+           ("n_deliv", "int32"), ("max_total", "int32"), ("start_off_us", "int32"), ("rank", "int32"),
+           ("running", "uint8"), ("tl_base", "int64"), ("tl_pool", "int32")]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def requests_to(src, device="cuda", pin=False):
+    """Copy a structure-of-arrays request table (attributes or dict of numpy arrays with the
+    AndesRequests field names) into torch tensors on `device` (u32 fields are carried as
+    int32 bit patterns, u64 as int64).  pin=True gives pinned host tensors instead."""
+    import numpy as np
+    torch = _torch()
+    out = {}
+    for name, dt in _FIELDS:
+        a = src[name] if isinstance(src, dict) else getattr(src, name)
+        if a is None:
+            out[name] = None
+            continue
+        a = np.ascontiguousarray(a)
+        view = {"int64": np.int64, "int32": np.int32, "uint8": np.uint8}[dt]
+        t = torch.from_numpy(a.view(view) if a.dtype.itemsize == np.dtype(view).itemsize else a.astype(view))
+        if name == "tl_pool" and t.numel() == 0:
+            t = torch.zeros(4, dtype=torch.int32)
+        if pin:
+            out[name] = t.pin_memory()
+        else:
+            out[name] = t.to(device)
+    return out
+
+
+def _req_struct(t: dict, n: int) -> Requests:
+    return Requests(n, *[_ptr(t[name]) for name, _ in _FIELDS])
+
+
+@dataclass
+class Decision:
+    serve_mask: object
+    admit: object
+    preempt: object
+    scalars: object
+    V: object
+    kstar: object
+
+    def scalar(self, name):
+        return int(self.scalars[SC_NAMES.index(name)])
+
+
+class Context:
+    """An andes_create context (device workspace sized by the limits)."""
+
+    def __init__(self, max_requests, max_B=256, max_tokens=1 << 24, max_running=4096, device=0):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise AndesError("no CUDA device: the Andes decision path runs only on the GPU (no CPU fallback)")
+        self._h = C.c_void_p()
+        lim = Limits(int(max_requests), int(max_B), int(max_tokens), int(max_running), int(device))
+        rc = lib().andes_create(C.byref(self._h), C.byref(lim))
+        if rc != 0:
+            raise AndesError(f"andes_create failed rc={rc}")
+        self.device = torch.device("cuda", device)
+        self.limits = lim
+
+    def close(self):
+        if self._h:
+            lib().andes_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        if rc < 0:
+            raise AndesError(f"{what} failed rc={rc}: {lib().andes_last_error(self._h).decode()}")
+        return rc
+
+    # -- andes_qoe_eval
+    def qoe_eval(self, req: dict, n: int, eval_time_us: int, mode=ANDES_EVAL_INFLIGHT, stream=None):
+        torch = _torch()
+        dev = self.device
+        q = torch.empty(n, dtype=torch.float32, device=dev)
+        q64 = torch.empty(n, dtype=torch.float64, device=dev)
+        sd = torch.empty(n, dtype=torch.int64, device=dev)
+        sw = torch.empty(n, dtype=torch.int64, device=dev)
+        m = torch.empty(n, dtype=torch.int32, device=dev)
+        out = QoeOut(_ptr(q), _ptr(q64), _ptr(sd), _ptr(sw), _ptr(m))
+        self._check(lib().andes_qoe_eval(self._h, C.byref(_req_struct(req, n)), int(eval_time_us), int(mode),
+                                         C.byref(out), _stream_ptr(stream)), "andes_qoe_eval")
+        return q, q64, sd, sw, m
+
+    # -- andes_gain_estimate
+    def gain_estimate(self, req: dict, n: int, now_us: int, horizon_us: int, tau, B_list, stream=None):
+        torch = _torch()
+        import numpy as np
+        Bl = np.ascontiguousarray(B_list, dtype=np.uint32)
+        gain = torch.empty((Bl.size, n), dtype=torch.float64, device=self.device)
+        key = torch.empty((Bl.size, n), dtype=torch.float32, device=self.device)
+        qw = torch.empty(n, dtype=torch.float64, device=self.device)
+        self._check(lib().andes_gain_estimate(self._h, C.byref(_req_struct(req, n)), int(now_us), int(horizon_us),
+                                              _ptr(tau), int(tau.numel()), Bl.ctypes.data, int(Bl.size),
+                                              _ptr(gain), _ptr(key), _ptr(qw), _stream_ptr(stream)),
+                    "andes_gain_estimate")
+        return gain, key, qw
+
+    # -- andes_schedule
+    def alloc_decision(self, n, B_cap, pin=False):
+        torch = _torch()
+        kw = dict(pin_memory=True) if pin else dict(device=self.device)
+        return Decision(serve_mask=torch.empty(max(n, 1), dtype=torch.uint8, **kw),
+                        admit=torch.empty(B_cap, dtype=torch.int32, **kw),
+                        preempt=torch.empty(max(n, 1), dtype=torch.int32, **kw),
+                        scalars=torch.empty(8, dtype=torch.int32, **kw),
+                        V=torch.empty(B_cap, dtype=torch.int64, **kw),
+                        kstar=torch.empty(B_cap, dtype=torch.int32, **kw))
+
+    def schedule(self, req: dict, n: int, now_us: int, horizon_us: int, tau, kv_capacity: int,
+                 preempt_cap=UINT32_MAX, cur_latency_us=0, flags=ANDES_FORCE, out: Decision | None = None,
+                 stream=None) -> Decision:
+        B_cap = int(tau.numel())
+        out = out or self.alloc_decision(n, B_cap)
+        p = SchedParams(int(now_us), int(horizon_us), B_cap, _ptr(tau), int(kv_capacity), int(preempt_cap),
+                        int(cur_latency_us), int(flags))
+        d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
+                         _ptr(out.V), _ptr(out.kstar))
+        self._check(lib().andes_schedule(self._h, C.byref(_req_struct(req, n)), C.byref(p), C.byref(d),
+                                         _stream_ptr(stream)), "andes_schedule")
+        return out
+
+    # -- andes_schedule_host (host buffers; copies inside the call; synchronous)
+    def schedule_host(self, req_host: dict, n: int, now_us: int, horizon_us: int, tau_host, kv_capacity: int,
+                      preempt_cap=UINT32_MAX, cur_latency_us=0, flags=ANDES_FORCE, out: Decision | None = None,
+                      stream=None):
+        B_cap = int(tau_host.numel())
+        out = out or self.alloc_decision(n, B_cap, pin=True)
+        p = SchedParams(int(now_us), int(horizon_us), B_cap, _ptr(tau_host), int(kv_capacity), int(preempt_cap),
+                        int(cur_latency_us), int(flags))
+        d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
+                         _ptr(out.V), _ptr(out.kstar))
+        rc = self._check(lib().andes_schedule_host(self._h, C.byref(_req_struct(req_host, n)), C.byref(p),
+                                                   C.byref(d), _stream_ptr(stream)), "andes_schedule_host")
+        return out, rc

@@ -1,0 +1,379 @@
+// api.cu -- the C ABI of libandes (include/andes.h): argument validation, workspace
+// ownership, and the kernel sequence of each entry point.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/andes.h"
+#include "device.cuh"
+#include "launch.h"
+
+using namespace andes;
+
+struct AndesCtx {
+  AndesLimits lim{};
+  int device = 0;
+  uint32_t sm_count = 0;
+  uint32_t scan_grid = 0;
+  uint32_t tiles_cap = 0;
+  Work w{};
+  std::vector<void*> allocs;
+  uint32_t* B_list_dev = nullptr;
+  uint32_t* err_pinned = nullptr;  // mapped/pinned copy of the device error word (debug checks)
+  // device mirrors for andes_schedule_host
+  struct Mirror {
+    int64_t* arrival;
+    uint32_t *ttft, *period, *ctx_len, *n_deliv, *max_total, *start_off, *rank;
+    uint8_t* running;
+    uint64_t* tl_base;
+    uint32_t* tl_pool;
+    uint32_t* tau;
+    uint8_t* serve_mask;
+    uint32_t *admit_idx, *preempt_idx, *scalars, *kstar;
+    int64_t* V;
+  } mir{};
+  std::string err;
+};
+
+namespace {
+
+const char* kVersion = "andes-b200 0.1 sm_100a";
+
+int set_err(AndesCtx* c, int code, const char* fmt, const char* detail = "") {
+  if (c) {
+    char buf[512];
+    snprintf(buf, sizeof buf, fmt, detail);
+    c->err = buf;
+  }
+  return code;
+}
+
+int cuda_check(AndesCtx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ANDES_OK;
+  if (c) c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return ANDES_E_CUDA;
+}
+
+template <class T>
+cudaError_t ctx_alloc(AndesCtx* c, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count ? count * sizeof(T) : sizeof(T));
+  if (e == cudaSuccess) {
+    c->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+  }
+  return e;
+}
+
+ReqView view_of(const AndesRequests* r) {
+  ReqView v;
+  v.n = r->n;
+  v.arrival = r->arrival_us;
+  v.ttft = r->ttft_us;
+  v.period = r->period_us;
+  v.ctx_len = r->ctx_len;
+  v.n_deliv = r->n_deliv;
+  v.max_total = r->max_total;
+  v.start_off = r->start_off_us;
+  v.rank = r->rank;
+  v.running = r->running;
+  v.tl_base = r->tl_base;
+  v.tl_pool = r->tl_pool;
+  return v;
+}
+
+int check_requests(AndesCtx* c, const AndesRequests* r, bool need_sched_fields) {
+  if (!r) return set_err(c, ANDES_E_INVAL, "req is NULL%s");
+  if (r->n > c->lim.max_requests) return set_err(c, ANDES_E_CAPACITY, "n exceeds limits.max_requests%s");
+  if (r->n == 0) return ANDES_OK;
+  if (!r->arrival_us || !r->ttft_us || !r->period_us || !r->n_deliv || !r->max_total || !r->tl_base)
+    return set_err(c, ANDES_E_INVAL, "a required request array is NULL%s");
+  if (need_sched_fields && (!r->ctx_len || !r->rank || !r->running))
+    return set_err(c, ANDES_E_INVAL, "ctx_len/rank/running are required%s");
+  if (!r->tl_pool) return set_err(c, ANDES_E_INVAL, "tl_pool is NULL%s");
+  if ((reinterpret_cast<uintptr_t>(r->tl_pool) & 15u) != 0)
+    return set_err(c, ANDES_E_INVAL, "tl_pool must be 16-byte aligned%s");
+  return ANDES_OK;
+}
+
+int pending_device_error(AndesCtx* c) {
+  if (c->err_pinned && *c->err_pinned) {
+    const uint32_t e = *c->err_pinned;
+    *c->err_pinned = 0;
+    char buf[128];
+    snprintf(buf, sizeof buf, "device precondition check failed (error word 0x%x)", e);
+    c->err = buf;
+    return (e & (kErrRunning | 128u)) ? ANDES_E_CAPACITY : ANDES_E_RANGE;
+  }
+  return ANDES_OK;
+}
+
+LaunchCfg cfg_of(AndesCtx* c, void* stream) {
+  LaunchCfg L;
+  L.stream = static_cast<cudaStream_t>(stream);
+  L.sm_count = c->sm_count;
+  L.scan_grid = c->scan_grid;
+  return L;
+}
+
+Work work_of(AndesCtx* c, uint32_t n) {
+  Work w = c->w;
+  (void)n;
+  return w;
+}
+
+// per-call reset of the small globals and the look-back status words
+int reset_call(AndesCtx* c, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(c->w.g, 0, sizeof(Globals), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->w.tile_status, 0, sizeof(unsigned long long) * c->tiles_cap, s);
+  return cuda_check(c, e, "memset");
+}
+
+int finish_call(AndesCtx* c, cudaStream_t s, bool debug) {
+  if (debug) {
+    cudaError_t e = cudaMemcpyAsync(c->err_pinned, &c->w.g->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_check(c, e, "error word copy");
+  }
+  return cuda_check(c, cudaGetLastError(), "kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* andes_version(void) { return kVersion; }
+
+const char* andes_last_error(const AndesCtx* ctx) {
+  if (!ctx) return "NULL context";
+  return ctx->err.c_str();
+}
+
+int andes_create(AndesCtx** out, const AndesLimits* lim) {
+  if (!out || !lim) return ANDES_E_INVAL;
+  *out = nullptr;
+  if (lim->max_requests == 0 || lim->max_B == 0 || lim->max_B > (uint32_t)kMaxB ||
+      lim->max_running > (uint32_t)kMaxRunning)
+    return ANDES_E_INVAL;
+  AndesCtx* c = new AndesCtx();
+  c->lim = *lim;
+  if (c->lim.max_running == 0) c->lim.max_running = kMaxRunning;
+  if (c->lim.max_tokens == 0) c->lim.max_tokens = 1;
+  c->device = lim->device;
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) {
+    int rc = cuda_check(c, e, "cudaSetDevice");
+    delete c;
+    return rc;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->sm_count = (uint32_t)sms;
+  const int bps = scan_blocks_per_sm();
+  c->scan_grid = (uint32_t)(sms * (bps > 0 ? bps : 1));
+  const uint32_t N = lim->max_requests;
+  c->tiles_cap = (uint32_t)((c->lim.max_tokens + kTile - 1) / kTile) + 2;
+  Work& w = c->w;
+  w.N_cap = N;
+  w.tiles_cap = c->tiles_cap;
+  if ((e = ctx_alloc(c, &w.m, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.edge, N)) != cudaSuccess || (e = ctx_alloc(c, &w.tile_owner, c->tiles_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.tile_status, c->tiles_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.mark, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.sel, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
+    int rc = cuda_check(c, e, "workspace allocation");
+    andes_destroy(c);
+    return rc;
+  }
+  cudaMemset(w.hist_l, 0, sizeof(uint32_t) * kHistL);
+  cudaMemset(w.mark, 0, N);
+  if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess) {
+    int rc = cuda_check(c, e, "pinned alloc");
+    andes_destroy(c);
+    return rc;
+  }
+  *c->err_pinned = 0;
+  // host-path mirrors
+  auto& m = c->mir;
+  const size_t T = c->lim.max_tokens;
+  if ((e = ctx_alloc(c, &m.arrival, N)) != cudaSuccess || (e = ctx_alloc(c, &m.ttft, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.period, N)) != cudaSuccess || (e = ctx_alloc(c, &m.ctx_len, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.n_deliv, N)) != cudaSuccess || (e = ctx_alloc(c, &m.max_total, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.start_off, N)) != cudaSuccess || (e = ctx_alloc(c, &m.rank, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.running, N)) != cudaSuccess || (e = ctx_alloc(c, &m.tl_base, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.tl_pool, T)) != cudaSuccess || (e = ctx_alloc(c, &m.tau, kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.serve_mask, N)) != cudaSuccess || (e = ctx_alloc(c, &m.admit_idx, kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.preempt_idx, N)) != cudaSuccess || (e = ctx_alloc(c, &m.scalars, ANDES_SC_COUNT)) != cudaSuccess ||
+      (e = ctx_alloc(c, &m.kstar, kMaxB)) != cudaSuccess || (e = ctx_alloc(c, &m.V, kMaxB)) != cudaSuccess) {
+    int rc = cuda_check(c, e, "host-path mirror allocation");
+    andes_destroy(c);
+    return rc;
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    int rc = cuda_check(c, e, "create sync");
+    andes_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return ANDES_OK;
+}
+
+int andes_destroy(AndesCtx* c) {
+  if (!c) return ANDES_E_INVAL;
+  cudaSetDevice(c->device);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->err_pinned) cudaFreeHost(c->err_pinned);
+  delete c;
+  return ANDES_OK;
+}
+
+int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, uint32_t mode,
+                   const AndesQoeOut* out, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if ((rc = check_requests(c, req, false))) return rc;
+  if (!out) return set_err(c, ANDES_E_INVAL, "out is NULL%s");
+  if (mode > ANDES_EVAL_FINAL) return set_err(c, ANDES_E_INVAL, "unknown mode%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LaunchCfg L = cfg_of(c, stream);
+  const ReqView r = view_of(req);
+  const Work w = work_of(c, r.n);
+  const bool fin = mode == ANDES_EVAL_FINAL;
+  if ((rc = reset_call(c, s))) return rc;
+  launch_prep(L, r, w, eval_time_us, fin, false, 0, false);
+  launch_scan(L, r, w, eval_time_us, fin);
+  launch_qoe_final(L, r, w, eval_time_us, fin, out->q, out->q64, out->s_delay, out->s_whole, out->m);
+  return finish_call(c, s, false);
+}
+
+int andes_gain_estimate(AndesCtx* c, const AndesRequests* req, int64_t now_us, uint32_t horizon_us,
+                        const uint32_t* tau_us, uint32_t B_cap, const uint32_t* B_list_host, uint32_t nB,
+                        double* gain_out, float* key_out, double* qwait_out, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if ((rc = check_requests(c, req, true))) return rc;
+  if (!tau_us || B_cap == 0 || B_cap > c->lim.max_B) return set_err(c, ANDES_E_INVAL, "bad tau/B_cap%s");
+  if (nB > (uint32_t)kMaxB) return set_err(c, ANDES_E_CAPACITY, "nB exceeds 1024%s");
+  if (nB && !B_list_host) return set_err(c, ANDES_E_INVAL, "B_list is NULL%s");
+  for (uint32_t b = 0; b < nB; ++b)
+    if (B_list_host[b] < 1 || B_list_host[b] > B_cap) return set_err(c, ANDES_E_INVAL, "B out of [1, B_cap]%s");
+  if (horizon_us == 0) return set_err(c, ANDES_E_INVAL, "horizon must be >= 1%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LaunchCfg L = cfg_of(c, stream);
+  const ReqView r = view_of(req);
+  const Work w = work_of(c, r.n);
+  const int64_t eval = now_us + (int64_t)horizon_us;
+  if ((rc = reset_call(c, s))) return rc;
+  if (nB) {
+    cudaError_t e = cudaMemcpyAsync(c->B_list_dev, B_list_host, sizeof(uint32_t) * nB, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_check(c, e, "B_list copy");
+  }
+  launch_prep(L, r, w, eval, false, false, 0, false);
+  launch_scan(L, r, w, eval, false);
+  launch_gain_estimate(L, r, w, now_us, horizon_us, tau_us, c->B_list_dev, nB, gain_out, key_out, qwait_out);
+  return finish_call(c, s, false);
+}
+
+int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams* p, AndesDecision* out,
+                   void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if ((rc = check_requests(c, req, true))) return rc;
+  if (!p || !out) return set_err(c, ANDES_E_INVAL, "params/out is NULL%s");
+  if (!p->tau_us || p->B_cap == 0 || p->B_cap > c->lim.max_B) return set_err(c, ANDES_E_INVAL, "bad tau/B_cap%s");
+  if (p->horizon_us == 0 || p->kv_capacity == 0) return set_err(c, ANDES_E_INVAL, "horizon and M must be >= 1%s");
+  if (!out->scalars || !out->V || !out->kstar || (req->n && (!out->serve_mask || !out->preempt_idx)) ||
+      !out->admit_idx)
+    return set_err(c, ANDES_E_INVAL, "a decision output is NULL%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LaunchCfg L = cfg_of(c, stream);
+  const ReqView r = view_of(req);
+  const Work w = work_of(c, r.n);
+  const int64_t eval = p->now_us + (int64_t)p->horizon_us;
+  const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
+  SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
+  if ((rc = reset_call(c, s))) return rc;
+  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug);
+  launch_bounds(L, r, w, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
+  launch_scan(L, r, w, eval, false);
+  launch_gain_keys(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap);
+  launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
+  launch_mask(L, r, w, o);
+  return finish_call(c, s, debug);
+}
+
+int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedParams* p, AndesDecision* out,
+                        void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  if (!rq || !p || !out) return set_err(c, ANDES_E_INVAL, "NULL argument%s");
+  if (rq->n > c->lim.max_requests) return set_err(c, ANDES_E_CAPACITY, "n exceeds limits.max_requests%s");
+  if (!p->tau_us || p->B_cap == 0 || p->B_cap > c->lim.max_B) return set_err(c, ANDES_E_INVAL, "bad tau/B_cap%s");
+  const uint32_t n = rq->n;
+  uint64_t span = 0;
+  if (n) {
+    if (!rq->tl_base || !rq->n_deliv) return set_err(c, ANDES_E_INVAL, "tl_base/n_deliv NULL%s");
+    span = rq->tl_base[n - 1] + rq->n_deliv[n - 1];
+  }
+  if (span > c->lim.max_tokens) return set_err(c, ANDES_E_CAPACITY, "timestamp pool exceeds limits.max_tokens%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto& m = c->mir;
+  cudaError_t e = cudaSuccess;
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    if (e == cudaSuccess && bytes && src) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  h2d(m.arrival, rq->arrival_us, 8ull * n);
+  h2d(m.ttft, rq->ttft_us, 4ull * n);
+  h2d(m.period, rq->period_us, 4ull * n);
+  h2d(m.ctx_len, rq->ctx_len, 4ull * n);
+  h2d(m.n_deliv, rq->n_deliv, 4ull * n);
+  h2d(m.max_total, rq->max_total, 4ull * n);
+  if (rq->start_off_us) h2d(m.start_off, rq->start_off_us, 4ull * n);
+  h2d(m.rank, rq->rank, 4ull * n);
+  h2d(m.running, rq->running, 1ull * n);
+  h2d(m.tl_base, rq->tl_base, 8ull * n);
+  h2d(m.tl_pool, rq->tl_pool, 4ull * span);
+  h2d(m.tau, p->tau_us, 4ull * p->B_cap);
+  if (e != cudaSuccess) return cuda_check(c, e, "host-to-device copy");
+  AndesRequests dr = *rq;
+  dr.arrival_us = m.arrival;
+  dr.ttft_us = m.ttft;
+  dr.period_us = m.period;
+  dr.ctx_len = m.ctx_len;
+  dr.n_deliv = m.n_deliv;
+  dr.max_total = m.max_total;
+  dr.start_off_us = rq->start_off_us ? m.start_off : nullptr;
+  dr.rank = m.rank;
+  dr.running = m.running;
+  dr.tl_base = m.tl_base;
+  dr.tl_pool = m.tl_pool;
+  AndesSchedParams dp = *p;
+  dp.tau_us = m.tau;
+  AndesDecision dd{m.serve_mask, m.admit_idx, m.preempt_idx, m.scalars, m.V, m.kstar};
+  int rc = andes_schedule(c, &dr, &dp, &dd, stream);
+  if (rc) return rc;
+  uint32_t sc[ANDES_SC_COUNT];
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    if (e == cudaSuccess && bytes && dst) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  };
+  d2h(sc, m.scalars, sizeof sc);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_check(c, e, "decision copy");
+  d2h(out->scalars, m.scalars, sizeof sc);
+  d2h(out->serve_mask, m.serve_mask, n);
+  d2h(out->admit_idx, m.admit_idx, 4ull * sc[ANDES_SC_N_ADMIT]);
+  d2h(out->preempt_idx, m.preempt_idx, 4ull * sc[ANDES_SC_N_PREEMPT]);
+  d2h(out->V, m.V, 8ull * p->B_cap);
+  d2h(out->kstar, m.kstar, 4ull * p->B_cap);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_check(c, e, "decision copy");
+  return (sc[ANDES_SC_FLAGS] & ANDES_F_TRIGGERED) ? ANDES_OK : ANDES_NOT_TRIGGERED;
+}
+
+}  // extern "C"

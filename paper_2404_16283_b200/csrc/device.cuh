@@ -1,0 +1,241 @@
+// device.cuh -- internal device-side definitions of libandes (sm_100a).
+//
+// Everything here is product code; it shares nothing with oracle/.
+// Notation follows PAPER.md section 3.1 / 4.1 and DESIGN.md "Closed forms":
+//   I_j  = ttft + (j-1) P                        ideal consumption time (reading R1)
+//   lat_j = d_j - I_j,  delta_j = max(0, max_{k<=j} lat_k)   actual-minus-ideal (R2)
+//   delta~_j = min(delta_j, t - I_j)             clamped at the evaluation time (R3)
+//   S_delay = sum_j delta~_j,  S_whole = m delta~_m + P m(m-1)/2     (Eq. 1-2)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace andes {
+
+// ---------------------------------------------------------------- constants
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (16 KiB)
+constexpr int kWindowCap = 1024;                  // request window staged per tile
+constexpr int kSelectThreads = 1024;
+constexpr int kMaxB = 1024;
+constexpr int kMaxRunning = 4096;
+constexpr uint32_t kHistL = 65536;                // exact histogram of l < 65535 (+ overflow)
+
+// tile status words (decoupled look-back), see k_qoe_scan
+constexpr unsigned long long kStAgg = 1ull << 62;
+constexpr unsigned long long kStPrefix = 2ull << 62;
+constexpr unsigned long long kStMask = 3ull << 62;
+constexpr unsigned long long kFlagBit = 1ull << 32;
+
+// device error word bits (ANDES_DEBUG_CHECKS)
+constexpr uint32_t kErrPeriod = 1u, kErrCtx = 2u, kErrBase = 4u, kErrTimes = 8u, kErrRank = 16u,
+                   kErrRunning = 32u, kErrDue = 64u, kErrTokens = 128u;
+
+// ---------------------------------------------------------------- views
+struct ReqView {
+  uint32_t n;
+  const int64_t* __restrict__ arrival;
+  const uint32_t* __restrict__ ttft;
+  const uint32_t* __restrict__ period;
+  const uint32_t* __restrict__ ctx_len;
+  const uint32_t* __restrict__ n_deliv;
+  const uint32_t* __restrict__ max_total;
+  const uint32_t* __restrict__ start_off;  // may be null
+  const uint32_t* __restrict__ rank;
+  const uint8_t* __restrict__ running;
+  const uint64_t* __restrict__ tl_base;
+  const uint32_t* __restrict__ tl_pool;
+};
+
+// Small per-call globals (zeroed by one memset node per call).
+struct Globals {
+  unsigned long long run_l;      // sum of l over running requests
+  unsigned long long pool_end;   // tl_base[n-1] + n_deliv[n-1]
+  uint32_t ntiles;               // scan tiles
+  uint32_t inv_minP;             // UINT32_MAX - min_i P_i (atomicMax)
+  uint32_t n_run;                // running requests appended to run_list
+  uint32_t done;                 // select CTAs finished (last-block pattern)
+  uint32_t B_lo, B_hi;           // candidate range
+  uint32_t triggered;
+  uint32_t err;                  // device error word (debug checks), copied out by the host
+  uint32_t slow;                 // slow-path flags
+  uint32_t pad[5];
+};
+
+struct Work {
+  uint32_t* m;               // [N] tokens due at the evaluation time
+  unsigned long long* spre;  // [N] sum of clamped delays of delivered due tokens
+  uint32_t* edge;            // [N] delta_g (g < m) or delta~_m (g >= m)
+  uint32_t* tile_owner;      // [tiles] last request with tl_base <= tile start
+  unsigned long long* tile_status;  // [tiles]
+  uint32_t* hist_l;          // [kHistL] histogram of min(l, kHistL-1)
+  uint32_t* run_list;        // [max_running]
+  uint8_t* mark;             // [N] bit0 in S_{B*}, bit1 preempted, bit2 admitted
+  uint32_t* keyrow;          // [max_B][N] ordered priority keys per candidate B
+  uint32_t* sel;             // [max_B][max_B] Algorithm 1 prefix per B, greedy order
+  Globals* g;
+  uint32_t N_cap;            // row stride of keyrow
+  uint32_t tiles_cap;        // capacity of tile_owner / tile_status
+};
+
+// ---------------------------------------------------------------- small helpers
+__host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t ordered_key(float f) {
+  // monotone map float -> u32 (larger float -> larger u32); -0 is canonicalised earlier
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_from_ordered(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+// composite sort key: descending priority, then ascending rank (reading R10)
+__device__ __forceinline__ unsigned long long composite(uint32_t okey, uint32_t rank) {
+  return ((unsigned long long)okey << 32) | (unsigned long long)(0xFFFFFFFFu - rank);
+}
+
+// due tokens at relative time t (reading R3): 0 if t < ttft, else floor((t - ttft)/P) + 1,
+// capped by max_total (reading R7).
+__device__ __forceinline__ uint32_t due_count(int64_t t, uint32_t ttft, uint32_t P, uint32_t max_total) {
+  if (t < (int64_t)ttft) return 0;
+  unsigned long long q = (unsigned long long)(t - (int64_t)ttft) / P + 1ull;
+  if (q > max_total) q = max_total;
+  return (uint32_t)q;
+}
+
+// clamp(floor(num/div), 0, cap) for div > 0, cap < 2^20, exact.
+// fp32 quotient estimate (abs error < 0.25 on quotients < 2^20) + one integer fix-up.
+__device__ __forceinline__ int64_t qdiv_clamped(int64_t num, int64_t div, int64_t cap) {
+  if (num <= 0) return 0;
+  if (num >= cap * div) return cap;
+  float qf = floorf(__fdividef((float)num, (float)div));
+  int64_t q = (int64_t)qf;
+  int64_t r = num - q * div;
+  if (r < 0) q -= 1;
+  else if (r >= div) q += 1;
+  return q;
+}
+
+// sum_{k=a+1..b} (w0 - k P)
+__device__ __forceinline__ int64_t sum_down(int64_t a, int64_t b, int64_t w0, int64_t P) {
+  int64_t c = b - a;
+  return c * w0 - P * ((c * (a + b + 1)) >> 1);
+}
+// sum_{k=a+1..b} (c0 + k e)
+__device__ __forceinline__ int64_t sum_up(int64_t a, int64_t b, int64_t c0, int64_t e) {
+  int64_t c = b - a;
+  return c * c0 + e * ((c * (a + b + 1)) >> 1);
+}
+
+// Eq. 3 with reading R4, IEEE binary64 round-to-nearest, no contraction.
+__device__ __forceinline__ double qoe_value(int64_t sd, int64_t sw) {
+  if (sw == 0) return 1.0;
+  return __dsub_rn(1.0, __ddiv_rn(__ll2double_rn(sd), __ll2double_rn(sw)));
+}
+
+// ---------------------------------------------------------------- per-request gain state
+// B-independent part of Q_wait / Q_serve(B) for one request.
+struct GainState {
+  int64_t w0;      // t - ttft - (g-1) P      : t - I_{g+k} = w0 - k P
+  int64_t c0;      // (now-a) + o - ttft - (g-1) P : lateness of new token k = c0 + k e
+  int64_t spre;    // sum_{j<=min(g,m)} delta~_j
+  int64_t cw;      // P m (m-1) / 2
+  int64_t dto;     // Delta t - o  (= w0 - c0)
+  uint32_t m, K;   // due tokens, undelivered due tokens (K = m - g if m > g else 0)
+  uint32_t P;
+  uint32_t h0;     // delta_g (0 if g == 0)
+  double qw;       // Q_wait (Eq. 3 on the real timeline)
+};
+
+__device__ __forceinline__ GainState make_state(const ReqView& r, const Work& w, uint32_t i, int64_t now,
+                                                uint32_t horizon) {
+  GainState s;
+  const int64_t a = r.arrival[i];
+  const int64_t t = now + (int64_t)horizon - a;
+  const uint32_t g = r.n_deliv[i];
+  const uint32_t m = w.m[i];
+  const uint32_t P = r.period[i];
+  const int64_t ttft = r.ttft[i];
+  const int64_t o = r.start_off ? (int64_t)r.start_off[i] : 0;
+  s.m = m;
+  s.P = P;
+  s.spre = (int64_t)w.spre[i];
+  s.cw = (int64_t)P * (((int64_t)m * ((int64_t)m - 1)) >> 1);
+  s.w0 = t - ttft - ((int64_t)g - 1) * (int64_t)P;
+  s.c0 = (now - a) + o - ttft - ((int64_t)g - 1) * (int64_t)P;
+  s.dto = (int64_t)horizon - o;
+  if (m == 0) {
+    s.K = 0;
+    s.h0 = 0;
+    s.qw = 1.0;
+  } else if (g >= m) {
+    s.K = 0;
+    s.h0 = 0;
+    const int64_t dm = (int64_t)w.edge[i];
+    s.qw = qoe_value(s.spre, (int64_t)m * dm + s.cw);
+  } else {
+    s.K = m - g;
+    s.h0 = (g == 0) ? 0u : w.edge[i];
+    const int64_t K = s.K;
+    const int64_t sd = s.spre + sum_down(0, K, s.w0, P);
+    const int64_t dm = s.w0 - K * (int64_t)P;  // = t - I_m
+    s.qw = qoe_value(sd, (int64_t)m * dm + s.cw);
+  }
+  return s;
+}
+
+// Q_serve(B) for tau = tau(B) (requires s.K >= 1): new token k delivered at
+// (now - a) + o + k tau, i.e. lateness c0 + k e with e = tau - P.
+__device__ __forceinline__ void serve_area(const GainState& s, uint32_t tau, int64_t& sd, int64_t& sw) {
+  const int64_t K = s.K, P = s.P, w0 = s.w0, c0 = s.c0, h0 = s.h0;
+  const int64_t e = (int64_t)tau - P;
+  int64_t sum, dm;
+  if (e < 0) {
+    // delta_{g+k} = h = max(h0, c0 + e) for every k >= 1
+    const int64_t h = max(h0, c0 + e);
+    const int64_t ks = qdiv_clamped(w0 - h, P, K);
+    sum = h * ks + sum_down(ks, K, w0, P);
+    dm = min(h, w0 - K * P);
+  } else {
+    const int64_t kx = min(qdiv_clamped(w0 - h0, P, K), qdiv_clamped(s.dto, (int64_t)tau, K));
+    int64_t nflat;
+    if (e == 0)
+      nflat = (c0 <= h0) ? kx : 0;
+    else
+      nflat = qdiv_clamped(h0 - c0, e, kx);
+    sum = h0 * nflat + sum_up(nflat, kx, c0, e) + sum_down(kx, K, w0, P);
+    dm = min(max(h0, c0 + K * e), w0 - K * P);
+  }
+  sd = s.spre + sum;
+  sw = (int64_t)s.m * dm + s.cw;
+}
+
+// gain = Q_serve(B) - Q_wait (Eq. 4); 0 exactly when no undelivered token is due.
+__device__ __forceinline__ double gain_at(const GainState& s, uint32_t tau) {
+  if (s.K == 0) return 0.0;
+  int64_t sd, sw;
+  serve_area(s, tau, sd, sw);
+  return __dsub_rn(qoe_value(sd, sw), s.qw);
+}
+
+// priority key (Eq. 6, reading R9): float(gain / l), -0 -> +0
+__device__ __forceinline__ float prio_key(double gain, uint32_t l) {
+  float k = __double2float_rn(__ddiv_rn(gain, (double)l));
+  return (__float_as_uint(k) << 1) == 0u ? 0.0f : k;
+}
+
+__device__ __forceinline__ long long gain_fixed(double gain) {
+  return __double2ll_rn(__dmul_rn(gain, 4294967296.0));
+}
+
+// ---------------------------------------------------------------- sync primitives
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace andes

@@ -1,0 +1,42 @@
+// launch.h -- internal host-side launchers of libandes (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "device.cuh"
+
+namespace andes {
+
+struct LaunchCfg {
+  cudaStream_t stream;
+  uint32_t sm_count;
+  uint32_t scan_grid;  // persistent grid of the timeline scan (all CTAs co-resident)
+};
+
+void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
+                 bool sched, uint64_t kv_cap, bool debug);
+void launch_bounds(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau, uint32_t B_cap,
+                   uint64_t M, uint32_t cur_latency, uint32_t flags);
+void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode);
+void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
+                      float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
+int scan_blocks_per_sm();
+
+struct SchedOut {
+  uint8_t* serve_mask;
+  uint32_t* admit_idx;
+  uint32_t* preempt_idx;
+  uint32_t* scalars;
+  int64_t* V;
+  uint32_t* kstar;
+};
+
+void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
+                          const uint32_t* tau, const uint32_t* B_list_dev, uint32_t nB, double* gain_out,
+                          float* key_out, double* qwait_out);
+void launch_gain_keys(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
+                      const uint32_t* tau, uint32_t B_cap);
+void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
+                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
+void launch_mask(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o);
+
+}  // namespace andes

@@ -1,0 +1,292 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bars: S_delay / S_whole exact (int64); QoE fp64 bit-equal and the
+fp32 QoE within 1e-5 relative (BASELINE north star); gains fp64 bit-equal; priority keys
+fp32 bit-equal; decisions (B*, serve set, admit and preempt lists in order, V(B), k*(B),
+scalars) identical.  Sizes span many 4096-token scan tiles with ragged tails, empty and
+degenerate cases, and the full BASELINE configurations (sampled where the oracle is slow).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def A():
+    import paper_2404_16283_b200 as A
+    from paper_2404_16283_b200 import build
+    build.build()
+    return A
+
+
+@pytest.fixture(scope="module")
+def ctx(A):
+    return A.Context(max_requests=1 << 17, max_B=256, max_tokens=1 << 24, max_running=4096)
+
+
+def _dev(A, snap):
+    return A.requests_to(snap)
+
+
+def _tau(snap):
+    return torch.from_numpy(np.asarray(snap.tau_us, np.uint32).view(np.int32)).cuda()
+
+
+# ---------------------------------------------------------------- S1 QoE
+def _check_qoe(A, ctx, orc, snap, eval_time, final):
+    q, q64, sd, sw, m = ctx.qoe_eval(_dev(A, snap), snap.n, eval_time,
+                                     A.ANDES_EVAL_FINAL if final else A.ANDES_EVAL_INFLIGHT)
+    torch.cuda.synchronize()
+    oq, osd, osw, om = orc.qoe_eval(snap, eval_time, final=final)
+    np.testing.assert_array_equal(m.cpu().numpy().view(np.uint32), om)
+    np.testing.assert_array_equal(sd.cpu().numpy(), osd)
+    np.testing.assert_array_equal(sw.cpu().numpy(), osw)
+    np.testing.assert_array_equal(q64.cpu().numpy(), oq)  # bit-equal fp64
+    qf = q.cpu().numpy()
+    assert np.all(np.abs(qf.astype(np.float64) - oq) <= 1e-5 * np.maximum(np.abs(oq), 1e-30) + 1e-30)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_qoe_random_small(A, ctx, orc, seed):
+    snap = W.random_small(seed, n=int(np.random.default_rng(seed).integers(1, 40)), max_tokens=300)
+    for final in (False, True):
+        _check_qoe(A, ctx, orc, snap, snap.now_us + snap.horizon_us, final)
+        _check_qoe(A, ctx, orc, snap, snap.now_us, final)
+
+
+def test_qoe_many_tiles_ragged(A, ctx, orc):
+    # ~4.7 tiles of tokens, a 100k-token request spanning many tiles, empty requests, a ragged tail
+    rng = np.random.default_rng(99)
+    snap = W.random_small(7, n=60, max_tokens=2000)
+    long = W.snapshot(300, seed=3)
+    for s in (snap, long):
+        _check_qoe(A, ctx, orc, s, s.now_us + s.horizon_us, False)
+        _check_qoe(A, ctx, orc, s, s.now_us, True)
+    # one request with 100,003 tokens on time then late, plus neighbours with 0 and 1 tokens
+    P, ttft = 1000, 5000
+    g = 100_003
+    d = ttft + np.arange(g, dtype=np.int64) * P + np.where(np.arange(g) > 50_000, 7_777, 0)
+    d = np.maximum.accumulate(d + rng.integers(-900, 900, g)).astype(np.uint32)
+    tl = [np.zeros(0, np.uint32), d, np.array([12], np.uint32), np.zeros(0, np.uint32)]
+    gg, base, pool = W._pack(tl)
+    n = 4
+    big = W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, ttft, np.uint32),
+                     period_us=np.full(n, P, np.uint32), ctx_len=np.ones(n, np.uint32), n_deliv=gg,
+                     max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                     rank=np.arange(n, dtype=np.uint32), running=np.zeros(n, np.uint8), tl_base=base,
+                     tl_pool=pool, now_us=int(d[-1]) + 10, horizon_us=2_000_000)
+    for final in (False, True):
+        _check_qoe(A, ctx, orc, big, big.now_us + 3_000_000, final)
+        _check_qoe(A, ctx, orc, big, big.now_us - 40_000_000, final)
+
+
+def test_qoe_config3_full(A, ctx, orc):
+    snap = W.config3()
+    # the oracle is fast enough for QoE (one walk per request)
+    _check_qoe(A, ctx, orc, snap, snap.now_us + snap.horizon_us, False)
+    _check_qoe(A, ctx, orc, snap, snap.now_us, True)
+
+
+# ---------------------------------------------------------------- S3 gains
+def _check_gains(A, ctx, orc, snap, B_list, sub=None):
+    gain, key, qw = ctx.gain_estimate(_dev(A, snap), snap.n, snap.now_us, snap.horizon_us, _tau(snap), B_list)
+    torch.cuda.synchronize()
+    gain, key, qw = gain.cpu().numpy(), key.cpu().numpy(), qw.cpu().numpy()
+    if sub is not None:
+        gain, key, qw = gain[:, sub], key[:, sub], qw[sub]
+        snap = snap.subset(sub)
+    og, ok, oqw = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, B_list)
+    np.testing.assert_array_equal(qw, oqw)
+    np.testing.assert_array_equal(gain, og)
+    np.testing.assert_array_equal(key.view(np.uint32), ok.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_gains_random_small(A, ctx, orc, seed):
+    snap = W.random_small(seed, n=int(np.random.default_rng(seed + 1).integers(1, 30)), max_tokens=200)
+    _check_gains(A, ctx, orc, snap, np.arange(1, snap.tau_us.size + 1))
+
+
+def test_gains_config2_full(A, ctx, orc):
+    snap = W.config2()
+    _check_gains(A, ctx, orc, snap, np.arange(1, 257))
+
+
+def test_gains_config3_sampled(A, ctx, orc):
+    snap = W.config3()
+    rng = np.random.default_rng(0)
+    sub = np.sort(rng.choice(snap.n, 600, replace=False))
+    _check_gains(A, ctx, orc, snap, np.array([1, 2, 3, 64, 127, 128, 200, 234, 235, 236, 255, 256]), sub)
+
+
+# ---------------------------------------------------------------- S0-S6 decisions
+def _run_sched(A, ctx, snap, flags=1, cap=None, cur_latency=0):
+    cap = snap.preempt_cap if cap is None else cap
+    d = ctx.schedule(_dev(A, snap), snap.n, snap.now_us, snap.horizon_us, _tau(snap), snap.kv_capacity,
+                     preempt_cap=cap, cur_latency_us=cur_latency, flags=flags)
+    torch.cuda.synchronize()
+    sc = d.scalars.cpu().numpy().view(np.uint32)
+    return dict(mask=d.serve_mask.cpu().numpy()[:snap.n], admit=d.admit.cpu().numpy().view(np.uint32)[:sc[2]],
+                preempt=d.preempt.cpu().numpy().view(np.uint32)[:sc[3]], sc=sc, V=d.V.cpu().numpy(),
+                kstar=d.kstar.cpu().numpy().view(np.uint32))
+
+
+def _check_sched(A, ctx, orc, snap, flags=1, cap=None, cur_latency=0):
+    cap = snap.preempt_cap if cap is None else cap
+    g = _run_sched(A, ctx, snap, flags, cap, cur_latency)
+    o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity, preempt_cap=cap,
+                     cur_latency_us=cur_latency, flags=flags)
+    trig = bool(g["sc"][6] & 1)
+    assert trig == (o.status == 0)
+    np.testing.assert_array_equal(g["mask"], o.serve_mask)
+    if trig:
+        assert [int(x) for x in g["sc"][[0, 1, 2, 3, 4, 5, 7]]] == [o.B_star, o.realized, o.admit.size,
+                                                                    o.preempt.size, o.B_lo, o.B_hi, o.k_star]
+        assert int(g["sc"][6]) & 7 == o.flags & 7
+        np.testing.assert_array_equal(g["admit"], o.admit)
+        np.testing.assert_array_equal(g["preempt"], o.preempt)
+        np.testing.assert_array_equal(g["V"], o.V)
+        np.testing.assert_array_equal(g["kstar"], o.kstar)
+    return g, o
+
+
+def test_golden_g1_on_gpu(A, ctx, orc):
+    from test_oracle_pins import g1_snapshot
+    for cap in (W.UINT32_MAX, 0, 1):
+        snap, d = g1_snapshot(cap)
+        g, o = _check_sched(A, ctx, orc, snap, cap=cap)
+        assert int(g["sc"][0]) == d["expected"]["B_star"]
+        assert g["V"][:3].tolist() == d["expected"]["V_by_B"][:3]
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_schedule_random_small(A, ctx, orc, seed):
+    snap = W.random_small(seed, B_cap=int(np.random.default_rng(seed).integers(1, 20)))
+    flags = [1, 3, 0, 2][seed % 4]
+    _check_sched(A, ctx, orc, snap, flags=flags, cur_latency=[0, 400_000][seed % 2])
+
+
+def test_schedule_ties_and_zero_gains(A, ctx, orc):
+    # every request on schedule far ahead -> all gains 0: selection by rank only
+    n = 300
+    tl = [np.arange(50, dtype=np.uint32) * 1000 for _ in range(n)]
+    g, base, pool = W._pack(tl)
+    rng = np.random.default_rng(5)
+    snap = W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, 1_000_000, np.uint32),
+                      period_us=np.full(n, 200_000, np.uint32), ctx_len=rng.integers(1, 40, n).astype(np.uint32),
+                      n_deliv=g, max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=rng.permutation(n).astype(np.uint32), running=(rng.random(n) < 0.3).astype(np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=1_000_000, horizon_us=2_000_000,
+                      tau_us=W.tau_table(64), kv_capacity=900)
+    for cap in (W.UINT32_MAX, 0, 3):
+        _check_sched(A, ctx, orc, snap, cap=cap)
+
+
+def test_schedule_config2_full(A, ctx, orc):
+    snap = W.config2()
+    _check_sched(A, ctx, orc, snap)
+    _check_sched(A, ctx, orc, snap, flags=3)
+    _check_sched(A, ctx, orc, snap, cap=16)
+
+
+def test_schedule_config3_properties(A, ctx, orc):
+    """Full-size config 3 (the bench workload, same launch): the oracle needs minutes, so check
+    (a) determinism, (b) B* / serve set against Algorithm 1 recomputed on host from the GPU's
+    gain_estimate keys at B*, whose parity is sampled in test_gains_config3_sampled, (c) the cap."""
+    snap = W.config3()
+    g1 = _run_sched(A, ctx, snap)
+    g2 = _run_sched(A, ctx, snap)
+    for k in g1:
+        np.testing.assert_array_equal(g1[k], g2[k])
+    sc = g1["sc"]
+    Bs, ks = int(sc[0]), int(sc[7])
+    assert sc[6] & 1 and 1 <= Bs <= 256 and sc[5] == 256
+    gain, key, qw = ctx.gain_estimate(_dev(A, snap), snap.n, snap.now_us, snap.horizon_us, _tau(snap), [Bs])
+    key = key.cpu().numpy()[0]
+    gain = gain.cpu().numpy()[0]
+    order = np.lexsort((snap.rank, -key.astype(np.float64)))
+    csum = np.cumsum(snap.ctx_len[order].astype(np.int64))
+    k = int(min(Bs, np.searchsorted(csum, snap.kv_capacity, side="right")))
+    assert k == ks
+    S = set(order[:k].tolist())
+    vfix = int(np.sum(np.rint(gain[order[:k]] * 2.0 ** 32).astype(np.int64)))
+    assert vfix == int(g1["V"][Bs - 1])
+    assert int(np.max(g1["V"])) == int(g1["V"][Bs - 1])
+    running = set(np.nonzero(snap.running)[0].tolist())
+    victims = running - S
+    assert int(sc[3]) == min(len(victims), snap.preempt_cap) or sc[6] & 4
+    assert set(g1["preempt"].tolist()) <= victims
+
+
+def test_schedule_host_path_matches(A, ctx, orc):
+    snap = W.config2()
+    g = _run_sched(A, ctx, snap, cap=16)
+    hreq = A.requests_to(snap, pin=True)
+    tau_h = torch.from_numpy(np.asarray(snap.tau_us, np.uint32).view(np.int32)).pin_memory()
+    out, rc = ctx.schedule_host(hreq, snap.n, snap.now_us, snap.horizon_us, tau_h, snap.kv_capacity,
+                                preempt_cap=16)
+    sc = out.scalars.numpy().view(np.uint32)
+    np.testing.assert_array_equal(sc, g["sc"])
+    np.testing.assert_array_equal(out.serve_mask.numpy()[:snap.n], g["mask"])
+    np.testing.assert_array_equal(out.preempt.numpy().view(np.uint32)[:sc[3]], g["preempt"])
+
+
+def test_not_triggered(A, ctx, orc):
+    snap = W.random_small(4, n=10)
+    snap.kv_capacity = 10_000
+    _check_sched(A, ctx, orc, snap, flags=0, cur_latency=0)
+
+
+# ---------------------------------------------------------------- config 1: 200-iteration driver
+def _iterate(A, ctx, orc, iters=200, seed=1):
+    """BASELINE config 1: 8 requests, ttft 1 s, 4.8 tok/s, M = 2048; each iteration the GPU
+    decision must equal the oracle's; the clock advances by tau(realized) and every served
+    request receives one token; finished requests leave."""
+    rng = np.random.default_rng(seed)
+    n = 8
+    prompt = rng.integers(150, 601, n)
+    out_len = rng.integers(20, 121, n)
+    arr = rng.integers(0, 2_000_001, n).astype(np.int64)
+    order = np.argsort(arr, kind="stable")
+    prompt, out_len, arr = prompt[order], out_len[order], arr[order]
+    tau = W.tau_table(8)
+    now = int(arr.max())
+    toks = [[] for _ in range(n)]
+    running = np.zeros(n, np.uint8)
+    alive = np.ones(n, bool)
+    checked = 0
+    for it in range(iters):
+        idx = np.nonzero(alive & (arr <= now))[0]
+        if idx.size == 0:
+            now += 100_000
+            continue
+        g, base, pool = W._pack([np.asarray(toks[i], np.uint32) for i in idx])
+        snap = W.Snapshot(arrival_us=arr[idx], ttft_us=np.full(idx.size, 1_000_000, np.uint32),
+                          period_us=np.full(idx.size, 208_333, np.uint32),
+                          ctx_len=(prompt[idx] + g).astype(np.uint32), n_deliv=g,
+                          max_total=np.full(idx.size, W.UINT32_MAX, np.uint32),
+                          start_off_us=np.zeros(idx.size, np.uint32), rank=idx.astype(np.uint32),
+                          running=running[idx], tl_base=base, tl_pool=pool, now_us=now, horizon_us=2_000_000,
+                          tau_us=tau, kv_capacity=2048)
+        gd, od = _check_sched(A, ctx, orc, snap, flags=1)
+        checked += 1
+        served = idx[np.nonzero(od.serve_mask)[0]]
+        realized = max(1, served.size)
+        now += int(tau[min(realized, tau.size) - 1])
+        running[:] = 0
+        for i in served:
+            toks[i].append(now - int(arr[i]))
+            running[i] = 1
+            if len(toks[i]) >= out_len[i]:
+                alive[i] = False
+                running[i] = 0
+    return checked
+
+
+def test_config1_iteration_driver(A, ctx, orc):
+    assert _iterate(A, ctx, orc) >= 150
