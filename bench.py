@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py -- Andes scheduling decisions/s at 64K live requests on B200 (BASELINE config 3),
+plus QoE-eval token-events/s against the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full Andes decision (S0-S6: trigger, timeline QoE scan, gains for every
+B = 1..256, Algorithm 1 per B, best B, preemption cap) over the config-3 snapshot, captured
+once in a CUDA graph and replayed; inputs resident in HBM; L2 flushed (256 MiB write)
+between timed steps; device time from CUDA events.  Under torchrun (N > 1) every rank
+schedules its own independent 64K-request instance (weak scaling, no data-path
+collective); rank 0 prints the JSON line with the max-over-ranks time.
+
+--impl reference times the CPU oracle (oracle/, plain C, one core) on a bounded sample of
+the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Andes sched decisions/s at 64K live requests; QoE-eval token-events/s vs HBM"
+WORKLOAD = ("config3: burst arrivals at 2x capacity, 64K live requests (ShareGPT-shaped), 50/50 "
+            "reading/listening, B=1..256 (pruning off), M=163840, dt=2s, preemption cap 16")
+UNIT = "decisions/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _hbm_peak():
+    p = _peaks()
+    if "hbm_gbs" in p:
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        if sm:
+            out["sm_mhz"] = statistics.median(sm)
+            out["sm_max_mhz"] = float(rows[0][2])
+            out["samples"] = len(sm)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip() == "Active" and nm not in out["reasons"]:
+                        out["reasons"].append(nm)
+        return out
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        lr = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl")
+        return dist, dist.get_rank(), ws, lr
+    return None, 0, 1, 0
+
+
+def _max_over_ranks(dist, x):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _token_events(snap):
+    import numpy as np
+    t = snap.now_us + snap.horizon_us - snap.arrival_us
+    m = np.where(t < snap.ttft_us, 0, (t - snap.ttft_us.astype(np.int64)) // snap.period_us + 1)
+    m = np.minimum(m, snap.max_total)
+    return int(np.minimum(snap.n_deliv, m).sum())
+
+
+def _tile(snap, reps):
+    """reps copies of a snapshot (same shape/statistics), for the QoE-eval throughput run."""
+    import numpy as np
+    from dataclasses import replace
+    n, T = snap.n, snap.n_tokens
+    base = np.concatenate([snap.tl_base + np.uint64(k * T) for k in range(reps)])
+    return replace(snap, arrival_us=np.tile(snap.arrival_us, reps), ttft_us=np.tile(snap.ttft_us, reps),
+                   period_us=np.tile(snap.period_us, reps), ctx_len=np.tile(snap.ctx_len, reps),
+                   n_deliv=np.tile(snap.n_deliv, reps), max_total=np.tile(snap.max_total, reps),
+                   start_off_us=np.tile(snap.start_off_us, reps),
+                   rank=np.arange(n * reps, dtype=np.uint32), running=np.tile(snap.running, reps),
+                   tl_base=base, tl_pool=np.tile(snap.tl_pool, reps))
+
+
+def cpu_baseline(snap, B_sample=8):
+    """The oracle as it stands (plain C, single thread) on the full 64K snapshot restricted to
+    B = 1..B_sample; scaled to a full decision by (256 + 1)/(B_sample + 1) walks."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us[:B_sample], snap.kv_capacity,
+                    preempt_cap=snap.preempt_cap, B_cap=B_sample)
+    dt = time.perf_counter() - t0
+    full_s = dt * (256 + 1) / (B_sample + 1)
+    return {"value": 1.0 / full_s, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"oracle_schedule on the full 64K config-3 snapshot with B=1..{B_sample} "
+                       f"({dt:.2f} s), scaled x{(257) / (B_sample + 1):.1f} to B=1..256 "
+                       f"(each B = one literal walk of every due token, plus Q_wait)")}
+
+
+def run_reference(args):
+    dist, rank, ws, _ = _dist()
+    if rank != 0:
+        return
+    import workloads as W
+    import oracle
+    oracle.build()
+    snap = W.config3()
+    b = 2
+    for _ in range(args.warmup):
+        oracle.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us[:b], snap.kv_capacity,
+                        preempt_cap=snap.preempt_cap, B_cap=b)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us[:b], snap.kv_capacity,
+                        preempt_cap=snap.preempt_cap, B_cap=b)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    full = dt * 257 / (b + 1)
+    v = 1.0 / full
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": full * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic (workloads.config3, seed 1)",
+            "config": {"workload": WORKLOAD},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step: oracle_schedule on the full 64K snapshot, B=1..{b}, "
+                                       f"{dt:.2f} s, scaled x{257 / (b + 1):.1f} to B=1..256"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2404_16283_b200 as A
+    import workloads as W
+    from paper_2404_16283_b200 import build as Bd
+
+    dist, rank, ws, lr = _dist()
+    Bd.build()
+    dev = torch.device("cuda", lr)
+    torch.cuda.set_device(dev)
+    snap = W.config3(seed=1 + rank)
+    n = snap.n
+    ev_tokens = _token_events(snap)
+    ctx = A.Context(max_requests=n, max_B=256, max_tokens=snap.n_tokens + 64, device=lr)
+    req = A.requests_to(snap, device=dev)
+    tau = torch.from_numpy(snap.tau_us.view(np.int32)).to(dev)
+    stream = torch.cuda.Stream(device=dev)
+    out = ctx.alloc_decision(n, 256)
+    ctx.profile_enable(True)
+    kw = dict(preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
+
+    def decide(s):
+        ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=s, **kw)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            decide(stream)
+        stream.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            decide(stream)
+        graph.replay()
+        stream.synchronize()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(max(args.warmup, 3)):
+            flush.zero_()
+            graph.replay()
+        stream.synchronize()
+
+        # ---- timed region: K decisions, L2 flushed between steps, CUDA events per step
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        stage_sum = [0.0] * A.N_STAGES
+        clk = Clocks(lr)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.start()
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            graph.replay()
+            ends[k].record(stream)
+            ends[k].synchronize()
+            st = ctx.profile_read()
+            stage_sum = [a + b for a, b in zip(stage_sum, st)]
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clocks = clk.stop()
+        step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        total_ms = _max_over_ranks(dist, sum(step_ms))
+        # L2-warm back-to-back replays (context)
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        w1.record(stream)
+        w1.synchronize()
+        warm_ms = w0.elapsed_time(w1) / args.steps
+
+    sc = out.scalars.cpu().numpy().view(np.uint32)
+    stage_ms = [x / args.steps for x in stage_sum]
+    ms_per_step = total_ms / args.steps
+    value = ws * args.steps / (total_ms / 1e3)
+
+    # ---- roofline of the dominant kernel
+    hbm_peak, hbm_src = _hbm_peak()
+    names = A.STAGES
+    dom = max(range(len(stage_ms)), key=lambda i: stage_ms[i])
+    scan_bytes = 4 * snap.n_tokens + 44 * n  # one read of every timestamp + per-request SoA/state
+    gain_bytes = 4 * n * 256 + 44 * n        # key rows written + state read
+    select_bytes = 4 * n * 256 * 2           # key rows read (>= 2 radix passes) -- L2-resident traffic
+    alg_bytes = {"scan": scan_bytes, "gain": gain_bytes, "select": select_bytes}
+    dom_name = names[dom]
+    if dom_name in alg_bytes:
+        ach = alg_bytes[dom_name] / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None, "peak_source": hbm_src,
+                "algorithmic_bytes_per_launch": alg_bytes[dom_name]}
+    else:
+        roof = {"kernel": dom_name, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None}
+    roof["stage_ms"] = dict(zip(names, stage_ms))
+    roof["stage_share"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
+
+    # ---- S1 alone at scale: QoE-eval token-events/s on a 1M-request population (config-4 size)
+    big = _tile(snap, 16)
+    qctx = A.Context(max_requests=big.n, max_B=8, max_tokens=big.n_tokens + 64, device=lr)
+    breq = A.requests_to(big, device=dev)
+    big_events = _token_events(big)
+    qctx.profile_enable(True)
+    q_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(max(args.warmup, 3) + 10):
+            flush.zero_()
+            qctx.qoe_eval(breq, big.n, big.now_us + big.horizon_us, A.ANDES_EVAL_INFLIGHT, stream=stream)
+            st = qctx.profile_read()
+            if k >= max(args.warmup, 3):
+                q_ms.append(st)
+    scan_ms = statistics.median([s[2] for s in q_ms])
+    qoe_ms = statistics.median([s[0] + s[2] + s[3] for s in q_ms])
+    qbytes = 4 * big.n_tokens + 44 * big.n
+    q_ach = qbytes / (scan_ms / 1e3) / 1e9
+    qoe_eval = {"metric": "QoE-eval token-events/s", "value": big_events / (qoe_ms / 1e3),
+                "unit": "token-events/s", "n_requests": big.n, "token_events": big_events,
+                "pool_tokens": big.n_tokens, "ms_per_eval": qoe_ms, "scan_ms": scan_ms,
+                "roofline": {"kernel": "k_qoe_scan", "bound": "hbm", "achieved": q_ach, "peak": hbm_peak,
+                             "unit": "GB/s", "frac": q_ach / hbm_peak, "traffic": None,
+                             "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
+    del qctx, breq
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    hreq = A.requests_to(snap, pin=True)
+    tau_h = torch.from_numpy(snap.tau_us.view(np.int32)).pin_memory()
+    hout = ctx.alloc_decision(n, 256, pin=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    ctx.profile_enable(False)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            ctx.schedule_host(hreq, n, snap.now_us, snap.horizon_us, tau_h, snap.kv_capacity, out=hout,
+                              stream=stream, **kw)
+        e_ms = []
+        for _ in range(e2e_steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.schedule_host(hreq, n, snap.now_us, snap.horizon_us, tau_h, snap.kv_capacity, out=hout,
+                              stream=stream, **kw)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+    e_total = _max_over_ranks(dist, sum(e_ms))
+    hsc = hout.scalars.numpy().view(np.uint32)
+    h2d = sum(t.numel() * t.element_size() for k, t in hreq.items() if t is not None) + tau_h.numel() * 4
+    d2h = 32 + n + 4 * int(hsc[2]) + 4 * int(hsc[3]) + 12 * 256 + 32
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64/f64",
+        "data": "synthetic (seeded ShareGPT-shaped cyclic-burst snapshot, workloads.config3; seed 1+rank)",
+        "config": {"workload": WORKLOAD, "n_requests": n, "pool_tokens": snap.n_tokens,
+                   "token_events": ev_tokens, "B_cap": 256, "l2": "flushed: 256 MiB write between timed steps",
+                   "launch": "one CUDA graph per decision (6 kernels)", "warm_l2_ms_per_step": warm_ms,
+                   "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}},
+        "roofline": roof,
+        "qoe_eval": qoe_eval,
+        "e2e": {"value": ws * e2e_steps / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "api": "andes_schedule_host (pinned host buffers)"},
+        "gpu_launches": 6 * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(snap)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -26,6 +26,8 @@
  *  - The library never allocates, frees or synchronises inside a device entry
  *    point; its workspace is sized by andes_create's limits.
  *  - One context per stream; contexts are not thread-safe.
+ *  - andes_qoe_eval / andes_gain_estimate / andes_schedule are stream-capture safe: a
+ *    decision can be captured once into a CUDA graph and replayed (same pointers/params).
  *  - Data preconditions (timestamps nondecreasing, 1 <= l_i <= M, ranks unique,
  *    tl_base nondecreasing) are checked on the device only when
  *    ANDES_DEBUG_CHECKS is set; a violation sets the context's device error word
@@ -177,6 +179,17 @@ int andes_schedule(AndesCtx *ctx, const AndesRequests *req, const AndesSchedPara
  * to have been created with max_tokens covering the pool. */
 int andes_schedule_host(AndesCtx *ctx, const AndesRequests *req_host, const AndesSchedParams *p_host,
                         AndesDecision *out_host, void *stream);
+
+/* Per-stage timing.  When enabled, andes_schedule records a CUDA event before its first
+ * and after each of its kernels on the call's stream (also under stream capture, so a
+ * captured CUDA graph of a decision carries the event-record nodes).  andes_profile_read
+ * blocks until the last recorded event completes and writes the elapsed milliseconds of
+ * each stage: [0] reset+prep (S0 inputs), [1] bounds (S0/S2), [2] timeline scan (S1),
+ * [3] gains for every B (S3), [4] Algorithm 1 per B + best B + cap (S4-S6), [5] serve mask.
+ * Errors: ANDES_E_INVAL (profiling off / nothing recorded), ANDES_E_CUDA. */
+#define ANDES_N_STAGES 6
+int andes_profile_enable(AndesCtx *ctx, int enable);
+int andes_profile_read(AndesCtx *ctx, float *stage_ms);
 
 /* Library version string, e.g. "andes-b200 0.1 sm_100a". */
 const char *andes_version(void);

@@ -35,7 +35,9 @@ UINT32_MAX = 0xFFFFFFFF
 SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags", "k_star"]
 
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
-           "andes_schedule", "andes_schedule_host", "andes_version"]
+           "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read"]
+N_STAGES = 6
+STAGES = ["prep", "bounds", "scan", "gain", "select", "mask"]
 
 
 class AndesError(RuntimeError):
@@ -93,6 +95,8 @@ def lib() -> C.CDLL:
                                           C.c_void_p]
         L.andes_schedule.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
                                      C.POINTER(DecisionPtrs), C.c_void_p]
+        L.andes_profile_enable.argtypes = [C.c_void_p, C.c_int]
+        L.andes_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
         L.andes_schedule_host.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
                                           C.POINTER(DecisionPtrs), C.c_void_p]
         _lib = L
@@ -194,6 +198,15 @@ class Context:
         if rc < 0:
             raise AndesError(f"{what} failed rc={rc}: {lib().andes_last_error(self._h).decode()}")
         return rc
+
+    # -- profiling hooks
+    def profile_enable(self, on=True):
+        self._check(lib().andes_profile_enable(self._h, int(bool(on))), "andes_profile_enable")
+
+    def profile_read(self):
+        buf = (C.c_float * N_STAGES)()
+        self._check(lib().andes_profile_read(self._h, buf), "andes_profile_read")
+        return list(buf)
 
     # -- andes_qoe_eval
     def qoe_eval(self, req: dict, n: int, eval_time_us: int, mode=ANDES_EVAL_INFLIGHT, stream=None):

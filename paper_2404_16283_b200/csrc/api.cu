@@ -34,6 +34,9 @@ struct AndesCtx {
     int64_t* V;
   } mir{};
   std::string err;
+  bool prof = false;
+  bool prof_recorded = false;
+  cudaEvent_t ev[ANDES_N_STAGES + 1] = {};
 };
 
 namespace {
@@ -130,6 +133,16 @@ int reset_call(AndesCtx* c, cudaStream_t s) {
   return cuda_check(c, e, "memset");
 }
 
+inline void mark(AndesCtx* c, int i, cudaStream_t s) {
+  if (!c->prof) return;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  if (st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(c->ev[i], s, cudaEventRecordExternal);  // a real record node in the graph
+  else
+    cudaEventRecord(c->ev[i], s);
+}
+
 int finish_call(AndesCtx* c, cudaStream_t s, bool debug) {
   if (debug) {
     cudaError_t e = cudaMemcpyAsync(c->err_pinned, &c->w.g->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
@@ -169,6 +182,8 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->sm_count = (uint32_t)sms;
+  init_kernels();
+  init_scan_kernels();
   const int bps = scan_blocks_per_sm();
   c->scan_grid = (uint32_t)(sms * (bps > 0 ? bps : 1));
   const uint32_t N = lim->max_requests;
@@ -222,9 +237,52 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   return ANDES_OK;
 }
 
+// Internal debugging hook (not part of include/andes.h): synchronous copy of a workspace array.
+int andes_debug_read(AndesCtx* c, int which, void* host, size_t bytes) {
+  if (!c || !host) return ANDES_E_INVAL;
+  const void* src = nullptr;
+  switch (which) {
+    case 0: src = c->w.tile_status; break;
+    case 1: src = c->w.spre; break;
+    case 2: src = c->w.edge; break;
+    case 3: src = c->w.m; break;
+    case 4: src = c->w.tile_owner; break;
+    case 5: src = c->w.g; break;
+    case 6: src = c->w.hist_l; break;
+    default: return ANDES_E_INVAL;
+  }
+  return cuda_check(c, cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost), "debug read");
+}
+
+int andes_profile_enable(AndesCtx* c, int enable) {
+  if (!c) return ANDES_E_INVAL;
+  if (enable && !c->ev[0]) {
+    for (int i = 0; i <= ANDES_N_STAGES; ++i) {
+      cudaError_t e = cudaEventCreate(&c->ev[i]);
+      if (e != cudaSuccess) return cuda_check(c, e, "cudaEventCreate");
+    }
+  }
+  c->prof = enable != 0;
+  return ANDES_OK;
+}
+
+int andes_profile_read(AndesCtx* c, float* stage_ms) {
+  if (!c || !stage_ms) return ANDES_E_INVAL;
+  if (!c->prof_recorded) return set_err(c, ANDES_E_INVAL, "no profiled call recorded%s");
+  cudaError_t e = cudaEventSynchronize(c->ev[ANDES_N_STAGES]);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaEventSynchronize");
+  for (int i = 0; i < ANDES_N_STAGES; ++i) {
+    e = cudaEventElapsedTime(&stage_ms[i], c->ev[i], c->ev[i + 1]);
+    if (e != cudaSuccess) return cuda_check(c, e, "cudaEventElapsedTime");
+  }
+  return ANDES_OK;
+}
+
 int andes_destroy(AndesCtx* c) {
   if (!c) return ANDES_E_INVAL;
   cudaSetDevice(c->device);
+  for (int i = 0; i <= ANDES_N_STAGES; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   for (void* p : c->allocs) cudaFree(p);
   if (c->err_pinned) cudaFreeHost(c->err_pinned);
   delete c;
@@ -244,10 +302,19 @@ int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, 
   const ReqView r = view_of(req);
   const Work w = work_of(c, r.n);
   const bool fin = mode == ANDES_EVAL_FINAL;
+  // profiled stages: [0] prep, [2] scan, [3] finalize (bounds/select/mask empty)
+  mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
   launch_prep(L, r, w, eval_time_us, fin, false, 0, false);
+  mark(c, 1, s);
+  mark(c, 2, s);
   launch_scan(L, r, w, eval_time_us, fin);
+  mark(c, 3, s);
   launch_qoe_final(L, r, w, eval_time_us, fin, out->q, out->q64, out->s_delay, out->s_whole, out->m);
+  mark(c, 4, s);
+  mark(c, 5, s);
+  mark(c, 6, s);
+  if (c->prof) c->prof_recorded = true;
   return finish_call(c, s, false);
 }
 
@@ -299,13 +366,21 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
+  mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
   launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug);
+  mark(c, 1, s);
   launch_bounds(L, r, w, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
+  mark(c, 2, s);
   launch_scan(L, r, w, eval, false);
+  mark(c, 3, s);
   launch_gain_keys(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap);
+  mark(c, 4, s);
   launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
+  mark(c, 5, s);
   launch_mask(L, r, w, o);
+  mark(c, 6, s);
+  if (c->prof) c->prof_recorded = true;
   return finish_call(c, s, debug);
 }
 

@@ -14,9 +14,11 @@ namespace andes {
 
 // ---------------------------------------------------------------- constants
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (16 KiB)
-constexpr int kWindowCap = 1024;                  // request window staged per tile
+constexpr int kScanItems = 32;
+constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (32 KiB)
+constexpr int kWinCap = 480;                      // requests staged per tile (window)
+constexpr int kCarryDirect = 2 * kTile;
+constexpr int kScanDynSmem = 2 * kTile * 4;      // double-buffered tiles (dynamic shared memory)           // head segments up to this long: carry read directly
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;
@@ -60,7 +62,8 @@ struct Globals {
   uint32_t triggered;
   uint32_t err;                  // device error word (debug checks), copied out by the host
   uint32_t slow;                 // slow-path flags
-  uint32_t pad[5];
+  uint32_t tile_ctr;             // dynamic tile counter of the timeline scan
+  uint32_t pad[4];
 };
 
 struct Work {

@@ -20,6 +20,7 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
 int scan_blocks_per_sm();
+void init_scan_kernels();
 
 struct SchedOut {
   uint8_t* serve_mask;
@@ -37,6 +38,7 @@ void launch_gain_keys(const LaunchCfg& L, const ReqView& r, const Work& w, int64
                       const uint32_t* tau, uint32_t B_cap);
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
+void init_kernels();
 void launch_mask(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o);
 
 }  // namespace andes

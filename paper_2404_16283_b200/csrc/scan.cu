@@ -10,6 +10,8 @@
 // memory with cp.async.bulk (TMA bulk copy, mbarrier completion), double-buffered,
 // by a persistent grid; the prefix max crosses tile boundaries through a single-pass
 // decoupled look-back on the segmented-max monoid (flag = segment start, value = max).
+#include <cstdlib>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -207,7 +209,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
@@ -232,29 +234,93 @@ struct ScanArgs {
   ReqView r;
   Work w;
   int64_t eval_abs;
+  uint32_t debug;  // ANDES_SCAN_DEBUG: poison tile buffers before each bulk copy, count survivors
 };
 
-// Issue the bulk copy of tile t into buffer buf (one elected thread).
+// Issue the bulk copy of tile t into buf (one elected thread); the 16-byte-aligned body
+// goes through the TMA bulk-copy engine, the < 4-token tail is copied by threads.
 __device__ __forceinline__ void issue_tile(const ScanArgs& A, uint32_t t, unsigned long long pool_end,
                                            uint32_t* buf, uint64_t* bar) {
   const unsigned long long p0 = (unsigned long long)t * kTile;
   const unsigned long long pend = min(p0 + (unsigned long long)kTile, pool_end);
-  const uint32_t cnt = (uint32_t)(pend - p0);
-  const uint32_t bulk = (cnt / 4u) * 16u;  // 16-byte multiple
+  const uint32_t bulk = ((uint32_t)(pend - p0) / 4u) * 16u;
+  if (A.debug) {
+    for (uint32_t i = 0; i < (uint32_t)kTile; ++i) buf[i] = 0xFFFFFFFFu;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   mbar_expect_tx(bar, bulk);
   if (bulk) bulk_g2s(buf, A.r.tl_pool + p0, bulk, bar);
+}
+
+// One request of a tile's window in tile-local coordinates (x = position - p0).
+struct Entry {
+  int32_t ls;     // local start (base - p0), clamped to [-1, kTile + 1]
+  int32_t vend;   // local end of the valid tokens (base + lim - p0), clamped to [-1, kTile]
+  uint32_t A;     // ideal time of local position 0: ttft + (p0 - base) P (mod 2^32); I(x) = A + x P
+  uint32_t U;     // t_rel - A (mod 2^32): t - I(x) = U - x P
+  uint32_t P;
+  int32_t epos;   // local position of the edge token (the last valid token) or -1
+  uint32_t ek;    // edge kind: 1 = delta_g (g < m, unclamped), 2 = delta~_m
+  uint32_t ridx;  // request index (0xFFFFFFFF: dummy / sentinel)
+};
+
+// Window entry q of a tile whose first request is r0 (dummy = a gap precedes request r0).
+template <bool kFinal>
+__device__ __forceinline__ Entry make_entry(const ScanArgs& A, unsigned long long p0, uint32_t r0, uint32_t dummy,
+                                            uint32_t wn, uint32_t q) {
+  Entry e;
+  if ((dummy && q == 0) || q >= wn) {
+    e.ls = (q >= wn) ? kTile + 1 : -1;
+    e.vend = -1;
+    e.A = 0; e.U = 0; e.P = 1; e.epos = -1; e.ek = 0; e.ridx = 0xFFFFFFFFu;
+    return e;
+  }
+  const ReqView& r = A.r;
+  const uint32_t ri = r0 + q - dummy;
+  const unsigned long long base = r.tl_base[ri];
+  const uint32_t g = r.n_deliv[ri];
+  const uint32_t m = kFinal ? g : A.w.m[ri];
+  const uint32_t lim = min(g, m);
+  const uint32_t P = r.period[ri];
+  const uint32_t ttft = r.ttft[ri];
+  const long long ls = (long long)base - (long long)p0;
+  const long long ve = ls + (long long)lim;
+  e.ls = (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+  e.vend = (int32_t)max(-1ll, min(ve, (long long)kTile));
+  e.A = ttft + (uint32_t)(unsigned long long)(-ls) * P;
+  uint32_t trel = 0;
+  if (!kFinal) trel = (uint32_t)(A.eval_abs - r.arrival[ri]);
+  e.U = trel - e.A;
+  e.P = P;
+  e.ridx = ri;
+  e.epos = -1;
+  e.ek = 0;
+  if (lim > 0) {
+    const long long x = ls + (long long)lim - 1;
+    if (x >= 0 && x < (long long)kTile) {
+      e.epos = (int32_t)x;
+      e.ek = (!kFinal && g < m) ? 1u : 2u;
+    }
+  }
+  return e;
 }
 
 }  // namespace
 
 template <bool kFinal>
 __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
-  __shared__ alignas(128) uint32_t s_tile[2][kTile];
+  extern __shared__ __align__(128) uint32_t s_dyn_tiles[];  // [2][kTile], dynamic (64 KiB)
+  uint32_t(*s_tile)[kTile] = reinterpret_cast<uint32_t(*)[kTile]>(s_dyn_tiles);
   __shared__ alignas(8) uint64_t s_bar[2];
-  __shared__ unsigned long long s_win[kWindowCap + 1];
+  __shared__ int32_t w_ls[kWinCap + 2], w_vend[kWinCap + 2], w_epos[kWinCap + 2];
+  __shared__ uint32_t w_A[kWinCap + 2], w_U[kWinCap + 2], w_P[kWinCap + 2], w_ek[kWinCap + 2],
+      w_ridx[kWinCap + 2];
+  __shared__ uint32_t s_own[kScanThreads + 1];
   __shared__ unsigned long long s_warp[kScanThreads / 32];
   __shared__ unsigned long long s_carry;
-  __shared__ uint32_t s_r0, s_wn;
+  __shared__ uint32_t s_tcur, s_tnext, s_r0, s_wn, s_dummy, s_mode, s_cmax;
+  __shared__ unsigned long long s_hbase;  // head request base / ideal info for the direct carry
+  __shared__ uint32_t s_hcnt, s_httft, s_hP;
 
   const ReqView& r = A.r;
   const Work& w = A.w;
@@ -262,130 +328,197 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
   const uint32_t ntiles = w.g->ntiles;
   const unsigned long long pool_end = w.g->pool_end;
   const uint32_t n = r.n;
+  // window entry q (shared memory when the tile's window fits, else straight from global)
+  auto fetch = [&](uint32_t q, bool win_ok, unsigned long long p0, uint32_t r0, uint32_t dummy,
+                   uint32_t wn) -> Entry {
+    if (win_ok) {
+      Entry e;
+      e.ls = w_ls[q]; e.vend = w_vend[q]; e.A = w_A[q]; e.U = w_U[q]; e.P = w_P[q];
+      e.epos = w_epos[q]; e.ek = w_ek[q]; e.ridx = w_ridx[q];
+      return e;
+    }
+    return make_entry<kFinal>(A, p0, r0, dummy, wn, q);
+  };
+  auto next_ls = [&](uint32_t q, bool win_ok, unsigned long long p0, uint32_t r0, uint32_t dummy,
+                     uint32_t wn) -> int32_t {
+    if (win_ok) return w_ls[q];
+    if (q >= wn) return kTile + 1;
+    if (dummy && q == 0) return -1;
+    const long long ls = (long long)r.tl_base[r0 + q - dummy] - (long long)p0;
+    return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+  };
 
   if (tid == 0) {
+    s_cmax = 0;
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // Tiles are claimed dynamically in increasing order, so every tile a CTA may wait on in
+    // the look-back belongs to a CTA that is already running.
+    const uint32_t t0 = atomicAdd(&w.g->tile_ctr, 1u);
+    s_tcur = t0;
+    if (t0 < ntiles) issue_tile(A, t0, pool_end, s_tile[0], &s_bar[0]);
   }
   __syncthreads();
-  uint32_t phase[2] = {0u, 0u};
-  uint32_t t = blockIdx.x;
-  if (tid == 0 && t < ntiles) issue_tile(A, t, pool_end, s_tile[0], &s_bar[0]);
-  uint32_t buf = 0;
+  uint32_t t = s_tcur;
+  uint32_t buf = 0, ph0 = 0, ph1 = 0;
 
-  for (; t < ntiles; t += gridDim.x, buf ^= 1u) {
+  for (; t < ntiles; buf ^= 1u) {
     const unsigned long long p0 = (unsigned long long)t * kTile;
-    const unsigned long long pend = min(p0 + (unsigned long long)kTile, pool_end);
-    // prefetch the next tile of this CTA into the other buffer (its previous generic-proxy
-    // reads/writes were ordered by the trailing __syncthreads; fence them against the
-    // async-proxy bulk write)
-    if (tid == 0 && t + gridDim.x < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile(A, t + gridDim.x, pool_end, s_tile[buf ^ 1u], &s_bar[buf ^ 1u]);
-    }
-
-    // request window: requests r0 .. r_end own the positions of this tile
+    const uint32_t tlen = (uint32_t)(min(p0 + (unsigned long long)kTile, pool_end) - p0);
     if (tid == 0) {
+      const uint32_t tn = atomicAdd(&w.g->tile_ctr, 1u);
+      s_tnext = tn;
+      if (tn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_tile(A, tn, pool_end, s_tile[buf ^ 1u], &s_bar[buf ^ 1u]);
+      }
       const uint32_t r0 = w.tile_owner[t];
       const uint32_t r_end = (t + 1 < ntiles) ? w.tile_owner[t + 1] : n - 1;
+      const unsigned long long b0 = r.tl_base[r0];
+      // a gap before the first request of the pool: prepend a dummy entry owning nothing
+      s_dummy = (b0 > p0) ? 1u : 0u;
       s_r0 = r0;
-      s_wn = r_end - r0 + 1;
+      s_wn = r_end - r0 + 1 + s_dummy;
     }
     __syncthreads();
-    const uint32_t r0 = s_r0, wn = s_wn;
-    const bool win_ok = wn <= kWindowCap;
-    if (win_ok)
-      for (uint32_t q = tid; q <= wn; q += kScanThreads)
-        s_win[q] = (r0 + q < n) ? r.tl_base[r0 + q] : ~0ull;
-    // tail tokens not covered by the 16-byte bulk copy
-    {
-      const uint32_t cnt = (uint32_t)(pend - p0);
-      const uint32_t bulk_tok = (cnt / 4u) * 4u;
-      if (tid < cnt - bulk_tok) s_tile[buf][bulk_tok + tid] = r.tl_pool[p0 + bulk_tok + tid];
-    }
-    mbar_wait(&s_bar[buf], phase[buf]);
-    phase[buf] ^= 1u;
-    __syncthreads();
-
-    // ---- locate this thread's first owner
-    const unsigned long long my0 = p0 + (unsigned long long)tid * kScanItems;
-    auto base_of = [&](uint32_t rr) -> unsigned long long {
-      if (rr >= n) return ~0ull;
-      if (win_ok && rr >= r0 && rr - r0 <= wn) return s_win[rr - r0];
-      return r.tl_base[rr];
-    };
-    uint32_t rr;
-    {
-      // largest rr in [r0, r0+wn-1] with base(rr) <= my0
-      uint32_t lo = r0, hi = r0 + wn - 1;
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo + 1) / 2;
-        if (base_of(mid) <= my0) lo = mid;
-        else hi = mid - 1;
-      }
-      rr = lo;
-    }
-    // ---- load my items
-    uint32_t d[kScanItems];
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(&s_tile[buf][tid * kScanItems]);
-#pragma unroll
-      for (int q = 0; q < kScanItems / 4; ++q) {
-        const uint4 v = src[q];
-        d[4 * q + 0] = v.x;
-        d[4 * q + 1] = v.y;
-        d[4 * q + 2] = v.z;
-        d[4 * q + 3] = v.w;
+    const uint32_t r0 = s_r0, wn = s_wn, dummy = s_dummy;
+    const bool win_ok = wn <= (uint32_t)kWinCap;
+    // ---- window: per-request tile-local parameters (one thread per request)
+    for (uint32_t q = tid; q <= kScanThreads; q += kScanThreads) s_own[q] = 0u;
+    if (win_ok) {
+      for (uint32_t q = tid; q <= wn; q += kScanThreads) {
+        const Entry e = make_entry<kFinal>(A, p0, r0, dummy, wn, q);
+        w_ls[q] = e.ls; w_vend[q] = e.vend; w_A[q] = e.A; w_U[q] = e.U; w_P[q] = e.P;
+        w_epos[q] = e.epos; w_ek[q] = e.ek; w_ridx[q] = e.ridx;
       }
     }
-    // ---- pass 1: lat+ per valid item and the thread aggregate
-    uint32_t lat[kScanItems];
-    uint32_t valid = 0;  // bit per item
-    uint32_t start = 0;  // bit per item: k == 0
-    unsigned long long agg = 0ull;
-    {
-      uint32_t cur = rr;
-      unsigned long long cb = base_of(cur), nb = base_of(cur + 1);
-      uint32_t lim = 0, P = 1, ttft = 0;
-      auto load_req = [&](uint32_t q) {
-        if (q < n) {
-          const uint32_t g = r.n_deliv[q];
-          const uint32_t m = w.m[q];
-          lim = kFinal ? g : min(g, m);
-          P = r.period[q];
-          ttft = r.ttft[q];
-        } else {
-          lim = 0;
-        }
-      };
-      load_req(cur);
-#pragma unroll
-      for (int j = 0; j < kScanItems; ++j) {
-        const unsigned long long pos = my0 + j;
-        lat[j] = 0;
-        if (pos >= pend) continue;
-        while (pos >= nb) {
-          ++cur;
-          cb = nb;
-          nb = base_of(cur + 1);
-          load_req(cur);
-        }
-        const unsigned long long k = pos - cb;
-        if (k < lim) {
-          const unsigned long long I = (unsigned long long)ttft + k * P;
-          const unsigned long long dd = d[j];
-          const uint32_t lp = dd > I ? (uint32_t)(dd - I) : 0u;
-          lat[j] = lp;
-          valid |= 1u << j;
-          if (k == 0) {
-            start |= 1u << j;
-            agg = kFlagBit | lp;
-          } else {
-            agg = (agg & kFlagBit) | max((uint32_t)agg, lp);
+    if (tid == 0) {
+      // head segment (request at window entry 0): carry source
+      s_mode = 0;  // 0: no carry needed, 1: direct, 2: look-back
+      s_carry = 0ull;
+      if (!dummy) {
+        const unsigned long long base = r.tl_base[r0];
+        if (base < p0) {
+          const uint32_t g = r.n_deliv[r0];
+          const uint32_t m = kFinal ? g : w.m[r0];
+          const unsigned long long lim = min(g, m);
+          const unsigned long long span = p0 - base;
+          if (lim > span) {  // the head segment has valid tokens inside this tile
+            s_hbase = base;
+            s_hcnt = (uint32_t)span;
+            s_httft = r.ttft[r0];
+            s_hP = r.period[r0];
+            s_mode = (span <= (unsigned long long)kCarryDirect) ? 1u : 2u;
           }
         }
       }
+    }
+    __syncthreads();
+    // ---- direct head carry: max lat+ of the head segment's tokens before p0 (short segments)
+    uint32_t cmax = 0;
+    if (s_mode == 1u) {
+      const unsigned long long hb = s_hbase;
+      const uint32_t cnt = s_hcnt, P = s_hP, ttft = s_httft;
+      for (uint32_t k = tid; k < cnt; k += kScanThreads) {
+        const uint32_t d = r.tl_pool[hb + k];
+        const uint32_t I = ttft + k * P;
+        cmax = max(cmax, max(d, I) - I);
+      }
+    }
+    // ---- owners: last window entry starting at or before each thread's first position
+    if (win_ok) {
+      for (uint32_t q = 1 + tid; q < wn; q += kScanThreads) {
+        const int32_t ls = w_ls[q];
+        if (ls < (int32_t)kTile) {
+          const uint32_t j = (ls <= 0) ? 0u : (uint32_t)(ls + kScanItems - 1) / kScanItems;
+          if (j < kScanThreads) atomicMax(&s_own[j], q);
+        }
+      }
+    }
+    // wait for this tile's data (issued one iteration ago); copy the ragged tail
+    {
+      const uint32_t bulk_tok = (tlen / 4u) * 4u;
+      if (tid < tlen - bulk_tok) s_tile[buf][bulk_tok + tid] = r.tl_pool[p0 + bulk_tok + tid];
+    }
+    if (buf == 0) { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
+    else { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
+    for (int o = 16; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    if (lane == 0 && cmax) atomicMax(&s_cmax, cmax);
+    __syncthreads();
+    if (A.debug) {
+      uint32_t bad = 0;
+      for (uint32_t i = tid; i < tlen; i += kScanThreads) bad += (s_tile[buf][i] == 0xFFFFFFFFu) ? 1u : 0u;
+      if (bad) atomicAdd(&w.g->slow, bad);
+    }
+    // inclusive max-scan of s_own over threads
+    uint32_t q;
+    {
+      uint32_t v = s_own[tid];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= (uint32_t)o) v = max(v, u);
+      }
+      __syncthreads();
+      if (lane == 31) s_own[kScanThreads - 1 - wid] = v;  // stash warp maxima at the top (temp)
+      __syncthreads();
+      uint32_t pre = 0;
+      for (uint32_t k = 0; k < wid; ++k) pre = max(pre, s_own[kScanThreads - 1 - k]);
+      q = max(v, pre);
+      if (!win_ok) {
+        // window above kWinCap: last entry starting at or before x0, by binary search in global
+        const long long my0 = (long long)(tid * kScanItems);
+        uint32_t lo = 0, hi = wn - 1;
+        while (lo < hi) {
+          const uint32_t mid = lo + (hi - lo + 1) / 2;
+          if (next_ls(mid, false, p0, r0, dummy, wn) <= my0) lo = mid;
+          else hi = mid - 1;
+        }
+        q = lo;
+      }
+    }
+    const uint32_t x0 = tid * kScanItems;
+    const uint32_t* tile = s_tile[buf];
+
+    // ---- pass 1: lat+ per item and the thread aggregate (flag = a segment starts here)
+    uint32_t lat[kScanItems];
+    unsigned long long agg;
+    {
+      uint32_t qq = q;
+      int32_t ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
+      Entry e = fetch(qq, win_ok, p0, r0, dummy, wn);
+      uint32_t P = e.P;
+      uint32_t I = e.A + x0 * P;
+      int32_t vend = e.vend;
+      agg = (e.ls == (int32_t)x0) ? kFlagBit : 0ull;
+      uint32_t v = 0;
+#pragma unroll
+      for (int j4 = 0; j4 < kScanItems; j4 += 4) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(&tile[x0 + j4]);
+        const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int32_t x = (int32_t)x0 + j4 + jj;
+          if (x == ns) {
+            do {
+              ++qq;
+              ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
+            } while (ns <= x);
+            const Entry e2 = fetch(qq, win_ok, p0, r0, dummy, wn);
+            P = e2.P;
+            I = e2.A + (uint32_t)x * P;
+            vend = e2.vend;
+            agg = kFlagBit;
+            v = 0;
+          }
+          uint32_t l = max(dd[jj], I) - I;
+          l = (x < vend) ? l : 0u;
+          I += P;
+          v = max(v, l);
+          lat[j4 + jj] = l;
+        }
+      }
+      agg |= v;
     }
     // ---- block-wide exclusive scan of thread aggregates
     unsigned long long incl = agg;
@@ -399,14 +532,15 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
     if (lane == 0) excl = 0ull;
     __syncthreads();
     unsigned long long warp_prefix = 0ull;
-    for (uint32_t q = 0; q < wid; ++q) warp_prefix = seg_combine(warp_prefix, s_warp[q]);
+    for (uint32_t k = 0; k < wid; ++k) warp_prefix = seg_combine(warp_prefix, s_warp[k]);
     excl = seg_combine(warp_prefix, excl);
-    // ---- tile look-back (thread 0)
+    // ---- tile carry: direct (head segment within kCarryDirect tokens) or decoupled look-back
     if (tid == 0) {
       unsigned long long tile_agg = 0ull;
-      for (uint32_t q = 0; q < kScanThreads / 32; ++q) tile_agg = seg_combine(tile_agg, s_warp[q]);
+      for (uint32_t k = 0; k < kScanThreads / 32; ++k) tile_agg = seg_combine(tile_agg, s_warp[k]);
       unsigned long long acc = 0ull;
-      if (t > 0) {
+      const uint32_t mode = s_mode;
+      if (mode == 2u && t > 0) {
         st_release(&w.tile_status[t], kStAgg | tile_agg);
         for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
           unsigned long long s;
@@ -416,64 +550,69 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
           acc = seg_combine(s & ~kStMask, acc);
           if ((s & kStMask) == kStPrefix || (acc & kFlagBit)) break;
         }
+      } else if (mode == 1u) {
+        acc = kFlagBit | s_cmax;
       }
       st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
       s_carry = acc;
+      s_cmax = 0;
     }
     __syncthreads();
     const unsigned long long carry = seg_combine(s_carry, excl);
 
-    // ---- pass 2: clamped delays, per-request partial sums, edges
+    // ---- pass 2: clamped delays, per-request partial sums, edge values
     {
-      uint32_t cur = rr;
-      unsigned long long cb = base_of(cur), nb = base_of(cur + 1);
-      uint32_t g = 0, m = 0, P = 1, ttft = 0;
-      int64_t trel = 0;
-      auto load_req = [&](uint32_t q) {
-        if (q < n) {
-          g = r.n_deliv[q];
-          m = kFinal ? g : w.m[q];
-          P = r.period[q];
-          ttft = r.ttft[q];
-          if (!kFinal) trel = A.eval_abs - r.arrival[q];
-        }
-      };
-      load_req(cur);
-      uint32_t pm = (uint32_t)carry;
+      uint32_t qq = q;
+      int32_t ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
+      Entry e = fetch(qq, win_ok, p0, r0, dummy, wn);
+      uint32_t P = e.P;
+      uint32_t u = e.U - x0 * P;
+      int32_t vend = e.vend;
+      int32_t epos = e.epos;
+      uint32_t ek = e.ek, ridx = e.ridx;
+      uint32_t pm = (e.ls == (int32_t)x0) ? 0u : (uint32_t)carry;
       unsigned long long sum = 0ull;
-      bool have = false;
 #pragma unroll
       for (int j = 0; j < kScanItems; ++j) {
-        if (!((valid >> j) & 1u)) continue;
-        const unsigned long long pos = my0 + j;
-        if (pos >= nb) {
-          if (have && sum) atomicAdd(&w.spre[cur], sum);
+        const int32_t x = (int32_t)x0 + j;
+        if (x == ns) {
+          if (sum) atomicAdd(&w.spre[ridx], sum);
           sum = 0ull;
-          have = false;
-          while (pos >= nb) {
-            ++cur;
-            cb = nb;
-            nb = base_of(cur + 1);
-          }
-          load_req(cur);
+          do {
+            ++qq;
+            ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
+          } while (ns <= x);
+          const Entry e2 = fetch(qq, win_ok, p0, r0, dummy, wn);
+          P = e2.P;
+          u = e2.U - (uint32_t)x * P;
+          vend = e2.vend;
+          epos = e2.epos;
+          ek = e2.ek;
+          ridx = e2.ridx;
+          pm = 0;
         }
-        const uint32_t k = (uint32_t)(pos - cb);
-        pm = ((start >> j) & 1u) ? lat[j] : max(pm, lat[j]);
+        pm = max(pm, lat[j]);
         uint32_t dt;
-        if (kFinal) {
-          dt = pm;
-        } else {
-          const int64_t u = trel - ((int64_t)ttft + (int64_t)k * P);  // t - I_{k+1} >= 0
-          dt = (int64_t)pm < u ? pm : (uint32_t)u;
-        }
-        sum += dt;
-        have = true;
-        if (!kFinal && k + 1 == g && g < m) w.edge[cur] = pm;  // delta_g
-        if (k + 1 == m && g >= m) w.edge[cur] = dt;           // delta~_m (FINAL: delta_g)
+        if (kFinal) dt = pm;
+        else dt = min(pm, u);
+        u -= P;
+        if (x < vend) sum += dt;
+        if (x == epos) w.edge[ridx] = (ek == 1u) ? pm : dt;
       }
-      if (have && sum) atomicAdd(&w.spre[cur], sum);
+      // the last piece may continue into the next lanes: segmented warp reduction by request
+      uint32_t key = ridx;
+      unsigned long long val = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, o);
+        const unsigned long long v2 = __shfl_down_sync(0xffffffffu, val, o);
+        if (lane + o < 32 && k2 == key) val += v2;
+      }
+      const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
+      if ((lane == 0 || kprev != key) && val && key != 0xFFFFFFFFu) atomicAdd(&w.spre[key], val);
     }
-    __syncthreads();  // buffers and window reused by the next tile
+    __syncthreads();  // tile buffer and window reused by the next tile
+    t = s_tnext;
   }
 }
 
@@ -526,11 +665,12 @@ void launch_bounds(const LaunchCfg& L, const ReqView& r, const Work& w, const ui
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode) {
   if (r.n == 0) return;
-  ScanArgs A{r, w, eval_abs};
+  static const uint32_t dbg = getenv("ANDES_SCAN_DEBUG") ? 1u : 0u;
+  ScanArgs A{r, w, eval_abs, dbg};
   if (final_mode)
-    k_qoe_scan<true><<<L.scan_grid, kScanThreads, 0, L.stream>>>(A);
+    k_qoe_scan<true><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A);
   else
-    k_qoe_scan<false><<<L.scan_grid, kScanThreads, 0, L.stream>>>(A);
+    k_qoe_scan<false><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
@@ -540,11 +680,16 @@ void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64
   k_qoe_final<<<blocks, 256, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, q, q64, sd, sw, m);
 }
 
+void init_scan_kernels() {
+  cudaFuncSetAttribute(k_qoe_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+}
+
 int scan_blocks_per_sm() {
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_qoe_scan<false>, kScanThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_qoe_scan<false>, kScanThreads, kScanDynSmem);
   int b2 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_qoe_scan<true>, kScanThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_qoe_scan<true>, kScanThreads, kScanDynSmem);
   return b < b2 ? b : b2;
 }
 

@@ -420,13 +420,12 @@ void launch_gain_keys(const LaunchCfg& L, const ReqView& r, const Work& w, int64
 
 static size_t select_smem() { return (sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
 
+void init_kernels() {
+  cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
+}
+
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
-    attr = true;
-  }
   SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o};
   k_select<<<B_cap, kSelThreads, select_smem(), L.stream>>>(A);
 }
