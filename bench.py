@@ -60,13 +60,28 @@ class Clocks:
         self.path = tempfile.mktemp(suffix=".csv")
         self.proc = None
 
-    def start(self):
+    def start(self, load=None, load_s=0.6):
+        """Start sampling; wait for the first sample, then run `load` (the timed work itself,
+        untimed) for load_s seconds so the samples see the clocks under this load."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 5.0:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.02)
+        if load is not None:
+            t0 = time.time()
+            while time.time() - t0 < load_s:
+                load()
 
     def stop(self):
         if self.proc is not None:
@@ -229,10 +244,16 @@ def run_ours(args):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         stage_sum = [0.0] * A.N_STAGES
         clk = Clocks(lr)
+
+        def _load():
+            for _ in range(20):
+                graph.replay()
+            stream.synchronize()
+
+        clk.start(load=_load)
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        clk.start()
         for k in range(args.steps):
             flush.zero_()
             starts[k].record(stream)
@@ -267,9 +288,7 @@ def run_ours(args):
     names = A.STAGES
     dom = max(range(len(stage_ms)), key=lambda i: stage_ms[i])
     scan_bytes = 4 * snap.n_tokens + 44 * n  # one read of every timestamp + per-request SoA/state
-    gain_bytes = 4 * n * 256 + 44 * n        # key rows written + state read
-    select_bytes = 4 * n * 256 * 2           # key rows read (>= 2 radix passes) -- L2-resident traffic
-    alg_bytes = {"scan": scan_bytes, "gain": gain_bytes, "select": select_bytes}
+    alg_bytes = {"scan": scan_bytes}
     dom_name = names[dom]
     if dom_name in alg_bytes:
         ach = alg_bytes[dom_name] / (stage_ms[dom] / 1e3) / 1e9
@@ -296,8 +315,8 @@ def run_ours(args):
             st = qctx.profile_read()
             if k >= max(args.warmup, 3):
                 q_ms.append(st)
-    scan_ms = statistics.median([s[2] for s in q_ms])
-    qoe_ms = statistics.median([s[0] + s[2] + s[3] for s in q_ms])
+    scan_ms = statistics.median([s[1] for s in q_ms])
+    qoe_ms = statistics.median([s[0] + s[1] + s[2] for s in q_ms])
     qbytes = 4 * big.n_tokens + 44 * big.n
     q_ach = qbytes / (scan_ms / 1e3) / 1e9
     qoe_eval = {"metric": "QoE-eval token-events/s", "value": big_events / (qoe_ms / 1e3),
@@ -340,13 +359,13 @@ def run_ours(args):
         "data": "synthetic (seeded ShareGPT-shaped cyclic-burst snapshot, workloads.config3; seed 1+rank)",
         "config": {"workload": WORKLOAD, "n_requests": n, "pool_tokens": snap.n_tokens,
                    "token_events": ev_tokens, "B_cap": 256, "l2": "flushed: 256 MiB write between timed steps",
-                   "launch": "one CUDA graph per decision (6 kernels)", "warm_l2_ms_per_step": warm_ms,
+                   "launch": "one CUDA graph per decision (5 kernels)", "warm_l2_ms_per_step": warm_ms,
                    "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}},
         "roofline": roof,
         "qoe_eval": qoe_eval,
         "e2e": {"value": ws * e2e_steps / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "andes_schedule_host (pinned host buffers)"},
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": 5 * args.steps,
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -184,8 +184,10 @@ int andes_schedule_host(AndesCtx *ctx, const AndesRequests *req_host, const Ande
  * and after each of its kernels on the call's stream (also under stream capture, so a
  * captured CUDA graph of a decision carries the event-record nodes).  andes_profile_read
  * blocks until the last recorded event completes and writes the elapsed milliseconds of
- * each stage: [0] reset+prep (S0 inputs), [1] bounds (S0/S2), [2] timeline scan (S1),
- * [3] gains for every B (S3), [4] Algorithm 1 per B + best B + cap (S4-S6), [5] serve mask.
+ * each stage.  andes_schedule: [0] reset + prep + trigger/B range (S0, S2), [1] timeline scan
+ * (S1), [2] per-request state and key bounds (S3a), [3] candidate keys for every B (S3b),
+ * [4] Algorithm 1 per B + best B + cap + serve mask (S4-S6), [5] unused (0).
+ * andes_qoe_eval: [0] prep, [1] timeline scan, [2] QoE finalize, [3..5] unused.
  * Errors: ANDES_E_INVAL (profiling off / nothing recorded), ANDES_E_CUDA. */
 #define ANDES_N_STAGES 6
 int andes_profile_enable(AndesCtx *ctx, int enable);

@@ -37,7 +37,7 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read"]
 N_STAGES = 6
-STAGES = ["prep", "bounds", "scan", "gain", "select", "mask"]
+STAGES = ["prep", "scan", "state", "cand", "select", "unused"]
 
 
 class AndesError(RuntimeError):

@@ -191,11 +191,16 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   Work& w = c->w;
   w.N_cap = N;
   w.tiles_cap = c->tiles_cap;
+  w.S_cap = N < kCandCap ? N : kCandCap;
   if ((e = ctx_alloc(c, &w.m, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.edge, N)) != cudaSuccess || (e = ctx_alloc(c, &w.tile_owner, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.tile_status, c->tiles_cap)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.mark, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess || (e = ctx_alloc(c, &w.hist_lb, kHistK)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.cand, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.sel, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
@@ -204,7 +209,8 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
     return rc;
   }
   cudaMemset(w.hist_l, 0, sizeof(uint32_t) * kHistL);
-  cudaMemset(w.mark, 0, N);
+  cudaMemset(w.hist_lb, 0, sizeof(uint32_t) * kHistK);
+  cudaMemset(w.hist_ub, 0, sizeof(uint32_t) * kHistK);
   if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess) {
     int rc = cuda_check(c, e, "pinned alloc");
     andes_destroy(c);
@@ -302,15 +308,15 @@ int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, 
   const ReqView r = view_of(req);
   const Work w = work_of(c, r.n);
   const bool fin = mode == ANDES_EVAL_FINAL;
-  // profiled stages: [0] prep, [2] scan, [3] finalize (bounds/select/mask empty)
+  // profiled stages: [0] prep, [1] timeline scan, [2] QoE finalize (others empty)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
   launch_prep(L, r, w, eval_time_us, fin, false, 0, false);
   mark(c, 1, s);
-  mark(c, 2, s);
   launch_scan(L, r, w, eval_time_us, fin);
-  mark(c, 3, s);
+  mark(c, 2, s);
   launch_qoe_final(L, r, w, eval_time_us, fin, out->q, out->q64, out->s_delay, out->s_whole, out->m);
+  mark(c, 3, s);
   mark(c, 4, s);
   mark(c, 5, s);
   mark(c, 6, s);
@@ -366,19 +372,20 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
+  // profiled stages: [0] reset + prep + S0/S2 bounds, [1] timeline scan (S1), [2] state + key
+  // bounds (S3a), [3] candidate keys (S3b), [4] Algorithm 1 per B + best B + cap + mask (S4-S6)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
-  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug);
+  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, p->tau_us, p->B_cap, p->cur_latency_us, p->flags);
   mark(c, 1, s);
-  launch_bounds(L, r, w, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
-  mark(c, 2, s);
   launch_scan(L, r, w, eval, false);
+  mark(c, 2, s);
+  launch_state(L, r, w, p->now_us, p->horizon_us);
   mark(c, 3, s);
-  launch_gain_keys(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap);
+  launch_cand(L, r, w, p->tau_us);
   mark(c, 4, s);
   launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
   mark(c, 5, s);
-  launch_mask(L, r, w, o);
   mark(c, 6, s);
   if (c->prof) c->prof_recorded = true;
   return finish_call(c, s, debug);

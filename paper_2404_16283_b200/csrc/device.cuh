@@ -22,7 +22,9 @@ constexpr int kScanDynSmem = 2 * kTile * 4;      // double-buffered tiles (dynam
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;
-constexpr uint32_t kHistL = 65536;                // exact histogram of l < 65535 (+ overflow)
+constexpr uint32_t kHistL = 4096;                 // exact histogram of l < 4095 (+ overflow bucket)
+constexpr uint32_t kHistK = 4096;                 // key histograms: top 12 bits of the ordered key
+constexpr uint32_t kCandCap = 16384;              // candidate capacity (requests) of the pruned path
 
 // tile status words (decoupled look-back), see k_qoe_scan
 constexpr unsigned long long kStAgg = 1ull << 62;
@@ -63,7 +65,23 @@ struct Globals {
   uint32_t err;                  // device error word (debug checks), copied out by the host
   uint32_t slow;                 // slow-path flags
   uint32_t tile_ctr;             // dynamic tile counter of the timeline scan
-  uint32_t pad[4];
+  uint32_t prep_done;            // prep CTAs finished (last-block pattern)
+  uint32_t state_done;           // state CTAs finished
+  uint32_t tau_lo, tau_hi;       // min / max tau(B) over the candidate range
+  uint32_t theta;                // ordered-key threshold: >= B_hi requests have LB >= theta
+  uint32_t n_surv;               // requests with UB >= theta (candidates)
+  uint32_t overflow;             // n_surv above the candidate capacity: full-N fallback
+  uint32_t cand_ctr;             // candidate slot counter
+  uint32_t pad[2];
+};
+
+// B-independent per-request state for the gain closed form,
+// written once per decision by k_state and read by the candidate / select / cap kernels.
+struct alignas(16) PackedState {
+  long long w0, c0, spre, cw, dto;
+  double qw;
+  uint32_t m, K, P, h0, l, rank;
+  uint32_t pad[2];
 };
 
 struct Work {
@@ -72,14 +90,20 @@ struct Work {
   uint32_t* edge;            // [N] delta_g (g < m) or delta~_m (g >= m)
   uint32_t* tile_owner;      // [tiles] last request with tl_base <= tile start
   unsigned long long* tile_status;  // [tiles]
-  uint32_t* hist_l;          // [kHistL] histogram of min(l, kHistL-1)
+  uint32_t* hist_l;          // [kHistL] histogram of min(l, kHistL-1) (self-cleaning)
+  uint32_t* hist_lb;         // [kHistK] histogram of lower-bound keys (self-cleaning)
+  uint32_t* hist_ub;         // [kHistK] histogram of upper-bound keys (self-cleaning)
   uint32_t* run_list;        // [max_running]
-  uint8_t* mark;             // [N] bit0 in S_{B*}, bit1 preempted, bit2 admitted
-  uint32_t* keyrow;          // [max_B][N] ordered priority keys per candidate B
-  uint32_t* sel;             // [max_B][max_B] Algorithm 1 prefix per B, greedy order
+  PackedState* st;           // [N]
+  uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
+  unsigned long long* cand;  // [max_B][S_cap] composite keys of the candidates per B
+  uint32_t* cand_idx;        // [S_cap] request index of candidate slot
+  uint32_t* keyrow;          // [max_B][N] fallback: ordered keys of every request per B
+  uint32_t* sel;             // [max_B][kMaxB] Algorithm 1 prefix per B, greedy order
   Globals* g;
   uint32_t N_cap;            // row stride of keyrow
   uint32_t tiles_cap;        // capacity of tile_owner / tile_status
+  uint32_t S_cap;            // candidate capacity (row stride of cand)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -184,6 +208,13 @@ __device__ __forceinline__ GainState make_state(const ReqView& r, const Work& w,
     const int64_t dm = s.w0 - K * (int64_t)P;  // = t - I_m
     s.qw = qoe_value(sd, (int64_t)m * dm + s.cw);
   }
+  return s;
+}
+
+__device__ __forceinline__ GainState unpack_state(const PackedState& p) {
+  GainState s;
+  s.w0 = p.w0; s.c0 = p.c0; s.spre = p.spre; s.cw = p.cw; s.dto = p.dto;
+  s.m = p.m; s.K = p.K; s.P = p.P; s.h0 = p.h0; s.qw = p.qw;
   return s;
 }
 

@@ -13,9 +13,8 @@ struct LaunchCfg {
 };
 
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug);
-void launch_bounds(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau, uint32_t B_cap,
-                   uint64_t M, uint32_t cur_latency, uint32_t flags);
+                 bool sched, uint64_t kv_cap, bool debug, const uint32_t* tau = nullptr, uint32_t B_cap = 0,
+                 uint32_t cur_latency = 0, uint32_t flags = 0);
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode);
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
@@ -34,11 +33,10 @@ struct SchedOut {
 void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                           const uint32_t* tau, const uint32_t* B_list_dev, uint32_t nB, double* gain_out,
                           float* key_out, double* qwait_out);
-void launch_gain_keys(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
-                      const uint32_t* tau, uint32_t B_cap);
+void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon);
+void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau);
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
 void init_kernels();
-void launch_mask(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o);
 
 }  // namespace andes

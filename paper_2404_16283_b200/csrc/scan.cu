@@ -17,14 +17,171 @@
 
 namespace andes {
 
-// ---------------------------------------------------------------- prep
+// ---------------------------------------------------------------- prep (+ S0/S2 in the last CTA)
+constexpr int kPrepThreads = 256;
+
+// S0 selective triggering (reading R15) and S2 batch-size range (P:L545-551,
+// reading R16), run by the last prep CTA once every request has been counted:
+//   B_max = number of shortest contexts that fit in M (exact l histogram, overflow slow path),
+//   B_min = largest B with tau(B) <= min_i P_i (only with ANDES_PRUNE), and the tau range
+//   over [B_lo, B_hi] used by the gain bounds.
+__device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __restrict__ tau, uint32_t B_cap,
+                             uint64_t M, uint32_t cur_latency, uint32_t flags) {
+  constexpr uint32_t NT = kPrepThreads, kPer = kHistL / NT;
+  __shared__ unsigned long long s_cnt[NT], s_sum[NT];
+  __shared__ uint32_t s_kM, s_Blo, s_tlo, s_thi;
+  const uint32_t tid = threadIdx.x, n = r.n;
+  const uint32_t minP = 0xFFFFFFFFu - __ldcg(&w.g->inv_minP);
+  const unsigned long long run_l = __ldcg(&w.g->run_l);
+  const bool trig = (flags & 1u) || (10ull * run_l > 9ull * M) || (n > 0 && cur_latency > minP);
+  const uint32_t need = min(B_cap, n);
+  uint32_t hv[kPer];
+  unsigned long long c = 0, sm = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    const uint32_t b = tid * kPer + q;
+    hv[q] = __ldcg(&w.hist_l[b]);
+    if (b < kHistL - 1) {
+      c += hv[q];
+      sm += (unsigned long long)hv[q] * b;
+    } else {
+      c += hv[q];  // overflow bucket: counted, value unknown (>= kHistL - 1)
+      sm += (unsigned long long)hv[q] * b;
+    }
+  }
+  s_cnt[tid] = c;
+  s_sum[tid] = sm;
+  if (tid == 0) {
+    s_kM = 0xFFFFFFFFu;
+    s_Blo = 1;
+    s_tlo = 0xFFFFFFFFu;
+    s_thi = 0;
+  }
+  __syncthreads();
+  for (uint32_t off = 1; off < NT; off <<= 1) {
+    unsigned long long a = 0, b2 = 0;
+    if (tid >= off) { a = s_cnt[tid - off]; b2 = s_sum[tid - off]; }
+    __syncthreads();
+    s_cnt[tid] += a;
+    s_sum[tid] += b2;
+    __syncthreads();
+  }
+  {
+    const unsigned long long c_ex = tid ? s_cnt[tid - 1] : 0ull;
+    const unsigned long long s_ex = tid ? s_sum[tid - 1] : 0ull;
+    const bool crosses = (s_cnt[tid] >= need || s_sum[tid] > M) && (c_ex < need && s_ex <= M);
+    if (crosses) {
+      unsigned long long k = c_ex, W = s_ex;
+      bool stop = false, ovf = false;
+      for (uint32_t q = 0; q < kPer && !stop; ++q) {
+        const uint32_t b = tid * kPer + q;
+        const uint32_t h = hv[q];
+        if (b == kHistL - 1 && h) { ovf = true; break; }
+        for (uint32_t z = 0; z < h; ++z) {
+          if (k >= need || W + b > M) { stop = true; break; }
+          W += b;
+          ++k;
+        }
+      }
+      s_kM = ovf && !stop && k < need ? 0xFFFFFFFEu : (uint32_t)min(k, (unsigned long long)need);
+    }
+  }
+  __syncthreads();
+  uint32_t kM = s_kM == 0xFFFFFFFFu ? 0u : s_kM;
+  if (kM == 0xFFFFFFFEu) {
+    // Slow path: the shortest contexts reach the overflow bucket (l >= kHistL - 1); take
+    // exact successive minima over all requests (rare: needs B_max contexts that long).
+    __shared__ unsigned long long s_red[NT / 32], s_best;
+    unsigned long long k = 0, W = 0;
+    for (uint32_t b = 0; b < kHistL - 1; ++b) {
+      const uint32_t h = __ldcg(&w.hist_l[b]);
+      k += h;
+      W += (unsigned long long)h * b;
+    }
+    unsigned long long last = 0;
+    bool first = true;
+    while (k < need) {
+      unsigned long long best = ~0ull;
+      for (uint32_t i = tid; i < n; i += NT) {
+        const uint32_t l = r.ctx_len[i];
+        if (l < kHistL - 1) continue;
+        const unsigned long long key = ((unsigned long long)l << 32) | i;
+        if ((first || key > last) && key < best) best = key;
+      }
+      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if ((tid & 31) == 0) s_red[tid >> 5] = best;
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long b2 = ~0ull;
+        for (uint32_t q = 0; q < NT / 32; ++q) b2 = min(b2, s_red[q]);
+        s_best = b2;
+      }
+      __syncthreads();
+      const unsigned long long b2 = s_best;
+      __syncthreads();
+      if (b2 == ~0ull || W + (b2 >> 32) > M) break;
+      W += b2 >> 32;
+      ++k;
+      last = b2;
+      first = false;
+    }
+    kM = (uint32_t)k;
+    if (tid == 0) atomicOr(&w.g->slow, 1u);
+  }
+  const uint32_t B_hi = min(need, kM);
+  // B_min (reading R16) and the tau range of the candidate B
+  if (flags & 2u) {
+    uint32_t best = 1;
+    for (uint32_t B = 1 + tid; B <= B_hi; B += NT)
+      if (tau[B - 1] <= minP) best = max(best, B);
+    atomicMax(&s_Blo, best);
+  }
+  __syncthreads();
+  const uint32_t B_lo = (B_hi == 0) ? 1u : min(s_Blo, B_hi);
+  {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    for (uint32_t B = B_lo + tid; B <= B_hi; B += NT) {
+      lo = min(lo, tau[B - 1]);
+      hi = max(hi, tau[B - 1]);
+    }
+    atomicMin(&s_tlo, lo);
+    atomicMax(&s_thi, hi);
+  }
+  // self-clean the l histogram for the next call
+  for (uint32_t b = tid; b < kHistL; b += NT) w.hist_l[b] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    w.g->B_hi = B_hi;
+    w.g->B_lo = B_lo;
+    w.g->tau_lo = s_tlo;
+    w.g->tau_hi = s_thi;
+    w.g->triggered = trig ? 1u : 0u;
+  }
+}
+
 // One pass over the requests: m_i, zeroed accumulators, tile owners, and for a
 // decision the trigger inputs (sum of running l, min period), the l histogram for
-// B_max and the running list.
-__global__ void k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode, uint32_t sched,
-                       uint64_t kv_cap, uint32_t debug) {
+// B_max and the running list; the last CTA then runs bounds_block.
+__global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
+                                                      uint32_t sched, uint64_t kv_cap, uint32_t debug,
+                                                      const uint32_t* __restrict__ tau, uint32_t B_cap,
+                                                      uint32_t cur_latency, uint32_t flags) {
+  __shared__ uint32_t s_last;
+  __shared__ uint32_t s_hl[kHistL];
+  __shared__ uint32_t s_minP, s_nrun;
+  __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
   uint32_t local_err = 0;
+  if (sched) {
+    for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
+    if (threadIdx.x == 0) {
+      s_minP = 0xFFFFFFFFu;
+      s_nrun = 0;
+      s_runl = 0;
+    }
+    __syncthreads();
+  }
+  uint32_t my_minP = 0xFFFFFFFFu;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t g = r.n_deliv[i];
     const uint32_t P = r.period[i];
@@ -59,10 +216,10 @@ __global__ void k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
     }
     if (sched) {
       const uint32_t l = r.ctx_len[i];
-      atomicMax(&w.g->inv_minP, 0xFFFFFFFFu - P);
-      atomicAdd(&w.hist_l[l < kHistL - 1 ? l : kHistL - 1], 1u);
+      my_minP = min(my_minP, P);
+      atomicAdd(&s_hl[l < kHistL - 1 ? l : kHistL - 1], 1u);
       if (r.running[i]) {
-        atomicAdd(&w.g->run_l, (unsigned long long)l);
+        atomicAdd(&s_runl, (unsigned long long)l);
         const uint32_t slot = atomicAdd(&w.g->n_run, 1u);
         if (slot < kMaxRunning) w.run_list[slot] = i;
       }
@@ -70,125 +227,23 @@ __global__ void k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
     }
   }
   if (local_err) atomicOr(&w.g->err, local_err);
-}
-
-// ---------------------------------------------------------------- bounds (1 CTA)
-// S0 selective triggering (reading R15) and S2 batch-size range
-// (reading R16): B_max = number of shortest contexts that fit in M,
-// B_min = largest B with tau(B) <= min_i P_i (only with ANDES_PRUNE).
-__global__ void __launch_bounds__(1024) k_bounds(ReqView r, Work w, const uint32_t* __restrict__ tau,
-                                                 uint32_t B_cap, uint64_t M, uint32_t cur_latency,
-                                                 uint32_t flags) {
-  __shared__ unsigned long long s_cnt[1024];
-  __shared__ unsigned long long s_sum[1024];
-  __shared__ uint32_t s_kM;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t n = r.n;
-  const uint32_t minP = 0xFFFFFFFFu - w.g->inv_minP;
-  const unsigned long long run_l = w.g->run_l;
-  const bool trig = (flags & 1u) || (10ull * run_l > 9ull * M) || (n > 0 && cur_latency > minP);
-  // per-thread slice of the exact l histogram: buckets [64 tid, 64 tid + 64)
-  constexpr uint32_t kPer = kHistL / 1024;
-  unsigned long long c = 0, s = 0;
-  for (uint32_t b = tid * kPer; b < (tid + 1) * kPer; ++b) {
-    const uint32_t h = w.hist_l[b];
-    c += h;
-    s += (unsigned long long)h * b;
-  }
-  s_cnt[tid] = c;
-  s_sum[tid] = s;
-  if (tid == 0) s_kM = 0xFFFFFFFFu;
+  if (!sched) return;
+  for (int o = 16; o; o >>= 1) my_minP = min(my_minP, __shfl_xor_sync(0xffffffffu, my_minP, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(&s_minP, my_minP);
   __syncthreads();
-  // inclusive scans (Hillis-Steele; 10 steps)
-  for (uint32_t off = 1; off < 1024; off <<= 1) {
-    unsigned long long a = 0, b2 = 0;
-    if (tid >= off) { a = s_cnt[tid - off]; b2 = s_sum[tid - off]; }
-    __syncthreads();
-    s_cnt[tid] += a;
-    s_sum[tid] += b2;
-    __syncthreads();
+  for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x)
+    if (s_hl[q]) atomicAdd(&w.hist_l[q], s_hl[q]);
+  if (threadIdx.x == 0) {
+    atomicMax(&w.g->inv_minP, 0xFFFFFFFFu - s_minP);
+    if (s_runl) atomicAdd(&w.g->run_l, s_runl);
   }
-  // k_M = max k with sum of the k smallest l <= M, needed only up to min(B_cap, n)
-  const uint32_t need = min(B_cap, n);
-  {
-    const unsigned long long c_ex = tid ? s_cnt[tid - 1] : 0ull;
-    const unsigned long long s_ex = tid ? s_sum[tid - 1] : 0ull;
-    // the thread whose slice contains the crossing (count reaches need or sum exceeds M)
-    const bool crosses = (s_cnt[tid] >= need || s_sum[tid] > M) && (c_ex < need && s_ex <= M);
-    if (crosses) {
-      unsigned long long k = c_ex, W = s_ex;
-      bool stop = false;
-      for (uint32_t b = tid * kPer; b < (tid + 1) * kPer && !stop; ++b) {
-        const uint32_t h = w.hist_l[b];
-        if (b == kHistL - 1 && h) break;  // overflow bucket: exact values needed, slow path below
-        for (uint32_t q = 0; q < h; ++q) {
-          if (k >= need || W + b > M) { stop = true; break; }
-          W += b;
-          ++k;
-        }
-      }
-      if (stop || k >= need) s_kM = (uint32_t)(k < need ? k : (unsigned long long)need);
-      else s_kM = 0xFFFFFFFEu;  // reached the overflow bucket
-    }
-  }
+  __threadfence();
   __syncthreads();
-  if (s_kM == 0xFFFFFFFFu) s_kM = 0;  // (not reachable for n >= 1 unless all l are in overflow)
+  if (threadIdx.x == 0) s_last = (atomicAdd(&w.g->prep_done, 1u) == gridDim.x - 1) ? 1u : 0u;
   __syncthreads();
-  uint32_t kM = s_kM;
-  if (kM == 0xFFFFFFFEu || (kM == 0 && n > 0 && s_cnt[1023] > 0)) {
-    // Slow path (l >= 65535 among the smallest): repeated exact minima over all requests.
-    __shared__ unsigned long long s_red[32];
-    __shared__ unsigned long long s_taken_key;
-    unsigned long long k = 0, W = 0;
-    for (uint32_t b = 0; b < kHistL - 1; ++b) {  // all small l first (they all fit: see crossing)
-      const uint32_t h = w.hist_l[b];
-      k += h;
-      W += (unsigned long long)h * b;
-    }
-    unsigned long long last = 0;  // (l << 32 | i) of the last taken large element
-    bool first = true;
-    while (k < need) {
-      unsigned long long best = ~0ull;
-      for (uint32_t i = tid; i < n; i += blockDim.x) {
-        const uint32_t l = r.ctx_len[i];
-        if (l < kHistL - 1) continue;
-        const unsigned long long key = ((unsigned long long)l << 32) | i;
-        if ((first || key > last) && key < best) best = key;
-      }
-      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if ((tid & 31) == 0) s_red[tid >> 5] = best;
-      __syncthreads();
-      if (tid == 0) {
-        unsigned long long b2 = ~0ull;
-        for (int q = 0; q < 32; ++q) b2 = min(b2, s_red[q]);
-        s_taken_key = b2;
-      }
-      __syncthreads();
-      const unsigned long long b2 = s_taken_key;
-      __syncthreads();
-      if (b2 == ~0ull || W + (b2 >> 32) > M) break;
-      W += b2 >> 32;
-      ++k;
-      last = b2;
-      first = false;
-    }
-    kM = (uint32_t)k;
-    if (tid == 0) atomicOr(&w.g->slow, 1u);
-  }
-  // self-clean the histogram for the next call (after every reader above)
-  __syncthreads();
-  for (uint32_t b = tid; b < kHistL; b += blockDim.x) w.hist_l[b] = 0u;
-  if (tid == 0) {
-    const uint32_t B_hi = min(min(B_cap, n), kM);
-    uint32_t B_lo = 1;
-    if (flags & 2u) {
-      for (uint32_t B = 1; B <= B_hi; ++B)
-        if (tau[B - 1] <= minP) B_lo = B;
-    }
-    w.g->B_hi = B_hi;
-    w.g->B_lo = (B_hi == 0) ? 1u : min(B_lo, B_hi);
-    w.g->triggered = trig ? 1u : 0u;
-  }
+  if (!s_last) return;
+  __threadfence();
+  bounds_block(r, w, tau, B_cap, kv_cap, cur_latency, flags);
 }
 
 // ---------------------------------------------------------------- K1 timeline scan
@@ -651,16 +706,11 @@ __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_
 
 // ---------------------------------------------------------------- host launchers
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug) {
-  if (r.n == 0) return;
-  const uint32_t blocks = umin32((r.n + 255) / 256, L.sm_count * 8);
-  k_prep<<<blocks, 256, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u, kv_cap,
-                                       debug ? 1u : 0u);
-}
-
-void launch_bounds(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau, uint32_t B_cap,
-                   uint64_t M, uint32_t cur_latency, uint32_t flags) {
-  k_bounds<<<1, 1024, 0, L.stream>>>(r, w, tau, B_cap, M, cur_latency, flags);
+                 bool sched, uint64_t kv_cap, bool debug, const uint32_t* tau, uint32_t B_cap,
+                 uint32_t cur_latency, uint32_t flags) {
+  const uint32_t blocks = r.n ? umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8) : 1u;
+  k_prep<<<blocks, kPrepThreads, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u, kv_cap,
+                                                debug ? 1u : 0u, tau, B_cap, cur_latency, flags);
 }
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode) {

@@ -1,6 +1,22 @@
-// select.cu -- S3-S6 of the decision: gains for every candidate B (Eq. 4/6), Algorithm 1
-// per B via an exact radix threshold-select on the (priority desc, rank asc) composite
-// key, best B, preemption cap (reading R18), serve-mask materialisation.
+// select.cu -- S3-S6 of the decision: gains for every candidate B (Eq. 4/6), Algorithm 1 per B,
+// best B, preemption cap (reading R18), serve-mask materialisation.
+//
+// Exact selection with bound-and-prune:
+//   k_state   per request: the B-independent state, and rigorous lower/upper bounds of its
+//             priority key over every candidate B.  S_delay and S_whole of Q_serve are
+//             nondecreasing in tau (deliveries only move later), and every rounded operation of
+//             the key (RN division, RN subtraction, RN64->RN32) is monotone, so evaluating the
+//             same fp chain at (S_delay(tau_lo), S_whole(tau_hi)) / (S_delay(tau_hi),
+//             S_whole(tau_lo)) bounds the computed key of every B with tau in [tau_lo, tau_hi].
+//             A histogram of the lower bounds gives theta with >= B_max requests whose key is
+//             >= theta at every B, so the exact top-B of every B lies among requests whose upper
+//             bound is >= theta ("survivors").
+//   k_cand    compacts the survivors and evaluates their exact keys for every B.
+//   k_select  per B: exact radix threshold-select of the top min(B, n) survivors by
+//             (key desc, rank asc), sort, Algorithm 1 walk; the last CTA picks
+//             B*, applies the cap and writes the outputs.
+// If the survivors exceed the candidate capacity, the same kernels fall back to evaluating and
+// selecting over all n requests (slow path, flagged).
 #include "device.cuh"
 #include "launch.h"
 
@@ -22,33 +38,15 @@ __global__ void k_gain_estimate(ReqView r, Work w, int64_t now, uint32_t horizon
   }
 }
 
-// ---------------------------------------------------------------- S3: keys for every B
-// One thread per request; the B-independent state (Q_wait, constants) is built once and the
-// closed form of Q_serve(B) is evaluated for every candidate B in [B_lo, B_hi].
-__global__ void __launch_bounds__(256) k_gain_keys(ReqView r, Work w, int64_t now, uint32_t horizon,
-                                                   const uint32_t* __restrict__ tau, uint32_t B_cap) {
-  __shared__ uint32_t s_tau[kMaxB];
-  if (!w.g->triggered) return;
-  const uint32_t B_lo = w.g->B_lo, B_hi = w.g->B_hi;
-  for (uint32_t q = threadIdx.x; q < B_cap; q += blockDim.x) s_tau[q] = tau[q];
-  __syncthreads();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
-    const GainState s = make_state(r, w, i, now, horizon);
-    const uint32_t l = r.ctx_len[i];
-    uint32_t* out = w.keyrow + i;
-    if (s.K == 0) {
-      const uint32_t z = ordered_key(0.0f);
-      for (uint32_t B = B_lo; B <= B_hi; ++B) out[(size_t)(B - 1) * w.N_cap] = z;
-      continue;
-    }
-    for (uint32_t B = B_lo; B <= B_hi; ++B) {
-      const double gn = gain_at(s, s_tau[B - 1]);
-      out[(size_t)(B - 1) * w.N_cap] = ordered_key(prio_key(gn, l));
-    }
-  }
+// ---------------------------------------------------------------- block helpers
+__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau) {
+  return ordered_key(prio_key(gain_at(unpack_state(p), tau), p.l));
 }
 
-// ---------------------------------------------------------------- block helpers
+__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau) {
+  return composite(okey_of(p, tau), p.rank);
+}
+
 template <int NT>
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -68,7 +66,6 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
 }
 
 // In-place bitonic sort of (key, idx) pairs in shared memory, size = power of two.
-// descending = true sorts by key descending.
 template <int NT>
 __device__ void bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t size, bool descending) {
   for (uint32_t k = 2; k <= size; k <<= 1) {
@@ -76,7 +73,7 @@ __device__ void bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t si
       for (uint32_t t = threadIdx.x; t < size; t += NT) {
         const uint32_t p = t ^ j;
         if (p > t) {
-          const bool up = ((t & k) == 0) == descending;  // region direction
+          const bool up = ((t & k) == 0) == descending;
           const unsigned long long a = key[t], b = key[p];
           if ((a < b) == up) {
             key[t] = b;
@@ -92,9 +89,161 @@ __device__ void bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t si
   }
 }
 
+// ---------------------------------------------------------------- S3a: state + key bounds
+constexpr int kStateThreads = 256;
+
+__global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
+  __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
+  __shared__ uint32_t s_last;
+  __shared__ unsigned long long s_sc[kStateThreads];
+  __shared__ uint32_t s_cut;
+  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t tlo = __ldcg(&w.g->tau_lo), thi = __ldcg(&w.g->tau_hi);
+  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
+    s_hlb[q] = 0u;
+    s_hub[q] = 0u;
+  }
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + tid; i < r.n; i += gridDim.x * blockDim.x) {
+    const GainState s = make_state(r, w, i, now, horizon);
+    PackedState p;
+    p.w0 = s.w0; p.c0 = s.c0; p.spre = s.spre; p.cw = s.cw; p.dto = s.dto; p.qw = s.qw;
+    p.m = s.m; p.K = s.K; p.P = s.P; p.h0 = s.h0; p.l = r.ctx_len[i]; p.rank = r.rank[i];
+    p.pad[0] = p.pad[1] = 0;
+    w.st[i] = p;
+    uint32_t lb, ub;
+    if (s.K == 0) {
+      lb = ub = ordered_key(0.0f);  // gain exactly 0 for every B
+    } else {
+      int64_t sd_lo, sw_lo, sd_hi, sw_hi;
+      serve_area(s, tlo, sd_lo, sw_lo);
+      serve_area(s, thi, sd_hi, sw_hi);
+      const double q_ub = qoe_value(sd_lo, sw_hi);
+      const double q_lb = (sw_lo == 0) ? 0.0 : qoe_value(sd_hi, sw_lo);
+      ub = ordered_key(prio_key(__dsub_rn(q_ub, s.qw), p.l));
+      lb = ordered_key(prio_key(__dsub_rn(q_lb, s.qw), p.l));
+    }
+    w.ub[i] = ub;
+    atomicAdd(&s_hlb[lb >> 20], 1u);
+    atomicAdd(&s_hub[ub >> 20], 1u);
+  }
+  __syncthreads();
+  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
+    if (s_hlb[q]) atomicAdd(&w.hist_lb[q], s_hlb[q]);
+    if (s_hub[q]) atomicAdd(&w.hist_ub[q], s_hub[q]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&w.g->state_done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // theta: lower edge of the highest bucket b* with #(LB in buckets >= b*) >= B_hi
+  constexpr uint32_t kPer = kHistK / kStateThreads;  // 16 buckets per thread, descending
+  const uint32_t need = __ldcg(&w.g->B_hi);
+  uint32_t cnt = 0;
+  for (uint32_t q = 0; q < kPer; ++q) cnt += __ldcg(&w.hist_lb[kHistK - 1 - (tid * kPer + q)]);
+  s_sc[tid] = cnt;
+  if (tid == 0) s_cut = 0;
+  __syncthreads();
+  for (uint32_t off = 1; off < kStateThreads; off <<= 1) {
+    unsigned long long a = (tid >= off) ? s_sc[tid - off] : 0ull;
+    __syncthreads();
+    s_sc[tid] += a;
+    __syncthreads();
+  }
+  {
+    const unsigned long long ex = tid ? s_sc[tid - 1] : 0ull;
+    if (ex < need && s_sc[tid] >= need) {
+      unsigned long long c2 = ex;
+      for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t b = kHistK - 1 - (tid * kPer + q);
+        c2 += __ldcg(&w.hist_lb[b]);
+        if (c2 >= need) {
+          s_cut = b;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t cut = s_cut;
+  // survivors: UB >= theta  <=>  UB bucket >= cut
+  uint32_t sv = 0;
+  for (uint32_t b = cut + tid; b < kHistK; b += kStateThreads) sv += __ldcg(&w.hist_ub[b]);
+  for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  __syncthreads();
+  if ((tid & 31) == 0) s_sc[tid >> 5] = sv;
+  __syncthreads();
+  // self-clean the histograms for the next call
+  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
+    w.hist_lb[q] = 0u;
+    w.hist_ub[q] = 0u;
+  }
+  if (tid == 0) {
+    unsigned long long tot = 0;
+    for (uint32_t q = 0; q < kStateThreads / 32; ++q) tot += s_sc[q];
+    w.g->theta = cut << 20;
+    w.g->n_surv = (uint32_t)tot;
+    w.g->overflow = (tot > w.S_cap) ? 1u : 0u;
+    if (tot > w.S_cap) atomicOr(&w.g->slow, 2u);
+  }
+}
+
+// ---------------------------------------------------------------- S3b: candidates
+constexpr int kCandThreads = 256;
+
+// Compaction of the survivors (UB >= theta) into cand_idx, warp-aggregated appends.
+__global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w) {
+  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0 || __ldcg(&w.g->overflow)) return;
+  const uint32_t theta = __ldcg(&w.g->theta);
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < r.n; i0 += gridDim.x * blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    const bool surv = (i < r.n) && (w.ub[i] >= theta);
+    const uint32_t bal = __ballot_sync(0xffffffffu, surv);
+    if (!bal) continue;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&w.g->cand_ctr, (uint32_t)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (surv) w.cand_idx[base + __popc(bal & ((1u << lane) - 1u))] = i;
+  }
+}
+
+// Exact keys of every (candidate, B) pair, spread over the whole grid; in the overflow
+// fallback, of every (request, B).
+__global__ void __launch_bounds__(kCandThreads) k_cand(ReqView r, Work w, const uint32_t* __restrict__ tau) {
+  __shared__ uint32_t s_tau[kMaxB];
+  if (!__ldcg(&w.g->triggered)) return;
+  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  if (B_hi == 0) return;
+  const uint32_t nB = B_hi - B_lo + 1;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t q = tid; q < nB; q += kCandThreads) s_tau[q] = tau[B_lo - 1 + q];
+  __syncthreads();
+  if (__ldcg(&w.g->overflow)) {
+    for (uint32_t i = blockIdx.x * blockDim.x + tid; i < r.n; i += gridDim.x * blockDim.x) {
+      const PackedState p = w.st[i];
+      uint32_t* out = w.keyrow + i;
+      for (uint32_t b = 0; b < nB; ++b) out[(size_t)(B_lo - 1 + b) * w.N_cap] = okey_of(p, s_tau[b]);
+    }
+    return;
+  }
+  const uint32_t ns = __ldcg(&w.g->n_surv);
+  const unsigned long long pairs = (unsigned long long)ns * nB;
+  for (unsigned long long pr = blockIdx.x * blockDim.x + tid; pr < pairs; pr += gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)(pr / nB), b = (uint32_t)(pr - (unsigned long long)j * nB);
+    const PackedState p = w.st[__ldcg(w.cand_idx + j)];
+    w.cand[(size_t)(B_lo - 1 + b) * w.S_cap + j] = comp_of(p, s_tau[b]);
+  }
+}
+
+// ---------------------------------------------------------------- S4: Algorithm 1 per B
 constexpr int kSelThreads = 512;
-constexpr int kSortCap = kMaxB;        // candidates per B
-constexpr int kVictCap = kMaxRunning;  // victims at B*
+constexpr int kSortCap = kMaxB;
+constexpr int kVictCap = kMaxRunning;
+constexpr int kRankCap = kVictCap - kSortCap;  // candidates ranked directly in shared memory
 
 struct SelectArgs {
   ReqView r;
@@ -110,20 +259,97 @@ struct SelectArgs {
 
 __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key, uint32_t* s_idx);
 
-// ---------------------------------------------------------------- S4: Algorithm 1 per B
-// CTA b handles B = b + 1.  Exact MSB-first radix select (8-bit digits) of the
-// k = min(B, n)-th largest composite (priority key, ~rank) over all n requests, then the
-// top k are sorted and walked exactly as Algorithm 1: take while the running
-// sum of l stays <= M (count <= B holds by construction), break at the first misfit.
+// Exact MSB-first radix select (8-bit digits) of the k-th largest of ne unique 64-bit
+// composites, then collection of the k largest into (s_key, s_idx), sorted descending.
+// comp(e, low) returns element e's composite (its low 32 bits are needed only when low is
+// true); id(e) the request index stored with it.
+template <class Comp, class Id>
+__device__ uint32_t select_top_k(uint32_t ne, uint32_t k, Comp comp, Id id, unsigned long long* s_key,
+                                 uint32_t* s_idx) {
+  __shared__ uint32_t s_hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_need, s_cnt;
+  __shared__ int s_stop;
+  const uint32_t tid = threadIdx.x;
+  unsigned long long prefix = 0ull, mask = 0ull;
+  uint32_t need = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t q = tid; q < 256; q += kSelThreads) s_hist[q] = 0u;
+    __syncthreads();
+    for (uint32_t e = tid; e < ne; e += kSelThreads) {
+      const unsigned long long c = comp(e, shift < 32);
+      if ((c & mask) == prefix) atomicAdd(&s_hist[(uint32_t)(c >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t cnt[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = s_hist[255 - 8 * tid - j];
+        tot += cnt[j];
+      }
+      uint32_t inc = tot;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= (uint32_t)o) inc += v;
+      }
+      const uint32_t exc = inc - tot;
+      if (exc < need && inc >= need) {
+        uint32_t above = exc;
+        for (int j = 0; j < 8; ++j) {
+          if (above + cnt[j] >= need) {
+            s_prefix = prefix | ((unsigned long long)(255 - 8 * tid - j) << shift);
+            s_need = need - above;
+            s_stop = (cnt[j] == need - above) ? 1 : 0;
+            break;
+          }
+          above += cnt[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    need = s_need;
+    mask |= 255ull << shift;
+    if (s_stop) break;
+  }
+  const unsigned long long theta = prefix;
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (uint32_t e = tid; e < ne; e += kSelThreads) {
+    const unsigned long long hi = comp(e, false) | 0xFFFFFFFFull;
+    if (hi < theta) continue;
+    const unsigned long long c = comp(e, true);
+    if (c >= theta) {
+      const uint32_t slot = atomicAdd(&s_cnt, 1u);
+      if (slot < (uint32_t)kSortCap) {
+        s_key[slot] = c;
+        s_idx[slot] = id(e);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = min(s_cnt, (uint32_t)kSortCap);
+  uint32_t size = 1;
+  while (size < cnt) size <<= 1;
+  for (uint32_t q = cnt + tid; q < size; q += kSelThreads) {
+    s_key[q] = 0ull;
+    s_idx[q] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
+  return cnt;
+}
+
+// CTA b handles B = b + 1: top min(B, n) requests by (key desc, rank asc), then Algorithm 1
+// (P:L514-529): take while the running sum of l stays <= M (count <= B by construction), break
+// at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken prefix.
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   extern __shared__ unsigned char s_dyn[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint32_t s_cnt;
-  __shared__ unsigned long long s_prefix;
-  __shared__ uint32_t s_need;
-  __shared__ int s_stop;
+  __shared__ unsigned long long s_ps[kSortCap];
+  __shared__ uint32_t s_k;
   __shared__ long long s_red[32];
   __shared__ uint32_t s_last;
 
@@ -132,8 +358,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   const uint32_t tid = threadIdx.x;
   const uint32_t B = blockIdx.x + 1;
   const uint32_t n = r.n;
-  const bool trig = w.g->triggered != 0;
-  const uint32_t B_lo = w.g->B_lo, B_hi = w.g->B_hi;
+  const bool trig = __ldcg(&w.g->triggered) != 0;
+  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
 
   if (!trig || B < B_lo || B > B_hi) {
     if (tid == 0) {
@@ -141,107 +367,70 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       A.o.kstar[B - 1] = 0u;
     }
   } else {
-    const uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
+    const uint32_t tB = A.tau[B - 1];
     const uint32_t k = min(B, n);
-    unsigned long long prefix = 0ull, mask = 0ull;
-    uint32_t need = k;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (uint32_t q = tid; q < 256; q += kSelThreads) s_hist[q] = 0u;
-      __syncthreads();
-      const bool lowpass = shift < 32;
-      for (uint32_t i = tid; i < n; i += kSelThreads) {
-        const unsigned long long c = lowpass ? composite(keys[i], r.rank[i]) : ((unsigned long long)keys[i] << 32);
-        if ((c & mask) == prefix) atomicAdd(&s_hist[(uint32_t)(c >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (tid < 32) {
-        // lane L covers buckets 255-8L .. 248-8L (descending)
-        uint32_t cnt[8], tot = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          cnt[j] = s_hist[255 - 8 * tid - j];
-          tot += cnt[j];
-        }
-        uint32_t inc = tot;
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-          if (tid >= (uint32_t)o) inc += v;
-        }
-        const uint32_t exc = inc - tot;
-        if (exc < need && inc >= need) {
-          uint32_t above = exc;
-          for (int j = 0; j < 8; ++j) {
-            if (above + cnt[j] >= need) {
-              const uint32_t bucket = 255 - 8 * tid - j;
-              s_prefix = prefix | ((unsigned long long)bucket << shift);
-              s_need = need - above;
-              s_stop = (cnt[j] == need - above) ? 1 : 0;
-              break;
-            }
-            above += cnt[j];
+    uint32_t cnt;
+    if (__ldcg(&w.g->overflow)) {
+      const uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
+      cnt = select_top_k(
+          n, k,
+          [&](uint32_t e, bool low) -> unsigned long long {
+            return low ? composite(keys[e], r.rank[e]) : ((unsigned long long)keys[e] << 32);
+          },
+          [&](uint32_t e) { return e; }, s_key, s_idx);
+    } else {
+      const unsigned long long* row = w.cand + (size_t)(B - 1) * w.S_cap;
+      const uint32_t ns = __ldcg(&w.g->n_surv);
+      if (ns <= (uint32_t)kRankCap) {
+        // rank counting: position of each candidate = number of larger composites (unique)
+        unsigned long long* s_all = s_key + kSortCap;  // scratch after the first kSortCap slots
+        for (uint32_t e = tid; e < ns; e += kSelThreads) s_all[e] = __ldcg(row + e);
+        __syncthreads();
+        for (uint32_t e = tid; e < ns; e += kSelThreads) {
+          const unsigned long long c = s_all[e];
+          uint32_t pos = 0;
+          for (uint32_t f = 0; f < ns; ++f) pos += (s_all[f] > c) ? 1u : 0u;
+          if (pos < k) {
+            s_key[pos] = c;
+            s_idx[pos] = __ldcg(w.cand_idx + e);
           }
         }
-      }
-      __syncthreads();
-      prefix = s_prefix;
-      need = s_need;
-      mask |= 255ull << shift;
-      if (s_stop) break;
-    }
-    // collect the k elements with composite >= prefix
-    const unsigned long long theta = prefix;
-    if (tid == 0) s_cnt = 0;
-    __syncthreads();
-    for (uint32_t i = tid; i < n; i += kSelThreads) {
-      const uint32_t okey = keys[i];
-      if (((unsigned long long)okey << 32 | 0xFFFFFFFFull) < theta) continue;  // cheap reject
-      const unsigned long long c = composite(okey, r.rank[i]);
-      if (c >= theta) {
-        const uint32_t slot = atomicAdd(&s_cnt, 1u);
-        if (slot < kSortCap) {
-          s_key[slot] = c;
-          s_idx[slot] = i;
-        }
+        __syncthreads();
+        cnt = k;
+      } else {
+        cnt = select_top_k(
+            ns, k, [&](uint32_t e, bool) -> unsigned long long { return __ldcg(row + e); },
+            [&](uint32_t e) { return __ldcg(w.cand_idx + e); }, s_key, s_idx);
       }
     }
-    __syncthreads();
-    const uint32_t cnt = min(s_cnt, (uint32_t)kSortCap);
-    uint32_t size = 1;
-    while (size < cnt) size <<= 1;
-    for (uint32_t q = cnt + tid; q < size; q += kSelThreads) {
-      s_key[q] = 0ull;
-      s_idx[q] = 0xFFFFFFFFu;
-    }
-    __syncthreads();
-    bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
-    // Algorithm 1 walk: prefix sums of l in greedy order (<= 1024 elements, 2 per thread)
-    __shared__ unsigned long long s_ps[kSortCap];
+    // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
+    // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
     for (uint32_t q = tid; q < cnt; q += kSelThreads) s_ps[q] = r.ctx_len[s_idx[q]];
     __syncthreads();
-    for (uint32_t off = 1; off < cnt; off <<= 1) {
-      unsigned long long v0 = 0, v1 = 0;
-      const uint32_t q0 = tid, q1 = tid + kSelThreads;
-      if (q0 < cnt && q0 >= off) v0 = s_ps[q0 - off];
-      if (q1 < cnt && q1 >= off) v1 = s_ps[q1 - off];
-      __syncthreads();
-      if (q0 < cnt) s_ps[q0] += v0;
-      if (q1 < cnt) s_ps[q1] += v1;
-      __syncthreads();
+    if (tid < 32) {
+      const uint32_t per = (cnt + 31) / 32, q0 = tid * per, q1 = min(cnt, q0 + per);
+      unsigned long long part = 0;
+      for (uint32_t q = q0; q < q1; ++q) part += s_ps[q];
+      unsigned long long inc = part;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= (uint32_t)o) inc += v;
+      }
+      unsigned long long run = inc - part;
+      uint32_t mine = 0;
+      for (uint32_t q = q0; q < q1; ++q) {
+        run += s_ps[q];
+        mine += (run <= A.M) ? 1u : 0u;
+      }
+      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      if (tid == 0) s_k = mine;
     }
-    // k* = number of leading prefix sums <= M (l >= 1: prefix sums strictly increase)
-    if (tid == 0) s_cnt = 0;
     __syncthreads();
-    uint32_t mine = 0;
-    for (uint32_t q = tid; q < cnt; q += kSelThreads) mine += (s_ps[q] <= A.M) ? 1u : 0u;
-    if (mine) atomicAdd(&s_cnt, mine);
-    __syncthreads();
-    const uint32_t kstar = s_cnt;
+    const uint32_t kstar = s_k;
     long long v = 0;
-    const uint32_t tB = A.tau[B - 1];
     for (uint32_t q = tid; q < kstar; q += kSelThreads) {
       const uint32_t i = s_idx[q];
-      const GainState s = make_state(r, w, i, A.now, A.horizon);
-      v += gain_fixed(gain_at(s, tB));
+      v += gain_fixed(gain_at(unpack_state(w.st[i]), tB));
       w.sel[(size_t)(B - 1) * kMaxB + q] = i;
     }
     v = block_sum_ll<kSelThreads>(v, s_red);
@@ -250,7 +439,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       A.o.kstar[B - 1] = kstar;
     }
   }
-  // last CTA finalises the decision
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(&w.g->done, 1u) == gridDim.x - 1) ? 1u : 0u;
@@ -261,57 +449,125 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   }
 }
 
-// ---------------------------------------------------------------- S5 + S6 (one CTA)
+// ---------------------------------------------------------------- S5 + S6 + outputs (one CTA)
 __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key, uint32_t* s_idx) {
   __shared__ uint32_t s_Bstar, s_kstar, s_nv;
+  __shared__ uint32_t s_sel[kSortCap];
+  __shared__ unsigned long long s_selk[kSortCap];
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x;
+  const uint32_t n = r.n;
   uint32_t* sc = A.o.scalars;
-  const bool trig = w.g->triggered != 0;
-  const uint32_t B_lo = w.g->B_lo, B_hi = w.g->B_hi;
-  const uint32_t n_run = min(w.g->n_run, (uint32_t)kMaxRunning);
-  if (w.g->n_run > (uint32_t)kMaxRunning && tid == 0) atomicOr(&w.g->err, kErrRunning);
+  const bool trig = __ldcg(&w.g->triggered) != 0;
+  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  const uint32_t n_run_all = __ldcg(&w.g->n_run);
+  const uint32_t n_run = min(n_run_all, (uint32_t)kMaxRunning);
+  if (n_run_all > (uint32_t)kMaxRunning && tid == 0) atomicOr(&w.g->err, kErrRunning);
   if (!trig) {
+    for (uint32_t i = tid; i < n; i += kSelThreads) A.o.serve_mask[i] = r.running[i] ? 1 : 0;
     if (tid == 0) {
       for (int q = 0; q < 8; ++q) sc[q] = 0u;
-      sc[1] = w.g->n_run;
+      sc[1] = n_run_all;
     }
     return;
   }
-  if (tid == 0) {
-    // S5: largest V over candidate B, ties to the larger B (reading R13)
-    uint32_t Bs = 0;
-    long long best = 0;
-    for (uint32_t B = B_lo; B <= B_hi; ++B) {
+  {
+    // S5: largest V over candidate B, ties to the larger B (reading R13).  Parallel
+    // arg-max on (V, B) pairs compared lexicographically.
+    __shared__ long long s_bv[kSelThreads / 32];
+    __shared__ uint32_t s_bb[kSelThreads / 32];
+    long long bv = (long long)0x8000000000000000ull;
+    uint32_t bb = 0;
+    for (uint32_t B = B_lo + tid; B <= B_hi; B += kSelThreads) {
       const long long v = __ldcg(A.o.V + (B - 1));
-      if (Bs == 0 || v >= best) {
-        best = v;
-        Bs = B;
+      if (bb == 0 || v > bv || (v == bv && B > bb)) {
+        bv = v;
+        bb = B;
       }
     }
-    s_Bstar = Bs;
-    s_kstar = Bs ? __ldcg(A.o.kstar + (Bs - 1)) : 0u;
+    for (int o = 16; o; o >>= 1) {
+      const long long v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const uint32_t b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+      if (b2 != 0 && (bb == 0 || v2 > bv || (v2 == bv && b2 > bb))) {
+        bv = v2;
+        bb = b2;
+      }
+    }
+    if ((tid & 31) == 0) {
+      s_bv[tid >> 5] = bv;
+      s_bb[tid >> 5] = bb;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      bv = s_bv[0];
+      bb = s_bb[0];
+      for (uint32_t q = 1; q < kSelThreads / 32; ++q)
+        if (s_bb[q] != 0 && (bb == 0 || s_bv[q] > bv || (s_bv[q] == bv && s_bb[q] > bb))) {
+          bv = s_bv[q];
+          bb = s_bb[q];
+        }
+      s_Bstar = bb;
+      s_kstar = bb ? __ldcg(A.o.kstar + (bb - 1)) : 0u;
+      s_nv = 0;
+    }
   }
+  // zero the serve mask (the non-cap result is exactly S_{B*})
+  for (uint32_t i = tid; i < n; i += kSelThreads) A.o.serve_mask[i] = 0;
   __syncthreads();
   const uint32_t Bs = s_Bstar, ks = s_kstar;
-  const uint32_t* sel = w.sel + (size_t)(Bs ? Bs - 1 : 0) * kMaxB;
-  for (uint32_t q = tid; q < ks; q += kSelThreads) w.mark[__ldcg(sel + q)] = 1u;
-  if (tid == 0) s_nv = 0;
+  const uint32_t tB = Bs ? A.tau[Bs - 1] : 0u;
+  // S_{B*} in greedy order, staged in shared memory with its l and running flags
+  __shared__ uint32_t s_gsel[kSortCap], s_gl[kSortCap];
+  __shared__ uint8_t s_grun[kSortCap];
+  for (uint32_t q = tid; q < ks; q += kSelThreads) {
+    const uint32_t i = __ldcg(w.sel + (size_t)(Bs - 1) * kMaxB + q);
+    s_gsel[q] = i;
+    s_gl[q] = r.ctx_len[i];
+    s_grun[q] = r.running[i];
+  }
   __syncthreads();
-  // victims: running requests outside S_{B*}, ordered by (key asc, rank desc)
+  const uint32_t* sel = s_gsel;
+  // sorted copy of S_{B*} (by request index) for membership tests
+  uint32_t size = 1;
+  while (size < ks) size <<= 1;
+  for (uint32_t q = tid; q < size; q += kSelThreads) {
+    s_selk[q] = (q < ks) ? (unsigned long long)sel[q] : ~0ull;
+    s_sel[q] = 0;
+  }
+  __syncthreads();
+  bitonic_sort<kSelThreads>(s_selk, s_sel, size, false);
+  auto in_S = [&](uint32_t i) -> bool {
+    uint32_t lo = 0, hi = ks;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_selk[mid] < i) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < ks && s_selk[lo] == i;
+  };
+  // victims R \ S_{B*} with their exact composite key at B*, sorted by (key asc, rank desc)
   for (uint32_t q = tid; q < n_run; q += kSelThreads) {
     const uint32_t i = w.run_list[q];
-    if (!(w.mark[i] & 1u)) {
+    if (!in_S(i)) {
       const uint32_t slot = atomicAdd(&s_nv, 1u);
-      const uint32_t okey = Bs ? w.keyrow[(size_t)(Bs - 1) * w.N_cap + i] : 0u;
-      s_key[slot] = ~composite(okey, r.rank[i]);  // descending of ~ = ascending of composite
+      s_key[slot] = ~comp_of(w.st[i], tB);  // descending of ~ = ascending of the composite
       s_idx[slot] = i;
     }
   }
+  // total l of the running set (for the cap)
+  __shared__ unsigned long long s_W0;
+  if (tid == 0) s_W0 = 0;
+  __syncthreads();
+  {
+    unsigned long long wl = 0;
+    for (uint32_t q = tid; q < n_run; q += kSelThreads) wl += r.ctx_len[w.run_list[q]];
+    for (int o = 16; o; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+    if ((tid & 31) == 0 && wl) atomicAdd(&s_W0, wl);
+  }
   __syncthreads();
   const uint32_t nv = s_nv;
-  uint32_t size = 1;
+  size = 1;
   while (size < nv) size <<= 1;
   for (uint32_t q = nv + tid; q < size; q += kSelThreads) {
     s_key[q] = 0ull;
@@ -319,29 +575,31 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
   }
   __syncthreads();
   bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
+  const uint32_t cap = A.preempt_cap;
+  const bool cap_hit = !(cap == 0xFFFFFFFFu || nv <= cap);
+  if (!cap_hit) {
+    for (uint32_t q = tid; q < ks; q += kSelThreads) A.o.serve_mask[sel[q]] = 1;
+    for (uint32_t q = tid; q < nv; q += kSelThreads) A.o.preempt_idx[q] = s_idx[q];
+  } else {
+    for (uint32_t q = tid; q < n_run; q += kSelThreads) A.o.serve_mask[w.run_list[q]] = 1;
+  }
+  __syncthreads();
   if (tid == 0) {
     // S6 preemption cap (reading R18), sequential over <= B* admits and nv victims
-    uint32_t flags = 1u;  // triggered
+    uint32_t flags = 1u;
     uint32_t n_adm = 0, n_pre = 0, realized = 0;
-    const uint32_t cap = A.preempt_cap;
-    if (cap == 0xFFFFFFFFu || nv <= cap) {
-      for (uint32_t q = 0; q < ks; ++q) {
-        const uint32_t i = sel[q];
-        if (!r.running[i]) A.o.admit_idx[n_adm++] = i;
-      }
-      for (uint32_t q = 0; q < nv; ++q) A.o.preempt_idx[n_pre++] = s_idx[q];
+    if (!cap_hit) {
+      for (uint32_t q = 0; q < ks; ++q)
+        if (!s_grun[q]) A.o.admit_idx[n_adm++] = sel[q];
+      n_pre = nv;
       realized = ks;
     } else {
       flags |= 2u;
-      unsigned long long W0 = 0;
-      uint32_t c0 = 0;
-      for (uint32_t q = 0; q < n_run; ++q) {
-        W0 += r.ctx_len[w.run_list[q]];
-        ++c0;
-      }
+      unsigned long long W0 = s_W0;
+      uint32_t c0 = n_run;
       for (uint32_t q = 0; q < cap; ++q) {
         const uint32_t i = s_idx[q];
-        w.mark[i] |= 2u;
+        A.o.serve_mask[i] = 0;
         A.o.preempt_idx[n_pre++] = i;
         W0 -= r.ctx_len[i];
         --c0;
@@ -350,7 +608,7 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
         flags |= 4u;  // memory beats the cap
         for (uint32_t q = cap; q < nv && W0 > A.M; ++q) {
           const uint32_t i = s_idx[q];
-          w.mark[i] |= 2u;
+          A.o.serve_mask[i] = 0;
           A.o.preempt_idx[n_pre++] = i;
           W0 -= r.ctx_len[i];
           --c0;
@@ -358,10 +616,10 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
       } else {
         for (uint32_t q = 0; q < ks; ++q) {
           const uint32_t i = sel[q];
-          if (r.running[i]) continue;
-          const uint32_t l = r.ctx_len[i];
+          if (s_grun[q]) continue;
+          const uint32_t l = s_gl[q];
           if (W0 + l <= A.M && c0 + 1 <= Bs) {
-            w.mark[i] |= 4u;
+            A.o.serve_mask[i] = 1;
             A.o.admit_idx[n_adm++] = i;
             W0 += l;
             ++c0;
@@ -372,8 +630,8 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
       }
       realized = c0;
     }
-    if (w.g->slow) flags |= 8u;
-    if (w.g->err & kErrRunning) flags |= 16u;
+    if (__ldcg(&w.g->slow)) flags |= 8u;
+    if (__ldcg(&w.g->err) & kErrRunning) flags |= 16u;
     sc[0] = Bs;
     sc[1] = realized;
     sc[2] = n_adm;
@@ -382,22 +640,6 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
     sc[5] = B_hi;
     sc[6] = flags;
     sc[7] = ks;
-  }
-}
-
-// ---------------------------------------------------------------- serve mask
-__global__ void k_mask(ReqView r, Work w, SchedOut o) {
-  const bool trig = w.g->triggered != 0;
-  const bool cap_hit = (__ldcg(o.scalars + 6) & 2u) != 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
-    const uint8_t mk = w.mark[i];
-    const uint8_t run = r.running[i];
-    uint8_t x;
-    if (!trig) x = run ? 1 : 0;
-    else if (cap_hit) x = ((run && !(mk & 2u)) || (mk & 4u)) ? 1 : 0;
-    else x = (mk & 1u) ? 1 : 0;
-    o.serve_mask[i] = x;
-    if (mk) w.mark[i] = 0;
   }
 }
 
@@ -411,11 +653,15 @@ void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, i
                                                 qwait_out);
 }
 
-void launch_gain_keys(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
-                      const uint32_t* tau, uint32_t B_cap) {
-  if (r.n == 0) return;
-  const uint32_t blocks = (r.n + 255) / 256;
-  k_gain_keys<<<blocks, 256, 0, L.stream>>>(r, w, now, horizon, tau, B_cap);
+void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon) {
+  const uint32_t blocks = r.n ? umin32((r.n + kStateThreads - 1) / kStateThreads, L.sm_count * 4) : 1u;
+  k_state<<<blocks, kStateThreads, 0, L.stream>>>(r, w, now, horizon);
+}
+
+void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau) {
+  const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count * 4) : 1u;
+  k_compact<<<cblocks, kCandThreads, 0, L.stream>>>(r, w);
+  k_cand<<<L.sm_count * 4, kCandThreads, 0, L.stream>>>(r, w, tau);
 }
 
 static size_t select_smem() { return (sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
@@ -428,12 +674,6 @@ void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t 
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
   SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o};
   k_select<<<B_cap, kSelThreads, select_smem(), L.stream>>>(A);
-}
-
-void launch_mask(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o) {
-  if (r.n == 0) return;
-  const uint32_t blocks = umin32((r.n + 255) / 256, L.sm_count * 8);
-  k_mask<<<blocks, 256, 0, L.stream>>>(r, w, o);
 }
 
 }  // namespace andes
