@@ -81,6 +81,9 @@ typedef struct {
                                      nondecreasing in i with tl_base[i+1] >= tl_base[i] + n_deliv[i] */
     const uint32_t *tl_pool;      /* delivery timestamps, us since arrival, nondecreasing per request,
                                      each <= now - arrival; 16-byte aligned                           */
+    uint64_t tl_len;              /* number of uint32 elements readable at tl_pool; must be >=
+                                     tl_base[n-1] + n_deliv[n-1] (the scan reads it through a TMA
+                                     tensor map bounded by tl_len)                                    */
 } AndesRequests;
 
 /* andes_qoe_eval modes */

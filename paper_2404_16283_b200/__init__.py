@@ -53,7 +53,8 @@ class Requests(C.Structure):
     _fields_ = [("n", C.c_uint32), ("arrival_us", C.c_void_p), ("ttft_us", C.c_void_p),
                 ("period_us", C.c_void_p), ("ctx_len", C.c_void_p), ("n_deliv", C.c_void_p),
                 ("max_total", C.c_void_p), ("start_off_us", C.c_void_p), ("rank", C.c_void_p),
-                ("running", C.c_void_p), ("tl_base", C.c_void_p), ("tl_pool", C.c_void_p)]
+                ("running", C.c_void_p), ("tl_base", C.c_void_p), ("tl_pool", C.c_void_p),
+                ("tl_len", C.c_uint64)]
 
 
 class SchedParams(C.Structure):
@@ -152,7 +153,7 @@ def requests_to(src, device="cuda", pin=False):
 
 
 def _req_struct(t: dict, n: int) -> Requests:
-    return Requests(n, *[_ptr(t[name]) for name, _ in _FIELDS])
+    return Requests(n, *[_ptr(t[name]) for name, _ in _FIELDS], int(t["tl_pool"].numel()))
 
 
 @dataclass

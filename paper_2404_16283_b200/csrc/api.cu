@@ -34,6 +34,11 @@ struct AndesCtx {
     int64_t* V;
   } mir{};
   std::string err;
+  // TMA tensor map of the current timestamp pool (re-encoded when the pool changes)
+  CUtensorMap pool_map{};
+  const void* map_ptr = nullptr;
+  uint64_t map_len = ~0ull;
+  uint32_t* zero_rows = nullptr;  // 128 zero bytes: TMA source when the pool has no full row
   bool prof = false;
   bool prof_recorded = false;
   cudaEvent_t ev[ANDES_N_STAGES + 1] = {};
@@ -83,6 +88,7 @@ ReqView view_of(const AndesRequests* r) {
   v.running = r->running;
   v.tl_base = r->tl_base;
   v.tl_pool = r->tl_pool;
+  v.tl_len = r->tl_len;
   return v;
 }
 
@@ -95,6 +101,8 @@ int check_requests(AndesCtx* c, const AndesRequests* r, bool need_sched_fields) 
   if (need_sched_fields && (!r->ctx_len || !r->rank || !r->running))
     return set_err(c, ANDES_E_INVAL, "ctx_len/rank/running are required%s");
   if (!r->tl_pool) return set_err(c, ANDES_E_INVAL, "tl_pool is NULL%s");
+  if (r->tl_len > (uint64_t)c->tiles_cap * kTile)
+    return set_err(c, ANDES_E_CAPACITY, "tl_len exceeds limits.max_tokens%s");
   if ((reinterpret_cast<uintptr_t>(r->tl_pool) & 15u) != 0)
     return set_err(c, ANDES_E_INVAL, "tl_pool must be 16-byte aligned%s");
   return ANDES_OK;
@@ -124,6 +132,42 @@ Work work_of(AndesCtx* c, uint32_t n) {
   Work w = c->w;
   (void)n;
   return w;
+}
+
+// 2D TMA view of the pool: rows of 32 u32 (128 B), 128-row boxes, 128-byte swizzle; tokens
+// past the last full row are read directly by the scan.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap** out) {
+  if (c->map_ptr == pool && c->map_len == len) {
+    *out = &c->pool_map;
+    return ANDES_OK;
+  }
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return set_err(c, ANDES_E_CUDA, "cuTensorMapEncodeTiled unavailable%s");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const uint64_t rows = len / 32;
+  void* base = rows ? (void*)pool : (void*)c->zero_rows;
+  cuuint64_t dims[2] = {32, rows ? rows : 1};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {32, kTile / 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&c->pool_map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(c, ANDES_E_CUDA, "cuTensorMapEncodeTiled failed%s");
+  c->map_ptr = pool;
+  c->map_len = len;
+  *out = &c->pool_map;
+  return ANDES_OK;
 }
 
 // per-call reset of the small globals and the look-back status words
@@ -200,7 +244,8 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.srec, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &c->zero_rows, 32)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.sel, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
@@ -209,6 +254,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
     return rc;
   }
   cudaMemset(w.hist_l, 0, sizeof(uint32_t) * kHistL);
+  cudaMemset(c->zero_rows, 0, 128);
   cudaMemset(w.hist_lb, 0, sizeof(uint32_t) * kHistK);
   cudaMemset(w.hist_ub, 0, sizeof(uint32_t) * kHistK);
   if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess) {
@@ -313,7 +359,11 @@ int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, 
   if ((rc = reset_call(c, s))) return rc;
   launch_prep(L, r, w, eval_time_us, fin, false, 0, false);
   mark(c, 1, s);
-  launch_scan(L, r, w, eval_time_us, fin);
+  {
+    const CUtensorMap* tm = nullptr;
+    if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
+    launch_scan(L, r, w, eval_time_us, fin, tm);
+  }
   mark(c, 2, s);
   launch_qoe_final(L, r, w, eval_time_us, fin, out->q, out->q64, out->s_delay, out->s_whole, out->m);
   mark(c, 3, s);
@@ -348,7 +398,11 @@ int andes_gain_estimate(AndesCtx* c, const AndesRequests* req, int64_t now_us, u
     if (e != cudaSuccess) return cuda_check(c, e, "B_list copy");
   }
   launch_prep(L, r, w, eval, false, false, 0, false);
-  launch_scan(L, r, w, eval, false);
+  {
+    const CUtensorMap* tm = nullptr;
+    if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
+    launch_scan(L, r, w, eval, false, tm);
+  }
   launch_gain_estimate(L, r, w, now_us, horizon_us, tau_us, c->B_list_dev, nB, gain_out, key_out, qwait_out);
   return finish_call(c, s, false);
 }
@@ -378,7 +432,11 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   if ((rc = reset_call(c, s))) return rc;
   launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, p->tau_us, p->B_cap, p->cur_latency_us, p->flags);
   mark(c, 1, s);
-  launch_scan(L, r, w, eval, false);
+  {
+    const CUtensorMap* tm = nullptr;
+    if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
+    launch_scan(L, r, w, eval, false, tm);
+  }
   mark(c, 2, s);
   launch_state(L, r, w, p->now_us, p->horizon_us);
   mark(c, 3, s);
@@ -435,6 +493,7 @@ int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedPa
   dr.running = m.running;
   dr.tl_base = m.tl_base;
   dr.tl_pool = m.tl_pool;
+  dr.tl_len = c->lim.max_tokens;
   AndesSchedParams dp = *p;
   dp.tau_us = m.tau;
   AndesDecision dd{m.serve_mask, m.admit_idx, m.preempt_idx, m.scalars, m.V, m.kstar};

@@ -8,17 +8,18 @@
 //   S_delay = sum_j delta~_j,  S_whole = m delta~_m + P m(m-1)/2     (Eq. 1-2)
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace andes {
 
 // ---------------------------------------------------------------- constants
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 32;
-constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (32 KiB)
-constexpr int kWinCap = 480;                      // requests staged per tile (window)
-constexpr int kCarryDirect = 2 * kTile;
-constexpr int kScanDynSmem = 2 * kTile * 4;      // double-buffered tiles (dynamic shared memory)           // head segments up to this long: carry read directly
+constexpr int kScanThreads = 128;
+constexpr int kScanItems = 32;                    // one 128-byte row of the pool per thread
+constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (16 KiB, one TMA box)
+constexpr int kWinCap = 256;                      // requests staged per tile (window)
+constexpr int kCarryDirect = kTile;               // head segments up to this long: carry read directly
+constexpr int kScanDynSmem = 2 * kTile * 4 + 1024;  // double-buffered tiles + 1 KiB alignment slack
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;
@@ -50,6 +51,17 @@ struct ReqView {
   const uint8_t* __restrict__ running;
   const uint64_t* __restrict__ tl_base;
   const uint32_t* __restrict__ tl_pool;
+  uint64_t tl_len;  // readable elements at tl_pool
+};
+
+// Per-request record of the timeline scan (written by prep).
+struct alignas(16) ScanRec {
+  unsigned long long base;  // tl_base
+  uint32_t lim;             // tokens to scan: min(g, m) (FINAL: g)
+  uint32_t P, ttft;
+  uint32_t trel;            // evaluation time - arrival (FINAL: unused)
+  uint32_t ek;              // edge kind of the last valid token: 1 delta_g (g < m), 2 delta~_m
+  uint32_t pad;
 };
 
 // Small per-call globals (zeroed by one memset node per call).
@@ -94,6 +106,7 @@ struct Work {
   uint32_t* hist_lb;         // [kHistK] histogram of lower-bound keys (self-cleaning)
   uint32_t* hist_ub;         // [kHistK] histogram of upper-bound keys (self-cleaning)
   uint32_t* run_list;        // [max_running]
+  ScanRec* srec;             // [N] timeline-scan records
   PackedState* st;           // [N]
   uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
   unsigned long long* cand;  // [max_B][S_cap] composite keys of the candidates per B

@@ -10,6 +10,8 @@
 // memory with cp.async.bulk (TMA bulk copy, mbarrier completion), double-buffered,
 // by a persistent grid; the prefix max crosses tile boundaries through a single-pass
 // decoupled look-back on the segmented-max monoid (flag = segment start, value = max).
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "device.cuh"
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
                                                       uint32_t cur_latency, uint32_t flags) {
   __shared__ uint32_t s_last;
   __shared__ uint32_t s_hl[kHistL];
-  __shared__ uint32_t s_minP, s_nrun;
+  __shared__ uint32_t s_minP;
   __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
   uint32_t local_err = 0;
@@ -176,7 +178,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
     if (threadIdx.x == 0) {
       s_minP = 0xFFFFFFFFu;
-      s_nrun = 0;
       s_runl = 0;
     }
     __syncthreads();
@@ -195,6 +196,17 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     w.m[i] = m;
     w.spre[i] = 0ull;
     w.edge[i] = 0u;
+    {
+      ScanRec sr;
+      sr.base = r.tl_base[i];
+      sr.lim = min(g, m);
+      sr.P = P;
+      sr.ttft = r.ttft[i];
+      sr.trel = final_mode ? 0u : (uint32_t)(eval_abs - r.arrival[i]);
+      sr.ek = (!final_mode && g < m) ? 1u : 2u;
+      sr.pad = 0u;
+      w.srec[i] = sr;
+    }
     // tile ownership: tiles whose start position p satisfies base_i <= p < base_{i+1}
     const unsigned long long base = r.tl_base[i];
     const unsigned long long next = (i + 1 < n) ? r.tl_base[i + 1] : base + g;
@@ -206,8 +218,13 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     }
     for (uint32_t t = t_lo; t < t_hi; ++t) w.tile_owner[t] = i;
     if (i + 1 == n) {
-      w.g->ntiles = min((uint32_t)((base + g + kTile - 1) / kTile), w.tiles_cap);
-      w.g->pool_end = min(base + g, (unsigned long long)w.tiles_cap * kTile);
+      unsigned long long pe = min(base + g, (unsigned long long)w.tiles_cap * kTile);
+      if (pe > r.tl_len) {  // pool shorter than the spans it claims: refuse (flagged), never overread
+        pe = r.tl_len;
+        local_err |= kErrTokens;
+      }
+      w.g->ntiles = (uint32_t)((pe + kTile - 1) / kTile);
+      w.g->pool_end = pe;
     }
     if (debug) {
       if (P == 0) local_err |= kErrPeriod;
@@ -270,11 +287,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// TMA: one [128 rows x 32 u32] box of the pool, 128-byte swizzled, completion on bar
+__device__ __forceinline__ void tma_tile(const CUtensorMap* tmap, void* dst, uint32_t row0, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(row0), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -285,27 +303,17 @@ __device__ __forceinline__ unsigned long long seg_combine(unsigned long long a, 
   return (a & kFlagBit) | v;
 }
 
+// byte offset of tile-local token x in a 128B-swizzled [128 x 32] u32 tile
+__device__ __forceinline__ uint32_t swz(uint32_t x) {
+  const uint32_t row = x >> 5, chunk = (x >> 2) & 7u;
+  return (row << 7) | ((chunk ^ (row & 7u)) << 4) | ((x & 3u) << 2);
+}
+
 struct ScanArgs {
   ReqView r;
   Work w;
   int64_t eval_abs;
-  uint32_t debug;  // ANDES_SCAN_DEBUG: poison tile buffers before each bulk copy, count survivors
 };
-
-// Issue the bulk copy of tile t into buf (one elected thread); the 16-byte-aligned body
-// goes through the TMA bulk-copy engine, the < 4-token tail is copied by threads.
-__device__ __forceinline__ void issue_tile(const ScanArgs& A, uint32_t t, unsigned long long pool_end,
-                                           uint32_t* buf, uint64_t* bar) {
-  const unsigned long long p0 = (unsigned long long)t * kTile;
-  const unsigned long long pend = min(p0 + (unsigned long long)kTile, pool_end);
-  const uint32_t bulk = ((uint32_t)(pend - p0) / 4u) * 16u;
-  if (A.debug) {
-    for (uint32_t i = 0; i < (uint32_t)kTile; ++i) buf[i] = 0xFFFFFFFFu;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  mbar_expect_tx(bar, bulk);
-  if (bulk) bulk_g2s(buf, A.r.tl_pool + p0, bulk, bar);
-}
 
 // One request of a tile's window in tile-local coordinates (x = position - p0).
 struct Entry {
@@ -319,10 +327,10 @@ struct Entry {
   uint32_t ridx;  // request index (0xFFFFFFFF: dummy / sentinel)
 };
 
-// Window entry q of a tile whose first request is r0 (dummy = a gap precedes request r0).
-template <bool kFinal>
-__device__ __forceinline__ Entry make_entry(const ScanArgs& A, unsigned long long p0, uint32_t r0, uint32_t dummy,
-                                            uint32_t wn, uint32_t q) {
+// Window entry q of a tile starting at p0 whose first request is r0 (dummy: a gap precedes
+// r0; q == wn: sentinel).  Out of line: used to fill the window and by overflowing windows.
+__device__ __noinline__ Entry entry_at(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
+                                       uint32_t dummy, uint32_t wn, uint32_t q) {
   Entry e;
   if ((dummy && q == 0) || q >= wn) {
     e.ls = (q >= wn) ? kTile + 1 : -1;
@@ -330,149 +338,124 @@ __device__ __forceinline__ Entry make_entry(const ScanArgs& A, unsigned long lon
     e.A = 0; e.U = 0; e.P = 1; e.epos = -1; e.ek = 0; e.ridx = 0xFFFFFFFFu;
     return e;
   }
-  const ReqView& r = A.r;
   const uint32_t ri = r0 + q - dummy;
-  const unsigned long long base = r.tl_base[ri];
-  const uint32_t g = r.n_deliv[ri];
-  const uint32_t m = kFinal ? g : A.w.m[ri];
-  const uint32_t lim = min(g, m);
-  const uint32_t P = r.period[ri];
-  const uint32_t ttft = r.ttft[ri];
-  const long long ls = (long long)base - (long long)p0;
-  const long long ve = ls + (long long)lim;
+  const ScanRec s = srec[ri];
+  const long long ls = (long long)s.base - (long long)p0;
+  const long long ve = ls + (long long)s.lim;
   e.ls = (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
   e.vend = (int32_t)max(-1ll, min(ve, (long long)kTile));
-  e.A = ttft + (uint32_t)(unsigned long long)(-ls) * P;
-  uint32_t trel = 0;
-  if (!kFinal) trel = (uint32_t)(A.eval_abs - r.arrival[ri]);
-  e.U = trel - e.A;
-  e.P = P;
+  e.A = s.ttft + (uint32_t)(unsigned long long)(-ls) * s.P;
+  e.U = s.trel - e.A;
+  e.P = s.P;
   e.ridx = ri;
   e.epos = -1;
   e.ek = 0;
-  if (lim > 0) {
-    const long long x = ls + (long long)lim - 1;
+  if (s.lim > 0) {
+    const long long x = ve - 1;
     if (x >= 0 && x < (long long)kTile) {
       e.epos = (int32_t)x;
-      e.ek = (!kFinal && g < m) ? 1u : 2u;
+      e.ek = s.ek;
     }
   }
   return e;
 }
 
+__device__ __noinline__ int32_t ls_at(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
+                                      uint32_t dummy, uint32_t wn, uint32_t q) {
+  if (q >= wn) return kTile + 1;
+  if (dummy && q == 0) return -1;
+  const long long ls = (long long)srec[r0 + q - dummy].base - (long long)p0;
+  return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+}
+
 }  // namespace
 
+// K1.  Persistent CTAs claim 4096-token tiles in increasing order; each tile arrives by one
+// TMA tensor copy into a double-buffered, 128B-swizzled shared-memory tile; each thread owns
+// one 32-token row (conflict-free LDS.128); requests overlapping the tile are staged in a
+// shared-memory window; the carry of the head segment is read directly (short segments) or
+// obtained by decoupled look-back (long segments).
 template <bool kFinal>
-__global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
-  extern __shared__ __align__(128) uint32_t s_dyn_tiles[];  // [2][kTile], dynamic (64 KiB)
-  uint32_t(*s_tile)[kTile] = reinterpret_cast<uint32_t(*)[kTile]>(s_dyn_tiles);
+__global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant__ ScanArgs A,
+                                                           const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ unsigned char s_dyn_raw[];
+  // two 16 KiB tile buffers, 1024-byte aligned for the 128B swizzle
+  unsigned char* s_tiles =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn_raw) + 1023) & ~uintptr_t(1023));
   __shared__ alignas(8) uint64_t s_bar[2];
   __shared__ int32_t w_ls[kWinCap + 2], w_vend[kWinCap + 2], w_epos[kWinCap + 2];
   __shared__ uint32_t w_A[kWinCap + 2], w_U[kWinCap + 2], w_P[kWinCap + 2], w_ek[kWinCap + 2],
       w_ridx[kWinCap + 2];
-  __shared__ uint32_t s_own[kScanThreads + 1];
   __shared__ unsigned long long s_warp[kScanThreads / 32];
+  __shared__ uint32_t s_cm[kScanThreads / 32];
   __shared__ unsigned long long s_carry;
-  __shared__ uint32_t s_tcur, s_tnext, s_r0, s_wn, s_dummy, s_mode, s_cmax;
-  __shared__ unsigned long long s_hbase;  // head request base / ideal info for the direct carry
-  __shared__ uint32_t s_hcnt, s_httft, s_hP;
+  __shared__ uint32_t s_tile_id[2], s_r0, s_wn, s_dummy, s_mode, s_hcnt, s_hP, s_httft;
+  __shared__ unsigned long long s_hbase;
 
   const ReqView& r = A.r;
   const Work& w = A.w;
+  const ScanRec* __restrict__ srec = w.srec;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t ntiles = w.g->ntiles;
   const unsigned long long pool_end = w.g->pool_end;
+  const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
   const uint32_t n = r.n;
-  // window entry q (shared memory when the tile's window fits, else straight from global)
-  auto fetch = [&](uint32_t q, bool win_ok, unsigned long long p0, uint32_t r0, uint32_t dummy,
-                   uint32_t wn) -> Entry {
-    if (win_ok) {
-      Entry e;
-      e.ls = w_ls[q]; e.vend = w_vend[q]; e.A = w_A[q]; e.U = w_U[q]; e.P = w_P[q];
-      e.epos = w_epos[q]; e.ek = w_ek[q]; e.ridx = w_ridx[q];
-      return e;
-    }
-    return make_entry<kFinal>(A, p0, r0, dummy, wn, q);
-  };
-  auto next_ls = [&](uint32_t q, bool win_ok, unsigned long long p0, uint32_t r0, uint32_t dummy,
-                     uint32_t wn) -> int32_t {
-    if (win_ok) return w_ls[q];
-    if (q >= wn) return kTile + 1;
-    if (dummy && q == 0) return -1;
-    const long long ls = (long long)r.tl_base[r0 + q - dummy] - (long long)p0;
-    return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
-  };
 
   if (tid == 0) {
-    s_cmax = 0;
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // Tiles are claimed dynamically in increasing order, so every tile a CTA may wait on in
-    // the look-back belongs to a CTA that is already running.
-    const uint32_t t0 = atomicAdd(&w.g->tile_ctr, 1u);
-    s_tcur = t0;
-    if (t0 < ntiles) issue_tile(A, t0, pool_end, s_tile[0], &s_bar[0]);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    // claim two tiles (increasing order: any tile waited on in a look-back is already owned by
+    // a running CTA)
+    for (int b = 0; b < 2; ++b) {
+      const uint32_t tt = atomicAdd(&w.g->tile_ctr, 1u);
+      s_tile_id[b] = tt;
+      if (tt < ntiles) {
+        mbar_expect_tx(&s_bar[b], kTile * 4u);
+        tma_tile(&tmap, s_tiles + b * (kTile * 4), tt * (kTile / 32), &s_bar[b]);
+      }
+    }
   }
   __syncthreads();
-  uint32_t t = s_tcur;
   uint32_t buf = 0, ph0 = 0, ph1 = 0;
-
-  for (; t < ntiles; buf ^= 1u) {
+  for (uint32_t t = s_tile_id[0]; t < ntiles; buf ^= 1u) {
     const unsigned long long p0 = (unsigned long long)t * kTile;
-    const uint32_t tlen = (uint32_t)(min(p0 + (unsigned long long)kTile, pool_end) - p0);
     if (tid == 0) {
-      const uint32_t tn = atomicAdd(&w.g->tile_ctr, 1u);
-      s_tnext = tn;
-      if (tn < ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_tile(A, tn, pool_end, s_tile[buf ^ 1u], &s_bar[buf ^ 1u]);
-      }
       const uint32_t r0 = w.tile_owner[t];
       const uint32_t r_end = (t + 1 < ntiles) ? w.tile_owner[t + 1] : n - 1;
-      const unsigned long long b0 = r.tl_base[r0];
-      // a gap before the first request of the pool: prepend a dummy entry owning nothing
+      const unsigned long long b0 = srec[r0].base;
       s_dummy = (b0 > p0) ? 1u : 0u;
       s_r0 = r0;
       s_wn = r_end - r0 + 1 + s_dummy;
+      // head segment (window entry 0): carry source
+      uint32_t mode = 0;  // 0: none needed, 1: direct read, 2: decoupled look-back
+      if (b0 < p0) {
+        const ScanRec h = srec[r0];
+        const unsigned long long span = p0 - b0;
+        if ((unsigned long long)h.lim > span) {
+          s_hbase = b0;
+          s_hcnt = (uint32_t)span;
+          s_httft = h.ttft;
+          s_hP = h.P;
+          mode = (span <= (unsigned long long)kCarryDirect) ? 1u : 2u;
+        }
+      }
+      s_mode = mode;
     }
     __syncthreads();
-    const uint32_t r0 = s_r0, wn = s_wn, dummy = s_dummy;
+    const uint32_t r0 = s_r0, wn = s_wn, dummy = s_dummy, mode = s_mode;
     const bool win_ok = wn <= (uint32_t)kWinCap;
-    // ---- window: per-request tile-local parameters (one thread per request)
-    for (uint32_t q = tid; q <= kScanThreads; q += kScanThreads) s_own[q] = 0u;
     if (win_ok) {
       for (uint32_t q = tid; q <= wn; q += kScanThreads) {
-        const Entry e = make_entry<kFinal>(A, p0, r0, dummy, wn, q);
+        const Entry e = entry_at(srec, p0, r0, dummy, wn, q);
         w_ls[q] = e.ls; w_vend[q] = e.vend; w_A[q] = e.A; w_U[q] = e.U; w_P[q] = e.P;
         w_epos[q] = e.epos; w_ek[q] = e.ek; w_ridx[q] = e.ridx;
       }
     }
-    if (tid == 0) {
-      // head segment (request at window entry 0): carry source
-      s_mode = 0;  // 0: no carry needed, 1: direct, 2: look-back
-      s_carry = 0ull;
-      if (!dummy) {
-        const unsigned long long base = r.tl_base[r0];
-        if (base < p0) {
-          const uint32_t g = r.n_deliv[r0];
-          const uint32_t m = kFinal ? g : w.m[r0];
-          const unsigned long long lim = min(g, m);
-          const unsigned long long span = p0 - base;
-          if (lim > span) {  // the head segment has valid tokens inside this tile
-            s_hbase = base;
-            s_hcnt = (uint32_t)span;
-            s_httft = r.ttft[r0];
-            s_hP = r.period[r0];
-            s_mode = (span <= (unsigned long long)kCarryDirect) ? 1u : 2u;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- direct head carry: max lat+ of the head segment's tokens before p0 (short segments)
+    // direct head carry: max lat+ of the head segment's tokens before p0
     uint32_t cmax = 0;
-    if (s_mode == 1u) {
+    if (mode == 1u) {
       const unsigned long long hb = s_hbase;
       const uint32_t cnt = s_hcnt, P = s_hP, ttft = s_httft;
       for (uint32_t k = tid; k < cnt; k += kScanThreads) {
@@ -481,101 +464,84 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
         cmax = max(cmax, max(d, I) - I);
       }
     }
-    // ---- owners: last window entry starting at or before each thread's first position
-    if (win_ok) {
-      for (uint32_t q = 1 + tid; q < wn; q += kScanThreads) {
-        const int32_t ls = w_ls[q];
-        if (ls < (int32_t)kTile) {
-          const uint32_t j = (ls <= 0) ? 0u : (uint32_t)(ls + kScanItems - 1) / kScanItems;
-          if (j < kScanThreads) atomicMax(&s_own[j], q);
-        }
-      }
-    }
-    // wait for this tile's data (issued one iteration ago); copy the ragged tail
-    {
-      const uint32_t bulk_tok = (tlen / 4u) * 4u;
-      if (tid < tlen - bulk_tok) s_tile[buf][bulk_tok + tid] = r.tl_pool[p0 + bulk_tok + tid];
-    }
+    for (int o = 16; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    if (lane == 0) s_cm[wid] = cmax;
+    // this tile's data
     if (buf == 0) { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
     else { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
-    for (int o = 16; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    if (lane == 0 && cmax) atomicMax(&s_cmax, cmax);
-    __syncthreads();
-    if (A.debug) {
-      uint32_t bad = 0;
-      for (uint32_t i = tid; i < tlen; i += kScanThreads) bad += (s_tile[buf][i] == 0xFFFFFFFFu) ? 1u : 0u;
-      if (bad) atomicAdd(&w.g->slow, bad);
-    }
-    // inclusive max-scan of s_own over threads
-    uint32_t q;
+    unsigned char* tile = s_tiles + buf * (kTile * 4);
     {
-      uint32_t v = s_own[tid];
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= (uint32_t)o) v = max(v, u);
-      }
-      __syncthreads();
-      if (lane == 31) s_own[kScanThreads - 1 - wid] = v;  // stash warp maxima at the top (temp)
-      __syncthreads();
-      uint32_t pre = 0;
-      for (uint32_t k = 0; k < wid; ++k) pre = max(pre, s_own[kScanThreads - 1 - k]);
-      q = max(v, pre);
-      if (!win_ok) {
-        // window above kWinCap: last entry starting at or before x0, by binary search in global
-        const long long my0 = (long long)(tid * kScanItems);
-        uint32_t lo = 0, hi = wn - 1;
-        while (lo < hi) {
-          const uint32_t mid = lo + (hi - lo + 1) / 2;
-          if (next_ls(mid, false, p0, r0, dummy, wn) <= my0) lo = mid;
-          else hi = mid - 1;
-        }
-        q = lo;
+      // tokens past the last full 32-token row of the pool view: read directly
+      const unsigned long long pe = min(p0 + (unsigned long long)kTile, pool_end);
+      if (pe > full_rows_end) {
+        const unsigned long long lo = max(p0, full_rows_end);
+        for (unsigned long long p = lo + tid; p < pe; p += kScanThreads)
+          *reinterpret_cast<uint32_t*>(tile + swz((uint32_t)(p - p0))) = r.tl_pool[p];
       }
     }
-    const uint32_t x0 = tid * kScanItems;
-    const uint32_t* tile = s_tile[buf];
+    __syncthreads();
 
-    // ---- pass 1: lat+ per item and the thread aggregate (flag = a segment starts here)
-    uint32_t lat[kScanItems];
+    auto LS = [&](uint32_t q) -> int32_t { return win_ok ? w_ls[q] : ls_at(srec, p0, r0, dummy, wn, q); };
+    auto GET = [&](uint32_t q) -> Entry {
+      if (win_ok) {
+        Entry e;
+        e.ls = w_ls[q]; e.vend = w_vend[q]; e.A = w_A[q]; e.U = w_U[q]; e.P = w_P[q];
+        e.epos = w_epos[q]; e.ek = w_ek[q]; e.ridx = w_ridx[q];
+        return e;
+      }
+      return entry_at(srec, p0, r0, dummy, wn, q);
+    };
+    // owner of this thread's first token: last window entry starting at or before it
+    const uint32_t x0 = tid * kScanItems;
+    uint32_t q0;
+    {
+      uint32_t lo = 0, hi = wn - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (LS(mid) <= (int32_t)x0) lo = mid;
+        else hi = mid - 1;
+      }
+      q0 = lo;
+    }
+    const uint32_t rowb = tid << 7, rsw = tid & 7u;
+
+    // ---- pass 1: thread aggregate of the segmented max of lat+ (flag = a segment starts here)
     unsigned long long agg;
     {
-      uint32_t qq = q;
-      int32_t ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
-      Entry e = fetch(qq, win_ok, p0, r0, dummy, wn);
-      uint32_t P = e.P;
-      uint32_t I = e.A + x0 * P;
+      uint32_t q = q0;
+      Entry e = GET(q);
+      int32_t ns = LS(q + 1);
+      uint32_t P = e.P, I = e.A + x0 * P;
       int32_t vend = e.vend;
-      agg = (e.ls == (int32_t)x0) ? kFlagBit : 0ull;
-      uint32_t v = 0;
-#pragma unroll
-      for (int j4 = 0; j4 < kScanItems; j4 += 4) {
-        const uint4 dv = *reinterpret_cast<const uint4*>(&tile[x0 + j4]);
+      uint32_t flag = (e.ls == (int32_t)x0) ? 1u : 0u, v = 0;
+#pragma unroll 1
+      for (uint32_t g = 0; g < kScanItems / 4; ++g) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
         const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          const int32_t x = (int32_t)x0 + j4 + jj;
+          const int32_t x = (int32_t)(x0 + 4 * g + jj);
           if (x == ns) {
             do {
-              ++qq;
-              ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
+              ++q;
+              ns = LS(q + 1);
             } while (ns <= x);
-            const Entry e2 = fetch(qq, win_ok, p0, r0, dummy, wn);
-            P = e2.P;
-            I = e2.A + (uint32_t)x * P;
-            vend = e2.vend;
-            agg = kFlagBit;
+            e = GET(q);
+            P = e.P;
+            I = e.A + (uint32_t)x * P;
+            vend = e.vend;
+            flag = 1u;
             v = 0;
           }
           uint32_t l = max(dd[jj], I) - I;
           l = (x < vend) ? l : 0u;
           I += P;
           v = max(v, l);
-          lat[j4 + jj] = l;
         }
       }
-      agg |= v;
+      agg = (flag ? kFlagBit : 0ull) | v;
     }
-    // ---- block-wide exclusive scan of thread aggregates
+    // ---- block-wide exclusive scan of thread aggregates (4 warps)
     unsigned long long incl = agg;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -586,16 +552,16 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
     unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
     if (lane == 0) excl = 0ull;
     __syncthreads();
-    unsigned long long warp_prefix = 0ull;
-    for (uint32_t k = 0; k < wid; ++k) warp_prefix = seg_combine(warp_prefix, s_warp[k]);
-    excl = seg_combine(warp_prefix, excl);
-    // ---- tile carry: direct (head segment within kCarryDirect tokens) or decoupled look-back
+    {
+      unsigned long long wp = 0ull;
+      for (uint32_t k = 0; k < wid; ++k) wp = seg_combine(wp, s_warp[k]);
+      excl = seg_combine(wp, excl);
+    }
     if (tid == 0) {
       unsigned long long tile_agg = 0ull;
       for (uint32_t k = 0; k < kScanThreads / 32; ++k) tile_agg = seg_combine(tile_agg, s_warp[k]);
       unsigned long long acc = 0ull;
-      const uint32_t mode = s_mode;
-      if (mode == 2u && t > 0) {
+      if (mode == 2u) {
         st_release(&w.tile_status[t], kStAgg | tile_agg);
         for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
           unsigned long long s;
@@ -606,53 +572,58 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
           if ((s & kStMask) == kStPrefix || (acc & kFlagBit)) break;
         }
       } else if (mode == 1u) {
-        acc = kFlagBit | s_cmax;
+        uint32_t cm = 0;
+        for (uint32_t k = 0; k < kScanThreads / 32; ++k) cm = max(cm, s_cm[k]);
+        acc = kFlagBit | cm;
       }
       st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
       s_carry = acc;
-      s_cmax = 0;
     }
     __syncthreads();
     const unsigned long long carry = seg_combine(s_carry, excl);
 
     // ---- pass 2: clamped delays, per-request partial sums, edge values
     {
-      uint32_t qq = q;
-      int32_t ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
-      Entry e = fetch(qq, win_ok, p0, r0, dummy, wn);
-      uint32_t P = e.P;
-      uint32_t u = e.U - x0 * P;
-      int32_t vend = e.vend;
-      int32_t epos = e.epos;
+      uint32_t q = q0;
+      Entry e = GET(q);
+      int32_t ns = LS(q + 1);
+      uint32_t P = e.P, I = e.A + x0 * P, u = e.U - x0 * P;
+      int32_t vend = e.vend, epos = e.epos;
       uint32_t ek = e.ek, ridx = e.ridx;
       uint32_t pm = (e.ls == (int32_t)x0) ? 0u : (uint32_t)carry;
       unsigned long long sum = 0ull;
+#pragma unroll 1
+      for (uint32_t g = 0; g < kScanItems / 4; ++g) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
+        const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
-      for (int j = 0; j < kScanItems; ++j) {
-        const int32_t x = (int32_t)x0 + j;
-        if (x == ns) {
-          if (sum) atomicAdd(&w.spre[ridx], sum);
-          sum = 0ull;
-          do {
-            ++qq;
-            ns = next_ls(qq + 1, win_ok, p0, r0, dummy, wn);
-          } while (ns <= x);
-          const Entry e2 = fetch(qq, win_ok, p0, r0, dummy, wn);
-          P = e2.P;
-          u = e2.U - (uint32_t)x * P;
-          vend = e2.vend;
-          epos = e2.epos;
-          ek = e2.ek;
-          ridx = e2.ridx;
-          pm = 0;
+        for (int jj = 0; jj < 4; ++jj) {
+          const int32_t x = (int32_t)(x0 + 4 * g + jj);
+          if (x == ns) {
+            if (sum) atomicAdd(&w.spre[ridx], sum);
+            sum = 0ull;
+            do {
+              ++q;
+              ns = LS(q + 1);
+            } while (ns <= x);
+            e = GET(q);
+            P = e.P;
+            I = e.A + (uint32_t)x * P;
+            u = e.U - (uint32_t)x * P;
+            vend = e.vend;
+            epos = e.epos;
+            ek = e.ek;
+            ridx = e.ridx;
+            pm = 0;
+          }
+          const uint32_t l = (x < vend) ? (max(dd[jj], I) - I) : 0u;
+          I += P;
+          pm = max(pm, l);
+          const uint32_t dt = kFinal ? pm : min(pm, u);
+          u -= P;
+          if (x < vend) sum += dt;
+          if (x == epos) w.edge[ridx] = (ek == 1u) ? pm : dt;
         }
-        pm = max(pm, lat[j]);
-        uint32_t dt;
-        if (kFinal) dt = pm;
-        else dt = min(pm, u);
-        u -= P;
-        if (x < vend) sum += dt;
-        if (x == epos) w.edge[ridx] = (ek == 1u) ? pm : dt;
       }
       // the last piece may continue into the next lanes: segmented warp reduction by request
       uint32_t key = ridx;
@@ -666,8 +637,19 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(ScanArgs A) {
       const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
       if ((lane == 0 || kprev != key) && val && key != 0xFFFFFFFFu) atomicAdd(&w.spre[key], val);
     }
-    __syncthreads();  // tile buffer and window reused by the next tile
-    t = s_tnext;
+    __syncthreads();  // tile buffer and window are reused below
+    // refill this buffer with a newly claimed tile (two tiles ahead)
+    if (tid == 0) {
+      const uint32_t tt = atomicAdd(&w.g->tile_ctr, 1u);
+      s_tile_id[buf] = tt;
+      if (tt < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&s_bar[buf], kTile * 4u);
+        tma_tile(&tmap, s_tiles + buf * (kTile * 4), tt * (kTile / 32), &s_bar[buf]);
+      }
+    }
+    __syncthreads();
+    t = s_tile_id[buf ^ 1u];
   }
 }
 
@@ -713,14 +695,14 @@ void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
                                                 debug ? 1u : 0u, tau, B_cap, cur_latency, flags);
 }
 
-void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode) {
+void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
+                 const CUtensorMap* tmap) {
   if (r.n == 0) return;
-  static const uint32_t dbg = getenv("ANDES_SCAN_DEBUG") ? 1u : 0u;
-  ScanArgs A{r, w, eval_abs, dbg};
+  ScanArgs A{r, w, eval_abs};
   if (final_mode)
-    k_qoe_scan<true><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A);
+    k_qoe_scan<true><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
   else
-    k_qoe_scan<false><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A);
+    k_qoe_scan<false><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,

@@ -45,8 +45,8 @@ def test_binding_loads_and_matches_exports(libpath):
 def test_sm100a_cubin_and_bulk_copy(libpath):
     sass = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", libpath], capture_output=True, text=True).stdout
-    assert "UBLKCP" in sass  # cp.async.bulk global->shared (TMA bulk copy) in the timeline scan
-    assert "SYNCS" in sass   # mbarrier transaction completion
+    assert "UTMALDG" in sass  # cp.async.bulk.tensor: TMA tile loads of the timeline scan
+    assert "SYNCS" in sass    # mbarrier transaction completion
 
 
 def test_no_gpu_raises_loudly(libpath):
