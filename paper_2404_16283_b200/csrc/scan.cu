@@ -322,20 +322,17 @@ struct Entry {
   uint32_t A;     // ideal time of local position 0: ttft + (p0 - base) P (mod 2^32); I(x) = A + x P
   uint32_t U;     // t_rel - A (mod 2^32): t - I(x) = U - x P
   uint32_t P;
-  int32_t epos;   // local position of the edge token (the last valid token) or -1
   uint32_t ek;    // edge kind: 1 = delta_g (g < m, unclamped), 2 = delta~_m
   uint32_t ridx;  // request index (0xFFFFFFFF: dummy / sentinel)
 };
 
-// Window entry q of a tile starting at p0 whose first request is r0 (dummy: a gap precedes
-// r0; q == wn: sentinel).  Out of line: used to fill the window and by overflowing windows.
-__device__ __noinline__ Entry entry_at(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
-                                       uint32_t dummy, uint32_t wn, uint32_t q) {
+__device__ __forceinline__ Entry make_entry(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
+                                            uint32_t dummy, uint32_t wn, uint32_t q) {
   Entry e;
   if ((dummy && q == 0) || q >= wn) {
     e.ls = (q >= wn) ? kTile + 1 : -1;
     e.vend = -1;
-    e.A = 0; e.U = 0; e.P = 1; e.epos = -1; e.ek = 0; e.ridx = 0xFFFFFFFFu;
+    e.A = 0; e.U = 0; e.P = 0; e.ek = 0; e.ridx = 0xFFFFFFFFu;
     return e;
   }
   const uint32_t ri = r0 + q - dummy;
@@ -347,25 +344,235 @@ __device__ __noinline__ Entry entry_at(const ScanRec* __restrict__ srec, unsigne
   e.A = s.ttft + (uint32_t)(unsigned long long)(-ls) * s.P;
   e.U = s.trel - e.A;
   e.P = s.P;
+  // the edge token (last valid token) is written only by the tile that contains it
+  e.ek = (ve >= 1 && ve <= (long long)kTile) ? s.ek : 0u;
   e.ridx = ri;
-  e.epos = -1;
-  e.ek = 0;
-  if (s.lim > 0) {
-    const long long x = ve - 1;
-    if (x >= 0 && x < (long long)kTile) {
-      e.epos = (int32_t)x;
-      e.ek = s.ek;
-    }
-  }
   return e;
 }
 
-__device__ __noinline__ int32_t ls_at(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
-                                      uint32_t dummy, uint32_t wn, uint32_t q) {
-  if (q >= wn) return kTile + 1;
-  if (dummy && q == 0) return -1;
-  const long long ls = (long long)srec[r0 + q - dummy].base - (long long)p0;
-  return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+// Window accessors: shared-memory window (hot path) or straight from the scan records when
+// the tile overlaps more than kWinCap requests (slow path, separate instantiation).
+struct SmemWin {
+  const int32_t *ls, *vend;
+  const uint32_t *A, *U, *P, *ek, *ridx;
+  __device__ __forceinline__ int32_t start(uint32_t q) const { return ls[q]; }
+  __device__ __forceinline__ Entry get(uint32_t q) const {
+    Entry e;
+    e.ls = ls[q]; e.vend = vend[q]; e.A = A[q]; e.U = U[q]; e.P = P[q]; e.ek = ek[q]; e.ridx = ridx[q];
+    return e;
+  }
+};
+struct GlobalWin {
+  const ScanRec* srec;
+  unsigned long long p0;
+  uint32_t r0, dummy, wn;
+  __device__ __forceinline__ int32_t start(uint32_t q) const {
+    if (q >= wn) return kTile + 1;
+    if (dummy && q == 0) return -1;
+    const long long ls = (long long)srec[r0 + q - dummy].base - (long long)p0;
+    return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+  }
+  __device__ __forceinline__ Entry get(uint32_t q) const { return make_entry(srec, p0, r0, dummy, wn, q); }
+};
+
+struct TileShared {
+  unsigned long long* warp;  // [kScanThreads / 32]
+  uint32_t* cm;              // [kScanThreads / 32]
+  unsigned long long* carry;
+};
+
+// Per-thread cursor over the window: the current request q, the next event position ev
+// (end of q's valid tokens, or the start of the next request), and the arithmetic state of
+// the valid ("live") or invalid ("null": lat = 0, delta~ = 0) range.
+struct Cursor {
+  uint32_t q;
+  int32_t vend, ns;
+  uint32_t P, I, u, Pu;
+  uint32_t ek, ridx;
+  bool live;
+};
+
+template <bool kFinal, class Win>
+__device__ __forceinline__ void cursor_enter(Cursor& c, const Win& win, uint32_t q, int32_t x) {
+  // enter request q at local position x (q's first position in this thread, or x0)
+  const Entry e = win.get(q);
+  c.q = q;
+  c.vend = e.vend;
+  c.ns = win.start(q + 1);
+  c.ek = e.ek;
+  c.ridx = e.ridx;
+  c.live = x < e.vend;
+  if (c.live) {
+    c.P = e.P;
+    c.I = e.A + (uint32_t)x * e.P;
+    c.u = kFinal ? 0xFFFFFFFFu : e.U - (uint32_t)x * e.P;
+    c.Pu = kFinal ? 0u : e.P;
+  } else {
+    c.P = 0; c.I = 0xFFFFFFFFu; c.u = 0; c.Pu = 0;
+  }
+}
+
+template <bool kFinal, class Win>
+__device__ __forceinline__ void cursor_next_request(Cursor& c, const Win& win, int32_t x) {
+  uint32_t q = c.q;
+  do {
+    ++q;
+  } while (win.start(q + 1) <= x);
+  cursor_enter<kFinal>(c, win, q, x);
+}
+
+template <bool kFinal, class Win>
+__device__ void tile_body(const ScanArgs& A, const Win& win, const unsigned char* tile, uint32_t wn, uint32_t t,
+                          uint32_t mode, const TileShared& sh) {
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int32_t x0 = (int32_t)(tid * kScanItems);
+  uint32_t q0;
+  {
+    uint32_t lo = 0, hi = wn - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (win.start(mid) <= x0) lo = mid;
+      else hi = mid - 1;
+    }
+    q0 = lo;
+  }
+  const uint32_t rowb = tid << 7, rsw = tid & 7u;
+  const bool starts_here = win.start(q0) == x0;
+
+  // ---- pass 1: the thread aggregate of the segmented max of lat+
+  unsigned long long agg;
+  {
+    Cursor c;
+    cursor_enter<kFinal>(c, win, q0, x0);
+    uint32_t flag = starts_here ? 1u : 0u, v = 0;
+    int32_t ev = min(c.live ? c.vend : c.ns, c.ns);
+#pragma unroll 1
+    for (uint32_t g = 0; g < kScanItems / 4; ++g) {
+      const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
+      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      const int32_t gx = x0 + (int32_t)(4 * g);
+      int32_t rel = ev - gx;  // items until the next event
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        if (rel == jj) {
+          const int32_t x = gx + jj;
+          if (x == c.ns) {
+            cursor_next_request<kFinal>(c, win, x);
+            flag = 1u;
+            v = 0;
+          } else {  // end of the valid tokens: null range until the next request
+            c.live = false; c.P = 0; c.I = 0xFFFFFFFFu;
+          }
+          ev = c.live ? min(c.vend, c.ns) : c.ns;
+          rel = ev - gx;
+        }
+        v = max(v, max(dd[jj], c.I) - c.I);
+        c.I += c.P;
+      }
+    }
+    agg = (flag ? kFlagBit : 0ull) | v;
+  }
+  // ---- block-wide exclusive scan of the thread aggregates
+  unsigned long long incl = agg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl = seg_combine(v, incl);
+  }
+  if (lane == 31) sh.warp[wid] = incl;
+  unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0ull;
+  __syncthreads();
+  {
+    unsigned long long wp = 0ull;
+    for (uint32_t k = 0; k < wid; ++k) wp = seg_combine(wp, sh.warp[k]);
+    excl = seg_combine(wp, excl);
+  }
+  if (tid == 0) {
+    unsigned long long tile_agg = 0ull;
+    for (uint32_t k = 0; k < kScanThreads / 32; ++k) tile_agg = seg_combine(tile_agg, sh.warp[k]);
+    unsigned long long acc = 0ull;
+    if (mode == 2u) {
+      st_release(&w.tile_status[t], kStAgg | tile_agg);
+      for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
+        unsigned long long s;
+        do {
+          s = ld_acquire(&w.tile_status[j]);
+        } while ((s & kStMask) == 0ull);
+        acc = seg_combine(s & ~kStMask, acc);
+        if ((s & kStMask) == kStPrefix || (acc & kFlagBit)) break;
+      }
+    } else if (mode == 1u) {
+      uint32_t cm = 0;
+      for (uint32_t k = 0; k < kScanThreads / 32; ++k) cm = max(cm, sh.cm[k]);
+      acc = kFlagBit | cm;
+    }
+    st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+    *sh.carry = acc;
+  }
+  __syncthreads();
+  const unsigned long long carry = seg_combine(*sh.carry, excl);
+
+  // ---- pass 2: clamped delays, per-request sums, edge values
+  {
+    Cursor c;
+    cursor_enter<kFinal>(c, win, q0, x0);
+    uint32_t pm = starts_here ? 0u : (uint32_t)carry;
+    uint32_t dt = 0;
+    unsigned long long sum = 0ull;
+    int32_t ev = c.live ? min(c.vend, c.ns) : c.ns;
+#pragma unroll 1
+    for (uint32_t g = 0; g < kScanItems / 4; ++g) {
+      const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
+      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      const int32_t gx = x0 + (int32_t)(4 * g);
+      int32_t rel = ev - gx;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        if (rel == jj) {
+          const int32_t x = gx + jj;
+          if (c.live && x == c.vend && x > x0 && c.ek) w.edge[c.ridx] = (c.ek == 1u) ? pm : dt;  // last valid token
+          if (x == c.ns) {
+            if (sum) atomicAdd(&w.spre[c.ridx], sum);
+            sum = 0ull;
+            cursor_next_request<kFinal>(c, win, x);
+            pm = 0;
+          } else {
+            c.live = false; c.P = 0; c.I = 0xFFFFFFFFu; c.u = 0; c.Pu = 0;
+          }
+          ev = c.live ? min(c.vend, c.ns) : c.ns;
+          rel = ev - gx;
+        }
+        pm = max(pm, max(dd[jj], c.I) - c.I);
+        c.I += c.P;
+        dt = min(pm, c.u);
+        c.u -= c.Pu;
+        sum += dt;
+      }
+    }
+    // the last valid token of the current request is this thread's last token
+    if (c.live && c.vend == x0 + kScanItems && c.ek) w.edge[c.ridx] = (c.ek == 1u) ? pm : dt;
+    // the last piece may continue into the next lanes: segmented warp reduction by request
+    uint32_t key = c.ridx;
+    unsigned long long val = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, o);
+      const unsigned long long v2 = __shfl_down_sync(0xffffffffu, val, o);
+      if (lane + o < 32 && k2 == key) val += v2;
+    }
+    const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
+    if ((lane == 0 || kprev != key) && val && key != 0xFFFFFFFFu) atomicAdd(&w.spre[key], val);
+  }
+}
+
+template <bool kFinal>
+__device__ __noinline__ void tile_body_global(const ScanArgs& A, const unsigned char* tile, unsigned long long p0,
+                                              uint32_t r0, uint32_t dummy, uint32_t wn, uint32_t t, uint32_t mode,
+                                              TileShared sh) {
+  GlobalWin win{A.w.srec, p0, r0, dummy, wn};
+  tile_body<kFinal>(A, win, tile, wn, t, mode, sh);
 }
 
 }  // namespace
@@ -379,11 +586,10 @@ template <bool kFinal>
 __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ unsigned char s_dyn_raw[];
-  // two 16 KiB tile buffers, 1024-byte aligned for the 128B swizzle
   unsigned char* s_tiles =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn_raw) + 1023) & ~uintptr_t(1023));
   __shared__ alignas(8) uint64_t s_bar[2];
-  __shared__ int32_t w_ls[kWinCap + 2], w_vend[kWinCap + 2], w_epos[kWinCap + 2];
+  __shared__ int32_t w_ls[kWinCap + 2], w_vend[kWinCap + 2];
   __shared__ uint32_t w_A[kWinCap + 2], w_U[kWinCap + 2], w_P[kWinCap + 2], w_ek[kWinCap + 2],
       w_ridx[kWinCap + 2];
   __shared__ unsigned long long s_warp[kScanThreads / 32];
@@ -400,14 +606,15 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   const unsigned long long pool_end = w.g->pool_end;
   const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
   const uint32_t n = r.n;
+  const TileShared sh{s_warp, s_cm, &s_carry};
+  const SmemWin swin{w_ls, w_vend, w_A, w_U, w_P, w_ek, w_ridx};
 
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    // claim two tiles (increasing order: any tile waited on in a look-back is already owned by
-    // a running CTA)
+    // claim two tiles (increasing order: a tile waited on in a look-back is owned by a running CTA)
     for (int b = 0; b < 2; ++b) {
       const uint32_t tt = atomicAdd(&w.g->tile_ctr, 1u);
       s_tile_id[b] = tt;
@@ -424,17 +631,15 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     if (tid == 0) {
       const uint32_t r0 = w.tile_owner[t];
       const uint32_t r_end = (t + 1 < ntiles) ? w.tile_owner[t + 1] : n - 1;
-      const unsigned long long b0 = srec[r0].base;
-      s_dummy = (b0 > p0) ? 1u : 0u;
+      const ScanRec h = srec[r0];
+      s_dummy = (h.base > p0) ? 1u : 0u;
       s_r0 = r0;
       s_wn = r_end - r0 + 1 + s_dummy;
-      // head segment (window entry 0): carry source
-      uint32_t mode = 0;  // 0: none needed, 1: direct read, 2: decoupled look-back
-      if (b0 < p0) {
-        const ScanRec h = srec[r0];
-        const unsigned long long span = p0 - b0;
+      uint32_t mode = 0;  // head-segment carry: 0 none needed, 1 direct read, 2 look-back
+      if (h.base < p0) {
+        const unsigned long long span = p0 - h.base;
         if ((unsigned long long)h.lim > span) {
-          s_hbase = b0;
+          s_hbase = h.base;
           s_hcnt = (uint32_t)span;
           s_httft = h.ttft;
           s_hP = h.P;
@@ -448,9 +653,9 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     const bool win_ok = wn <= (uint32_t)kWinCap;
     if (win_ok) {
       for (uint32_t q = tid; q <= wn; q += kScanThreads) {
-        const Entry e = entry_at(srec, p0, r0, dummy, wn, q);
+        const Entry e = make_entry(srec, p0, r0, dummy, wn, q);
         w_ls[q] = e.ls; w_vend[q] = e.vend; w_A[q] = e.A; w_U[q] = e.U; w_P[q] = e.P;
-        w_epos[q] = e.epos; w_ek[q] = e.ek; w_ridx[q] = e.ridx;
+        w_ek[q] = e.ek; w_ridx[q] = e.ridx;
       }
     }
     // direct head carry: max lat+ of the head segment's tokens before p0
@@ -466,7 +671,6 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     }
     for (int o = 16; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
     if (lane == 0) s_cm[wid] = cmax;
-    // this tile's data
     if (buf == 0) { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
     else { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
     unsigned char* tile = s_tiles + buf * (kTile * 4);
@@ -480,163 +684,8 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
       }
     }
     __syncthreads();
-
-    auto LS = [&](uint32_t q) -> int32_t { return win_ok ? w_ls[q] : ls_at(srec, p0, r0, dummy, wn, q); };
-    auto GET = [&](uint32_t q) -> Entry {
-      if (win_ok) {
-        Entry e;
-        e.ls = w_ls[q]; e.vend = w_vend[q]; e.A = w_A[q]; e.U = w_U[q]; e.P = w_P[q];
-        e.epos = w_epos[q]; e.ek = w_ek[q]; e.ridx = w_ridx[q];
-        return e;
-      }
-      return entry_at(srec, p0, r0, dummy, wn, q);
-    };
-    // owner of this thread's first token: last window entry starting at or before it
-    const uint32_t x0 = tid * kScanItems;
-    uint32_t q0;
-    {
-      uint32_t lo = 0, hi = wn - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (LS(mid) <= (int32_t)x0) lo = mid;
-        else hi = mid - 1;
-      }
-      q0 = lo;
-    }
-    const uint32_t rowb = tid << 7, rsw = tid & 7u;
-
-    // ---- pass 1: thread aggregate of the segmented max of lat+ (flag = a segment starts here)
-    unsigned long long agg;
-    {
-      uint32_t q = q0;
-      Entry e = GET(q);
-      int32_t ns = LS(q + 1);
-      uint32_t P = e.P, I = e.A + x0 * P;
-      int32_t vend = e.vend;
-      uint32_t flag = (e.ls == (int32_t)x0) ? 1u : 0u, v = 0;
-#pragma unroll 1
-      for (uint32_t g = 0; g < kScanItems / 4; ++g) {
-        const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
-        const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int32_t x = (int32_t)(x0 + 4 * g + jj);
-          if (x == ns) {
-            do {
-              ++q;
-              ns = LS(q + 1);
-            } while (ns <= x);
-            e = GET(q);
-            P = e.P;
-            I = e.A + (uint32_t)x * P;
-            vend = e.vend;
-            flag = 1u;
-            v = 0;
-          }
-          uint32_t l = max(dd[jj], I) - I;
-          l = (x < vend) ? l : 0u;
-          I += P;
-          v = max(v, l);
-        }
-      }
-      agg = (flag ? kFlagBit : 0ull) | v;
-    }
-    // ---- block-wide exclusive scan of thread aggregates (4 warps)
-    unsigned long long incl = agg;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl = seg_combine(v, incl);
-    }
-    if (lane == 31) s_warp[wid] = incl;
-    unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) excl = 0ull;
-    __syncthreads();
-    {
-      unsigned long long wp = 0ull;
-      for (uint32_t k = 0; k < wid; ++k) wp = seg_combine(wp, s_warp[k]);
-      excl = seg_combine(wp, excl);
-    }
-    if (tid == 0) {
-      unsigned long long tile_agg = 0ull;
-      for (uint32_t k = 0; k < kScanThreads / 32; ++k) tile_agg = seg_combine(tile_agg, s_warp[k]);
-      unsigned long long acc = 0ull;
-      if (mode == 2u) {
-        st_release(&w.tile_status[t], kStAgg | tile_agg);
-        for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
-          unsigned long long s;
-          do {
-            s = ld_acquire(&w.tile_status[j]);
-          } while ((s & kStMask) == 0ull);
-          acc = seg_combine(s & ~kStMask, acc);
-          if ((s & kStMask) == kStPrefix || (acc & kFlagBit)) break;
-        }
-      } else if (mode == 1u) {
-        uint32_t cm = 0;
-        for (uint32_t k = 0; k < kScanThreads / 32; ++k) cm = max(cm, s_cm[k]);
-        acc = kFlagBit | cm;
-      }
-      st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
-      s_carry = acc;
-    }
-    __syncthreads();
-    const unsigned long long carry = seg_combine(s_carry, excl);
-
-    // ---- pass 2: clamped delays, per-request partial sums, edge values
-    {
-      uint32_t q = q0;
-      Entry e = GET(q);
-      int32_t ns = LS(q + 1);
-      uint32_t P = e.P, I = e.A + x0 * P, u = e.U - x0 * P;
-      int32_t vend = e.vend, epos = e.epos;
-      uint32_t ek = e.ek, ridx = e.ridx;
-      uint32_t pm = (e.ls == (int32_t)x0) ? 0u : (uint32_t)carry;
-      unsigned long long sum = 0ull;
-#pragma unroll 1
-      for (uint32_t g = 0; g < kScanItems / 4; ++g) {
-        const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
-        const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int32_t x = (int32_t)(x0 + 4 * g + jj);
-          if (x == ns) {
-            if (sum) atomicAdd(&w.spre[ridx], sum);
-            sum = 0ull;
-            do {
-              ++q;
-              ns = LS(q + 1);
-            } while (ns <= x);
-            e = GET(q);
-            P = e.P;
-            I = e.A + (uint32_t)x * P;
-            u = e.U - (uint32_t)x * P;
-            vend = e.vend;
-            epos = e.epos;
-            ek = e.ek;
-            ridx = e.ridx;
-            pm = 0;
-          }
-          const uint32_t l = (x < vend) ? (max(dd[jj], I) - I) : 0u;
-          I += P;
-          pm = max(pm, l);
-          const uint32_t dt = kFinal ? pm : min(pm, u);
-          u -= P;
-          if (x < vend) sum += dt;
-          if (x == epos) w.edge[ridx] = (ek == 1u) ? pm : dt;
-        }
-      }
-      // the last piece may continue into the next lanes: segmented warp reduction by request
-      uint32_t key = ridx;
-      unsigned long long val = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, o);
-        const unsigned long long v2 = __shfl_down_sync(0xffffffffu, val, o);
-        if (lane + o < 32 && k2 == key) val += v2;
-      }
-      const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
-      if ((lane == 0 || kprev != key) && val && key != 0xFFFFFFFFu) atomicAdd(&w.spre[key], val);
-    }
+    if (win_ok) tile_body<kFinal>(A, swin, tile, wn, t, mode, sh);
+    else tile_body_global<kFinal>(A, tile, p0, r0, dummy, wn, t, mode, sh);
     __syncthreads();  // tile buffer and window are reused below
     // refill this buffer with a newly claimed tile (two tiles ahead)
     if (tid == 0) {
@@ -648,7 +697,6 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
         tma_tile(&tmap, s_tiles + buf * (kTile * 4), tt * (kTile / 32), &s_bar[buf]);
       }
     }
-    __syncthreads();
     t = s_tile_id[buf ^ 1u];
   }
 }
