@@ -243,11 +243,13 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.cand_g, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.srec, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &c->zero_rows, 32)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.sel, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.sel_thr, (size_t)lim->max_B)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
@@ -289,6 +291,18 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   return ANDES_OK;
 }
 
+// Internal debugging hook: %globaltimer stamps from the decision kernels (8192 slots).
+int andes_debug_trace(AndesCtx* c, int enable) {
+  if (!c) return ANDES_E_INVAL;
+  if (enable && !c->w.trace) {
+    cudaError_t e = ctx_alloc(c, &c->w.trace, 8192);
+    if (e != cudaSuccess) return cuda_check(c, e, "trace alloc");
+    cudaMemset(c->w.trace, 0, 8192 * 8);
+  }
+  if (!enable) c->w.trace = nullptr;
+  return ANDES_OK;
+}
+
 // Internal debugging hook (not part of include/andes.h): synchronous copy of a workspace array.
 int andes_debug_read(AndesCtx* c, int which, void* host, size_t bytes) {
   if (!c || !host) return ANDES_E_INVAL;
@@ -301,6 +315,7 @@ int andes_debug_read(AndesCtx* c, int which, void* host, size_t bytes) {
     case 4: src = c->w.tile_owner; break;
     case 5: src = c->w.g; break;
     case 6: src = c->w.hist_l; break;
+    case 7: src = c->w.trace; break;
     default: return ANDES_E_INVAL;
   }
   return cuda_check(c, cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost), "debug read");
@@ -430,12 +445,12 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   // bounds (S3a), [3] candidate keys (S3b), [4] Algorithm 1 per B + best B + cap + mask (S4-S6)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
-  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, p->tau_us, p->B_cap, p->cur_latency_us, p->flags);
+  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
   mark(c, 1, s);
   {
-    const CUtensorMap* tm = nullptr;
+    const CUtensorMap* tm = &c->pool_map;
     if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
-    launch_scan(L, r, w, eval, false, tm);
+    launch_scan(L, r, w, eval, false, tm, true, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
   }
   mark(c, 2, s);
   launch_state(L, r, w, p->now_us, p->horizon_us);

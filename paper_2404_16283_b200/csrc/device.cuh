@@ -110,10 +110,13 @@ struct Work {
   PackedState* st;           // [N]
   uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
   unsigned long long* cand;  // [max_B][S_cap] composite keys of the candidates per B
+  long long* cand_g;         // [max_B][S_cap] llrint(gain 2^32) of the candidates per B
   uint32_t* cand_idx;        // [S_cap] request index of candidate slot
   uint32_t* keyrow;          // [max_B][N] fallback: ordered keys of every request per B
   uint32_t* sel;             // [max_B][kMaxB] Algorithm 1 prefix per B, greedy order
+  unsigned long long* sel_thr;  // [max_B] composite of the k*-th selected request per B
   Globals* g;
+  unsigned long long* trace; // optional %globaltimer stamps (internal debugging), may be null
   uint32_t N_cap;            // row stride of keyrow
   uint32_t tiles_cap;        // capacity of tile_owner / tile_status
   uint32_t S_cap;            // candidate capacity (row stride of cand)
@@ -274,6 +277,16 @@ __device__ __forceinline__ float prio_key(double gain, uint32_t l) {
 __device__ __forceinline__ long long gain_fixed(double gain) {
   return __double2ll_rn(__dmul_rn(gain, 4294967296.0));
 }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ANDES_TRACE(w, slot)                                  \
+  do {                                                        \
+    if ((w).trace && threadIdx.x == 0) (w).trace[(slot)] = gtimer(); \
+  } while (0)
 
 // ---------------------------------------------------------------- sync primitives
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {

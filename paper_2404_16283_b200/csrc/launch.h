@@ -13,10 +13,10 @@ struct LaunchCfg {
 };
 
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug, const uint32_t* tau = nullptr, uint32_t B_cap = 0,
-                 uint32_t cur_latency = 0, uint32_t flags = 0);
+                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask = nullptr);
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 const CUtensorMap* tmap);
+                 const CUtensorMap* tmap, bool sched = false, const uint32_t* tau = nullptr, uint32_t B_cap = 0,
+                 uint64_t M = 0, uint32_t cur_latency = 0, uint32_t flags = 0);
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
 int scan_blocks_per_sm();

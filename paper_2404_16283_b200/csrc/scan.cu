@@ -29,7 +29,7 @@ constexpr int kPrepThreads = 256;
 //   over [B_lo, B_hi] used by the gain bounds.
 __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __restrict__ tau, uint32_t B_cap,
                              uint64_t M, uint32_t cur_latency, uint32_t flags) {
-  constexpr uint32_t NT = kPrepThreads, kPer = kHistL / NT;
+  constexpr uint32_t NT = kScanThreads, kPer = kHistL / NT;
   __shared__ unsigned long long s_cnt[NT], s_sum[NT];
   __shared__ uint32_t s_kM, s_Blo, s_tlo, s_thi;
   const uint32_t tid = threadIdx.x, n = r.n;
@@ -161,14 +161,12 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
   }
 }
 
-// One pass over the requests: m_i, zeroed accumulators, tile owners, and for a
-// decision the trigger inputs (sum of running l, min period), the l histogram for
-// B_max and the running list; the last CTA then runs bounds_block.
+// One pass over the requests: m_i, zeroed accumulators, scan records, tile owners, and for a
+// decision the trigger inputs (sum of running l, min period), the l histogram for B_max,
+// the running list and the status-quo serve mask (bounds_block then runs in the scan's CTA 0).
 __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
                                                       uint32_t sched, uint64_t kv_cap, uint32_t debug,
-                                                      const uint32_t* __restrict__ tau, uint32_t B_cap,
-                                                      uint32_t cur_latency, uint32_t flags) {
-  __shared__ uint32_t s_last;
+                                                      uint8_t* __restrict__ serve_mask) {
   __shared__ uint32_t s_hl[kHistL];
   __shared__ uint32_t s_minP;
   __shared__ unsigned long long s_runl;
@@ -234,6 +232,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     if (sched) {
       const uint32_t l = r.ctx_len[i];
       my_minP = min(my_minP, P);
+      serve_mask[i] = r.running[i] ? 1 : 0;  // status quo; the decision edits only the changes
       atomicAdd(&s_hl[l < kHistL - 1 ? l : kHistL - 1], 1u);
       if (r.running[i]) {
         atomicAdd(&s_runl, (unsigned long long)l);
@@ -254,13 +253,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     atomicMax(&w.g->inv_minP, 0xFFFFFFFFu - s_minP);
     if (s_runl) atomicAdd(&w.g->run_l, s_runl);
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&w.g->prep_done, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  bounds_block(r, w, tau, B_cap, kv_cap, cur_latency, flags);
 }
 
 // ---------------------------------------------------------------- K1 timeline scan
@@ -313,6 +305,12 @@ struct ScanArgs {
   ReqView r;
   Work w;
   int64_t eval_abs;
+  // decision only: S0/S2 bounds computed by CTA 0 before it joins the scan
+  uint32_t sched;
+  const uint32_t* tau;
+  uint32_t B_cap;
+  uint64_t M;
+  uint32_t cur_latency, flags;
 };
 
 // One request of a tile's window in tile-local coordinates (x = position - p0).
@@ -608,6 +606,11 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   const uint32_t n = r.n;
   const TileShared sh{s_warp, s_cm, &s_carry};
   const SmemWin swin{w_ls, w_vend, w_A, w_U, w_P, w_ek, w_ridx};
+  if (A.sched && blockIdx.x == 0) {
+    bounds_block(r, w, A.tau, A.B_cap, A.M, A.cur_latency, A.flags);
+    __syncthreads();
+  }
+  if (n == 0) return;
 
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -736,21 +739,23 @@ __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_
 
 // ---------------------------------------------------------------- host launchers
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug, const uint32_t* tau, uint32_t B_cap,
-                 uint32_t cur_latency, uint32_t flags) {
-  const uint32_t blocks = r.n ? umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8) : 1u;
+                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask) {
+  if (r.n == 0) return;
+  const uint32_t blocks = umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8);
   k_prep<<<blocks, kPrepThreads, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u, kv_cap,
-                                                debug ? 1u : 0u, tau, B_cap, cur_latency, flags);
+                                                debug ? 1u : 0u, serve_mask);
 }
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 const CUtensorMap* tmap) {
-  if (r.n == 0) return;
-  ScanArgs A{r, w, eval_abs};
+                 const CUtensorMap* tmap, bool sched, const uint32_t* tau, uint32_t B_cap, uint64_t M,
+                 uint32_t cur_latency, uint32_t flags) {
+  if (r.n == 0 && !sched) return;
+  ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags};
+  const uint32_t grid = r.n ? L.scan_grid : 1u;
   if (final_mode)
-    k_qoe_scan<true><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
+    k_qoe_scan<true><<<grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
   else
-    k_qoe_scan<false><<<L.scan_grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
+    k_qoe_scan<false><<<grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,

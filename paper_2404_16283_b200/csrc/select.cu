@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
   __shared__ uint32_t s_cut;
   if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
   const uint32_t tid = threadIdx.x;
+  if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
   const uint32_t tlo = __ldcg(&w.g->tau_lo), thi = __ldcg(&w.g->tau_hi);
   for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
     s_hlb[q] = 0u;
@@ -135,10 +136,12 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
   }
   __threadfence();
   __syncthreads();
+  if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
   if (tid == 0) s_last = (atomicAdd(&w.g->state_done, 1u) == gridDim.x - 1) ? 1u : 0u;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  ANDES_TRACE(w, 2200);
   // theta: lower edge of the highest bucket b* with #(LB in buckets >= b*) >= B_hi
   constexpr uint32_t kPer = kHistK / kStateThreads;  // 16 buckets per thread, descending
   const uint32_t need = __ldcg(&w.g->B_hi);
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
     w.g->overflow = (tot > w.S_cap) ? 1u : 0u;
     if (tot > w.S_cap) atomicOr(&w.g->slow, 2u);
   }
+  ANDES_TRACE(w, 2201);
 }
 
 // ---------------------------------------------------------------- S3b: candidates
@@ -235,7 +239,10 @@ __global__ void __launch_bounds__(kCandThreads) k_cand(ReqView r, Work w, const 
   for (unsigned long long pr = blockIdx.x * blockDim.x + tid; pr < pairs; pr += gridDim.x * blockDim.x) {
     const uint32_t j = (uint32_t)(pr / nB), b = (uint32_t)(pr - (unsigned long long)j * nB);
     const PackedState p = w.st[__ldcg(w.cand_idx + j)];
-    w.cand[(size_t)(B_lo - 1 + b) * w.S_cap + j] = comp_of(p, s_tau[b]);
+    const double gn = gain_at(unpack_state(p), s_tau[b]);
+    const size_t o = (size_t)(B_lo - 1 + b) * w.S_cap + j;
+    w.cand[o] = composite(ordered_key(prio_key(gn, p.l)), p.rank);
+    w.cand_g[o] = gain_fixed(gn);
   }
 }
 
@@ -349,9 +356,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
   __shared__ unsigned long long s_ps[kSortCap];
+  __shared__ long long s_gf[kSortCap];
   __shared__ uint32_t s_k;
   __shared__ long long s_red[32];
-  __shared__ uint32_t s_last;
 
   const ReqView& r = A.r;
   const Work& w = A.w;
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   const uint32_t n = r.n;
   const bool trig = __ldcg(&w.g->triggered) != 0;
   const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  ANDES_TRACE(w, 2 * blockIdx.x);
 
   if (!trig || B < B_lo || B > B_hi) {
     if (tid == 0) {
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
           for (uint32_t f = 0; f < ns; ++f) pos += (s_all[f] > c) ? 1u : 0u;
           if (pos < k) {
             s_key[pos] = c;
-            s_idx[pos] = __ldcg(w.cand_idx + e);
+            s_idx[pos] = e;  // candidate slot
           }
         }
         __syncthreads();
@@ -400,8 +408,17 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       } else {
         cnt = select_top_k(
             ns, k, [&](uint32_t e, bool) -> unsigned long long { return __ldcg(row + e); },
-            [&](uint32_t e) { return __ldcg(w.cand_idx + e); }, s_key, s_idx);
+            [&](uint32_t e) { return e; }, s_key, s_idx);
       }
+      // slots -> request indices; the objective of a slot is its stored gfix
+      for (uint32_t q = tid; q < cnt; q += kSelThreads) {
+        const uint32_t e = s_idx[q];
+        s_ps[q] = (unsigned long long)__ldcg(w.cand_g + (size_t)(B - 1) * w.S_cap + e);  // temp: gfix
+        s_idx[q] = __ldcg(w.cand_idx + e);
+      }
+      __syncthreads();
+      for (uint32_t q = tid; q < cnt; q += kSelThreads) s_gf[q] = (long long)s_ps[q];
+      __syncthreads();
     }
     // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
     // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
@@ -428,55 +445,78 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     __syncthreads();
     const uint32_t kstar = s_k;
     long long v = 0;
+    const bool ovf = __ldcg(&w.g->overflow) != 0;
     for (uint32_t q = tid; q < kstar; q += kSelThreads) {
       const uint32_t i = s_idx[q];
-      v += gain_fixed(gain_at(unpack_state(w.st[i]), tB));
+      v += ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
       w.sel[(size_t)(B - 1) * kMaxB + q] = i;
     }
     v = block_sum_ll<kSelThreads>(v, s_red);
     if (tid == 0) {
       A.o.V[B - 1] = v;
       A.o.kstar[B - 1] = kstar;
+      w.sel_thr[B - 1] = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite: membership test
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&w.g->done, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    finalize_decision(A, s_key, s_idx);
+  ANDES_TRACE(w, 2 * blockIdx.x + 1);
+}
+
+// In-place inclusive prefix sums of v[0..cnt) (cnt <= 8 * kSelThreads) by the whole CTA.
+__device__ void block_inclusive_scan(unsigned long long* v, uint32_t cnt, unsigned long long* s_tmp) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (cnt + kSelThreads - 1) / kSelThreads;
+  const uint32_t lo = min(cnt, tid * per), hi = min(cnt, lo + per);
+  unsigned long long part = 0;
+  for (uint32_t q = lo; q < hi; ++q) part += v[q];
+  unsigned long long inc = part;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += x;
   }
+  if (lane == 31) s_tmp[wid] = inc;
+  __syncthreads();
+  unsigned long long wpre = 0;
+  for (uint32_t k = 0; k < wid; ++k) wpre += s_tmp[k];
+  unsigned long long run = wpre + inc - part;
+  for (uint32_t q = lo; q < hi; ++q) {
+    run += v[q];
+    v[q] = run;
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- S5 + S6 + outputs (one CTA)
+// serve_mask already holds the running set (written by prep); the decision edits only the
+// admitted and the preempted entries.
 __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key, uint32_t* s_idx) {
-  __shared__ uint32_t s_Bstar, s_kstar, s_nv;
-  __shared__ uint32_t s_sel[kSortCap];
-  __shared__ unsigned long long s_selk[kSortCap];
+  __shared__ uint32_t s_Bstar, s_kstar, s_nv, s_na;
+  __shared__ unsigned long long s_thr, s_W0;
+  __shared__ long long s_bv[kSelThreads / 32];
+  __shared__ uint32_t s_bb[kSelThreads / 32];
+  __shared__ unsigned long long s_tmp[kSelThreads / 32];
+  __shared__ uint32_t s_adm[kSortCap];
+  __shared__ unsigned long long s_acum[kSortCap];
+  __shared__ uint32_t s_aflag[kSortCap];
+  unsigned long long* s_vcum = reinterpret_cast<unsigned long long*>(s_idx + kVictCap);  // [kVictCap]
   const ReqView& r = A.r;
   const Work& w = A.w;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t n = r.n;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t* sc = A.o.scalars;
+  ANDES_TRACE(w, 2100);
   const bool trig = __ldcg(&w.g->triggered) != 0;
   const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
   const uint32_t n_run_all = __ldcg(&w.g->n_run);
   const uint32_t n_run = min(n_run_all, (uint32_t)kMaxRunning);
   if (n_run_all > (uint32_t)kMaxRunning && tid == 0) atomicOr(&w.g->err, kErrRunning);
   if (!trig) {
-    for (uint32_t i = tid; i < n; i += kSelThreads) A.o.serve_mask[i] = r.running[i] ? 1 : 0;
     if (tid == 0) {
       for (int q = 0; q < 8; ++q) sc[q] = 0u;
       sc[1] = n_run_all;
     }
     return;
   }
+  // S5: largest V over candidate B, ties to the larger B (reading R13)
   {
-    // S5: largest V over candidate B, ties to the larger B (reading R13).  Parallel
-    // arg-max on (V, B) pairs compared lexicographically.
-    __shared__ long long s_bv[kSelThreads / 32];
-    __shared__ uint32_t s_bb[kSelThreads / 32];
     long long bv = (long long)0x8000000000000000ull;
     uint32_t bb = 0;
     for (uint32_t B = B_lo + tid; B <= B_hi; B += kSelThreads) {
@@ -494,9 +534,9 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
         bb = b2;
       }
     }
-    if ((tid & 31) == 0) {
-      s_bv[tid >> 5] = bv;
-      s_bb[tid >> 5] = bb;
+    if (lane == 0) {
+      s_bv[wid] = bv;
+      s_bb[wid] = bb;
     }
     __syncthreads();
     if (tid == 0) {
@@ -509,127 +549,113 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
         }
       s_Bstar = bb;
       s_kstar = bb ? __ldcg(A.o.kstar + (bb - 1)) : 0u;
+      s_thr = bb ? __ldcg(w.sel_thr + (bb - 1)) : ~0ull;
       s_nv = 0;
+      s_W0 = 0;
     }
+    __syncthreads();
   }
-  // zero the serve mask (the non-cap result is exactly S_{B*})
-  for (uint32_t i = tid; i < n; i += kSelThreads) A.o.serve_mask[i] = 0;
-  __syncthreads();
+  ANDES_TRACE(w, 2101);
   const uint32_t Bs = s_Bstar, ks = s_kstar;
+  const unsigned long long thr = s_thr;
   const uint32_t tB = Bs ? A.tau[Bs - 1] : 0u;
-  // S_{B*} in greedy order, staged in shared memory with its l and running flags
-  __shared__ uint32_t s_gsel[kSortCap], s_gl[kSortCap];
-  __shared__ uint8_t s_grun[kSortCap];
-  for (uint32_t q = tid; q < ks; q += kSelThreads) {
-    const uint32_t i = __ldcg(w.sel + (size_t)(Bs - 1) * kMaxB + q);
-    s_gsel[q] = i;
-    s_gl[q] = r.ctx_len[i];
-    s_grun[q] = r.running[i];
-  }
-  __syncthreads();
-  const uint32_t* sel = s_gsel;
-  // sorted copy of S_{B*} (by request index) for membership tests
-  uint32_t size = 1;
-  while (size < ks) size <<= 1;
-  for (uint32_t q = tid; q < size; q += kSelThreads) {
-    s_selk[q] = (q < ks) ? (unsigned long long)sel[q] : ~0ull;
-    s_sel[q] = 0;
-  }
-  __syncthreads();
-  bitonic_sort<kSelThreads>(s_selk, s_sel, size, false);
-  auto in_S = [&](uint32_t i) -> bool {
-    uint32_t lo = 0, hi = ks;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (s_selk[mid] < i) lo = mid + 1;
-      else hi = mid;
-    }
-    return lo < ks && s_selk[lo] == i;
-  };
-  // victims R \ S_{B*} with their exact composite key at B*, sorted by (key asc, rank desc)
-  for (uint32_t q = tid; q < n_run; q += kSelThreads) {
-    const uint32_t i = w.run_list[q];
-    if (!in_S(i)) {
-      const uint32_t slot = atomicAdd(&s_nv, 1u);
-      s_key[slot] = ~comp_of(w.st[i], tB);  // descending of ~ = ascending of the composite
-      s_idx[slot] = i;
-    }
-  }
-  // total l of the running set (for the cap)
-  __shared__ unsigned long long s_W0;
-  if (tid == 0) s_W0 = 0;
-  __syncthreads();
+  // victims R \ S_{B*}: running requests whose composite at B* is below the k*-th selected
+  // composite (composites are unique), keyed for the (key asc, rank desc) order
   {
     unsigned long long wl = 0;
-    for (uint32_t q = tid; q < n_run; q += kSelThreads) wl += r.ctx_len[w.run_list[q]];
+    for (uint32_t q = tid; q < n_run; q += kSelThreads) {
+      const uint32_t i = w.run_list[q];
+      wl += r.ctx_len[i];
+      const unsigned long long c = Bs ? comp_of(w.st[i], tB) : 0ull;
+      if (ks == 0 || c < thr) {
+        const uint32_t slot = atomicAdd(&s_nv, 1u);
+        s_key[slot] = ~c;  // descending of ~ = ascending of the composite
+        s_idx[slot] = i;
+      }
+    }
     for (int o = 16; o; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
-    if ((tid & 31) == 0 && wl) atomicAdd(&s_W0, wl);
+    if (lane == 0 && wl) atomicAdd(&s_W0, wl);
+  }
+  // admits S \ R in greedy order: ordered compaction of S_{B*}
+  const uint32_t* selg = w.sel + (size_t)(Bs ? Bs - 1 : 0) * kMaxB;
+  for (uint32_t q = tid; q < ks; q += kSelThreads) {
+    const uint32_t i = __ldcg(selg + q);
+    s_adm[q] = i;
+    s_acum[q] = r.running[i] ? 0ull : 1ull;
   }
   __syncthreads();
   const uint32_t nv = s_nv;
-  size = 1;
+  uint32_t size = 1;
   while (size < nv) size <<= 1;
   for (uint32_t q = nv + tid; q < size; q += kSelThreads) {
     s_key[q] = 0ull;
     s_idx[q] = 0xFFFFFFFFu;
   }
+  block_inclusive_scan(s_acum, ks, s_tmp);
+  for (uint32_t q = tid; q < ks; q += kSelThreads)
+    if (s_acum[q] != (q ? s_acum[q - 1] : 0ull)) s_aflag[s_acum[q] - 1] = s_adm[q];
+  if (tid == 0) s_na = ks ? (uint32_t)s_acum[ks - 1] : 0u;
   __syncthreads();
+  const uint32_t na = s_na;  // s_aflag[0..na) = admits in greedy order
   bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
+  ANDES_TRACE(w, 2102);
   const uint32_t cap = A.preempt_cap;
   const bool cap_hit = !(cap == 0xFFFFFFFFu || nv <= cap);
+  uint32_t n_pre, n_adm, flags = 1u, realized;
   if (!cap_hit) {
-    for (uint32_t q = tid; q < ks; q += kSelThreads) A.o.serve_mask[sel[q]] = 1;
-    for (uint32_t q = tid; q < nv; q += kSelThreads) A.o.preempt_idx[q] = s_idx[q];
+    n_pre = nv;
+    n_adm = na;
+    realized = ks;
   } else {
-    for (uint32_t q = tid; q < n_run; q += kSelThreads) A.o.serve_mask[w.run_list[q]] = 1;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // S6 preemption cap (reading R18), sequential over <= B* admits and nv victims
-    uint32_t flags = 1u;
-    uint32_t n_adm = 0, n_pre = 0, realized = 0;
-    if (!cap_hit) {
-      for (uint32_t q = 0; q < ks; ++q)
-        if (!s_grun[q]) A.o.admit_idx[n_adm++] = sel[q];
-      n_pre = nv;
-      realized = ks;
+    flags |= 2u;
+    // W0 after preempting the first cap victims; memory beats the cap (reading R18 step 5)
+    for (uint32_t q = tid; q < nv; q += kSelThreads) s_vcum[q] = r.ctx_len[s_idx[q]];
+    __syncthreads();
+    block_inclusive_scan(s_vcum, nv, s_tmp);
+    const unsigned long long W0 = s_W0 - (cap ? s_vcum[cap - 1] : 0ull);
+    const uint32_t c0 = n_run - cap;
+    if (W0 > A.M) {
+      flags |= 4u;
+      // smallest e >= 1 with s_W0 - vcum[cap + e - 1] <= M
+      __shared__ uint32_t s_e;
+      if (tid == 0) s_e = nv;
+      __syncthreads();
+      for (uint32_t q = cap + tid; q < nv; q += kSelThreads)
+        if (s_W0 - s_vcum[q] <= A.M) atomicMin(&s_e, q + 1);
+      __syncthreads();
+      n_pre = s_e;
+      n_adm = 0;
+      realized = n_run - n_pre;
     } else {
-      flags |= 2u;
-      unsigned long long W0 = s_W0;
-      uint32_t c0 = n_run;
-      for (uint32_t q = 0; q < cap; ++q) {
-        const uint32_t i = s_idx[q];
-        A.o.serve_mask[i] = 0;
-        A.o.preempt_idx[n_pre++] = i;
-        W0 -= r.ctx_len[i];
-        --c0;
-      }
-      if (W0 > A.M) {
-        flags |= 4u;  // memory beats the cap
-        for (uint32_t q = cap; q < nv && W0 > A.M; ++q) {
-          const uint32_t i = s_idx[q];
-          A.o.serve_mask[i] = 0;
-          A.o.preempt_idx[n_pre++] = i;
-          W0 -= r.ctx_len[i];
-          --c0;
-        }
-      } else {
-        for (uint32_t q = 0; q < ks; ++q) {
-          const uint32_t i = sel[q];
-          if (s_grun[q]) continue;
-          const uint32_t l = s_gl[q];
-          if (W0 + l <= A.M && c0 + 1 <= Bs) {
-            A.o.serve_mask[i] = 1;
-            A.o.admit_idx[n_adm++] = i;
-            W0 += l;
-            ++c0;
-          } else {
-            break;
-          }
-        }
-      }
-      realized = c0;
+      // admit in greedy order while W0 + l <= M and c0 + 1 <= B*, break at the first misfit
+      for (uint32_t q = tid; q < na; q += kSelThreads) s_acum[q] = r.ctx_len[s_aflag[q]];
+      __syncthreads();
+      block_inclusive_scan(s_acum, na, s_tmp);
+      __shared__ uint32_t s_a;
+      if (tid == 0) s_a = 0;
+      __syncthreads();
+      uint32_t mine = 0;
+      for (uint32_t q = tid; q < na; q += kSelThreads)
+        mine += (W0 + s_acum[q] <= A.M && c0 + q + 1 <= Bs) ? 1u : 0u;
+      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      if (lane == 0 && mine) atomicAdd(&s_a, mine);
+      __syncthreads();
+      n_pre = cap;
+      n_adm = s_a;
+      realized = c0 + n_adm;
     }
+  }
+  for (uint32_t q = tid; q < n_pre; q += kSelThreads) {
+    const uint32_t i = s_idx[q];
+    A.o.preempt_idx[q] = i;
+    A.o.serve_mask[i] = 0;
+  }
+  for (uint32_t q = tid; q < n_adm; q += kSelThreads) {
+    const uint32_t i = s_aflag[q];
+    A.o.admit_idx[q] = i;
+    A.o.serve_mask[i] = 1;
+  }
+  if (tid == 0) {
     if (__ldcg(&w.g->slow)) flags |= 8u;
     if (__ldcg(&w.g->err) & kErrRunning) flags |= 16u;
     sc[0] = Bs;
@@ -641,6 +667,14 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
     sc[6] = flags;
     sc[7] = ks;
   }
+  ANDES_TRACE(w, 2105);
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_finalize(SelectArgs A) {
+  extern __shared__ unsigned char s_dyn[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
+  finalize_decision(A, s_key, s_idx);
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -665,15 +699,18 @@ void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint
 }
 
 static size_t select_smem() { return (sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
+static size_t finalize_smem() { return (2 * sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
 
 void init_kernels() {
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
+  cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)finalize_smem());
 }
 
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
   SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o};
   k_select<<<B_cap, kSelThreads, select_smem(), L.stream>>>(A);
+  k_finalize<<<1, kSelThreads, finalize_smem(), L.stream>>>(A);
 }
 
 }  // namespace andes
