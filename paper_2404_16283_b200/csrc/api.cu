@@ -237,7 +237,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   w.tiles_cap = c->tiles_cap;
   w.S_cap = N < kCandCap ? N : kCandCap;
   if ((e = ctx_alloc(c, &w.m, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre, N)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.edge, N)) != cudaSuccess || (e = ctx_alloc(c, &w.tile_owner, c->tiles_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.edge, N)) != cudaSuccess || (e = ctx_alloc(c, &w.tile_meta, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.tile_status, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess || (e = ctx_alloc(c, &w.hist_lb, kHistK)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
@@ -295,9 +295,9 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
 int andes_debug_trace(AndesCtx* c, int enable) {
   if (!c) return ANDES_E_INVAL;
   if (enable && !c->w.trace) {
-    cudaError_t e = ctx_alloc(c, &c->w.trace, 8192);
+    cudaError_t e = ctx_alloc(c, &c->w.trace, 1 << 16);
     if (e != cudaSuccess) return cuda_check(c, e, "trace alloc");
-    cudaMemset(c->w.trace, 0, 8192 * 8);
+    cudaMemset(c->w.trace, 0, (1 << 16) * 8);
   }
   if (!enable) c->w.trace = nullptr;
   return ANDES_OK;
@@ -312,7 +312,7 @@ int andes_debug_read(AndesCtx* c, int which, void* host, size_t bytes) {
     case 1: src = c->w.spre; break;
     case 2: src = c->w.edge; break;
     case 3: src = c->w.m; break;
-    case 4: src = c->w.tile_owner; break;
+    case 4: src = c->w.tile_meta; break;
     case 5: src = c->w.g; break;
     case 6: src = c->w.hist_l; break;
     case 7: src = c->w.trace; break;

@@ -14,12 +14,15 @@
 namespace andes {
 
 // ---------------------------------------------------------------- constants
-constexpr int kScanThreads = 128;
-constexpr int kScanItems = 32;                    // one 128-byte row of the pool per thread
-constexpr int kTile = kScanThreads * kScanItems;  // tokens per scan tile (16 KiB, one TMA box)
-constexpr int kWinCap = 256;                      // requests staged per tile (window)
-constexpr int kCarryDirect = kTile;               // head segments up to this long: carry read directly
-constexpr int kScanDynSmem = 2 * kTile * 4 + 1024;  // double-buffered tiles + 1 KiB alignment slack
+constexpr int kScanThreads = 128;                 // 4 independent warps per CTA
+constexpr int kScanItems = 32;                    // one 128-byte row of the pool per lane
+constexpr int kWTile = 32 * kScanItems;           // tokens per warp-tile (4 KiB, one TMA box)
+constexpr int kTile = kWTile;                     // tiling unit of tile_meta / tile_status
+constexpr int kWWinCap = 32;                      // window entries (+ sentinel) per warp
+constexpr int kOvfCap = 128;                      // the CTA's shared overflow window (dense tiles)
+constexpr int kCarryDirect = 4096;                // head segments up to this long: carry read directly
+constexpr int kWarpSmem = 2 * kWTile * 4 + kWWinCap * 32;  // 2 tiles + records (1 KiB multiple)
+constexpr int kScanDynSmem = (kScanThreads / 32) * kWarpSmem + kOvfCap * 32 + 1024;  // + align slack
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;
@@ -52,6 +55,16 @@ struct ReqView {
   const uint64_t* __restrict__ tl_base;
   const uint32_t* __restrict__ tl_pool;
   uint64_t tl_len;  // readable elements at tl_pool
+};
+
+// Per-tile descriptor of the timeline scan (written by prep): the request owning the tile's
+// first position and the source of its head-segment carry.
+struct alignas(16) TileMeta {
+  unsigned long long hbase;  // tl_base of r0
+  uint32_t r0;               // last request with tl_base <= tile start
+  uint32_t flags;            // bit 0: gap before r0 (dummy window entry); bits 1-2: carry mode
+  uint32_t hcnt;             // tokens of r0 before the tile (direct carry)
+  uint32_t httft, hP, pad;
 };
 
 // Per-request record of the timeline scan (written by prep).
@@ -100,7 +113,7 @@ struct Work {
   uint32_t* m;               // [N] tokens due at the evaluation time
   unsigned long long* spre;  // [N] sum of clamped delays of delivered due tokens
   uint32_t* edge;            // [N] delta_g (g < m) or delta~_m (g >= m)
-  uint32_t* tile_owner;      // [tiles] last request with tl_base <= tile start
+  TileMeta* tile_meta;       // [tiles] per-tile descriptor
   unsigned long long* tile_status;  // [tiles]
   uint32_t* hist_l;          // [kHistL] histogram of min(l, kHistL-1) (self-cleaning)
   uint32_t* hist_lb;         // [kHistK] histogram of lower-bound keys (self-cleaning)

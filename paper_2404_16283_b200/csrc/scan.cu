@@ -22,6 +22,8 @@ namespace andes {
 // ---------------------------------------------------------------- prep (+ S0/S2 in the last CTA)
 constexpr int kPrepThreads = 256;
 
+__device__ __forceinline__ void bounds_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kScanThreads) : "memory"); }
+
 // S0 selective triggering (reading R15) and S2 batch-size range (P:L545-551,
 // reading R16), run by the last prep CTA once every request has been counted:
 //   B_max = number of shortest contexts that fit in M (exact l histogram, overflow slow path),
@@ -59,14 +61,14 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
     s_tlo = 0xFFFFFFFFu;
     s_thi = 0;
   }
-  __syncthreads();
+  bounds_sync();
   for (uint32_t off = 1; off < NT; off <<= 1) {
     unsigned long long a = 0, b2 = 0;
     if (tid >= off) { a = s_cnt[tid - off]; b2 = s_sum[tid - off]; }
-    __syncthreads();
+    bounds_sync();
     s_cnt[tid] += a;
     s_sum[tid] += b2;
-    __syncthreads();
+    bounds_sync();
   }
   {
     const unsigned long long c_ex = tid ? s_cnt[tid - 1] : 0ull;
@@ -88,7 +90,7 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
       s_kM = ovf && !stop && k < need ? 0xFFFFFFFEu : (uint32_t)min(k, (unsigned long long)need);
     }
   }
-  __syncthreads();
+  bounds_sync();
   uint32_t kM = s_kM == 0xFFFFFFFFu ? 0u : s_kM;
   if (kM == 0xFFFFFFFEu) {
     // Slow path: the shortest contexts reach the overflow bucket (l >= kHistL - 1); take
@@ -112,15 +114,15 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
       }
       for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
       if ((tid & 31) == 0) s_red[tid >> 5] = best;
-      __syncthreads();
+      bounds_sync();
       if (tid == 0) {
         unsigned long long b2 = ~0ull;
         for (uint32_t q = 0; q < NT / 32; ++q) b2 = min(b2, s_red[q]);
         s_best = b2;
       }
-      __syncthreads();
+      bounds_sync();
       const unsigned long long b2 = s_best;
-      __syncthreads();
+      bounds_sync();
       if (b2 == ~0ull || W + (b2 >> 32) > M) break;
       W += b2 >> 32;
       ++k;
@@ -138,7 +140,7 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
       if (tau[B - 1] <= minP) best = max(best, B);
     atomicMax(&s_Blo, best);
   }
-  __syncthreads();
+  bounds_sync();
   const uint32_t B_lo = (B_hi == 0) ? 1u : min(s_Blo, B_hi);
   {
     uint32_t lo = 0xFFFFFFFFu, hi = 0;
@@ -151,7 +153,7 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
   }
   // self-clean the l histogram for the next call
   for (uint32_t b = tid; b < kHistL; b += NT) w.hist_l[b] = 0u;
-  __syncthreads();
+  bounds_sync();
   if (tid == 0) {
     w.g->B_hi = B_hi;
     w.g->B_lo = B_lo;
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
   uint32_t local_err = 0;
+  if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x);
   if (sched) {
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
     if (threadIdx.x == 0) {
@@ -208,20 +211,42 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     // tile ownership: tiles whose start position p satisfies base_i <= p < base_{i+1}
     const unsigned long long base = r.tl_base[i];
     const unsigned long long next = (i + 1 < n) ? r.tl_base[i + 1] : base + g;
-    const uint32_t t_lo = (i == 0) ? 0u : (uint32_t)((base + kTile - 1) / kTile);
-    uint32_t t_hi = (uint32_t)((next + kTile - 1) / kTile);
+    const uint32_t t_lo = (i == 0) ? 0u : (uint32_t)((base + kWTile - 1) / kWTile);
+    uint32_t t_hi = (uint32_t)((next + kWTile - 1) / kWTile);
     if (t_hi > w.tiles_cap) {  // pool span above limits.max_tokens: refuse (flagged), never overrun
       t_hi = w.tiles_cap;
       local_err |= kErrTokens;
     }
-    for (uint32_t t = t_lo; t < t_hi; ++t) w.tile_owner[t] = i;
+    for (uint32_t t = t_lo; t < t_hi; ++t) {
+      // descriptor of tile t (its start position p0 lies in [base_i, base_{i+1})): first request,
+      // gap flag, and the head segment's carry source (0 none, 1 direct, 2 look-back)
+      const unsigned long long p0 = (unsigned long long)t * kWTile;
+      TileMeta tm;
+      tm.hbase = base;
+      tm.r0 = i;
+      uint32_t mode = 0, hcnt = 0;
+      if (base < p0) {
+        const unsigned long long span = p0 - base;
+        const uint32_t lim = final_mode ? g : min(g, m);
+        if ((unsigned long long)lim > span) {
+          hcnt = (uint32_t)span;
+          mode = (span <= (unsigned long long)kCarryDirect) ? 1u : 2u;
+        }
+      }
+      tm.flags = (base > p0 ? 1u : 0u) | (mode << 1);
+      tm.hcnt = hcnt;
+      tm.httft = r.ttft[i];
+      tm.hP = P;
+      tm.pad = 0;
+      w.tile_meta[t] = tm;
+    }
     if (i + 1 == n) {
-      unsigned long long pe = min(base + g, (unsigned long long)w.tiles_cap * kTile);
+      unsigned long long pe = min(base + g, (unsigned long long)w.tiles_cap * kWTile);
       if (pe > r.tl_len) {  // pool shorter than the spans it claims: refuse (flagged), never overread
         pe = r.tl_len;
         local_err |= kErrTokens;
       }
-      w.g->ntiles = (uint32_t)((pe + kTile - 1) / kTile);
+      w.g->ntiles = (uint32_t)((pe + kWTile - 1) / kWTile);
       w.g->pool_end = pe;
     }
     if (debug) {
@@ -253,6 +278,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     atomicMax(&w.g->inv_minP, 0xFFFFFFFFu - s_minP);
     if (s_runl) atomicAdd(&w.g->run_l, s_runl);
   }
+  if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x + 1);
 }
 
 // ---------------------------------------------------------------- K1 timeline scan
@@ -279,13 +305,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// TMA: one [128 rows x 32 u32] box of the pool, 128-byte swizzled, completion on bar
+// TMA: one [32 rows x 32 u32] box of the pool (one warp-tile), 128-byte swizzled
 __device__ __forceinline__ void tma_tile(const CUtensorMap* tmap, void* dst, uint32_t row0, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
           "r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(row0), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
 // segmented max monoid on (flag, value): combine(a, b) with a earlier than b
@@ -295,7 +326,7 @@ __device__ __forceinline__ unsigned long long seg_combine(unsigned long long a, 
   return (a & kFlagBit) | v;
 }
 
-// byte offset of tile-local token x in a 128B-swizzled [128 x 32] u32 tile
+// byte offset of tile-local token x in a 128B-swizzled [rows x 32] u32 tile
 __device__ __forceinline__ uint32_t swz(uint32_t x) {
   const uint32_t row = x >> 5, chunk = (x >> 2) & 7u;
   return (row << 7) | ((chunk ^ (row & 7u)) << 4) | ((x & 3u) << 2);
@@ -315,116 +346,101 @@ struct ScanArgs {
 
 // One request of a tile's window in tile-local coordinates (x = position - p0).
 struct Entry {
-  int32_t ls;     // local start (base - p0), clamped to [-1, kTile + 1]
-  int32_t vend;   // local end of the valid tokens (base + lim - p0), clamped to [-1, kTile]
+  int32_t ls;     // local start (base - p0), clamped to [-1, kWTile + 1]
+  int32_t vend;   // local end of the valid tokens (base + lim - p0), clamped to [-1, kWTile]
   uint32_t A;     // ideal time of local position 0: ttft + (p0 - base) P (mod 2^32); I(x) = A + x P
-  uint32_t U;     // t_rel - A (mod 2^32): t - I(x) = U - x P
+  uint32_t trel;  // t - arrival: clamp of the consumption times (R3)
   uint32_t P;
-  uint32_t ek;    // edge kind: 1 = delta_g (g < m, unclamped), 2 = delta~_m
+  uint32_t ek;    // edge kind (1 = delta_g, 2 = delta~_m) when the last valid token is in this tile, else 0
   uint32_t ridx;  // request index (0xFFFFFFFF: dummy / sentinel)
+  uint32_t pad;
 };
+static_assert(sizeof(Entry) == 32, "Entry is two 16-byte shared-memory vectors");
 
-__device__ __forceinline__ Entry make_entry(const ScanRec* __restrict__ srec, unsigned long long p0, uint32_t r0,
-                                            uint32_t dummy, uint32_t wn, uint32_t q) {
+__device__ __forceinline__ Entry entry_of(const ScanRec& s, uint32_t ri, unsigned long long p0) {
   Entry e;
-  if ((dummy && q == 0) || q >= wn) {
-    e.ls = (q >= wn) ? kTile + 1 : -1;
-    e.vend = -1;
-    e.A = 0; e.U = 0; e.P = 0; e.ek = 0; e.ridx = 0xFFFFFFFFu;
-    return e;
-  }
-  const uint32_t ri = r0 + q - dummy;
-  const ScanRec s = srec[ri];
   const long long ls = (long long)s.base - (long long)p0;
   const long long ve = ls + (long long)s.lim;
-  e.ls = (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
-  e.vend = (int32_t)max(-1ll, min(ve, (long long)kTile));
+  e.ls = (int32_t)max(-1ll, min(ls, (long long)kWTile + 1));
+  e.vend = (int32_t)max(-1ll, min(ve, (long long)kWTile));
   e.A = s.ttft + (uint32_t)(unsigned long long)(-ls) * s.P;
-  e.U = s.trel - e.A;
+  e.trel = s.trel;
+  e.pad = 0;
   e.P = s.P;
-  // the edge token (last valid token) is written only by the tile that contains it
-  e.ek = (ve >= 1 && ve <= (long long)kTile) ? s.ek : 0u;
+  e.ek = (ve >= 1 && ve <= (long long)kWTile) ? s.ek : 0u;
   e.ridx = ri;
   return e;
 }
 
-// Window accessors: shared-memory window (hot path) or straight from the scan records when
-// the tile overlaps more than kWinCap requests (slow path, separate instantiation).
-struct SmemWin {
-  const int32_t *ls, *vend;
-  const uint32_t *A, *U, *P, *ek, *ridx;
-  __device__ __forceinline__ int32_t start(uint32_t q) const { return ls[q]; }
-  __device__ __forceinline__ Entry get(uint32_t q) const {
-    Entry e;
-    e.ls = ls[q]; e.vend = vend[q]; e.A = A[q]; e.U = U[q]; e.P = P[q]; e.ek = ek[q]; e.ridx = ridx[q];
-    return e;
-  }
-};
-struct GlobalWin {
-  const ScanRec* srec;
+__device__ __forceinline__ Entry null_entry(bool sentinel) {
+  Entry e;
+  e.ls = sentinel ? kWTile + 1 : -1;
+  e.vend = -1;
+  e.A = 0; e.trel = 0; e.P = 0; e.ek = 0; e.ridx = 0xFFFFFFFFu; e.pad = 0;
+  return e;
+}
+
+// Window = requests r0 .. r0+wn-1-dummy overlapping the tile (entry 0 is a dummy when a gap
+// precedes r0), from their raw scan records (warp-staged in shared memory, or global memory
+// when the tile overlaps more than kWWinCap requests).
+struct RawWin {
+  const ScanRec* rec;
   unsigned long long p0;
   uint32_t r0, dummy, wn;
   __device__ __forceinline__ int32_t start(uint32_t q) const {
-    if (q >= wn) return kTile + 1;
+    if (q >= wn) return kWTile + 1;
     if (dummy && q == 0) return -1;
-    const long long ls = (long long)srec[r0 + q - dummy].base - (long long)p0;
-    return (int32_t)max(-1ll, min(ls, (long long)kTile + 1));
+    const long long ls = (long long)rec[q - dummy].base - (long long)p0;
+    return (int32_t)max(-1ll, min(ls, (long long)kWTile + 1));
   }
-  __device__ __forceinline__ Entry get(uint32_t q) const { return make_entry(srec, p0, r0, dummy, wn, q); }
-};
-
-struct TileShared {
-  unsigned long long* warp;  // [kScanThreads / 32]
-  uint32_t* cm;              // [kScanThreads / 32]
-  unsigned long long* carry;
-};
-
-// Per-thread cursor over the window: the current request q, the next event position ev
-// (end of q's valid tokens, or the start of the next request), and the arithmetic state of
-// the valid ("live") or invalid ("null": lat = 0, delta~ = 0) range.
-struct Cursor {
-  uint32_t q;
-  int32_t vend, ns;
-  uint32_t P, I, u, Pu;
-  uint32_t ek, ridx;
-  bool live;
-};
-
-template <bool kFinal, class Win>
-__device__ __forceinline__ void cursor_enter(Cursor& c, const Win& win, uint32_t q, int32_t x) {
-  // enter request q at local position x (q's first position in this thread, or x0)
-  const Entry e = win.get(q);
-  c.q = q;
-  c.vend = e.vend;
-  c.ns = win.start(q + 1);
-  c.ek = e.ek;
-  c.ridx = e.ridx;
-  c.live = x < e.vend;
-  if (c.live) {
-    c.P = e.P;
-    c.I = e.A + (uint32_t)x * e.P;
-    c.u = kFinal ? 0xFFFFFFFFu : e.U - (uint32_t)x * e.P;
-    c.Pu = kFinal ? 0u : e.P;
-  } else {
-    c.P = 0; c.I = 0xFFFFFFFFu; c.u = 0; c.Pu = 0;
+  __device__ __forceinline__ Entry get(uint32_t q) const {
+    if (q >= wn || (dummy && q == 0)) return null_entry(q >= wn);
+    return entry_of(rec[q - dummy], r0 + q - dummy, p0);
   }
-}
+  // (unused helper kept for the global path)
+  // owner of position x given start(q + 1) <= x: the last q' > q with start(q') <= x.  Runs of
+  // empty requests (no tokens yet) share one start; binary search keeps them O(log) per event.
+  __device__ __forceinline__ uint32_t advance(uint32_t q, int32_t x) const {
+    uint32_t lo = q + 1;
+    if (start(lo + 1) > x) return lo;
+    uint32_t hi = wn - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (start(mid) <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+};
+
+// One warp-tile: 32 lanes x 32 tokens.  Tokens of request q at local position x have ideal
+// time I(x) = e.A + x P; the actual consumption time follows A_x = max(d_x, A_{x-1} + P)
+// (reading R2) and is clamped at t (R3).  Pass 1 builds the segmented max of lat+ (the carry
+// monoid), pass 2 sums T~ per piece and subtracts the closed-form sum of I.
+// Window of precomputed tile-local entries in the warp's shared memory: entries 0..wn-1
+// (entry 0 the dummy when a gap precedes r0) and a sentinel at wn (start kWTile + 1).
+struct EntWin {
+  uint32_t base;  // shared address of entry 0
+  __device__ __forceinline__ int32_t start(uint32_t q) const {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(base + q * 32u));
+    return v;
+  }
+  __device__ __forceinline__ Entry get(uint32_t q) const {
+    const uint4 a = ld_shared_v4(base + q * 32u), b = ld_shared_v4(base + q * 32u + 16u);
+    Entry e;
+    e.ls = (int32_t)a.x; e.vend = (int32_t)a.y; e.A = a.z; e.trel = a.w;
+    e.P = b.x; e.ek = b.y; e.ridx = b.z; e.pad = b.w;
+    return e;
+  }
+};
 
 template <bool kFinal, class Win>
-__device__ __forceinline__ void cursor_next_request(Cursor& c, const Win& win, int32_t x) {
-  uint32_t q = c.q;
-  do {
-    ++q;
-  } while (win.start(q + 1) <= x);
-  cursor_enter<kFinal>(c, win, q, x);
-}
-
-template <bool kFinal, class Win>
-__device__ void tile_body(const ScanArgs& A, const Win& win, const unsigned char* tile, uint32_t wn, uint32_t t,
-                          uint32_t mode, const TileShared& sh) {
+__device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn, uint32_t t,
+                                          uint32_t mode, uint32_t cdirect) {
   const Work& w = A.w;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int32_t x0 = (int32_t)(tid * kScanItems);
+  const uint32_t lane = threadIdx.x & 31;
+  const int32_t x0 = (int32_t)(lane * kScanItems);
   uint32_t q0;
   {
     uint32_t lo = 0, hi = wn - 1;
@@ -435,273 +451,359 @@ __device__ void tile_body(const ScanArgs& A, const Win& win, const unsigned char
     }
     q0 = lo;
   }
-  const uint32_t rowb = tid << 7, rsw = tid & 7u;
-  const bool starts_here = win.start(q0) == x0;
+  const uint32_t rowb = tile_s + (lane << 7), rsw = lane & 7u;
+  const Entry e0 = win.get(q0);
+  const bool starts_here = e0.ls == x0;
 
-  // ---- pass 1: the thread aggregate of the segmented max of lat+
+  // ---- pass 1
   unsigned long long agg;
   {
-    Cursor c;
-    cursor_enter<kFinal>(c, win, q0, x0);
-    uint32_t flag = starts_here ? 1u : 0u, v = 0;
-    int32_t ev = min(c.live ? c.vend : c.ns, c.ns);
+    Entry e = e0;
+    uint32_t q = q0;
+    int32_t ns = win.start(q + 1);
+    bool live = x0 < e.vend;
+    uint32_t P = live ? e.P : 0u;
+    uint32_t Z = e.A + (uint32_t)x0 * e.P - e.P;  // I(x0) - P: lateness-0 baseline
+    uint32_t flag = starts_here ? 1u : 0u, vfz = 0;
+    int32_t ev = live ? min(e.vend, ns) : ns;
 #pragma unroll 1
     for (uint32_t g = 0; g < kScanItems / 4; ++g) {
-      const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
-      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      const uint4 dv = ld_shared_v4(rowb | ((g ^ rsw) << 4));
       const int32_t gx = x0 + (int32_t)(4 * g);
-      int32_t rel = ev - gx;  // items until the next event
+      if (ev - gx >= 4) {
+        Z = max(Z + P, dv.x);
+        Z = max(Z + P, dv.y);
+        Z = max(Z + P, dv.z);
+        Z = max(Z + P, dv.w);
+        continue;
+      }
+      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        if (rel == jj) {
-          const int32_t x = gx + jj;
-          if (x == c.ns) {
-            cursor_next_request<kFinal>(c, win, x);
-            flag = 1u;
-            v = 0;
-          } else {  // end of the valid tokens: null range until the next request
-            c.live = false; c.P = 0; c.I = 0xFFFFFFFFu;
+        const int32_t x = gx + jj;
+        if (x == ev) {
+          if (live && x == e.vend) {
+            vfz = Z - (e.A + (uint32_t)(x - 1) * e.P);
+            live = false;
+            P = 0;
           }
-          ev = c.live ? min(c.vend, c.ns) : c.ns;
-          rel = ev - gx;
+          if (x == ns) {
+            do {
+              ++q;
+              ns = win.start(q + 1);
+            } while (ns <= x);
+            e = win.get(q);
+            live = x < e.vend;
+            P = live ? e.P : 0u;
+            Z = e.A + (uint32_t)x * e.P - e.P;
+            flag = 1u;
+            vfz = 0;
+          }
+          ev = live ? min(e.vend, ns) : ns;
         }
-        v = max(v, max(dd[jj], c.I) - c.I);
-        c.I += c.P;
+        Z = max(Z + P, dd[jj]);
       }
     }
+    const uint32_t v = live ? Z - (e.A + (uint32_t)(x0 + kScanItems - 1) * e.P) : vfz;
     agg = (flag ? kFlagBit : 0ull) | v;
   }
-  // ---- block-wide exclusive scan of the thread aggregates
+  // ---- warp scan + tile carry
   unsigned long long incl = agg;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= (uint32_t)o) incl = seg_combine(v, incl);
   }
-  if (lane == 31) sh.warp[wid] = incl;
   unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0ull;
-  __syncthreads();
-  {
-    unsigned long long wp = 0ull;
-    for (uint32_t k = 0; k < wid; ++k) wp = seg_combine(wp, sh.warp[k]);
-    excl = seg_combine(wp, excl);
-  }
-  if (tid == 0) {
-    unsigned long long tile_agg = 0ull;
-    for (uint32_t k = 0; k < kScanThreads / 32; ++k) tile_agg = seg_combine(tile_agg, sh.warp[k]);
-    unsigned long long acc = 0ull;
-    if (mode == 2u) {
-      st_release(&w.tile_status[t], kStAgg | tile_agg);
-      for (int64_t j = (int64_t)t - 1; j >= 0; --j) {
-        unsigned long long s;
+  const unsigned long long tile_agg = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long acc = 0ull;
+  if (mode == 2u) {
+    // decoupled look-back, 32 predecessors per step (lane k reads tile t-1-k): stop at the
+    // newest inclusive prefix or segment head; combine older-to-newer with a shuffle tree
+    if (lane == 0) st_release(&w.tile_status[t], kStAgg | tile_agg);
+    for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
+      const int64_t j = jhi - (int64_t)lane;
+      unsigned long long s = kStPrefix;  // before the pool: empty prefix
+      if (j >= 0) {
         do {
           s = ld_acquire(&w.tile_status[j]);
         } while ((s & kStMask) == 0ull);
-        acc = seg_combine(s & ~kStMask, acc);
-        if ((s & kStMask) == kStPrefix || (acc & kFlagBit)) break;
       }
-    } else if (mode == 1u) {
-      uint32_t cm = 0;
-      for (uint32_t k = 0; k < kScanThreads / 32; ++k) cm = max(cm, sh.cm[k]);
-      acc = kFlagBit | cm;
+      const bool stop = (s & kStMask) == kStPrefix || (s & kFlagBit);
+      const uint32_t bal = __ballot_sync(0xffffffffu, stop);
+      const uint32_t kst = bal ? (uint32_t)(__ffs(bal) - 1) : 31u;
+      unsigned long long v = (lane <= kst) ? (s & ~kStMask) : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = seg_combine(u, v);
+      }
+      acc = seg_combine(__shfl_sync(0xffffffffu, v, 0), acc);
+      if (bal) break;
     }
-    st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
-    *sh.carry = acc;
+  } else if (mode == 1u) {
+    acc = kFlagBit | cdirect;
   }
-  __syncthreads();
-  const unsigned long long carry = seg_combine(*sh.carry, excl);
+  if (lane == 0) st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+  const uint32_t carry = (uint32_t)seg_combine(acc, excl);
 
-  // ---- pass 2: clamped delays, per-request sums, edge values
+  // ---- pass 2
   {
-    Cursor c;
-    cursor_enter<kFinal>(c, win, q0, x0);
-    uint32_t pm = starts_here ? 0u : (uint32_t)carry;
-    uint32_t dt = 0;
-    unsigned long long sum = 0ull;
-    int32_t ev = c.live ? min(c.vend, c.ns) : c.ns;
+    Entry e = e0;
+    uint32_t q = q0;
+    int32_t ns = win.start(q + 1);
+    bool live = x0 < e.vend;
+    uint32_t P = live ? e.P : 0u;
+    uint32_t tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
+    uint32_t Acur = e.A + (uint32_t)x0 * e.P - e.P + (starts_here ? 0u : carry);
+    int32_t xs = x0;
+    unsigned long long sumT = 0ull;
+    int32_t ev = live ? min(e.vend, ns) : ns;
+    auto flush = [&](int32_t xe) {
+      const uint32_t nn = (uint32_t)(xe - xs);
+      const uint32_t Is = e.A + (uint32_t)xs * e.P;
+      const unsigned long long sumI =
+          (unsigned long long)nn * Is + (unsigned long long)e.P * (((unsigned long long)nn * (nn - 1)) >> 1);
+      const unsigned long long d = sumT - sumI;
+      if (d) atomicAdd(&w.spre[e.ridx], d);
+    };
+    auto edge = [&]() {
+      const uint32_t Il = e.A + (uint32_t)(e.vend - 1) * e.P;
+      w.edge[e.ridx] = (e.ek == 1u) ? Acur - Il : min(Acur, tcl) - Il;
+    };
 #pragma unroll 1
     for (uint32_t g = 0; g < kScanItems / 4; ++g) {
-      const uint4 dv = *reinterpret_cast<const uint4*>(tile + (rowb | ((g ^ rsw) << 4)));
-      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      const uint4 dv = ld_shared_v4(rowb | ((g ^ rsw) << 4));
       const int32_t gx = x0 + (int32_t)(4 * g);
-      int32_t rel = ev - gx;
+      if (ev - gx >= 4) {
+        Acur = max(Acur + P, dv.x);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.y);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.z);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.w);
+        sumT += min(Acur, tcl);
+        continue;
+      }
+      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        if (rel == jj) {
-          const int32_t x = gx + jj;
-          if (c.live && x == c.vend && x > x0 && c.ek) w.edge[c.ridx] = (c.ek == 1u) ? pm : dt;  // last valid token
-          if (x == c.ns) {
-            if (sum) atomicAdd(&w.spre[c.ridx], sum);
-            sum = 0ull;
-            cursor_next_request<kFinal>(c, win, x);
-            pm = 0;
-          } else {
-            c.live = false; c.P = 0; c.I = 0xFFFFFFFFu; c.u = 0; c.Pu = 0;
+        const int32_t x = gx + jj;
+        if (x == ev) {
+          if (live && x == e.vend) {
+            flush(x);
+            if (e.ek) edge();
+            live = false;
+            P = 0;
+            tcl = 0;
           }
-          ev = c.live ? min(c.vend, c.ns) : c.ns;
-          rel = ev - gx;
+          if (x == ns) {
+            do {
+              ++q;
+              ns = win.start(q + 1);
+            } while (ns <= x);
+            e = win.get(q);
+            live = x < e.vend;
+            P = live ? e.P : 0u;
+            tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
+            Acur = e.A + (uint32_t)x * e.P - e.P;
+            xs = x;
+            sumT = 0ull;
+          }
+          ev = live ? min(e.vend, ns) : ns;
         }
-        pm = max(pm, max(dd[jj], c.I) - c.I);
-        c.I += c.P;
-        dt = min(pm, c.u);
-        c.u -= c.Pu;
-        sum += dt;
+        Acur = max(Acur + P, dd[jj]);
+        sumT += min(Acur, tcl);
       }
     }
-    // the last valid token of the current request is this thread's last token
-    if (c.live && c.vend == x0 + kScanItems && c.ek) w.edge[c.ridx] = (c.ek == 1u) ? pm : dt;
-    // the last piece may continue into the next lanes: segmented warp reduction by request
-    uint32_t key = c.ridx;
-    unsigned long long val = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, o);
-      const unsigned long long v2 = __shfl_down_sync(0xffffffffu, val, o);
-      if (lane + o < 32 && k2 == key) val += v2;
+    if (live) {
+      const int32_t xe = x0 + kScanItems;
+      flush(xe);
+      if (e.vend == xe && e.ek) edge();
     }
-    const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
-    if ((lane == 0 || kprev != key) && val && key != 0xFFFFFFFFu) atomicAdd(&w.spre[key], val);
   }
 }
 
 template <bool kFinal>
-__device__ __noinline__ void tile_body_global(const ScanArgs& A, const unsigned char* tile, unsigned long long p0,
-                                              uint32_t r0, uint32_t dummy, uint32_t wn, uint32_t t, uint32_t mode,
-                                              TileShared sh) {
-  GlobalWin win{A.w.srec, p0, r0, dummy, wn};
-  tile_body<kFinal>(A, win, tile, wn, t, mode, sh);
+__device__ __noinline__ void warp_tile_global(const ScanArgs& A, uint32_t tile_s, unsigned long long p0, uint32_t r0,
+                                              uint32_t dummy, uint32_t wn, uint32_t t, uint32_t mode,
+                                              uint32_t cdirect) {
+  RawWin win{A.w.srec + r0, p0, r0, dummy, wn};
+  warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect);
 }
 
 }  // namespace
 
-// K1.  Persistent CTAs claim 4096-token tiles in increasing order; each tile arrives by one
-// TMA tensor copy into a double-buffered, 128B-swizzled shared-memory tile; each thread owns
-// one 32-token row (conflict-free LDS.128); requests overlapping the tile are staged in a
-// shared-memory window; the carry of the head segment is read directly (short segments) or
-// obtained by decoupled look-back (long segments).
+// K1.  Persistent CTAs of independent warps.  Each warp claims 1024-token warp-tiles in
+// increasing order, double-buffers them with TMA tensor copies (32 rows x 128 B, 128B swizzle,
+// one mbarrier per buffer), stages the tile's request records in its own shared-memory window,
+// reads the head segment's earlier tokens directly when it started <= kCarryDirect tokens
+// before the tile (else decoupled look-back on per-warp-tile status words), and scans with
+// warp shuffles only: no CTA-wide barriers on the hot path.
 template <bool kFinal>
 __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ unsigned char s_dyn_raw[];
-  unsigned char* s_tiles =
+  unsigned char* s_base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ alignas(8) uint64_t s_bar[2];
-  __shared__ int32_t w_ls[kWinCap + 2], w_vend[kWinCap + 2];
-  __shared__ uint32_t w_A[kWinCap + 2], w_U[kWinCap + 2], w_P[kWinCap + 2], w_ek[kWinCap + 2],
-      w_ridx[kWinCap + 2];
-  __shared__ unsigned long long s_warp[kScanThreads / 32];
-  __shared__ uint32_t s_cm[kScanThreads / 32];
-  __shared__ unsigned long long s_carry;
-  __shared__ uint32_t s_tile_id[2], s_r0, s_wn, s_dummy, s_mode, s_hcnt, s_hP, s_httft;
-  __shared__ unsigned long long s_hbase;
+  __shared__ alignas(8) uint64_t s_bar[kScanThreads / 32][2];
+  __shared__ uint32_t s_ovf_owner;  // 0 free, else 1 + the warp using the CTA's overflow window
 
   const ReqView& r = A.r;
   const Work& w = A.w;
-  const ScanRec* __restrict__ srec = w.srec;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t n = r.n;
+  if (tid == 0) s_ovf_owner = 0u;
+  __syncthreads();
+  if (blockIdx.x < 1000) ANDES_TRACE(w, 5000 + 2 * blockIdx.x);
+  if (A.sched && blockIdx.x == 0) {
+    bounds_block(r, w, A.tau, A.B_cap, A.M, A.cur_latency, A.flags);
+    bounds_sync();
+    ANDES_TRACE(w, 2300);
+  }
+  if (n == 0) return;
   const uint32_t ntiles = w.g->ntiles;
   const unsigned long long pool_end = w.g->pool_end;
   const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
-  const uint32_t n = r.n;
-  const TileShared sh{s_warp, s_cm, &s_carry};
-  const SmemWin swin{w_ls, w_vend, w_A, w_U, w_P, w_ek, w_ridx};
-  if (A.sched && blockIdx.x == 0) {
-    bounds_block(r, w, A.tau, A.B_cap, A.M, A.cur_latency, A.flags);
-    __syncthreads();
-  }
-  if (n == 0) return;
+  unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles + records
+  Entry* const went_own = reinterpret_cast<Entry*>(wbase + 2 * kWTile * 4);
+  Entry* const went_ovf = reinterpret_cast<Entry*>(s_base + (kScanThreads / 32) * kWarpSmem);
+  uint64_t* bar = s_bar[wid];
 
-  if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+  uint32_t tcur = 0, tnext = 0;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    // claim two tiles (increasing order: a tile waited on in a look-back is owned by a running CTA)
-    for (int b = 0; b < 2; ++b) {
-      const uint32_t tt = atomicAdd(&w.g->tile_ctr, 1u);
-      s_tile_id[b] = tt;
-      if (tt < ntiles) {
-        mbar_expect_tx(&s_bar[b], kTile * 4u);
-        tma_tile(&tmap, s_tiles + b * (kTile * 4), tt * (kTile / 32), &s_bar[b]);
-      }
+    tcur = atomicAdd(&w.g->tile_ctr, 1u);
+    tnext = atomicAdd(&w.g->tile_ctr, 1u);
+    if (tcur < ntiles) {
+      mbar_expect_tx(&bar[0], kWTile * 4u);
+      tma_tile(&tmap, wbase, tcur * (kWTile / 32), &bar[0]);
+    }
+    if (tnext < ntiles) {
+      mbar_expect_tx(&bar[1], kWTile * 4u);
+      tma_tile(&tmap, wbase + kWTile * 4, tnext * (kWTile / 32), &bar[1]);
     }
   }
-  __syncthreads();
+  __syncwarp();
+  tcur = __shfl_sync(0xffffffffu, tcur, 0);
+  tnext = __shfl_sync(0xffffffffu, tnext, 0);
   uint32_t buf = 0, ph0 = 0, ph1 = 0;
-  for (uint32_t t = s_tile_id[0]; t < ntiles; buf ^= 1u) {
-    const unsigned long long p0 = (unsigned long long)t * kTile;
-    if (tid == 0) {
-      const uint32_t r0 = w.tile_owner[t];
-      const uint32_t r_end = (t + 1 < ntiles) ? w.tile_owner[t + 1] : n - 1;
-      const ScanRec h = srec[r0];
-      s_dummy = (h.base > p0) ? 1u : 0u;
-      s_r0 = r0;
-      s_wn = r_end - r0 + 1 + s_dummy;
-      uint32_t mode = 0;  // head-segment carry: 0 none needed, 1 direct read, 2 look-back
-      if (h.base < p0) {
-        const unsigned long long span = p0 - h.base;
-        if ((unsigned long long)h.lim > span) {
-          s_hbase = h.base;
-          s_hcnt = (uint32_t)span;
-          s_httft = h.ttft;
-          s_hP = h.P;
-          mode = (span <= (unsigned long long)kCarryDirect) ? 1u : 2u;
+  while (tcur < ntiles) {
+    const unsigned long long p0 = (unsigned long long)tcur * kWTile;
+    // tile descriptor (prep) and the window's request records
+    TileMeta tm;
+    uint32_t r_end = 0;
+    if (lane == 0) {
+      tm = w.tile_meta[tcur];
+      r_end = (tcur + 1 < ntiles) ? w.tile_meta[tcur + 1].r0 : n - 1;
+    }
+    const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
+    const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
+    const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
+    const uint32_t httft = __shfl_sync(0xffffffffu, tm.httft, 0);
+    const uint32_t hP = __shfl_sync(0xffffffffu, tm.hP, 0);
+    const unsigned long long hbase = __shfl_sync(0xffffffffu, tm.hbase, 0);
+    r_end = __shfl_sync(0xffffffffu, r_end, 0);
+    const uint32_t dummy = flags & 1u, mode = (flags >> 1) & 3u;
+    const uint32_t wn = r_end - r0 + 1 + dummy;
+    const uint32_t nrec = wn - dummy;
+    // tile-local entries of the window, without requests that have no valid token here
+    // (lim == 0: their pool span is dead either way); the owner r0 is always kept
+    // (a dense tile borrows the CTA's larger overflow window when it is free)
+    Entry* went = went_own;
+    uint32_t cap = kWWinCap;
+    bool ovf = false;
+    if (wn >= (uint32_t)kWWinCap) {
+      uint32_t got = 0;
+      if (lane == 0) got = atomicCAS(&s_ovf_owner, 0u, wid + 1u) == 0u;
+      ovf = __shfl_sync(0xffffffffu, got, 0) != 0u;
+      if (ovf) {
+        went = went_ovf;
+        cap = kOvfCap;
+      }
+    }
+    uint32_t wc = dummy;
+    if (dummy && lane == 0) went[0] = null_entry(false);
+    for (uint32_t c0 = 0; c0 < nrec && wc < cap; c0 += 32) {
+      const uint32_t k = c0 + lane;
+      ScanRec sr;
+      bool keep = false;
+      if (k < nrec) {
+        sr = w.srec[r0 + k];
+        keep = k == 0 || sr.lim != 0u;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      const uint32_t pos = wc + __popc(bal & ((1u << lane) - 1u));
+      if (keep && pos < cap) went[pos] = entry_of(sr, r0 + k, p0);
+      wc += __popc(bal);
+    }
+    const bool win_ok = wc < cap;  // entries + sentinel fit the window
+    if (win_ok && lane == 0) went[wc] = null_entry(true);
+    // direct head carry
+    uint32_t cm = 0;
+    if (mode == 1u) {
+      for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
+        uint32_t d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t kk = k0 + u * 32 + lane;
+          d[u] = kk < hcnt ? __ldg(&r.tl_pool[hbase + kk]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t kk = k0 + u * 32 + lane;
+          const uint32_t I = httft + kk * hP;
+          if (kk < hcnt) cm = max(cm, max(d[u], I) - I);
         }
       }
-      s_mode = mode;
+      for (int o = 16; o; o >>= 1) cm = max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
     }
-    __syncthreads();
-    const uint32_t r0 = s_r0, wn = s_wn, dummy = s_dummy, mode = s_mode;
-    const bool win_ok = wn <= (uint32_t)kWinCap;
-    if (win_ok) {
-      for (uint32_t q = tid; q <= wn; q += kScanThreads) {
-        const Entry e = make_entry(srec, p0, r0, dummy, wn, q);
-        w_ls[q] = e.ls; w_vend[q] = e.vend; w_A[q] = e.A; w_U[q] = e.U; w_P[q] = e.P;
-        w_ek[q] = e.ek; w_ridx[q] = e.ridx;
-      }
-    }
-    // direct head carry: max lat+ of the head segment's tokens before p0
-    uint32_t cmax = 0;
-    if (mode == 1u) {
-      const unsigned long long hb = s_hbase;
-      const uint32_t cnt = s_hcnt, P = s_hP, ttft = s_httft;
-      for (uint32_t k = tid; k < cnt; k += kScanThreads) {
-        const uint32_t d = r.tl_pool[hb + k];
-        const uint32_t I = ttft + k * P;
-        cmax = max(cmax, max(d, I) - I);
-      }
-    }
-    for (int o = 16; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    if (lane == 0) s_cm[wid] = cmax;
-    if (buf == 0) { mbar_wait(&s_bar[0], ph0); ph0 ^= 1u; }
-    else { mbar_wait(&s_bar[1], ph1); ph1 ^= 1u; }
-    unsigned char* tile = s_tiles + buf * (kTile * 4);
+    // this tile's data
+    if (buf == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
+    else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+    unsigned char* tile = wbase + buf * (kWTile * 4);
     {
-      // tokens past the last full 32-token row of the pool view: read directly
-      const unsigned long long pe = min(p0 + (unsigned long long)kTile, pool_end);
+      const unsigned long long pe = min(p0 + (unsigned long long)kWTile, pool_end);
       if (pe > full_rows_end) {
         const unsigned long long lo = max(p0, full_rows_end);
-        for (unsigned long long p = lo + tid; p < pe; p += kScanThreads)
+        for (unsigned long long p = lo + lane; p < pe; p += 32)
           *reinterpret_cast<uint32_t*>(tile + swz((uint32_t)(p - p0))) = r.tl_pool[p];
       }
     }
-    __syncthreads();
-    if (win_ok) tile_body<kFinal>(A, swin, tile, wn, t, mode, sh);
-    else tile_body_global<kFinal>(A, tile, p0, r0, dummy, wn, t, mode, sh);
-    __syncthreads();  // tile buffer and window are reused below
-    // refill this buffer with a newly claimed tile (two tiles ahead)
-    if (tid == 0) {
-      const uint32_t tt = atomicAdd(&w.g->tile_ctr, 1u);
-      s_tile_id[buf] = tt;
+    __syncwarp();
+    const unsigned long long t_body = (w.trace && tcur < 16384) ? gtimer() : 0ull;
+    if (win_ok) {
+      EntWin win{smem_u32(went)};
+      warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm);
+    } else {
+      warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm);
+    }
+    // refill this buffer with a newly claimed warp-tile (two ahead)
+    __syncwarp();
+    if (ovf && lane == 0) atomicExch(&s_ovf_owner, 0u);
+    if (t_body && lane == 0) {
+      w.trace[16384 + 2 * tcur] = t_body;
+      w.trace[16384 + 2 * tcur + 1] = gtimer();
+    }
+    uint32_t tt = 0;
+    if (lane == 0) {
+      tt = atomicAdd(&w.g->tile_ctr, 1u);
       if (tt < ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&s_bar[buf], kTile * 4u);
-        tma_tile(&tmap, s_tiles + buf * (kTile * 4), tt * (kTile / 32), &s_bar[buf]);
+        mbar_expect_tx(&bar[buf], kWTile * 4u);
+        tma_tile(&tmap, tile, tt * (kWTile / 32), &bar[buf]);
       }
     }
-    t = s_tile_id[buf ^ 1u];
+    tt = __shfl_sync(0xffffffffu, tt, 0);
+    tcur = tnext;
+    tnext = tt;
+    buf ^= 1u;
   }
+  if (w.trace && blockIdx.x < 1000 && lane == 0) atomicMax(&w.trace[5000 + 2 * blockIdx.x + 1], gtimer());
 }
 
 // ---------------------------------------------------------------- qoe finalize

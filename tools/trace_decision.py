@@ -1,4 +1,6 @@
-"""Internal timeline of one config-3 decision from %globaltimer stamps (andes_debug_trace)."""
+"""Internal timeline of one config-3 decision from %globaltimer stamps (andes_debug_trace).
+Slots: 7000+2b prep CTA b start/end; 5000+2b scan CTA b start/end; 2300 bounds end (scan CTA 0);
+3000+2b state CTA b; 2200/2201 state last block; 0+2b select CTA b; 2100.. finalize phases."""
 import ctypes as C
 import os
 import sys
@@ -18,19 +20,50 @@ L = A.lib()
 L.andes_debug_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]
 L.andes_debug_trace.argtypes = [C.c_void_p, C.c_int]
 print("trace rc", L.andes_debug_trace(ctx._h, 1))
-for it in range(4):
+for it in range(int(os.environ.get("ITERS", "4"))):
+    if it == int(os.environ.get("ITERS", "4")) - 1:
+        L.andes_debug_trace(ctx._h, 0)
+        L.andes_debug_trace(ctx._h, 1)
     d = ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=16)
 torch.cuda.synchronize()
-tr = np.zeros(8192, np.uint64)
+tr = np.zeros(1 << 16, np.uint64)
 print("read rc", L.andes_debug_read(ctx._h, 7, tr.ctypes.data, tr.nbytes))
-g = np.zeros(26, np.uint32)
-print("read rc", L.andes_debug_read(ctx._h, 5, g.ctypes.data, 104), g.tolist())
-sel = tr[:512].astype(np.int64).reshape(256, 2)
-t0 = sel[:, 0][sel[:, 0] > 0].min()
-st = tr[3000:4024].astype(np.int64).reshape(512, 2)
-st = st[st[:, 0] > 0]
-print("state CTAs: first start", (st[:, 0].min() - t0) / 1e3, "last end", (st[:, 1].max() - t0) / 1e3, "us rel. select start")
-print("state last-block", [(int(tr[s]) - t0) / 1e3 for s in (2200, 2201)])
-print("select CTA start spread us", (sel[:, 0].max() - t0) / 1e3, "end min/med/max",
-      [(x - t0) / 1e3 for x in (sel[:, 1].min(), int(np.median(sel[:, 1])), sel[:, 1].max())])
-print("finalize phases us", [round((int(tr[s]) - t0) / 1e3, 2) for s in range(2100, 2106)])
+tr = tr.astype(np.int64)
+
+
+def span(lo, hi):
+    x = tr[lo:hi].reshape(-1, 2)
+    x = x[x[:, 0] > 0]
+    return x
+
+
+pr = span(7000, 8024)
+t0 = pr[:, 0].min()
+us = lambda v: round((int(v) - t0) / 1e3, 2)  # noqa: E731
+print("prep CTAs", len(pr), "start", us(pr[:, 0].min()), "end max", us(pr[:, 1].max()))
+sc = span(5000, 7000)
+print("scan CTAs", len(sc), "start min/max", us(sc[:, 0].min()), us(sc[:, 0].max()), "bounds end", us(tr[2300]),
+      "end min/med/max", us(sc[:, 1].min()), us(np.median(sc[:, 1])), us(sc[:, 1].max()))
+st = span(3000, 4024)
+print("state CTAs", len(st), "start", us(st[:, 0].min()), "end", us(st[:, 1].max()), "last-block",
+      us(tr[2200]), us(tr[2201]))
+sel = span(0, 512)
+print("select CTAs", len(sel), "start", us(sel[:, 0].min()), us(sel[:, 0].max()), "end min/med/max",
+      us(sel[:, 1].min()), us(np.median(sel[:, 1])), us(sel[:, 1].max()))
+print("finalize phases", [us(tr[s]) for s in range(2100, 2106) if tr[s]])
+
+tl = tr[16384:16384 + 2 * 16384].reshape(-1, 2)
+ok = tl[:, 0] > 0
+ids = np.where(ok)[0]
+dur = (tl[ok, 1] - tl[ok, 0]) / 1e3
+print("tiles traced", ok.sum(), "body us median/p90/p99/max", np.percentile(dur, [50, 90, 99, 100]).round(2))
+order = np.argsort(-dur)[:12]
+base = snap.tl_base.astype(np.int64)
+starts = np.bincount(base // 1024, minlength=len(tl))
+for k in order:
+    t = ids[k]
+    print("  tile", t, "dur", round(dur[k], 2), "start", us(tl[t, 0]), "end", us(tl[t, 1]), "req starts", starts[t])
+ends = np.sort(tl[ok, 1])
+print("tile end percentiles us", [us(np.percentile(ends, p)) for p in (50, 90, 99, 99.9, 100)])
+last = ids[np.argsort(-tl[ok, 1])[:8]]
+print("last tiles to finish", [(int(t), us(tl[t, 0]), us(tl[t, 1])) for t in last])
