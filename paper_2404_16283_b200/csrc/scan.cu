@@ -454,27 +454,56 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   const uint32_t rowb = tile_s + (lane << 7), rsw = lane & 7u;
   const Entry e0 = win.get(q0);
   const bool starts_here = e0.ls == x0;
+  // Pieces that start in this row are final after one pass.  The row's first piece, when it
+  // continues a request from an earlier row, is computed with zero carry-in; its sum and edge
+  // are held back until the carry is known and recomputed only if the carry is non-zero
+  // (A_x = max(Z_x, I_x + c), Z the zero-carry recurrence).
+  const bool held = !starts_here && x0 < e0.vend;
+  unsigned long long h_sum = 0ull;
+  int32_t h_xe = x0;
+  uint32_t h_edge = 0u;  // edge value of the held piece (valid when its vend is in this row)
+  bool h_has_edge = false;
 
-  // ---- pass 1
+  auto flush = [&](const Entry& e, int32_t xs, int32_t xe, unsigned long long sumT) {
+    const uint32_t nn = (uint32_t)(xe - xs);
+    const uint32_t Is = e.A + (uint32_t)xs * e.P;
+    const unsigned long long sumI =
+        (unsigned long long)nn * Is + (unsigned long long)e.P * (((unsigned long long)nn * (nn - 1)) >> 1);
+    const unsigned long long d = sumT - sumI;
+    if (d) atomicAdd(&w.spre[e.ridx], d);
+  };
+  auto edge_val = [&](const Entry& e, uint32_t Acur, uint32_t tcl) -> uint32_t {
+    const uint32_t Il = e.A + (uint32_t)(e.vend - 1) * e.P;
+    return (e.ek == 1u) ? Acur - Il : min(Acur, tcl) - Il;
+  };
+
   unsigned long long agg;
   {
     Entry e = e0;
     uint32_t q = q0;
     int32_t ns = win.start(q + 1);
     bool live = x0 < e.vend;
+    bool first = held;
     uint32_t P = live ? e.P : 0u;
-    uint32_t Z = e.A + (uint32_t)x0 * e.P - e.P;  // I(x0) - P: lateness-0 baseline
+    uint32_t tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
+    uint32_t Acur = e.A + (uint32_t)x0 * e.P - e.P;  // zero-carry baseline I(x0) - P
     uint32_t flag = starts_here ? 1u : 0u, vfz = 0;
+    int32_t xs = x0;
+    unsigned long long sumT = 0ull;
     int32_t ev = live ? min(e.vend, ns) : ns;
 #pragma unroll 1
     for (uint32_t g = 0; g < kScanItems / 4; ++g) {
       const uint4 dv = ld_shared_v4(rowb | ((g ^ rsw) << 4));
       const int32_t gx = x0 + (int32_t)(4 * g);
       if (ev - gx >= 4) {
-        Z = max(Z + P, dv.x);
-        Z = max(Z + P, dv.y);
-        Z = max(Z + P, dv.z);
-        Z = max(Z + P, dv.w);
+        Acur = max(Acur + P, dv.x);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.y);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.z);
+        sumT += min(Acur, tcl);
+        Acur = max(Acur + P, dv.w);
+        sumT += min(Acur, tcl);
         continue;
       }
       const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
@@ -483,9 +512,21 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
         const int32_t x = gx + jj;
         if (x == ev) {
           if (live && x == e.vend) {
-            vfz = Z - (e.A + (uint32_t)(x - 1) * e.P);
+            const uint32_t ev_val = e.ek ? edge_val(e, Acur, tcl) : 0u;
+            if (first) {
+              h_sum = sumT;
+              h_xe = x;
+              h_has_edge = e.ek != 0u;
+              h_edge = ev_val;
+              first = false;
+            } else {
+              flush(e, xs, x, sumT);
+              if (e.ek) w.edge[e.ridx] = ev_val;
+            }
+            vfz = Acur - (e.A + (uint32_t)(x - 1) * e.P);
             live = false;
             P = 0;
+            tcl = 0;
           }
           if (x == ns) {
             do {
@@ -495,16 +536,34 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
             e = win.get(q);
             live = x < e.vend;
             P = live ? e.P : 0u;
-            Z = e.A + (uint32_t)x * e.P - e.P;
+            tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
+            Acur = e.A + (uint32_t)x * e.P - e.P;
+            xs = x;
+            sumT = 0ull;
             flag = 1u;
             vfz = 0;
           }
           ev = live ? min(e.vend, ns) : ns;
         }
-        Z = max(Z + P, dd[jj]);
+        Acur = max(Acur + P, dd[jj]);
+        sumT += min(Acur, tcl);
       }
     }
-    const uint32_t v = live ? Z - (e.A + (uint32_t)(x0 + kScanItems - 1) * e.P) : vfz;
+    const int32_t xe = x0 + kScanItems;
+    if (live) {
+      const bool has_edge = e.vend == xe && e.ek;
+      const uint32_t ev_val = has_edge ? edge_val(e, Acur, tcl) : 0u;
+      if (first) {
+        h_sum = sumT;
+        h_xe = xe;
+        h_has_edge = has_edge;
+        h_edge = ev_val;
+      } else {
+        flush(e, xs, xe, sumT);
+        if (has_edge) w.edge[e.ridx] = ev_val;
+      }
+    }
+    const uint32_t v = live ? Acur - (e.A + (uint32_t)(xe - 1) * e.P) : vfz;
     agg = (flag ? kFlagBit : 0ull) | v;
   }
   // ---- warp scan + tile carry
@@ -548,81 +607,31 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   if (lane == 0) st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
   const uint32_t carry = (uint32_t)seg_combine(acc, excl);
 
-  // ---- pass 2
-  {
-    Entry e = e0;
-    uint32_t q = q0;
-    int32_t ns = win.start(q + 1);
-    bool live = x0 < e.vend;
-    uint32_t P = live ? e.P : 0u;
-    uint32_t tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
-    uint32_t Acur = e.A + (uint32_t)x0 * e.P - e.P + (starts_here ? 0u : carry);
-    int32_t xs = x0;
-    unsigned long long sumT = 0ull;
-    int32_t ev = live ? min(e.vend, ns) : ns;
-    auto flush = [&](int32_t xe) {
-      const uint32_t nn = (uint32_t)(xe - xs);
-      const uint32_t Is = e.A + (uint32_t)xs * e.P;
-      const unsigned long long sumI =
-          (unsigned long long)nn * Is + (unsigned long long)e.P * (((unsigned long long)nn * (nn - 1)) >> 1);
-      const unsigned long long d = sumT - sumI;
-      if (d) atomicAdd(&w.spre[e.ridx], d);
-    };
-    auto edge = [&]() {
-      const uint32_t Il = e.A + (uint32_t)(e.vend - 1) * e.P;
-      w.edge[e.ridx] = (e.ek == 1u) ? Acur - Il : min(Acur, tcl) - Il;
-    };
+  // ---- the held first piece, now that its carry-in is known
+  if (held) {
+    if (carry != 0u) {
+      const uint32_t P = e0.P;
+      const uint32_t tcl = kFinal ? 0xFFFFFFFFu : e0.trel;
+      uint32_t Acur = e0.A + (uint32_t)x0 * P - P + carry;
+      unsigned long long sumT = 0ull;
+      const uint32_t nh = (uint32_t)(h_xe - x0);  // 1..32 tokens
 #pragma unroll 1
-    for (uint32_t g = 0; g < kScanItems / 4; ++g) {
-      const uint4 dv = ld_shared_v4(rowb | ((g ^ rsw) << 4));
-      const int32_t gx = x0 + (int32_t)(4 * g);
-      if (ev - gx >= 4) {
-        Acur = max(Acur + P, dv.x);
-        sumT += min(Acur, tcl);
-        Acur = max(Acur + P, dv.y);
-        sumT += min(Acur, tcl);
-        Acur = max(Acur + P, dv.z);
-        sumT += min(Acur, tcl);
-        Acur = max(Acur + P, dv.w);
-        sumT += min(Acur, tcl);
-        continue;
-      }
-      const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      for (uint32_t g = 0; 4 * g < nh; ++g) {
+        const uint4 dv = ld_shared_v4(rowb | ((g ^ rsw) << 4));
+        const uint32_t dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int32_t x = gx + jj;
-        if (x == ev) {
-          if (live && x == e.vend) {
-            flush(x);
-            if (e.ek) edge();
-            live = false;
-            P = 0;
-            tcl = 0;
+        for (int jj = 0; jj < 4; ++jj) {
+          if (4 * g + jj < nh) {
+            Acur = max(Acur + P, dd[jj]);
+            sumT += min(Acur, tcl);
           }
-          if (x == ns) {
-            do {
-              ++q;
-              ns = win.start(q + 1);
-            } while (ns <= x);
-            e = win.get(q);
-            live = x < e.vend;
-            P = live ? e.P : 0u;
-            tcl = live ? (kFinal ? 0xFFFFFFFFu : e.trel) : 0u;
-            Acur = e.A + (uint32_t)x * e.P - e.P;
-            xs = x;
-            sumT = 0ull;
-          }
-          ev = live ? min(e.vend, ns) : ns;
         }
-        Acur = max(Acur + P, dd[jj]);
-        sumT += min(Acur, tcl);
       }
+      h_sum = sumT;
+      if (h_has_edge) h_edge = edge_val(e0, Acur, tcl);
     }
-    if (live) {
-      const int32_t xe = x0 + kScanItems;
-      flush(xe);
-      if (e.vend == xe && e.ek) edge();
-    }
+    flush(e0, x0, h_xe, h_sum);
+    if (h_has_edge) w.edge[e0.ridx] = h_edge;
   }
 }
 
