@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libandes (include/andes.h): argument validation, workspace
 // ownership, and the kernel sequence of each entry point.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -10,6 +11,16 @@
 #include "launch.h"
 
 using namespace andes;
+
+// Programmatic dependent launch is off by default: measured on config 3 it did not shorten the
+// decision (88 us without vs 92 us with, L2 flushed).  ANDES_PDL=1 turns it on.
+bool andes::pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("ANDES_PDL");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 
 struct AndesCtx {
   AndesLimits lim{};
@@ -172,8 +183,8 @@ int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap*
 
 // per-call reset of the small globals and the look-back status words
 int reset_call(AndesCtx* c, cudaStream_t s) {
+  // (the look-back status words are zeroed by k_prep, tile by tile)
   cudaError_t e = cudaMemsetAsync(c->w.g, 0, sizeof(Globals), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->w.tile_status, 0, sizeof(unsigned long long) * c->tiles_cap, s);
   return cuda_check(c, e, "memset");
 }
 
@@ -242,14 +253,15 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess || (e = ctx_alloc(c, &w.hist_lb, kHistK)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.cand, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.cand_g, (size_t)lim->max_B * w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.srec, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &c->zero_rows, 32)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.sel, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.sel_thr, (size_t)lim->max_B)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.stage_pre, (size_t)lim->max_B * kStageRun)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.stage_adm, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.stage_sc, (size_t)lim->max_B)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);

@@ -26,9 +26,10 @@ constexpr int kScanDynSmem = (kScanThreads / 32) * kWarpSmem + kOvfCap * 32 + 10
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;
+constexpr int kStageRun = kMaxRunning / 2;        // running requests handled by the per-B cap staging
 constexpr uint32_t kHistL = 4096;                 // exact histogram of l < 4095 (+ overflow bucket)
 constexpr uint32_t kHistK = 4096;                 // key histograms: top 12 bits of the ordered key
-constexpr uint32_t kCandCap = 16384;              // candidate capacity (requests) of the pruned path
+constexpr uint32_t kCandCap = 3071;               // survivor capacity of the pruned path (k_select scratch)
 
 // tile status words (decoupled look-back), see k_qoe_scan
 constexpr unsigned long long kStAgg = 1ull << 62;
@@ -122,17 +123,18 @@ struct Work {
   ScanRec* srec;             // [N] timeline-scan records
   PackedState* st;           // [N]
   uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
-  unsigned long long* cand;  // [max_B][S_cap] composite keys of the candidates per B
-  long long* cand_g;         // [max_B][S_cap] llrint(gain 2^32) of the candidates per B
   uint32_t* cand_idx;        // [S_cap] request index of candidate slot
   uint32_t* keyrow;          // [max_B][N] fallback: ordered keys of every request per B
   uint32_t* sel;             // [max_B][kMaxB] Algorithm 1 prefix per B, greedy order
   unsigned long long* sel_thr;  // [max_B] composite of the k*-th selected request per B
+  uint32_t* stage_pre;       // [max_B][kStageRun] preempt list per candidate B (cap applied)
+  uint32_t* stage_adm;       // [max_B][kMaxB] admit list per candidate B
+  uint4* stage_sc;           // [max_B] {n_pre, n_adm, realized, flags} per candidate B
   Globals* g;
   unsigned long long* trace; // optional %globaltimer stamps (internal debugging), may be null
   uint32_t N_cap;            // row stride of keyrow
   uint32_t tiles_cap;        // capacity of tile_owner / tile_status
-  uint32_t S_cap;            // candidate capacity (row stride of cand)
+  uint32_t S_cap;            // survivor capacity of cand_idx
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -310,5 +312,21 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Self-contained status words (flag + value in one 64-bit word): relaxed strong accesses suffice,
+// no fence is needed because nothing else is published through them.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Programmatic dependent launch (every decision kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its stream successor start
+// launching early, and waits for its predecessor's completion (and memory) before reading it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 }  // namespace andes

@@ -1,10 +1,32 @@
 // launch.h -- internal host-side launchers of libandes (not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include "device.cuh"
 
 namespace andes {
+
+// Programmatic dependent launch: off unless the environment sets ANDES_PDL=1 (see api.cu).
+bool pdl_enabled();
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin while its stream
+// predecessor finishes; it must call pdl_wait() before touching the predecessor's results.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 struct LaunchCfg {
   cudaStream_t stream;

@@ -81,11 +81,12 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
         const uint32_t b = tid * kPer + q;
         const uint32_t h = hv[q];
         if (b == kHistL - 1 && h) { ovf = true; break; }
-        for (uint32_t z = 0; z < h; ++z) {
-          if (k >= need || W + b > M) { stop = true; break; }
-          W += b;
-          ++k;
-        }
+        // take min(h, need - k, floor((M - W) / b)) contexts of length b
+        unsigned long long take = min((unsigned long long)h, need - k);
+        if (b > 0) take = min(take, (M - W) / b);
+        W += take * b;
+        k += take;
+        if (take < h) stop = true;
       }
       s_kM = ovf && !stop && k < need ? 0xFFFFFFFEu : (uint32_t)min(k, (unsigned long long)need);
     }
@@ -174,6 +175,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
   uint32_t local_err = 0;
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x);
   if (sched) {
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
       tm.hP = P;
       tm.pad = 0;
       w.tile_meta[t] = tm;
+      w.tile_status[t] = 0ull;  // look-back status of this call (read only by the scan, after prep)
     }
     if (i + 1 == n) {
       unsigned long long pe = min(base + g, (unsigned long long)w.tiles_cap * kWTile);
@@ -580,13 +584,13 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   if (mode == 2u) {
     // decoupled look-back, 32 predecessors per step (lane k reads tile t-1-k): stop at the
     // newest inclusive prefix or segment head; combine older-to-newer with a shuffle tree
-    if (lane == 0) st_release(&w.tile_status[t], kStAgg | tile_agg);
+    if (lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
     for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
       const int64_t j = jhi - (int64_t)lane;
       unsigned long long s = kStPrefix;  // before the pool: empty prefix
       if (j >= 0) {
         do {
-          s = ld_acquire(&w.tile_status[j]);
+          s = ld_relaxed(&w.tile_status[j]);
         } while ((s & kStMask) == 0ull);
       }
       const bool stop = (s & kStMask) == kStPrefix || (s & kFlagBit);
@@ -604,7 +608,7 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   } else if (mode == 1u) {
     acc = kFlagBit | cdirect;
   }
-  if (lane == 0) st_release(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
   const uint32_t carry = (uint32_t)seg_combine(acc, excl);
 
   // ---- the held first piece, now that its carry-in is known
@@ -665,6 +669,8 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t n = r.n;
   if (tid == 0) s_ovf_owner = 0u;
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   if (blockIdx.x < 1000) ANDES_TRACE(w, 5000 + 2 * blockIdx.x);
   if (A.sched && blockIdx.x == 0) {
@@ -820,6 +826,8 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
 // undelivered due tokens sit at t, Eq. 1-3).
 __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode, float* q,
                             double* q64, int64_t* sdo, int64_t* swo, uint32_t* mo) {
+  pdl_wait();
+  pdl_trigger();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     const uint32_t g = r.n_deliv[i], m = w.m[i];
     const int64_t P = r.period[i];
@@ -853,8 +861,8 @@ void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
                  bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask) {
   if (r.n == 0) return;
   const uint32_t blocks = umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8);
-  k_prep<<<blocks, kPrepThreads, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u, kv_cap,
-                                                debug ? 1u : 0u, serve_mask);
+  launch_pdl(k_prep, blocks, kPrepThreads, 0, L.stream, r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u,
+             kv_cap, debug ? 1u : 0u, serve_mask);
 }
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
@@ -864,16 +872,16 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
   ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags};
   const uint32_t grid = r.n ? L.scan_grid : 1u;
   if (final_mode)
-    k_qoe_scan<true><<<grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
+    launch_pdl(k_qoe_scan<true>, grid, kScanThreads, kScanDynSmem, L.stream, A, *tmap);
   else
-    k_qoe_scan<false><<<grid, kScanThreads, kScanDynSmem, L.stream>>>(A, *tmap);
+    launch_pdl(k_qoe_scan<false>, grid, kScanThreads, kScanDynSmem, L.stream, A, *tmap);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m) {
   if (r.n == 0) return;
   const uint32_t blocks = umin32((r.n + 255) / 256, L.sm_count * 8);
-  k_qoe_final<<<blocks, 256, 0, L.stream>>>(r, w, eval_abs, final_mode ? 1u : 0u, q, q64, sd, sw, m);
+  launch_pdl(k_qoe_final, blocks, 256, 0, L.stream, r, w, eval_abs, final_mode ? 1u : 0u, q, q64, sd, sw, m);
 }
 
 void init_scan_kernels() {

@@ -8,15 +8,15 @@
 //             the key (RN division, RN subtraction, RN64->RN32) is monotone, so evaluating the
 //             same fp chain at (S_delay(tau_lo), S_whole(tau_hi)) / (S_delay(tau_hi),
 //             S_whole(tau_lo)) bounds the computed key of every B with tau in [tau_lo, tau_hi].
-//             A histogram of the lower bounds gives theta with >= B_max requests whose key is
-//             >= theta at every B, so the exact top-B of every B lies among requests whose upper
-//             bound is >= theta ("survivors").
-//   k_cand    compacts the survivors and evaluates their exact keys for every B.
-//   k_select  per B: exact radix threshold-select of the top min(B, n) survivors by
-//             (key desc, rank asc), sort, Algorithm 1 walk; the last CTA picks
-//             B*, applies the cap and writes the outputs.
-// If the survivors exceed the candidate capacity, the same kernels fall back to evaluating and
-// selecting over all n requests (slow path, flagged).
+//             Histograms of the bounds follow.
+//   k_compact theta from the lower-bound histogram: >= B_max requests have key >= theta at every
+//             B, so the exact top-B of every B lies among the requests whose upper bound is
+//             >= theta ("survivors"); compacts them.
+//   k_select  one CTA per B: exact keys of the survivors at B, their order by rank counting
+//             (key desc, rank asc), Algorithm 1 walk, V(B), and B's preemption-cap
+//             result staged; the last CTA picks B* and writes the outputs.
+// If the survivors exceed the capacity, k_select evaluates every request at its B and
+// radix-selects instead (slow path, flagged).
 #include "device.cuh"
 #include "launch.h"
 
@@ -26,6 +26,8 @@ namespace andes {
 __global__ void k_gain_estimate(ReqView r, Work w, int64_t now, uint32_t horizon, const uint32_t* __restrict__ tau,
                                 const uint32_t* __restrict__ B_list, uint32_t nB, double* gain_out, float* key_out,
                                 double* qwait_out) {
+  pdl_wait();
+  pdl_trigger();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     const GainState s = make_state(r, w, i, now, horizon);
     const uint32_t l = r.ctx_len[i];
@@ -91,12 +93,12 @@ __device__ void bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t si
 
 // ---------------------------------------------------------------- S3a: state + key bounds
 constexpr int kStateThreads = 256;
+constexpr int kCandThreads = 256;
 
 __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
   __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
-  __shared__ uint32_t s_last;
-  __shared__ unsigned long long s_sc[kStateThreads];
-  __shared__ uint32_t s_cut;
+  pdl_wait();
+  pdl_trigger();
   if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
@@ -134,74 +136,86 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
     if (s_hlb[q]) atomicAdd(&w.hist_lb[q], s_hlb[q]);
     if (s_hub[q]) atomicAdd(&w.hist_ub[q], s_hub[q]);
   }
-  __threadfence();
-  __syncthreads();
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
-  if (tid == 0) s_last = (atomicAdd(&w.g->state_done, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  ANDES_TRACE(w, 2200);
-  // theta: lower edge of the highest bucket b* with #(LB in buckets >= b*) >= B_hi
-  constexpr uint32_t kPer = kHistK / kStateThreads;  // 16 buckets per thread, descending
-  const uint32_t need = __ldcg(&w.g->B_hi);
-  uint32_t cnt = 0;
-  for (uint32_t q = 0; q < kPer; ++q) cnt += __ldcg(&w.hist_lb[kHistK - 1 - (tid * kPer + q)]);
-  s_sc[tid] = cnt;
-  if (tid == 0) s_cut = 0;
-  __syncthreads();
-  for (uint32_t off = 1; off < kStateThreads; off <<= 1) {
-    unsigned long long a = (tid >= off) ? s_sc[tid - off] : 0ull;
-    __syncthreads();
-    s_sc[tid] += a;
-    __syncthreads();
+}
+
+// ---------------------------------------------------------------- S3b: candidates
+
+// theta = lower edge of the highest LB bucket b* with #(LB in buckets >= b*) >= B_hi, and the
+// survivor count #(UB bucket >= b*); computed redundantly by every CTA of k_compact from the
+// completed histograms (16 KB each, L2-resident), so no CTA waits on a last-block reduction.
+__device__ __forceinline__ void theta_of(const Work& w, uint32_t need, uint32_t& cut, uint32_t& nsurv) {
+  constexpr uint32_t NT = kCandThreads, kPer = kHistK / NT;  // 16 buckets per thread, descending
+  __shared__ uint32_t s_w[NT / 32], s_cut, s_sv[NT / 32];
+  __shared__ uint32_t s_h[kHistK];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // coalesced loads of both histograms; survivors partial sums by bucket later
+  uint32_t hu[kPer];
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    s_h[q * NT + tid] = __ldcg(&w.hist_lb[q * NT + tid]);
+    hu[q] = __ldcg(&w.hist_ub[q * NT + tid]);
   }
-  {
-    const unsigned long long ex = tid ? s_sc[tid - 1] : 0ull;
-    if (ex < need && s_sc[tid] >= need) {
-      unsigned long long c2 = ex;
-      for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t b = kHistK - 1 - (tid * kPer + q);
-        c2 += __ldcg(&w.hist_lb[b]);
-        if (c2 >= need) {
-          s_cut = b;
-          break;
-        }
+  __syncthreads();
+  uint32_t h[kPer], cnt = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    h[q] = s_h[kHistK - 1 - (tid * kPer + q)];
+    cnt += h[q];
+  }
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += v;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  if (tid == 0) s_cut = 0u;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (uint32_t k = 0; k < wid; ++k) wpre += s_w[k];
+  const uint32_t ex = wpre + inc - cnt;
+  if (ex < need && ex + cnt >= need) {
+    uint32_t c2 = ex;
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      c2 += h[q];
+      if (c2 >= need) {
+        s_cut = kHistK - 1 - (tid * kPer + q);
+        break;
       }
     }
   }
   __syncthreads();
-  const uint32_t cut = s_cut;
-  // survivors: UB >= theta  <=>  UB bucket >= cut
+  cut = s_cut;
   uint32_t sv = 0;
-  for (uint32_t b = cut + tid; b < kHistK; b += kStateThreads) sv += __ldcg(&w.hist_ub[b]);
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) sv += (q * NT + tid >= cut) ? hu[q] : 0u;
   for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  if (lane == 0) s_sv[wid] = sv;
   __syncthreads();
-  if ((tid & 31) == 0) s_sc[tid >> 5] = sv;
-  __syncthreads();
-  // self-clean the histograms for the next call
-  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
-    w.hist_lb[q] = 0u;
-    w.hist_ub[q] = 0u;
-  }
-  if (tid == 0) {
-    unsigned long long tot = 0;
-    for (uint32_t q = 0; q < kStateThreads / 32; ++q) tot += s_sc[q];
-    w.g->theta = cut << 20;
-    w.g->n_surv = (uint32_t)tot;
-    w.g->overflow = (tot > w.S_cap) ? 1u : 0u;
-    if (tot > w.S_cap) atomicOr(&w.g->slow, 2u);
-  }
-  ANDES_TRACE(w, 2201);
+  nsurv = 0;
+  for (uint32_t k = 0; k < NT / 32; ++k) nsurv += s_sv[k];
 }
-
-// ---------------------------------------------------------------- S3b: candidates
-constexpr int kCandThreads = 256;
 
 // Compaction of the survivors (UB >= theta) into cand_idx, warp-aggregated appends.
 __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w) {
-  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0 || __ldcg(&w.g->overflow)) return;
-  const uint32_t theta = __ldcg(&w.g->theta);
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
+  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
+  uint32_t cut, ns;
+  theta_of(w, __ldcg(&w.g->B_hi), cut, ns);
+  if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
+  const uint32_t theta = cut << 20;
+  const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w.g->theta = theta;
+    w.g->n_surv = ns;
+    w.g->overflow = ovf ? 1u : 0u;
+    if (ovf) atomicOr(&w.g->slow, 2u);
+  }
+  if (ovf) return;
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < r.n; i0 += gridDim.x * blockDim.x) {
     const uint32_t i = i0 + threadIdx.x;
@@ -213,37 +227,7 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (surv) w.cand_idx[base + __popc(bal & ((1u << lane) - 1u))] = i;
   }
-}
-
-// Exact keys of every (candidate, B) pair, spread over the whole grid; in the overflow
-// fallback, of every (request, B).
-__global__ void __launch_bounds__(kCandThreads) k_cand(ReqView r, Work w, const uint32_t* __restrict__ tau) {
-  __shared__ uint32_t s_tau[kMaxB];
-  if (!__ldcg(&w.g->triggered)) return;
-  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
-  if (B_hi == 0) return;
-  const uint32_t nB = B_hi - B_lo + 1;
-  const uint32_t tid = threadIdx.x;
-  for (uint32_t q = tid; q < nB; q += kCandThreads) s_tau[q] = tau[B_lo - 1 + q];
-  __syncthreads();
-  if (__ldcg(&w.g->overflow)) {
-    for (uint32_t i = blockIdx.x * blockDim.x + tid; i < r.n; i += gridDim.x * blockDim.x) {
-      const PackedState p = w.st[i];
-      uint32_t* out = w.keyrow + i;
-      for (uint32_t b = 0; b < nB; ++b) out[(size_t)(B_lo - 1 + b) * w.N_cap] = okey_of(p, s_tau[b]);
-    }
-    return;
-  }
-  const uint32_t ns = __ldcg(&w.g->n_surv);
-  const unsigned long long pairs = (unsigned long long)ns * nB;
-  for (unsigned long long pr = blockIdx.x * blockDim.x + tid; pr < pairs; pr += gridDim.x * blockDim.x) {
-    const uint32_t j = (uint32_t)(pr / nB), b = (uint32_t)(pr - (unsigned long long)j * nB);
-    const PackedState p = w.st[__ldcg(w.cand_idx + j)];
-    const double gn = gain_at(unpack_state(p), s_tau[b]);
-    const size_t o = (size_t)(B_lo - 1 + b) * w.S_cap + j;
-    w.cand[o] = composite(ordered_key(prio_key(gn, p.l)), p.rank);
-    w.cand_g[o] = gain_fixed(gn);
-  }
+  if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x + 1);
 }
 
 // ---------------------------------------------------------------- S4: Algorithm 1 per B
@@ -264,7 +248,15 @@ struct SelectArgs {
   SchedOut o;
 };
 
-__device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key, uint32_t* s_idx);
+struct FinSmem {
+  unsigned long long* key;   // [kVictCap] victim sort keys
+  uint32_t* idx;             // [kVictCap] victim request indices
+  unsigned long long* vcum;  // [kVictCap] prefix sums of victim l / sort scratch
+  uint32_t* adm;             // [kSortCap] S_{B*} in greedy order
+  unsigned long long* acum;  // [kSortCap] admit prefix sums
+  uint32_t* aflag;           // [kSortCap] admits (S \ R) in greedy order
+};
+__device__ void finalize_decision(const SelectArgs& A, const FinSmem& F);
 
 // Exact MSB-first radix select (8-bit digits) of the k-th largest of ne unique 64-bit
 // composites, then collection of the k largest into (s_key, s_idx), sorted descending.
@@ -348,119 +340,6 @@ __device__ uint32_t select_top_k(uint32_t ne, uint32_t k, Comp comp, Id id, unsi
   return cnt;
 }
 
-// CTA b handles B = b + 1: top min(B, n) requests by (key desc, rank asc), then Algorithm 1
-// (P:L514-529): take while the running sum of l stays <= M (count <= B by construction), break
-// at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken prefix.
-__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
-  extern __shared__ unsigned char s_dyn[];
-  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
-  __shared__ unsigned long long s_ps[kSortCap];
-  __shared__ long long s_gf[kSortCap];
-  __shared__ uint32_t s_k;
-  __shared__ long long s_red[32];
-
-  const ReqView& r = A.r;
-  const Work& w = A.w;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t B = blockIdx.x + 1;
-  const uint32_t n = r.n;
-  const bool trig = __ldcg(&w.g->triggered) != 0;
-  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
-  ANDES_TRACE(w, 2 * blockIdx.x);
-
-  if (!trig || B < B_lo || B > B_hi) {
-    if (tid == 0) {
-      A.o.V[B - 1] = (long long)0x8000000000000000ull;
-      A.o.kstar[B - 1] = 0u;
-    }
-  } else {
-    const uint32_t tB = A.tau[B - 1];
-    const uint32_t k = min(B, n);
-    uint32_t cnt;
-    if (__ldcg(&w.g->overflow)) {
-      const uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
-      cnt = select_top_k(
-          n, k,
-          [&](uint32_t e, bool low) -> unsigned long long {
-            return low ? composite(keys[e], r.rank[e]) : ((unsigned long long)keys[e] << 32);
-          },
-          [&](uint32_t e) { return e; }, s_key, s_idx);
-    } else {
-      const unsigned long long* row = w.cand + (size_t)(B - 1) * w.S_cap;
-      const uint32_t ns = __ldcg(&w.g->n_surv);
-      if (ns <= (uint32_t)kRankCap) {
-        // rank counting: position of each candidate = number of larger composites (unique)
-        unsigned long long* s_all = s_key + kSortCap;  // scratch after the first kSortCap slots
-        for (uint32_t e = tid; e < ns; e += kSelThreads) s_all[e] = __ldcg(row + e);
-        __syncthreads();
-        for (uint32_t e = tid; e < ns; e += kSelThreads) {
-          const unsigned long long c = s_all[e];
-          uint32_t pos = 0;
-          for (uint32_t f = 0; f < ns; ++f) pos += (s_all[f] > c) ? 1u : 0u;
-          if (pos < k) {
-            s_key[pos] = c;
-            s_idx[pos] = e;  // candidate slot
-          }
-        }
-        __syncthreads();
-        cnt = k;
-      } else {
-        cnt = select_top_k(
-            ns, k, [&](uint32_t e, bool) -> unsigned long long { return __ldcg(row + e); },
-            [&](uint32_t e) { return e; }, s_key, s_idx);
-      }
-      // slots -> request indices; the objective of a slot is its stored gfix
-      for (uint32_t q = tid; q < cnt; q += kSelThreads) {
-        const uint32_t e = s_idx[q];
-        s_ps[q] = (unsigned long long)__ldcg(w.cand_g + (size_t)(B - 1) * w.S_cap + e);  // temp: gfix
-        s_idx[q] = __ldcg(w.cand_idx + e);
-      }
-      __syncthreads();
-      for (uint32_t q = tid; q < cnt; q += kSelThreads) s_gf[q] = (long long)s_ps[q];
-      __syncthreads();
-    }
-    // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
-    // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
-    for (uint32_t q = tid; q < cnt; q += kSelThreads) s_ps[q] = r.ctx_len[s_idx[q]];
-    __syncthreads();
-    if (tid < 32) {
-      const uint32_t per = (cnt + 31) / 32, q0 = tid * per, q1 = min(cnt, q0 + per);
-      unsigned long long part = 0;
-      for (uint32_t q = q0; q < q1; ++q) part += s_ps[q];
-      unsigned long long inc = part;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (tid >= (uint32_t)o) inc += v;
-      }
-      unsigned long long run = inc - part;
-      uint32_t mine = 0;
-      for (uint32_t q = q0; q < q1; ++q) {
-        run += s_ps[q];
-        mine += (run <= A.M) ? 1u : 0u;
-      }
-      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-      if (tid == 0) s_k = mine;
-    }
-    __syncthreads();
-    const uint32_t kstar = s_k;
-    long long v = 0;
-    const bool ovf = __ldcg(&w.g->overflow) != 0;
-    for (uint32_t q = tid; q < kstar; q += kSelThreads) {
-      const uint32_t i = s_idx[q];
-      v += ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
-      w.sel[(size_t)(B - 1) * kMaxB + q] = i;
-    }
-    v = block_sum_ll<kSelThreads>(v, s_red);
-    if (tid == 0) {
-      A.o.V[B - 1] = v;
-      A.o.kstar[B - 1] = kstar;
-      w.sel_thr[B - 1] = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite: membership test
-    }
-  }
-  ANDES_TRACE(w, 2 * blockIdx.x + 1);
-}
-
 // In-place inclusive prefix sums of v[0..cnt) (cnt <= 8 * kSelThreads) by the whole CTA.
 __device__ void block_inclusive_scan(unsigned long long* v, uint32_t cnt, unsigned long long* s_tmp) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -475,8 +354,8 @@ __device__ void block_inclusive_scan(unsigned long long* v, uint32_t cnt, unsign
   }
   if (lane == 31) s_tmp[wid] = inc;
   __syncthreads();
-  unsigned long long wpre = 0;
-  for (uint32_t k = 0; k < wid; ++k) wpre += s_tmp[k];
+  unsigned long long wpre = lane < wid ? s_tmp[lane] : 0ull;  // kSelThreads / 32 <= 32 warps
+  for (int o = 16; o; o >>= 1) wpre += __shfl_xor_sync(0xffffffffu, wpre, o);
   unsigned long long run = wpre + inc - part;
   for (uint32_t q = lo; q < hi; ++q) {
     run += v[q];
@@ -488,16 +367,18 @@ __device__ void block_inclusive_scan(unsigned long long* v, uint32_t cnt, unsign
 // ---------------------------------------------------------------- S5 + S6 + outputs (one CTA)
 // serve_mask already holds the running set (written by prep); the decision edits only the
 // admitted and the preempted entries.
-__device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key, uint32_t* s_idx) {
+__device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
   __shared__ uint32_t s_Bstar, s_kstar, s_nv, s_na;
   __shared__ unsigned long long s_thr, s_W0;
   __shared__ long long s_bv[kSelThreads / 32];
   __shared__ uint32_t s_bb[kSelThreads / 32];
   __shared__ unsigned long long s_tmp[kSelThreads / 32];
-  __shared__ uint32_t s_adm[kSortCap];
-  __shared__ unsigned long long s_acum[kSortCap];
-  __shared__ uint32_t s_aflag[kSortCap];
-  unsigned long long* s_vcum = reinterpret_cast<unsigned long long*>(s_idx + kVictCap);  // [kVictCap]
+  unsigned long long* const s_key = F.key;
+  uint32_t* const s_idx = F.idx;
+  uint32_t* const s_adm = F.adm;
+  unsigned long long* const s_acum = F.acum;
+  uint32_t* const s_aflag = F.aflag;
+  unsigned long long* const s_vcum = F.vcum;
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -597,7 +478,21 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
   if (tid == 0) s_na = ks ? (uint32_t)s_acum[ks - 1] : 0u;
   __syncthreads();
   const uint32_t na = s_na;  // s_aflag[0..na) = admits in greedy order
-  bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
+  if (nv <= 2u * kSelThreads) {
+    // victim order by rank counting (sort keys are unique): position = #larger keys
+    uint32_t* const s_tmpidx = reinterpret_cast<uint32_t*>(s_vcum);
+    for (uint32_t q = tid; q < nv; q += kSelThreads) {
+      const unsigned long long c = s_key[q];
+      uint32_t pos = 0;
+      for (uint32_t f = 0; f < nv; ++f) pos += (s_key[f] > c) ? 1u : 0u;
+      s_tmpidx[pos] = s_idx[q];
+    }
+    __syncthreads();
+    for (uint32_t q = tid; q < nv; q += kSelThreads) s_idx[q] = s_tmpidx[q];
+    __syncthreads();
+  } else {
+    bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
+  }
   ANDES_TRACE(w, 2102);
   const uint32_t cap = A.preempt_cap;
   const bool cap_hit = !(cap == 0xFFFFFFFFu || nv <= cap);
@@ -670,11 +565,350 @@ __device__ void finalize_decision(const SelectArgs& A, unsigned long long* s_key
   ANDES_TRACE(w, 2105);
 }
 
-__global__ void __launch_bounds__(kSelThreads) k_finalize(SelectArgs A) {
+
+// Preemption cap (reading R18) for candidate B, precomputed by B's select CTA so that the final
+// step only picks B* and copies: victims R \ S_B (running requests whose composite at B is below
+// the k*-th selected composite) sorted by (key asc, rank desc); admits S_B \ R in greedy order;
+// then the cap walk.  Staged per B: preempt list, admit list, {n_pre, n_adm, realized, flags}.
+// Requires n_run <= kStageRun (the last CTA falls back to finalize_decision otherwise).
+__device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t kstar, unsigned long long thr,
+                          const uint32_t* s_sel, unsigned long long* vkey, uint32_t* vidx, unsigned long long* vcum,
+                          unsigned long long* acum, uint32_t* aflag) {
+  __shared__ uint32_t s_nv, s_na, s_e, s_a;
+  __shared__ unsigned long long s_W0;
+  __shared__ unsigned long long s_tmp[kSelThreads / 32];
+  const ReqView& r = A.r;
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t n_run = __ldcg(&w.g->n_run);
+  if (tid == 0) {
+    s_nv = 0;
+    s_W0 = 0;
+    s_e = 0;
+    s_a = 0;
+  }
+  __syncthreads();
+  {
+    unsigned long long wl = 0;
+    for (uint32_t q = tid; q < n_run; q += kSelThreads) {
+      const uint32_t i = __ldcg(w.run_list + q);
+      const PackedState st = w.st[i];
+      wl += st.l;
+      const unsigned long long c = comp_of(st, tB);
+      if (kstar == 0 || c < thr) {
+        const uint32_t slot = atomicAdd(&s_nv, 1u);
+        vkey[slot] = ~c;  // descending of ~c = ascending composite
+        vidx[slot] = i;
+      }
+    }
+    for (int o = 16; o; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+    if (lane == 0 && wl) atomicAdd(&s_W0, wl);
+  }
+  for (uint32_t q = tid; q < kstar; q += kSelThreads) acum[q] = r.running[s_sel[q]] ? 0ull : 1ull;
+  __syncthreads();
+  block_inclusive_scan(acum, kstar, s_tmp);
+  for (uint32_t q = tid; q < kstar; q += kSelThreads)
+    if (acum[q] != (q ? acum[q - 1] : 0ull)) aflag[acum[q] - 1] = s_sel[q];
+  if (tid == 0) s_na = kstar ? (uint32_t)acum[kstar - 1] : 0u;
+  // victim order by rank counting (keys unique)
+  const uint32_t nv = s_nv;
+  {
+    uint32_t* const tmp = reinterpret_cast<uint32_t*>(vcum);
+    for (uint32_t q = tid; q < nv; q += kSelThreads) {
+      const unsigned long long c = vkey[q];
+      uint32_t pos = 0;
+#pragma unroll 4
+      for (uint32_t f = 0; f < nv; ++f) pos += (vkey[f] > c) ? 1u : 0u;
+      tmp[pos] = vidx[q];
+    }
+    __syncthreads();
+    for (uint32_t q = tid; q < nv; q += kSelThreads) vidx[q] = tmp[q];
+    __syncthreads();
+  }
+  const uint32_t na = s_na;
+  const uint32_t cap = A.preempt_cap;
+  const bool cap_hit = !(cap == 0xFFFFFFFFu || nv <= cap);
+  uint32_t n_pre, n_adm, flags = 1u, realized;
+  if (!cap_hit) {
+    n_pre = nv;
+    n_adm = na;
+    realized = kstar;
+  } else {
+    flags |= 2u;
+    for (uint32_t q = tid; q < nv; q += kSelThreads) vcum[q] = r.ctx_len[vidx[q]];
+    __syncthreads();
+    block_inclusive_scan(vcum, nv, s_tmp);
+    const unsigned long long W0a = s_W0;
+    const unsigned long long W0 = W0a - (cap ? vcum[cap - 1] : 0ull);
+    const uint32_t c0 = n_run - cap;
+    if (W0 > A.M) {
+      flags |= 4u;  // memory beats the cap: keep preempting in victim order
+      if (tid == 0) s_e = nv;
+      __syncthreads();
+      for (uint32_t q = cap + tid; q < nv; q += kSelThreads)
+        if (W0a - vcum[q] <= A.M) atomicMin(&s_e, q + 1);
+      __syncthreads();
+      n_pre = s_e;
+      n_adm = 0;
+      realized = n_run - n_pre;
+    } else {
+      for (uint32_t q = tid; q < na; q += kSelThreads) acum[q] = r.ctx_len[aflag[q]];
+      __syncthreads();
+      block_inclusive_scan(acum, na, s_tmp);
+      uint32_t mine = 0;
+      for (uint32_t q = tid; q < na; q += kSelThreads) mine += (W0 + acum[q] <= A.M && c0 + q + 1 <= B) ? 1u : 0u;
+      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      if (lane == 0 && mine) atomicAdd(&s_a, mine);
+      __syncthreads();
+      n_pre = cap;
+      n_adm = s_a;
+      realized = c0 + n_adm;
+    }
+  }
+  uint32_t* pre = w.stage_pre + (size_t)(B - 1) * kStageRun;
+  uint32_t* adm = w.stage_adm + (size_t)(B - 1) * kMaxB;
+  for (uint32_t q = tid; q < n_pre; q += kSelThreads) pre[q] = vidx[q];
+  for (uint32_t q = tid; q < n_adm; q += kSelThreads) adm[q] = aflag[q];
+  if (tid == 0) w.stage_sc[B - 1] = make_uint4(n_pre, n_adm, realized, flags);
+}
+
+// S5 + copy of B*'s staged cap result into the outputs (last CTA of k_select).
+__device__ bool finalize_fast(const SelectArgs& A) {
+  __shared__ long long s_bv[kSelThreads / 32];
+  __shared__ uint32_t s_bb[kSelThreads / 32];
+  __shared__ uint32_t s_Bstar;
+  const ReqView& r = A.r;
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  {
+    long long bv = (long long)0x8000000000000000ull;
+    uint32_t bb = 0;
+    for (uint32_t B = B_lo + tid; B <= B_hi; B += kSelThreads) {
+      const long long v = __ldcg(A.o.V + (B - 1));
+      if (bb == 0 || v > bv || (v == bv && B > bb)) {
+        bv = v;
+        bb = B;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const long long v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const uint32_t b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+      if (b2 != 0 && (bb == 0 || v2 > bv || (v2 == bv && b2 > bb))) {
+        bv = v2;
+        bb = b2;
+      }
+    }
+    if (lane == 0) {
+      s_bv[wid] = bv;
+      s_bb[wid] = bb;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      bv = s_bv[0];
+      bb = s_bb[0];
+      for (uint32_t q = 1; q < kSelThreads / 32; ++q)
+        if (s_bb[q] != 0 && (bb == 0 || s_bv[q] > bv || (s_bv[q] == bv && s_bb[q] > bb))) {
+          bv = s_bv[q];
+          bb = s_bb[q];
+        }
+      s_Bstar = bb;
+    }
+    __syncthreads();
+  }
+  const uint32_t Bs = s_Bstar;
+  if (Bs == 0) return false;  // no candidate B: general path
+  const uint4 sc4 = __ldcg(w.stage_sc + (Bs - 1));
+  const uint32_t n_pre = sc4.x, n_adm = sc4.y;
+  const uint32_t* pre = w.stage_pre + (size_t)(Bs - 1) * kStageRun;
+  const uint32_t* adm = w.stage_adm + (size_t)(Bs - 1) * kMaxB;
+  for (uint32_t q = tid; q < n_pre; q += kSelThreads) {
+    const uint32_t i = __ldcg(pre + q);
+    A.o.preempt_idx[q] = i;
+    A.o.serve_mask[i] = 0;
+  }
+  for (uint32_t q = tid; q < n_adm; q += kSelThreads) {
+    const uint32_t i = __ldcg(adm + q);
+    A.o.admit_idx[q] = i;
+    A.o.serve_mask[i] = 1;
+  }
+  if (tid == 0) {
+    uint32_t flags = sc4.w;
+    if (__ldcg(&w.g->slow)) flags |= 8u;
+    uint32_t* sc = A.o.scalars;
+    sc[0] = Bs;
+    sc[1] = sc4.z;
+    sc[2] = n_adm;
+    sc[3] = n_pre;
+    sc[4] = B_lo;
+    sc[5] = B_hi;
+    sc[6] = flags;
+    sc[7] = __ldcg(A.o.kstar + (Bs - 1));
+  }
+  (void)r;
+  return true;
+}
+
+// CTA b handles B = b + 1: top min(B, n) requests by (key desc, rank asc), then Algorithm 1
+// (P:L514-529): take while the running sum of l stays <= M (count <= B by construction), break
+// at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken prefix; then B's cap result
+// is staged (stage_cap) and the last CTA to finish picks B* and writes the outputs.
+__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   extern __shared__ unsigned char s_dyn[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
-  finalize_decision(A, s_key, s_idx);
+  unsigned long long* s_vc = reinterpret_cast<unsigned long long*>(s_idx + kVictCap);
+  __shared__ unsigned long long s_ps[kSortCap];
+  __shared__ long long s_gf[kSortCap];
+  __shared__ uint32_t s_k, s_last;
+  __shared__ long long s_red[32];
+
+  const ReqView& r = A.r;
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t B = blockIdx.x + 1;
+  const uint32_t n = r.n;
+  pdl_wait();
+  pdl_trigger();
+  // the key histograms were consumed by k_compact: self-clean them for the next call
+  for (uint32_t q = blockIdx.x * blockDim.x + tid; q < kHistK; q += gridDim.x * blockDim.x) {
+    w.hist_lb[q] = 0u;
+    w.hist_ub[q] = 0u;
+  }
+  const bool trig = __ldcg(&w.g->triggered) != 0;
+  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  const bool ovf = __ldcg(&w.g->overflow) != 0;
+  const uint32_t ns = __ldcg(&w.g->n_surv);
+  const uint32_t n_run = __ldcg(&w.g->n_run);
+  ANDES_TRACE(w, 2 * blockIdx.x);
+
+  if (!trig || B < B_lo || B > B_hi) {
+    if (tid == 0) {
+      A.o.V[B - 1] = (long long)0x8000000000000000ull;
+      A.o.kstar[B - 1] = 0u;
+    }
+  } else {
+    const uint32_t tB = A.tau[B - 1];
+    const uint32_t k = min(B, n);
+    uint32_t cnt;
+    if (ovf) {
+      // overflow fallback: exact keys of every request at B (row B of keyrow), radix select
+      uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
+      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB);
+      __syncthreads();
+      cnt = select_top_k(
+          n, k,
+          [&](uint32_t e, bool low) -> unsigned long long {
+            return low ? composite(keys[e], r.rank[e]) : ((unsigned long long)keys[e] << 32);
+          },
+          [&](uint32_t e) { return e; }, s_key, s_idx);
+    } else {
+      // exact keys of the survivors at B (S3 for this B), then their order by rank counting:
+      // position = number of larger composites (unique); two composites per 16-byte load,
+      // the odd tail padded with 0 (never larger).  Scratch: composites past the first
+      // kSortCap slots of s_key, gfix in s_vc, request indices past kSortCap in s_idx.
+      unsigned long long* s_all = s_key + kSortCap;
+      uint32_t* s_ri = s_idx + kSortCap;
+      long long* s_gall = reinterpret_cast<long long*>(s_vc);
+      for (uint32_t e = tid; e < ns; e += kSelThreads) {
+        const uint32_t i = __ldcg(w.cand_idx + e);
+        const PackedState p = w.st[i];
+        const double gn = gain_at(unpack_state(p), tB);
+        s_all[e] = composite(ordered_key(prio_key(gn, p.l)), p.rank);
+        s_gall[e] = gain_fixed(gn);
+        s_ri[e] = i;
+      }
+      if (tid == 0) s_all[ns] = 0ull;
+      __syncthreads();
+      if (blockIdx.x == 255) ANDES_TRACE(w, 2400);
+      const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(s_all);
+      const uint32_t np = (ns + 1) >> 1;
+      for (uint32_t e = tid; e < ns; e += kSelThreads) {
+        const unsigned long long c = s_all[e];
+        uint32_t pos = 0;
+#pragma unroll 8
+        for (uint32_t f = 0; f < np; ++f) {
+          const ulonglong2 v = a2[f];
+          pos += (v.x > c ? 1u : 0u) + (v.y > c ? 1u : 0u);
+        }
+        if (pos < k) {
+          s_key[pos] = c;
+          s_idx[pos] = s_ri[e];
+          s_gf[pos] = s_gall[e];
+        }
+      }
+      __syncthreads();
+      if (blockIdx.x == 255) ANDES_TRACE(w, 2401);
+      cnt = k;
+    }
+    // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
+    // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
+    if (blockIdx.x == 255) ANDES_TRACE(w, 2402);
+    for (uint32_t q = tid; q < cnt; q += kSelThreads) s_ps[q] = r.ctx_len[s_idx[q]];
+    __syncthreads();
+    if (blockIdx.x == 255) ANDES_TRACE(w, 2403);
+    if (tid < 32) {
+      const uint32_t per = (cnt + 31) / 32, q0 = tid * per, q1 = min(cnt, q0 + per);
+      unsigned long long part = 0;
+      for (uint32_t q = q0; q < q1; ++q) part += s_ps[q];
+      unsigned long long inc = part;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= (uint32_t)o) inc += v;
+      }
+      unsigned long long run = inc - part;
+      uint32_t mine = 0;
+      for (uint32_t q = q0; q < q1; ++q) {
+        run += s_ps[q];
+        mine += (run <= A.M) ? 1u : 0u;
+      }
+      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      if (tid == 0) s_k = mine;
+    }
+    __syncthreads();
+    const uint32_t kstar = s_k;
+    long long v = 0;
+    for (uint32_t q = tid; q < kstar; q += kSelThreads) {
+      const uint32_t i = s_idx[q];
+      v += ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
+      w.sel[(size_t)(B - 1) * kMaxB + q] = i;
+    }
+    v = block_sum_ll<kSelThreads>(v, s_red);
+    const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
+    if (tid == 0) {
+      A.o.V[B - 1] = v;
+      A.o.kstar[B - 1] = kstar;
+      w.sel_thr[B - 1] = thr;
+    }
+    if (blockIdx.x == 255) ANDES_TRACE(w, 2404);
+    if (n_run <= (uint32_t)kStageRun) {
+      // victims and their prefix sums live past the first kStageRun slots of s_key / s_idx
+      stage_cap(A, B, tB, kstar, thr, s_idx, s_key + kStageRun, s_idx + kStageRun, s_vc,
+                reinterpret_cast<unsigned long long*>(s_ps), reinterpret_cast<uint32_t*>(s_gf));
+    }
+    if (blockIdx.x == 255) ANDES_TRACE(w, 2405);
+  }
+  ANDES_TRACE(w, 2 * blockIdx.x + 1);
+  // the last CTA to finish runs S5 + S6 (last-block pattern)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&w.g->done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  ANDES_TRACE(w, 2100);
+  if (trig && n_run <= (uint32_t)kStageRun && finalize_fast(A)) {
+    ANDES_TRACE(w, 2105);
+    return;
+  }
+  FinSmem F;
+  F.key = s_key;
+  F.idx = s_idx;
+  F.vcum = s_vc;
+  F.acum = s_ps;
+  F.adm = reinterpret_cast<uint32_t*>(s_gf);
+  F.aflag = reinterpret_cast<uint32_t*>(s_gf) + kSortCap;
+  finalize_decision(A, F);
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -683,34 +917,32 @@ void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, i
                           float* key_out, double* qwait_out) {
   if (r.n == 0) return;
   const uint32_t blocks = umin32((r.n + 255) / 256, L.sm_count * 8);
-  k_gain_estimate<<<blocks, 256, 0, L.stream>>>(r, w, now, horizon, tau, B_list_dev, nB, gain_out, key_out,
-                                                qwait_out);
+  launch_pdl(k_gain_estimate, blocks, 256, 0, L.stream, r, w, now, horizon, tau, B_list_dev, nB, gain_out, key_out,
+             qwait_out);
 }
 
 void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon) {
   const uint32_t blocks = r.n ? umin32((r.n + kStateThreads - 1) / kStateThreads, L.sm_count * 4) : 1u;
-  k_state<<<blocks, kStateThreads, 0, L.stream>>>(r, w, now, horizon);
+  launch_pdl(k_state, blocks, kStateThreads, 0, L.stream, r, w, now, horizon);
 }
 
 void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau) {
-  const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count * 4) : 1u;
-  k_compact<<<cblocks, kCandThreads, 0, L.stream>>>(r, w);
-  k_cand<<<L.sm_count * 4, kCandThreads, 0, L.stream>>>(r, w, tau);
+  const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count) : 1u;
+  launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w);
+  (void)tau;
 }
 
-static size_t select_smem() { return (sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
-static size_t finalize_smem() { return (2 * sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
+// victims keys + indices + prefix sums (the fused S5/S6 tail needs all three)
+static size_t select_smem() { return (2 * sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
 
 void init_kernels() {
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
-  cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)finalize_smem());
 }
 
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
   SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o};
-  k_select<<<B_cap, kSelThreads, select_smem(), L.stream>>>(A);
-  k_finalize<<<1, kSelThreads, finalize_smem(), L.stream>>>(A);
+  launch_pdl(k_select, B_cap, kSelThreads, select_smem(), L.stream, A);
 }
 
 }  // namespace andes

@@ -290,3 +290,21 @@ def _iterate(A, ctx, orc, iters=200, seed=1):
 
 def test_config1_iteration_driver(A, ctx, orc):
     assert _iterate(A, ctx, orc) >= 150
+
+
+def test_schedule_survivor_overflow_fallback(A, ctx, orc):
+    """More survivors than the pruned path holds (identical late requests: every bound ties, so
+    every request survives): k_select evaluates every request at its B and radix-selects
+    (ANDES_F_SLOW_PATH); the decision must still equal the oracle's."""
+    n = 3500
+    tl = [(np.arange(6, dtype=np.uint32) * 250_000 + 1_400_000) for _ in range(n)]
+    g, base, pool = W._pack(tl)
+    rng = np.random.default_rng(11)
+    snap = W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, 1_000_000, np.uint32),
+                      period_us=np.full(n, 208_333, np.uint32), ctx_len=np.full(n, 100, np.uint32),
+                      n_deliv=g, max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=rng.permutation(n).astype(np.uint32), running=(rng.random(n) < 0.02).astype(np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=3_000_000, horizon_us=2_000_000,
+                      tau_us=W.tau_table(48), kv_capacity=4000)
+    gg, o = _check_sched(A, ctx, orc, snap, cap=5)
+    assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH

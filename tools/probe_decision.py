@@ -22,7 +22,7 @@ for it in range(5):
     st = ctx.profile_read()
 torch.cuda.synchronize()
 g = np.zeros(32, np.uint32)
-rc = L.andes_debug_read(ctx._h, 5, g.ctypes.data.__index__() if hasattr(g.ctypes.data, "__index__") else g.ctypes.data, 104)
+rc = L.andes_debug_read(ctx._h, 5, g.ctypes.data, 96)
 print("debug_read rc", rc)
 names = ["run_l_lo", "run_l_hi", "pool_end_lo", "pool_end_hi", "ntiles", "inv_minP", "n_run", "done", "B_lo",
          "B_hi", "triggered", "err", "slow", "tile_ctr", "prep_done", "state_done", "tau_lo", "tau_hi", "theta",
