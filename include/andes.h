@@ -183,6 +183,51 @@ int andes_schedule(AndesCtx *ctx, const AndesRequests *req, const AndesSchedPara
 int andes_schedule_host(AndesCtx *ctx, const AndesRequests *req_host, const AndesSchedParams *p_host,
                         AndesDecision *out_host, void *stream);
 
+/* ---- Multi-GPU decision ------------------------------------------
+ * One process per GPU; rank g holds a contiguous range of the population (its requests have
+ * global indices base_g .. base_g + n_g - 1, base_g = n_0 + ... + n_{g-1}; the rank fields must
+ * be unique over all ranks).  The decision runs as ANDES_SHARD_STEPS asynchronous steps on the
+ * caller's stream.  After step s (s = 0..3) the caller all-gathers every rank's send block of
+ * xbytes[s] bytes, in rank order, into each rank's recv buffer of world * xbytes[s] bytes
+ * (ncclAllGather / torch.distributed.all_gather_into_tensor on the same stream), and passes that
+ * recv buffer to step s + 1:
+ *   step 0: request prep + timeline scan (S1), round-0 block: trigger inputs, l histogram
+ *   step 1: global trigger and B range (S0, S2), gain state and key bounds (S3), round-1 block:
+ *           the rank's lower-bound key histogram
+ *   step 2: global theta, survivors, exact keys at every B, round-2 block: per B the rank's
+ *           top-min(B, survivors) in Algorithm 1's order
+ *   step 3: merge of the ranks' lists, Algorithm 1's walk, V(B), B* (S4, S5), round-3 block:
+ *           the rank's preemption victims at B*
+ *   step 4: preemption cap (S6) and outputs.
+ * Outputs: scalars, V, kstar are replicated (identical on every rank); admit_idx and
+ * preempt_idx hold GLOBAL request indices (identical on every rank; preempt_idx must hold the
+ * global victim count, at most 4096); serve_mask covers this rank's n requests.  The decision
+ * equals andes_schedule on the concatenated population bit for bit (all payloads are integers).
+ * Limits: world <= ANDES_MAX_WORLD, running requests per rank <= 2048 (else ANDES_E_CAPACITY on
+ * the next call).  Send and recv buffers are DEVICE memory owned by the caller, 16-byte aligned. */
+#define ANDES_SHARD_ROUNDS 4
+#define ANDES_SHARD_STEPS 5
+#define ANDES_MAX_WORLD 8
+typedef struct {
+    uint32_t world;                       /* number of ranks, 1..ANDES_MAX_WORLD             */
+    uint32_t rank;                        /* this rank, < world                             */
+    uint32_t B_cap;                       /* must equal AndesSchedParams.B_cap of the calls */
+    uint32_t pad;
+    uint64_t xbytes[ANDES_SHARD_ROUNDS];  /* send block bytes after step s                  */
+} AndesShard;
+
+/* Fills *out for (world, rank, B_cap).  Errors: ANDES_E_INVAL. */
+int andes_shard_init(AndesCtx *ctx, uint32_t world, uint32_t rank, uint32_t B_cap, AndesShard *out);
+
+/* One step (0..ANDES_SHARD_STEPS-1) of the sharded decision; `local` is this rank's request
+ * table (DEVICE memory, as for andes_schedule).  recv: NULL for step 0, else the gathered blocks
+ * of round step-1.  send: this rank's block of round `step` (steps 0..3; NULL for step 4).
+ * Every step must be issued with the same req / params / out.  Errors: ANDES_E_INVAL,
+ * ANDES_E_CAPACITY, ANDES_E_RANGE, ANDES_E_CUDA. */
+int andes_schedule_shard(AndesCtx *ctx, const AndesShard *shard, uint32_t step, const AndesRequests *local,
+                         const AndesSchedParams *p, AndesDecision *out, const void *recv, void *send,
+                         void *stream);
+
 /* Per-stage timing.  When enabled, andes_schedule records a CUDA event before its first
  * and after each of its kernels on the call's stream (also under stream capture, so a
  * captured CUDA graph of a decision carries the event-record nodes).  andes_profile_read

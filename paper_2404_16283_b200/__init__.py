@@ -10,6 +10,9 @@ Entry points (same names as the C ABI):
     Context.gain_estimate   -> andes_gain_estimate
     Context.schedule        -> andes_schedule
     Context.schedule_host   -> andes_schedule_host
+    Context.shard_init      -> andes_shard_init
+    Context.schedule_shard  -> andes_schedule_shard (one step); schedule_sharded() runs all steps
+                               with a caller-supplied all-gather (torch.distributed / NCCL)
 """
 from __future__ import annotations
 
@@ -35,7 +38,11 @@ UINT32_MAX = 0xFFFFFFFF
 SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags", "k_star"]
 
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
-           "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read"]
+           "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
+           "andes_shard_init", "andes_schedule_shard"]
+SHARD_ROUNDS = 4
+SHARD_STEPS = 5
+MAX_WORLD = 8
 N_STAGES = 6
 STAGES = ["prep", "scan", "state", "cand", "select", "unused"]
 
@@ -66,6 +73,11 @@ class SchedParams(C.Structure):
 class DecisionPtrs(C.Structure):
     _fields_ = [("serve_mask", C.c_void_p), ("admit_idx", C.c_void_p), ("preempt_idx", C.c_void_p),
                 ("scalars", C.c_void_p), ("V", C.c_void_p), ("kstar", C.c_void_p)]
+
+
+class Shard(C.Structure):
+    _fields_ = [("world", C.c_uint32), ("rank", C.c_uint32), ("B_cap", C.c_uint32), ("pad", C.c_uint32),
+                ("xbytes", C.c_uint64 * SHARD_ROUNDS)]
 
 
 class QoeOut(C.Structure):
@@ -100,6 +112,10 @@ def lib() -> C.CDLL:
         L.andes_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
         L.andes_schedule_host.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
                                           C.POINTER(DecisionPtrs), C.c_void_p]
+        L.andes_shard_init.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Shard)]
+        L.andes_schedule_shard.argtypes = [C.c_void_p, C.POINTER(Shard), C.c_uint32, C.POINTER(Requests),
+                                           C.POINTER(SchedParams), C.POINTER(DecisionPtrs), C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
         _lib = L
     return _lib
 
@@ -274,3 +290,80 @@ class Context:
         rc = self._check(lib().andes_schedule_host(self._h, C.byref(_req_struct(req_host, n)), C.byref(p),
                                                    C.byref(d), _stream_ptr(stream)), "andes_schedule_host")
         return out, rc
+
+    # -- multi-GPU decision (andes_shard_init / andes_schedule_shard)
+    def shard_init(self, world: int, rank: int, B_cap: int) -> Shard:
+        sh = Shard()
+        self._check(lib().andes_shard_init(self._h, int(world), int(rank), int(B_cap), C.byref(sh)),
+                    "andes_shard_init")
+        return sh
+
+    def alloc_shard_buffers(self, sh: Shard):
+        """Device send blocks (one per round) and recv buffers (world blocks each)."""
+        torch = _torch()
+        send = [torch.empty(int(sh.xbytes[k]), dtype=torch.uint8, device=self.device) for k in range(SHARD_ROUNDS)]
+        recv = [torch.empty(int(sh.world) * int(sh.xbytes[k]), dtype=torch.uint8, device=self.device)
+                for k in range(SHARD_ROUNDS)]
+        return send, recv
+
+    def schedule_shard(self, sh: Shard, step: int, req: dict, n: int, now_us: int, horizon_us: int, tau,
+                       kv_capacity: int, out: Decision, recv=None, send=None, preempt_cap=UINT32_MAX,
+                       cur_latency_us=0, flags=ANDES_FORCE, stream=None):
+        p = SchedParams(int(now_us), int(horizon_us), int(tau.numel()), _ptr(tau), int(kv_capacity),
+                        int(preempt_cap), int(cur_latency_us), int(flags))
+        d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
+                         _ptr(out.V), _ptr(out.kstar))
+        self._check(lib().andes_schedule_shard(self._h, C.byref(sh), int(step), C.byref(_req_struct(req, n)),
+                                               C.byref(p), C.byref(d), _ptr(recv), _ptr(send),
+                                               _stream_ptr(stream)), "andes_schedule_shard")
+
+    def alloc_shard_decision(self, n, B_cap):
+        """Decision buffers of a sharded call: preempt_idx holds the global victim list."""
+        torch = _torch()
+        d = self.alloc_decision(n, B_cap)
+        d.preempt = torch.empty(4096, dtype=torch.int32, device=self.device)
+        return d
+
+
+def torch_allgather(group=None):
+    """allgather(send, recv) over torch.distributed: every rank's send block, in rank order, into
+    recv (NCCL on GPUs; also works with gloo on CPU tensors)."""
+    import torch.distributed as dist
+
+    def ag(send, recv):
+        try:
+            dist.all_gather_into_tensor(recv, send, group=group)
+        except (RuntimeError, NotImplementedError, AttributeError):
+            dist.all_gather(list(recv.chunk(dist.get_world_size(group))), send, group=group)
+    return ag
+
+
+def run_shard_steps(step_fn, allgather, send, recv, steps=SHARD_STEPS):
+    """Host orchestration of a sharded decision: step s runs on this rank (step_fn(s, recv_prev,
+    send_s)); after every step but the last, this rank's send block is all-gathered in rank order
+    into recv[s] (allgather(send_s, recv_s), e.g. torch.distributed.all_gather_into_tensor).
+    Argument marshalling only: every step's arithmetic runs in the library's kernels."""
+    prev = None
+    for s in range(steps):
+        cur = send[s] if s < len(send) else None
+        step_fn(s, prev, cur)
+        if cur is not None:
+            allgather(cur, recv[s])
+            prev = recv[s]
+    return prev
+
+
+def schedule_sharded(ctx: Context, sh: Shard, req: dict, n: int, now_us: int, horizon_us: int, tau,
+                     kv_capacity: int, allgather, out: Decision | None = None, bufs=None, preempt_cap=UINT32_MAX,
+                     cur_latency_us=0, flags=ANDES_FORCE, stream=None) -> Decision:
+    """One sharded decision on this rank.  allgather(send, recv) must gather every rank's send
+    block in rank order into recv on `stream` (torch.distributed.all_gather_into_tensor)."""
+    out = out or ctx.alloc_shard_decision(n, int(tau.numel()))
+    send, recv = bufs or ctx.alloc_shard_buffers(sh)
+
+    def step(s, prev, cur):
+        ctx.schedule_shard(sh, s, req, n, now_us, horizon_us, tau, kv_capacity, out, recv=prev, send=cur,
+                           preempt_cap=preempt_cap, cur_latency_us=cur_latency_us, flags=flags, stream=stream)
+
+    run_shard_steps(step, allgather, send, recv)
+    return out

@@ -239,6 +239,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   c->sm_count = (uint32_t)sms;
   init_kernels();
   init_scan_kernels();
+  init_shard_kernels();
   const int bps = scan_blocks_per_sm();
   c->scan_grid = (uint32_t)(sms * (bps > 0 ? bps : 1));
   const uint32_t N = lim->max_requests;
@@ -262,6 +263,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.stage_pre, (size_t)lim->max_B * kStageRun)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.stage_adm, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.stage_sc, (size_t)lim->max_B)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.xm, tri_off(lim->max_B + 1))) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
@@ -467,13 +469,88 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   mark(c, 2, s);
   launch_state(L, r, w, p->now_us, p->horizon_us);
   mark(c, 3, s);
-  launch_cand(L, r, w, p->tau_us);
+  launch_compact(L, r, w, nullptr, 1u);
   mark(c, 4, s);
   launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
   mark(c, 5, s);
   mark(c, 6, s);
   if (c->prof) c->prof_recorded = true;
   return finish_call(c, s, debug);
+}
+
+int andes_shard_init(AndesCtx* c, uint32_t world, uint32_t rank, uint32_t B_cap, AndesShard* out) {
+  if (!c || !out) return ANDES_E_INVAL;
+  if (world == 0 || world > kMaxWorld || rank >= world) return set_err(c, ANDES_E_INVAL, "bad world/rank%s");
+  if (B_cap == 0 || B_cap > c->lim.max_B) return set_err(c, ANDES_E_INVAL, "bad B_cap%s");
+  out->world = world;
+  out->rank = rank;
+  out->B_cap = B_cap;
+  out->pad = 0;
+  out->xbytes[0] = sizeof(ShardSummary);
+  out->xbytes[1] = sizeof(uint32_t) * kHistK;
+  out->xbytes[2] = sizeof(XEntry) * tri_off(B_cap + 1);
+  out->xbytes[3] = sizeof(ShardVictims);
+  return ANDES_OK;
+}
+
+int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const AndesRequests* req,
+                         const AndesSchedParams* p, AndesDecision* out, const void* recv, void* send, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  if (!sh || sh->world == 0 || sh->world > kMaxWorld || sh->rank >= sh->world)
+    return set_err(c, ANDES_E_INVAL, "bad shard plan%s");
+  if (step >= ANDES_SHARD_STEPS) return set_err(c, ANDES_E_INVAL, "step out of range%s");
+  if ((step > 0 && !recv) || (step < ANDES_SHARD_ROUNDS && !send))
+    return set_err(c, ANDES_E_INVAL, "recv/send buffer is NULL%s");
+  if ((reinterpret_cast<uintptr_t>(recv) | reinterpret_cast<uintptr_t>(send)) & 15u)
+    return set_err(c, ANDES_E_INVAL, "recv/send must be 16-byte aligned%s");
+  int rc = ANDES_OK;
+  if (step == 0 && (rc = pending_device_error(c))) return rc;
+  if ((rc = check_requests(c, req, true))) return rc;
+  if (!p || !out) return set_err(c, ANDES_E_INVAL, "params/out is NULL%s");
+  if (!p->tau_us || p->B_cap == 0 || p->B_cap != sh->B_cap || p->B_cap > c->lim.max_B)
+    return set_err(c, ANDES_E_INVAL, "bad tau/B_cap (must match the shard plan)%s");
+  if (p->horizon_us == 0 || p->kv_capacity == 0) return set_err(c, ANDES_E_INVAL, "horizon and M must be >= 1%s");
+  if (!out->scalars || !out->V || !out->kstar || !out->preempt_idx || !out->admit_idx ||
+      (req->n && !out->serve_mask))
+    return set_err(c, ANDES_E_INVAL, "a decision output is NULL%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LaunchCfg L = cfg_of(c, stream);
+  const ReqView r = view_of(req);
+  const Work w = work_of(c, r.n);
+  const int64_t eval = p->now_us + (int64_t)p->horizon_us;
+  const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
+  SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
+  switch (step) {
+    case 0: {
+      if ((rc = reset_call(c, s))) return rc;
+      launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
+      const CUtensorMap* tm = &c->pool_map;
+      if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
+      launch_scan(L, r, w, eval, false, tm);
+      launch_shard_summary(L, r, w, p->B_cap, static_cast<ShardSummary*>(send));
+      break;
+    }
+    case 1:
+      launch_shard_bounds(L, w, static_cast<const ShardSummary*>(recv), sh->world, sh->rank, p->tau_us, p->B_cap,
+                          p->kv_capacity, p->cur_latency_us, p->flags);
+      launch_state(L, r, w, p->now_us, p->horizon_us);
+      launch_shard_copy_lb(L, w, static_cast<uint32_t*>(send));
+      break;
+    case 2:
+      launch_compact(L, r, w, static_cast<const uint32_t*>(recv), sh->world);
+      launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o,
+                    static_cast<XEntry*>(send));
+      break;
+    case 3:
+      launch_shard_merge(L, r, w, static_cast<const XEntry*>(recv), sh->world, p->tau_us, p->B_cap, p->kv_capacity,
+                         o, static_cast<ShardVictims*>(send));
+      break;
+    default:
+      launch_shard_cap(L, r, w, static_cast<const ShardVictims*>(recv), sh->world, p->B_cap, p->kv_capacity,
+                       p->preempt_cap, o);
+      return finish_call(c, s, debug);
+  }
+  return finish_call(c, s, false);
 }
 
 int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedParams* p, AndesDecision* out,

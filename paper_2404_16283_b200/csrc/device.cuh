@@ -98,7 +98,11 @@ struct Globals {
   uint32_t n_surv;               // requests with UB >= theta (candidates)
   uint32_t overflow;             // n_surv above the candidate capacity: full-N fallback
   uint32_t cand_ctr;             // candidate slot counter
-  uint32_t pad[2];
+  // multi-GPU decision (shard.cu); run_l / inv_minP hold the global values after step 1
+  uint32_t shard_base;           // global index of this rank's first request
+  uint32_t n_global;             // requests over all ranks
+  uint32_t n_run_global;         // running requests over all ranks
+  uint32_t shard_Bstar;          // B* (step 3 -> step 4)
 };
 
 // B-independent per-request state for the gain closed form,
@@ -109,6 +113,34 @@ struct alignas(16) PackedState {
   uint32_t m, K, P, h0, l, rank;
   uint32_t pad[2];
 };
+
+// ---------------------------------------------------------------- multi-GPU exchange blocks
+// Round 0: one rank's trigger / batch-size-range inputs.
+struct ShardSummary {
+  uint32_t n, n_run, minP, has_ovf;  // has_ovf: ovf[] holds this rank's smallest long contexts
+  unsigned long long run_l;
+  uint32_t pad[2];
+  uint32_t hist[kHistL];             // l histogram (last bin: l >= kHistL - 1)
+  uint32_t ovf[kMaxB];               // smallest l >= kHistL - 1, ascending, UINT32_MAX padded
+};
+// Round 2: one entry of a rank's local top-B list of candidate B (Algorithm 1's order).
+struct alignas(8) XEntry {
+  unsigned long long comp;  // composite (key desc, rank asc); 0 = padding
+  long long gfix;           // llrint(gain 2^32)
+  uint32_t l;               // context length
+  uint32_t gidx;            // global request index | 0x80000000 if running
+};
+static_assert(sizeof(XEntry) == 24, "XEntry layout");
+// Round 3: one rank's preemption victims at B* (running requests outside S_{B*}).
+struct VictimX {
+  unsigned long long comp;
+  uint32_t l, gidx;
+};
+struct ShardVictims {
+  uint32_t count, pad[3];
+  VictimX v[kStageRun];
+};
+__host__ __device__ __forceinline__ size_t tri_off(uint32_t B) { return (size_t)B * (B - 1) / 2; }
 
 struct Work {
   uint32_t* m;               // [N] tokens due at the evaluation time
@@ -130,6 +162,7 @@ struct Work {
   uint32_t* stage_pre;       // [max_B][kStageRun] preempt list per candidate B (cap applied)
   uint32_t* stage_adm;       // [max_B][kMaxB] admit list per candidate B
   uint4* stage_sc;           // [max_B] {n_pre, n_adm, realized, flags} per candidate B
+  XEntry* xm;                // [tri(max_B + 1)] merged Algorithm 1 prefixes per B (multi-GPU)
   Globals* g;
   unsigned long long* trace; // optional %globaltimer stamps (internal debugging), may be null
   uint32_t N_cap;            // row stride of keyrow

@@ -59,7 +59,20 @@ void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, i
 void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon);
 void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau);
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
-                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
+                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o,
+                   XEntry* xsend = nullptr);
+void launch_compact(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* lb_src, uint32_t G);
+// multi-GPU decision steps (shard.cu)
+constexpr uint32_t kMaxWorld = 8;
+void launch_shard_summary(const LaunchCfg& L, const ReqView& r, const Work& w, uint32_t B_cap, ShardSummary* out);
+void launch_shard_bounds(const LaunchCfg& L, const Work& w, const ShardSummary* all, uint32_t G, uint32_t rank,
+                         const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t cur_latency, uint32_t flags);
+void launch_shard_copy_lb(const LaunchCfg& L, const Work& w, uint32_t* send);
+void launch_shard_merge(const LaunchCfg& L, const ReqView& r, const Work& w, const XEntry* recv, uint32_t G,
+                        const uint32_t* tau, uint32_t B_cap, uint64_t M, const SchedOut& o, ShardVictims* send);
+void launch_shard_cap(const LaunchCfg& L, const ReqView& r, const Work& w, const ShardVictims* recv, uint32_t G,
+                      uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
+void init_shard_kernels();
 void init_kernels();
 
 }  // namespace andes

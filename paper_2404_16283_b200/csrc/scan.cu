@@ -401,20 +401,6 @@ struct RawWin {
     if (q >= wn || (dummy && q == 0)) return null_entry(q >= wn);
     return entry_of(rec[q - dummy], r0 + q - dummy, p0);
   }
-  // (unused helper kept for the global path)
-  // owner of position x given start(q + 1) <= x: the last q' > q with start(q') <= x.  Runs of
-  // empty requests (no tokens yet) share one start; binary search keeps them O(log) per event.
-  __device__ __forceinline__ uint32_t advance(uint32_t q, int32_t x) const {
-    uint32_t lo = q + 1;
-    if (start(lo + 1) > x) return lo;
-    uint32_t hi = wn - 1;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (start(mid) <= x) lo = mid;
-      else hi = mid - 1;
-    }
-    return lo;
-  }
 };
 
 // One warp-tile: 32 lanes x 32 tokens.  Tokens of request q at local position x have ideal

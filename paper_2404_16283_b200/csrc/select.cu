@@ -17,6 +17,7 @@
 //             result staged; the last CTA picks B* and writes the outputs.
 // If the survivors exceed the capacity, k_select evaluates every request at its B and
 // radix-selects instead (slow path, flagged).
+#include "block.cuh"
 #include "device.cuh"
 #include "launch.h"
 
@@ -36,57 +37,6 @@ __global__ void k_gain_estimate(ReqView r, Work w, int64_t now, uint32_t horizon
       const double gn = gain_at(s, tau[B_list[b] - 1]);
       if (gain_out) gain_out[(size_t)b * r.n + i] = gn;
       if (key_out) key_out[(size_t)b * r.n + i] = prio_key(gn, l);
-    }
-  }
-}
-
-// ---------------------------------------------------------------- block helpers
-__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau) {
-  return ordered_key(prio_key(gain_at(unpack_state(p), tau), p.l));
-}
-
-__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau) {
-  return composite(okey_of(p, tau), p.rank);
-}
-
-template <int NT>
-__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  long long t = 0;
-  if (threadIdx.x < 32) {
-    t = (threadIdx.x < NT / 32) ? red[threadIdx.x] : 0;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  t = red[0];
-  __syncthreads();
-  return t;
-}
-
-// In-place bitonic sort of (key, idx) pairs in shared memory, size = power of two.
-template <int NT>
-__device__ void bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t size, bool descending) {
-  for (uint32_t k = 2; k <= size; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t t = threadIdx.x; t < size; t += NT) {
-        const uint32_t p = t ^ j;
-        if (p > t) {
-          const bool up = ((t & k) == 0) == descending;
-          const unsigned long long a = key[t], b = key[p];
-          if ((a < b) == up) {
-            key[t] = b;
-            key[p] = a;
-            const uint32_t x = idx[t];
-            idx[t] = idx[p];
-            idx[p] = x;
-          }
-        }
-      }
-      __syncthreads();
     }
   }
 }
@@ -144,7 +94,9 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
 // theta = lower edge of the highest LB bucket b* with #(LB in buckets >= b*) >= B_hi, and the
 // survivor count #(UB bucket >= b*); computed redundantly by every CTA of k_compact from the
 // completed histograms (16 KB each, L2-resident), so no CTA waits on a last-block reduction.
-__device__ __forceinline__ void theta_of(const Work& w, uint32_t need, uint32_t& cut, uint32_t& nsurv) {
+// lb_src: G lower-bound histograms (stride kHistK), summed (multi-GPU: one per rank).
+__device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, uint32_t G, uint32_t need,
+                                         uint32_t& cut, uint32_t& nsurv) {
   constexpr uint32_t NT = kCandThreads, kPer = kHistK / NT;  // 16 buckets per thread, descending
   __shared__ uint32_t s_w[NT / 32], s_cut, s_sv[NT / 32];
   __shared__ uint32_t s_h[kHistK];
@@ -153,7 +105,9 @@ __device__ __forceinline__ void theta_of(const Work& w, uint32_t need, uint32_t&
   uint32_t hu[kPer];
 #pragma unroll
   for (uint32_t q = 0; q < kPer; ++q) {
-    s_h[q * NT + tid] = __ldcg(&w.hist_lb[q * NT + tid]);
+    uint32_t v = 0;
+    for (uint32_t g = 0; g < G; ++g) v += __ldcg(&lb_src[(size_t)g * kHistK + q * NT + tid]);
+    s_h[q * NT + tid] = v;
     hu[q] = __ldcg(&w.hist_ub[q * NT + tid]);
   }
   __syncthreads();
@@ -199,13 +153,13 @@ __device__ __forceinline__ void theta_of(const Work& w, uint32_t need, uint32_t&
 }
 
 // Compaction of the survivors (UB >= theta) into cand_idx, warp-aggregated appends.
-__global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w) {
+__global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, const uint32_t* lb_src, uint32_t G) {
   pdl_wait();
   pdl_trigger();
   if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
   if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
   uint32_t cut, ns;
-  theta_of(w, __ldcg(&w.g->B_hi), cut, ns);
+  theta_of(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, __ldcg(&w.g->B_hi), cut, ns);
   if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
   const uint32_t theta = cut << 20;
   const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
@@ -231,11 +185,6 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w) {
 }
 
 // ---------------------------------------------------------------- S4: Algorithm 1 per B
-constexpr int kSelThreads = 512;
-constexpr int kSortCap = kMaxB;
-constexpr int kVictCap = kMaxRunning;
-constexpr int kRankCap = kVictCap - kSortCap;  // candidates ranked directly in shared memory
-
 struct SelectArgs {
   ReqView r;
   Work w;
@@ -246,6 +195,7 @@ struct SelectArgs {
   uint64_t M;
   uint32_t preempt_cap;
   SchedOut o;
+  XEntry* xsend;  // multi-GPU step 2: this rank's local top-B lists (no walk / cap here)
 };
 
 struct FinSmem {
@@ -257,112 +207,6 @@ struct FinSmem {
   uint32_t* aflag;           // [kSortCap] admits (S \ R) in greedy order
 };
 __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F);
-
-// Exact MSB-first radix select (8-bit digits) of the k-th largest of ne unique 64-bit
-// composites, then collection of the k largest into (s_key, s_idx), sorted descending.
-// comp(e, low) returns element e's composite (its low 32 bits are needed only when low is
-// true); id(e) the request index stored with it.
-template <class Comp, class Id>
-__device__ uint32_t select_top_k(uint32_t ne, uint32_t k, Comp comp, Id id, unsigned long long* s_key,
-                                 uint32_t* s_idx) {
-  __shared__ uint32_t s_hist[256];
-  __shared__ unsigned long long s_prefix;
-  __shared__ uint32_t s_need, s_cnt;
-  __shared__ int s_stop;
-  const uint32_t tid = threadIdx.x;
-  unsigned long long prefix = 0ull, mask = 0ull;
-  uint32_t need = k;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (uint32_t q = tid; q < 256; q += kSelThreads) s_hist[q] = 0u;
-    __syncthreads();
-    for (uint32_t e = tid; e < ne; e += kSelThreads) {
-      const unsigned long long c = comp(e, shift < 32);
-      if ((c & mask) == prefix) atomicAdd(&s_hist[(uint32_t)(c >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      uint32_t cnt[8], tot = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        cnt[j] = s_hist[255 - 8 * tid - j];
-        tot += cnt[j];
-      }
-      uint32_t inc = tot;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (tid >= (uint32_t)o) inc += v;
-      }
-      const uint32_t exc = inc - tot;
-      if (exc < need && inc >= need) {
-        uint32_t above = exc;
-        for (int j = 0; j < 8; ++j) {
-          if (above + cnt[j] >= need) {
-            s_prefix = prefix | ((unsigned long long)(255 - 8 * tid - j) << shift);
-            s_need = need - above;
-            s_stop = (cnt[j] == need - above) ? 1 : 0;
-            break;
-          }
-          above += cnt[j];
-        }
-      }
-    }
-    __syncthreads();
-    prefix = s_prefix;
-    need = s_need;
-    mask |= 255ull << shift;
-    if (s_stop) break;
-  }
-  const unsigned long long theta = prefix;
-  if (tid == 0) s_cnt = 0;
-  __syncthreads();
-  for (uint32_t e = tid; e < ne; e += kSelThreads) {
-    const unsigned long long hi = comp(e, false) | 0xFFFFFFFFull;
-    if (hi < theta) continue;
-    const unsigned long long c = comp(e, true);
-    if (c >= theta) {
-      const uint32_t slot = atomicAdd(&s_cnt, 1u);
-      if (slot < (uint32_t)kSortCap) {
-        s_key[slot] = c;
-        s_idx[slot] = id(e);
-      }
-    }
-  }
-  __syncthreads();
-  const uint32_t cnt = min(s_cnt, (uint32_t)kSortCap);
-  uint32_t size = 1;
-  while (size < cnt) size <<= 1;
-  for (uint32_t q = cnt + tid; q < size; q += kSelThreads) {
-    s_key[q] = 0ull;
-    s_idx[q] = 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  bitonic_sort<kSelThreads>(s_key, s_idx, size, true);
-  return cnt;
-}
-
-// In-place inclusive prefix sums of v[0..cnt) (cnt <= 8 * kSelThreads) by the whole CTA.
-__device__ void block_inclusive_scan(unsigned long long* v, uint32_t cnt, unsigned long long* s_tmp) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t per = (cnt + kSelThreads - 1) / kSelThreads;
-  const uint32_t lo = min(cnt, tid * per), hi = min(cnt, lo + per);
-  unsigned long long part = 0;
-  for (uint32_t q = lo; q < hi; ++q) part += v[q];
-  unsigned long long inc = part;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long x = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= (uint32_t)o) inc += x;
-  }
-  if (lane == 31) s_tmp[wid] = inc;
-  __syncthreads();
-  unsigned long long wpre = lane < wid ? s_tmp[lane] : 0ull;  // kSelThreads / 32 <= 32 warps
-  for (int o = 16; o; o >>= 1) wpre += __shfl_xor_sync(0xffffffffu, wpre, o);
-  unsigned long long run = wpre + inc - part;
-  for (uint32_t q = lo; q < hi; ++q) {
-    run += v[q];
-    v[q] = run;
-  }
-  __syncthreads();
-}
 
 // ---------------------------------------------------------------- S5 + S6 + outputs (one CTA)
 // serve_mask already holds the running set (written by prep); the decision edits only the
@@ -789,7 +633,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     }
   } else {
     const uint32_t tB = A.tau[B - 1];
-    const uint32_t k = min(B, n);
+    // multi-GPU: a rank's local top list may be shorter than B (survivors are global)
+    const uint32_t k = A.xsend ? min(B, ovf ? n : ns) : min(B, n);
     uint32_t cnt;
     if (ovf) {
       // overflow fallback: exact keys of every request at B (row B of keyrow), radix select
@@ -841,6 +686,29 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       if (blockIdx.x == 255) ANDES_TRACE(w, 2401);
       cnt = k;
     }
+    if (A.xsend) {
+      // multi-GPU step 2: publish this rank's top-k of B in order (padded to B); the merge of
+      // all ranks' lists and Algorithm 1's walk run in k_shard_merge
+      const uint32_t base = __ldcg(&w.g->shard_base);
+      XEntry* dst = A.xsend + tri_off(B);
+      for (uint32_t q = tid; q < B; q += kSelThreads) {
+        XEntry x;
+        if (q < cnt) {
+          const uint32_t i = s_idx[q];
+          x.comp = s_key[q];
+          x.gfix = ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
+          x.l = r.ctx_len[i];
+          x.gidx = (base + i) | (r.running[i] ? 0x80000000u : 0u);
+        } else {
+          x.comp = 0ull;
+          x.gfix = 0;
+          x.l = 0u;
+          x.gidx = 0xFFFFFFFFu;
+        }
+        dst[q] = x;
+      }
+      return;
+    }
     // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
     // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
     if (blockIdx.x == 255) ANDES_TRACE(w, 2402);
@@ -889,6 +757,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     if (blockIdx.x == 255) ANDES_TRACE(w, 2405);
   }
   ANDES_TRACE(w, 2 * blockIdx.x + 1);
+  if (A.xsend) return;
   // the last CTA to finish runs S5 + S6 (last-block pattern)
   __threadfence();
   __syncthreads();
@@ -926,9 +795,14 @@ void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t n
   launch_pdl(k_state, blocks, kStateThreads, 0, L.stream, r, w, now, horizon);
 }
 
+void launch_compact(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* lb_src, uint32_t G) {
+  const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count) : 1u;
+  launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w, lb_src, G);
+}
+
 void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau) {
   const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count) : 1u;
-  launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w);
+  launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w, (const uint32_t*)nullptr, 1u);
   (void)tau;
 }
 
@@ -940,8 +814,9 @@ void init_kernels() {
 }
 
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
-                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
-  SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o};
+                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o,
+                   XEntry* xsend) {
+  SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o, xsend};
   launch_pdl(k_select, B_cap, kSelThreads, select_smem(), L.stream, A);
 }
 
