@@ -11,6 +11,10 @@ between timed steps; device time from CUDA events.  Under torchrun (N > 1) every
 schedules its own independent 64K-request instance (weak scaling, no data-path
 collective); rank 0 prints the JSON line with the max-over-ranks time.
 
+The line also carries config4_sharded: the 2^20-request population (BASELINE config 4) split
+into contiguous shards over the ranks, one decision through the multi-GPU entry point
+(andes_schedule_shard; NCCL all-gathers between its steps at N > 1), device time max over ranks.
+
 --impl reference times the CPU oracle (oracle/, plain C, one core) on a bounded sample of
 the same workload (rank 0 only).
 """
@@ -141,16 +145,96 @@ def _token_events(snap):
 
 def _tile(snap, reps):
     """reps copies of a snapshot (same shape/statistics), for the QoE-eval throughput run."""
+    import workloads as W
+    return W.tile(snap, reps)
+
+
+def sharded_decision(args, dist, rank, ws, lr, stream, flush):
+    """Config 4: 2^20 live requests sharded over the ws ranks (contiguous ranges), one full
+    decision through andes_schedule_shard: five step graphs, the four all-gathers between them
+    (NCCL over NVLink at ws > 1; a device copy at ws = 1).  Device time per decision, max over
+    ranks, L2 flushed before each decision."""
     import numpy as np
-    from dataclasses import replace
-    n, T = snap.n, snap.n_tokens
-    base = np.concatenate([snap.tl_base + np.uint64(k * T) for k in range(reps)])
-    return replace(snap, arrival_us=np.tile(snap.arrival_us, reps), ttft_us=np.tile(snap.ttft_us, reps),
-                   period_us=np.tile(snap.period_us, reps), ctx_len=np.tile(snap.ctx_len, reps),
-                   n_deliv=np.tile(snap.n_deliv, reps), max_total=np.tile(snap.max_total, reps),
-                   start_off_us=np.tile(snap.start_off_us, reps),
-                   rank=np.arange(n * reps, dtype=np.uint32), running=np.tile(snap.running, reps),
-                   tl_base=base, tl_pool=np.tile(snap.tl_pool, reps))
+    import torch
+
+    import paper_2404_16283_b200 as A
+    import workloads as W
+
+    dev = torch.device("cuda", lr)
+    big = W.config4()
+    cuts = np.linspace(0, big.n, ws + 1).astype(np.int64)
+    mine = W.shard(big, int(cuts[rank]), int(cuts[rank + 1]))
+    ctx = A.Context(max_requests=max(mine.n, 1), max_B=256, max_tokens=mine.n_tokens + 64, device=lr)
+    req = A.requests_to(mine, device=dev)
+    tau = torch.from_numpy(big.tau_us.view(np.int32)).to(dev)
+    sh = ctx.shard_init(ws, rank, 256)
+    send, recv = ctx.alloc_shard_buffers(sh)
+    out = ctx.alloc_shard_decision(mine.n, 256)
+    ag = A.torch_allgather() if dist is not None else (lambda a, b: b.copy_(a))
+    kw = dict(preempt_cap=big.preempt_cap, flags=A.ANDES_FORCE, stream=stream)
+
+    def step(s_):
+        ctx.schedule_shard(sh, s_, req, mine.n, big.now_us, big.horizon_us, tau, big.kv_capacity, out,
+                           recv=recv[s_ - 1] if s_ else None, send=send[s_] if s_ < A.SHARD_ROUNDS else None, **kw)
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            A.run_shard_steps(lambda s_, p_, c_: step(s_), ag, send, recv)
+        stream.synchronize()
+        graphs = []
+        for s_ in range(A.SHARD_STEPS):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(s_)
+            graphs.append(g)
+
+        def decide():
+            for s_ in range(A.SHARD_STEPS):
+                graphs[s_].replay()
+                if s_ < A.SHARD_ROUNDS:
+                    ag(send[s_], recv[s_])
+
+        for _ in range(max(args.warmup, 3)):
+            flush.zero_()
+            decide()
+        stream.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            if dist is not None:
+                dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            decide()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    total = _max_over_ranks(dist, sum(ms))
+    sc = out.scalars.cpu().numpy().view(np.uint32).copy()
+    res = {"workload": "config4: 2^20 live requests (config 3 x16, running batch in the first copy), "
+                       "contiguous shards over the ranks, B=1..256, M=163840, preemption cap 16",
+           "n_requests": int(big.n), "world": ws, "requests_per_rank": int(mine.n),
+           "ms_per_decision": total / args.steps, "decisions_per_s": args.steps / (total / 1e3),
+           "launch": "5 step CUDA graphs + 4 all-gathers (NCCL at world > 1)",
+           "xbytes_per_round": [int(x) for x in sh.xbytes],
+           "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}}
+    if dist is not None:
+        t = torch.from_numpy(sc.view(np.int32)).to(dev)
+        allsc = [torch.empty_like(t) for _ in range(ws)]
+        dist.all_gather(allsc, t)
+        res["replicated_scalars_identical"] = all(bool(torch.equal(x, t)) for x in allsc)
+    else:
+        # world 1: the sharded decision must equal andes_schedule on the same population
+        ref = ctx.schedule(req, mine.n, big.now_us, big.horizon_us, tau, big.kv_capacity,
+                           preempt_cap=big.preempt_cap, flags=A.ANDES_FORCE)
+        torch.cuda.synchronize()
+        res["equals_single_gpu_decision"] = bool(
+            np.array_equal(ref.scalars.cpu().numpy(), out.scalars.cpu().numpy())
+            and np.array_equal(ref.V.cpu().numpy(), out.V.cpu().numpy())
+            and np.array_equal(ref.serve_mask.cpu().numpy()[:mine.n], out.serve_mask.cpu().numpy()[:mine.n]))
+    del ctx, req
+    return res
 
 
 def cpu_baseline(snap, B_sample=8):
@@ -340,6 +424,9 @@ def run_ours(args):
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
     del qctx, breq
 
+    # ---- config 4: the 2^20-request population sharded over the ranks (multi-GPU decision)
+    config4 = None if args.no_sharded else sharded_decision(args, dist, rank, ws, lr, stream, flush)
+
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     hreq = A.requests_to(snap, pin=True)
     tau_h = torch.from_numpy(snap.tau_us.view(np.int32)).pin_memory()
@@ -376,6 +463,7 @@ def run_ours(args):
                    "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}},
         "roofline": roof,
         "qoe_eval": qoe_eval,
+        "config4_sharded": config4,
         "e2e": {"value": ws * e2e_steps / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "andes_schedule_host (pinned host buffers)"},
         "gpu_launches": KERNELS_PER_DECISION * args.steps,
@@ -396,6 +484,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 sharded decision")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

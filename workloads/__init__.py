@@ -187,6 +187,40 @@ def config3(seed=1, n=65536) -> Snapshot:
                     name=f"cfg3-{n // 1024}k-s{seed}")
 
 
+def tile(snap: Snapshot, reps: int, running_copies: int | None = None) -> Snapshot:
+    """reps copies of a snapshot back to back (same shape and statistics), ranks renumbered
+    0..n*reps-1; the running flag is kept in the first `running_copies` copies only (default all)."""
+    n, T = snap.n, snap.n_tokens
+    base = np.concatenate([snap.tl_base + np.uint64(k * T) for k in range(reps)])
+    run = np.tile(snap.running, reps)
+    if running_copies is not None:
+        run[running_copies * n:] = 0
+    return replace(snap, arrival_us=np.tile(snap.arrival_us, reps), ttft_us=np.tile(snap.ttft_us, reps),
+                   period_us=np.tile(snap.period_us, reps), ctx_len=np.tile(snap.ctx_len, reps),
+                   n_deliv=np.tile(snap.n_deliv, reps), max_total=np.tile(snap.max_total, reps),
+                   start_off_us=np.tile(snap.start_off_us, reps),
+                   rank=np.arange(n * reps, dtype=np.uint32), running=run, tl_base=base,
+                   tl_pool=np.tile(snap.tl_pool, reps), name=f"{snap.name}x{reps}")
+
+
+def shard(snap: Snapshot, lo: int, hi: int) -> Snapshot:
+    """Requests lo..hi-1 as a contiguous shard with its own pool (the multi-GPU layout)."""
+    b0 = int(snap.tl_base[lo]) if lo < snap.n else snap.n_tokens
+    b1 = int(snap.tl_base[hi - 1]) + int(snap.n_deliv[hi - 1]) if hi > lo else b0
+    sl = slice(lo, hi)
+    return replace(snap, arrival_us=snap.arrival_us[sl], ttft_us=snap.ttft_us[sl], period_us=snap.period_us[sl],
+                   ctx_len=snap.ctx_len[sl], n_deliv=snap.n_deliv[sl], max_total=snap.max_total[sl],
+                   start_off_us=snap.start_off_us[sl], rank=snap.rank[sl], running=snap.running[sl],
+                   tl_base=(snap.tl_base[sl] - np.uint64(b0)).astype(np.uint64),
+                   tl_pool=snap.tl_pool[b0:b1], name=f"{snap.name}[{lo}:{hi}]")
+
+
+def config4(seed=1, reps=16) -> Snapshot:
+    """BASELINE config 4: 2^20 live requests (config 3 scaled: 16 copies of the 64K snapshot,
+    the running batch kept in the first copy so it fits M), for the sharded decision."""
+    return tile(config3(seed), reps, running_copies=1)
+
+
 def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True) -> Snapshot:
     """Small adversarial instances for parity: arbitrary periods, ttft, offsets,
     max_total caps, deliveries ahead of / behind schedule, pauses, ties."""
