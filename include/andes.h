@@ -158,6 +158,16 @@ const char *andes_last_error(const AndesCtx *ctx);
 int andes_qoe_eval(AndesCtx *ctx, const AndesRequests *req, int64_t eval_time_us, uint32_t mode,
                    const AndesQoeOut *out, void *stream);
 
+/* Sweep of independent scenarios (BASELINE config 5; end-of-trace QoE): FINAL-mode QoE of
+ * every request (m = g, no clamp; reading R19), then per scenario s the mean over its requests
+ * with g >= 1, where scenario s holds requests [scen_off[s], scen_off[s+1]) (DEVICE u32[S+1],
+ * nondecreasing, scen_off[S] <= n).  mean_out f64[S] (0 when no request has a token),
+ * count_out u32[S] optional (requests averaged).  The mean is a fixed-order fp64 reduction
+ * (deterministic; within 1e-12 relative of the exact mean of the per-request fp64 QoE).
+ * Errors: ANDES_E_INVAL, ANDES_E_CAPACITY, ANDES_E_CUDA. */
+int andes_qoe_scenario_mean(AndesCtx *ctx, const AndesRequests *req, const uint32_t *scen_off, uint32_t S,
+                            double *mean_out, uint32_t *count_out, void *stream);
+
 /* S3 materialised for an explicit list of B (parity and inspection):
  * gain_out f64[nB*n] = Q_serve,i(B) - Q_wait,i (Eq. 4), key_out f32[nB*n] =
  * float(gain / l_i) with -0 -> +0 (Eq. 6, reading R9); row b is B = B_list_host[b]

@@ -10,6 +10,7 @@ Entry points (same names as the C ABI):
     Context.gain_estimate   -> andes_gain_estimate
     Context.schedule        -> andes_schedule
     Context.schedule_host   -> andes_schedule_host
+    Context.qoe_scenario_mean -> andes_qoe_scenario_mean (config-5 sweeps)
     Context.shard_init      -> andes_shard_init
     Context.schedule_shard  -> andes_schedule_shard (one step); schedule_sharded() runs all steps
                                with a caller-supplied all-gather (torch.distributed / NCCL)
@@ -39,7 +40,7 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
-           "andes_shard_init", "andes_schedule_shard"]
+           "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -112,6 +113,8 @@ def lib() -> C.CDLL:
         L.andes_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
         L.andes_schedule_host.argtypes = [C.c_void_p, C.POINTER(Requests), C.POINTER(SchedParams),
                                           C.POINTER(DecisionPtrs), C.c_void_p]
+        L.andes_qoe_scenario_mean.argtypes = [C.c_void_p, C.POINTER(Requests), C.c_void_p, C.c_uint32,
+                                              C.c_void_p, C.c_void_p, C.c_void_p]
         L.andes_shard_init.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Shard)]
         L.andes_schedule_shard.argtypes = [C.c_void_p, C.POINTER(Shard), C.c_uint32, C.POINTER(Requests),
                                            C.POINTER(SchedParams), C.POINTER(DecisionPtrs), C.c_void_p, C.c_void_p,
@@ -238,6 +241,18 @@ class Context:
         self._check(lib().andes_qoe_eval(self._h, C.byref(_req_struct(req, n)), int(eval_time_us), int(mode),
                                          C.byref(out), _stream_ptr(stream)), "andes_qoe_eval")
         return q, q64, sd, sw, m
+
+    # -- andes_qoe_scenario_mean
+    def qoe_scenario_mean(self, req: dict, n: int, scen_off, stream=None):
+        """scen_off: device int32 tensor [S+1] of request offsets; returns (mean f64[S], count i32[S])."""
+        torch = _torch()
+        S = int(scen_off.numel()) - 1
+        mean = torch.empty(max(S, 1), dtype=torch.float64, device=self.device)
+        cnt = torch.empty(max(S, 1), dtype=torch.int32, device=self.device)
+        self._check(lib().andes_qoe_scenario_mean(self._h, C.byref(_req_struct(req, n)), _ptr(scen_off), S,
+                                                  _ptr(mean), _ptr(cnt), _stream_ptr(stream)),
+                    "andes_qoe_scenario_mean")
+        return mean[:S], cnt[:S]
 
     # -- andes_gain_estimate
     def gain_estimate(self, req: dict, n: int, now_us: int, horizon_us: int, tau, B_list, stream=None):

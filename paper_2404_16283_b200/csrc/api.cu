@@ -403,6 +403,36 @@ int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, 
   return finish_call(c, s, false);
 }
 
+int andes_qoe_scenario_mean(AndesCtx* c, const AndesRequests* req, const uint32_t* scen_off, uint32_t S,
+                            double* mean_out, uint32_t* count_out, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if ((rc = check_requests(c, req, false))) return rc;
+  if (S && (!scen_off || !mean_out)) return set_err(c, ANDES_E_INVAL, "scen_off/mean_out is NULL%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LaunchCfg L = cfg_of(c, stream);
+  const ReqView r = view_of(req);
+  const Work w = work_of(c, r.n);
+  mark(c, 0, s);
+  if ((rc = reset_call(c, s))) return rc;
+  launch_prep(L, r, w, 0, true, false, 0, false);
+  mark(c, 1, s);
+  {
+    const CUtensorMap* tm = nullptr;
+    if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
+    launch_scan(L, r, w, 0, true, tm);
+  }
+  mark(c, 2, s);
+  launch_scenario_mean(L, r, w, scen_off, S, mean_out, count_out);
+  mark(c, 3, s);
+  mark(c, 4, s);
+  mark(c, 5, s);
+  mark(c, 6, s);
+  if (c->prof) c->prof_recorded = true;
+  return finish_call(c, s, false);
+}
+
 int andes_gain_estimate(AndesCtx* c, const AndesRequests* req, int64_t now_us, uint32_t horizon_us,
                         const uint32_t* tau_us, uint32_t B_cap, const uint32_t* B_list_host, uint32_t nB,
                         double* gain_out, float* key_out, double* qwait_out, void* stream) {

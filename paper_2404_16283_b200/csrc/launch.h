@@ -41,6 +41,8 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
                  uint64_t M = 0, uint32_t cur_latency = 0, uint32_t flags = 0);
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
+void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* off, uint32_t S,
+                          double* mean_out, uint32_t* count_out);
 int scan_blocks_per_sm();
 void init_scan_kernels();
 

@@ -842,7 +842,55 @@ __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_
   (void)final_mode;
 }
 
+// ---------------------------------------------------------------- config-5 sweep: scenario means
+// One CTA per scenario s: QoE of its requests [off[s], off[s+1]) in FINAL mode (m = g, Eq. 1-3,
+// reading R19) and their mean over the requests with g >= 1 ("averaged across all
+// requests").  Fixed-order reduction (strided per-thread sums, then a fixed tree): deterministic.
+constexpr int kScenThreads = 256;
+__global__ void __launch_bounds__(kScenThreads) k_scenario_mean(ReqView r, Work w, const uint32_t* __restrict__ off,
+                                                                uint32_t S, double* mean_out, uint32_t* count_out) {
+  __shared__ double s_sum[kScenThreads];
+  __shared__ uint32_t s_cnt[kScenThreads];
+  pdl_wait();
+  pdl_trigger();
+  for (uint32_t sc = blockIdx.x; sc < S; sc += gridDim.x) {
+    const uint32_t lo = off[sc], hi = off[sc + 1];
+    double acc = 0.0;
+    uint32_t cnt = 0;
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kScenThreads) {
+      const uint32_t g = r.n_deliv[i];
+      if (g == 0) continue;
+      const int64_t P = r.period[i];
+      const int64_t sw = (int64_t)g * (int64_t)w.edge[i] + P * (((int64_t)g * ((int64_t)g - 1)) >> 1);
+      acc = __dadd_rn(acc, qoe_value((int64_t)w.spre[i], sw));
+      ++cnt;
+    }
+    s_sum[threadIdx.x] = acc;
+    s_cnt[threadIdx.x] = cnt;
+    __syncthreads();
+    for (uint32_t h = kScenThreads / 2; h; h >>= 1) {
+      if (threadIdx.x < h) {
+        s_sum[threadIdx.x] = __dadd_rn(s_sum[threadIdx.x], s_sum[threadIdx.x + h]);
+        s_cnt[threadIdx.x] += s_cnt[threadIdx.x + h];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      mean_out[sc] = s_cnt[0] ? __ddiv_rn(s_sum[0], (double)s_cnt[0]) : 0.0;
+      if (count_out) count_out[sc] = s_cnt[0];
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- host launchers
+void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* off, uint32_t S,
+                          double* mean_out, uint32_t* count_out) {
+  if (S == 0) return;
+  launch_pdl(k_scenario_mean, umin32(S, L.sm_count * 8), kScenThreads, 0, L.stream, r, w, off, S, mean_out,
+             count_out);
+}
+
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                  bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask) {
   if (r.n == 0) return;

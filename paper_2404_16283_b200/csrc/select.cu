@@ -102,14 +102,19 @@ __device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, 
   __shared__ uint32_t s_h[kHistK];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // coalesced loads of both histograms; survivors partial sums by bucket later
-  uint32_t hu[kPer];
+  // kPer independent loads per histogram (one round trip each, not kPer in sequence)
+  uint32_t hu[kPer], v[kPer];
 #pragma unroll
   for (uint32_t q = 0; q < kPer; ++q) {
-    uint32_t v = 0;
-    for (uint32_t g = 0; g < G; ++g) v += __ldcg(&lb_src[(size_t)g * kHistK + q * NT + tid]);
-    s_h[q * NT + tid] = v;
+    v[q] = __ldcg(&lb_src[q * NT + tid]);
     hu[q] = __ldcg(&w.hist_ub[q * NT + tid]);
   }
+  for (uint32_t g = 1; g < G; ++g) {
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) v[q] += __ldcg(&lb_src[(size_t)g * kHistK + q * NT + tid]);
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) s_h[q * NT + tid] = v[q];
   __syncthreads();
   uint32_t h[kPer], cnt = 0;
 #pragma unroll

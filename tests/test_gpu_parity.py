@@ -308,3 +308,24 @@ def test_schedule_survivor_overflow_fallback(A, ctx, orc):
                       tau_us=W.tau_table(48), kv_capacity=4000)
     gg, o = _check_sched(A, ctx, orc, snap, cap=5)
     assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
+
+
+# ---------------------------------------------------------------- config-5 sweep: scenario means
+def test_scenario_means_match_oracle(A, ctx, orc):
+    """andes_qoe_scenario_mean vs the oracle: FINAL-mode QoE per request (R19), mean over g >= 1
+    per scenario.  Counts exact; means within 1e-12 relative of the exact (fsum) mean."""
+    import math
+    scen = [(1, 0.5), (2, 1.0), (3, 2.05), (4, 1.5), (5, 0.75)]
+    snap, off = W.sweep(scen, n_base=60)
+    # an empty scenario and a scenario whose requests have no tokens
+    off = np.concatenate([off[:2], off[1:2], off[2:]]).astype(np.uint32)
+    mean, cnt = ctx.qoe_scenario_mean(_dev(A, snap), snap.n, torch.from_numpy(off.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    mean, cnt = mean.cpu().numpy(), cnt.cpu().numpy()
+    q, sd, sw, m = orc.qoe_eval(snap, 0, final=True)
+    for s in range(off.size - 1):
+        sel = np.arange(off[s], off[s + 1])
+        sel = sel[snap.n_deliv[sel] >= 1]
+        assert int(cnt[s]) == sel.size
+        exact = math.fsum(q[sel]) / sel.size if sel.size else 0.0
+        assert abs(mean[s] - exact) <= 1e-12 * max(1.0, abs(exact)), (s, mean[s], exact)

@@ -221,6 +221,73 @@ def config4(seed=1, reps=16) -> Snapshot:
     return tile(config3(seed), reps, running_copies=1)
 
 
+SWEEP_RHOS = tuple(round(0.50 + 0.05 * k, 2) for k in range(32))  # load factors 0.50 .. 2.05
+
+
+def sweep_scenario(seed: int, rho: float, n_base: int = 2000, window_s: float = 1200.0, listen_frac: float = 0.5,
+                   dataset: str = "sharegpt"):
+    """One config-5 scenario: a 20-minute cyclic-burst trace of ~n_base*rho requests
+    whose timelines are COMPLETE (g = output length), drawn from a parametric load model instead of
+    a scheduler: queue wait ~ Exp(2 s * rho^3), prefill input/5000 s, token gaps
+    tau(min(256, ceil(128 rho))) +-10%, one pause U[0.5, 5] s with probability min(0.5, 0.1 rho^2).
+    Vectorised (no per-request Python loop).  Returns the SoA arrays (relative timestamps, us)."""
+    rng = np.random.default_rng([int(seed), int(round(rho * 100))])
+    n = max(1, int(round(n_base * rho)))
+    inp, out = sample_lengths(rng, n, dataset)
+    g = out.astype(np.int64)  # completed requests deliver their whole output
+    # arrivals: unit-rate Poisson mapped through the cyclic-burst cumulative intensity
+    mean_rate = n / window_s
+    r_b, burst = 2.0 * mean_rate, 0.35
+    r_0 = (1.0 - 2.0 * burst) / (1.0 - burst) * mean_rate
+    lam_cycle = window_s * (burst * r_b + (1 - burst) * r_0)
+    u = np.cumsum(rng.exponential(1.0, n))
+    cyc, rem = np.divmod(u, lam_cycle)
+    tb = burst * window_s * r_b
+    t_in = np.where(rem < tb, rem / r_b, burst * window_s + (rem - tb) / r_0)
+    arr_us = np.rint((cyc * window_s + t_in) * 1e6).astype(np.int64)
+    wait = rng.exponential(2e6 * rho ** 3, n)
+    first = wait + 200.0 * inp
+    gap = float(tau_table(B_CAP)[min(256, int(np.ceil(128 * rho))) - 1])
+    T = int(g.sum())
+    start = np.concatenate([[0], np.cumsum(g)[:-1]])
+    steps = gap * (1.0 + rng.uniform(-0.1, 0.1, T))
+    steps[start] = first
+    pause_on = (rng.random(n) < min(0.5, 0.1 * rho * rho)) & (g > 1)
+    k = np.minimum(rng.integers(1, np.maximum(g, 2)), np.maximum(g - 1, 1))
+    plen = rng.uniform(0.5e6, 5e6, n)
+    steps[start[pause_on] + k[pause_on]] += plen[pause_on]
+    ts = np.cumsum(steps)
+    seg0 = np.repeat(ts[start] - steps[start], g)
+    pool = np.floor(ts - seg0).astype(np.uint32)
+    ttft = np.maximum(200 * inp, 1_000_000).astype(np.uint32)
+    period = np.where(rng.random(n) < listen_frac, LISTEN_PERIOD_US, READ_PERIOD_US).astype(np.uint32)
+    return dict(arrival_us=arr_us, ttft_us=ttft, period_us=period, ctx_len=(inp + g).astype(np.uint32),
+                n_deliv=g.astype(np.uint32), tl_pool=pool)
+
+
+def sweep(scenarios, n_base: int = 2000) -> tuple[Snapshot, np.ndarray]:
+    """Concatenation of sweep_scenario(seed, rho) for every (seed, rho) in `scenarios` (requests
+    grouped by scenario, pools packed back to back, ranks unique); returns the population and the
+    request offsets u32[S+1] of the scenarios (BASELINE config 5: 32 seeds x SWEEP_RHOS)."""
+    parts = [sweep_scenario(sd, rho, n_base) for sd, rho in scenarios]
+    cat = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    g = cat["n_deliv"].astype(np.uint64)
+    base = np.concatenate([[0], np.cumsum(g)[:-1]]).astype(np.uint64)
+    n = int(g.size)
+    off = np.concatenate([[0], np.cumsum([p["n_deliv"].size for p in parts])]).astype(np.uint32)
+    snap = Snapshot(arrival_us=cat["arrival_us"], ttft_us=cat["ttft_us"], period_us=cat["period_us"],
+                    ctx_len=cat["ctx_len"], n_deliv=cat["n_deliv"], max_total=np.full(n, UINT32_MAX, np.uint32),
+                    start_off_us=np.zeros(n, np.uint32), rank=np.arange(n, dtype=np.uint32),
+                    running=np.zeros(n, np.uint8), tl_base=base, tl_pool=cat["tl_pool"], now_us=0,
+                    name=f"sweep-{len(parts)}")
+    return snap, off
+
+
+def config5_scenarios(seeds: int = 32, rhos=SWEEP_RHOS):
+    """BASELINE config 5: 1024 scenarios = 32 trace seeds x 32 load factors."""
+    return [(sd, rho) for sd in range(1, seeds + 1) for rho in rhos]
+
+
 def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True) -> Snapshot:
     """Small adversarial instances for parity: arbitrary periods, ttft, offsets,
     max_total caps, deliveries ahead of / behind schedule, pauses, ties."""
