@@ -11,7 +11,8 @@ between timed steps; device time from CUDA events.  Under torchrun (N > 1) every
 schedules its own independent 64K-request instance (weak scaling, no data-path
 collective); rank 0 prints the JSON line with the max-over-ranks time.
 
-The line also carries config4_sharded: the 2^20-request population (BASELINE config 4) split
+The line also carries config5_sweep (1024 independent scenarios split over the ranks, end-of-trace
+QoE mean per scenario) and config4_sharded: the 2^20-request population (BASELINE config 4) split
 into contiguous shards over the ranks, one decision through the multi-GPU entry point
 (andes_schedule_shard; NCCL all-gathers between its steps at N > 1), device time max over ranks.
 
@@ -147,6 +148,71 @@ def _tile(snap, reps):
     """reps copies of a snapshot (same shape/statistics), for the QoE-eval throughput run."""
     import workloads as W
     return W.tile(snap, reps)
+
+
+def sweep_run(args, dist, rank, ws, lr, stream):
+    """Config 5: 1024 independent scenarios (32 trace seeds x 32 load factors) split over the
+    ranks (contiguous blocks, replicas only: no data-path collective), FINAL-mode QoE of every
+    request and the mean per scenario (andes_qoe_scenario_mean); the means are gathered to rank 0
+    at the end (the one exchange).  Inputs are larger than L2 (~4 GB of timestamps)."""
+    import numpy as np
+    import torch
+
+    import paper_2404_16283_b200 as A
+    import workloads as W
+
+    dev = torch.device("cuda", lr)
+    scen = W.config5_scenarios()
+    S = len(scen)
+    lo, hi = rank * S // ws, (rank + 1) * S // ws
+    t0 = time.time()
+    snap, off = W.sweep(scen[lo:hi])
+    gen_s = time.time() - t0
+    ctx = A.Context(max_requests=max(snap.n, 1), max_B=8, max_tokens=snap.n_tokens + 64, device=lr)
+    req = A.requests_to(snap, device=dev)
+    offd = torch.from_numpy(off.view(np.int32)).to(dev)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            ctx.qoe_scenario_mean(req, snap.n, offd, stream=stream)
+        stream.synchronize()
+        reps = max(3, min(args.steps, 10))
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        if dist is not None:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(reps):
+            mean, cnt = ctx.qoe_scenario_mean(req, snap.n, offd, stream=stream)
+        b.record(stream)
+        b.synchronize()
+    ms = _max_over_ranks(dist, a.elapsed_time(b) / reps)
+    tokens = int(_sum_over_ranks(dist, snap.n_tokens))
+    nreq = int(_sum_over_ranks(dist, snap.n))
+    if dist is not None:  # C4: the scenario means to every rank (rank 0 reports)
+        allm = [torch.empty_like(mean) for _ in range(ws)]
+        dist.all_gather(allm, mean.contiguous())
+        mean = torch.cat(allm)
+    mq = mean.cpu().numpy()
+    rh = np.array([r for _, r in scen])
+    by_rho = {f"{r:.2f}": float(mq[rh == r].mean()) for r in (0.5, 1.0, 1.5, 2.0)}
+    bytes_ = 4 * tokens + 44 * nreq
+    res = {"workload": "config5: 1024 scenarios (32 seeds x rho 0.50..2.05), ~2000*rho requests each, complete "
+                       "ShareGPT-shaped timelines from the parametric load model; FINAL-mode QoE, mean per scenario",
+           "scenarios": S, "requests": nreq, "token_events": tokens, "ms_per_sweep": ms,
+           "scenarios_per_s": S / (ms / 1e3), "token_events_per_s": tokens / (ms / 1e3),
+           "achieved_GBs": bytes_ / (ms / 1e3) / 1e9, "host_generation_s": round(gen_s, 1),
+           "mean_qoe_at_rho": by_rho, "l2": "inputs ~4 GB > L2 (no flush needed)"}
+    del ctx, req
+    return res
+
+
+def _sum_over_ranks(dist, x):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
 
 
 def sharded_decision(args, dist, rank, ws, lr, stream, flush):
@@ -427,6 +493,9 @@ def run_ours(args):
     # ---- config 4: the 2^20-request population sharded over the ranks (multi-GPU decision)
     config4 = None if args.no_sharded else sharded_decision(args, dist, rank, ws, lr, stream, flush)
 
+    # ---- config 5: the 1024-scenario sweep (end-of-trace QoE per scenario)
+    sweep = None if args.no_sweep else sweep_run(args, dist, rank, ws, lr, stream)
+
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     hreq = A.requests_to(snap, pin=True)
     tau_h = torch.from_numpy(snap.tau_us.view(np.int32)).pin_memory()
@@ -464,6 +533,7 @@ def run_ours(args):
         "roofline": roof,
         "qoe_eval": qoe_eval,
         "config4_sharded": config4,
+        "config5_sweep": sweep,
         "e2e": {"value": ws * e2e_steps / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "andes_schedule_host (pinned host buffers)"},
         "gpu_launches": KERNELS_PER_DECISION * args.steps,
@@ -485,6 +555,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 sharded decision")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 scenario sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
