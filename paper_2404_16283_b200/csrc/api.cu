@@ -46,7 +46,7 @@ struct AndesCtx {
   } mir{};
   std::string err;
   // TMA tensor map of the current timestamp pool (re-encoded when the pool changes)
-  CUtensorMap pool_map{};
+  CUtensorMap pool_map[2]{};  // [0] 128B-swizzled tiles, [1] plain tiles (16-byte aligned timelines)
   const void* map_ptr = nullptr;
   uint64_t map_len = ~0ull;
   uint32_t* zero_rows = nullptr;  // 128 zero bytes: TMA source when the pool has no full row
@@ -153,7 +153,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 
 int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap** out) {
   if (c->map_ptr == pool && c->map_len == len) {
-    *out = &c->pool_map;
+    *out = c->pool_map;
     return ANDES_OK;
   }
   static EncodeTiledFn encode = nullptr;
@@ -171,13 +171,15 @@ int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap*
   cuuint64_t strides[1] = {128};
   cuuint32_t box[2] = {32, kTile / 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(&c->pool_map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, base, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_err(c, ANDES_E_CUDA, "cuTensorMapEncodeTiled failed%s");
+  for (int k = 0; k < 2; ++k) {
+    CUresult r = encode(&c->pool_map[k], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, k ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(c, ANDES_E_CUDA, "cuTensorMapEncodeTiled failed%s");
+  }
   c->map_ptr = pool;
   c->map_len = len;
-  *out = &c->pool_map;
+  *out = c->pool_map;
   return ANDES_OK;
 }
 
@@ -492,7 +494,7 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
   mark(c, 1, s);
   {
-    const CUtensorMap* tm = &c->pool_map;
+    const CUtensorMap* tm = c->pool_map;
     if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
     launch_scan(L, r, w, eval, false, tm, true, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
   }
@@ -554,7 +556,7 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
     case 0: {
       if ((rc = reset_call(c, s))) return rc;
       launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
-      const CUtensorMap* tm = &c->pool_map;
+      const CUtensorMap* tm = c->pool_map;
       if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
       launch_scan(L, r, w, eval, false, tm);
       launch_shard_summary(L, r, w, p->B_cap, static_cast<ShardSummary*>(send));

@@ -103,6 +103,8 @@ struct Globals {
   uint32_t n_global;             // requests over all ranks
   uint32_t n_run_global;         // running requests over all ranks
   uint32_t shard_Bstar;          // B* (step 3 -> step 4)
+  uint32_t unal;                 // prep: some timeline does not start on a 16-byte boundary
+  uint32_t pad_[3];
 };
 
 // B-independent per-request state for the gain closed form,

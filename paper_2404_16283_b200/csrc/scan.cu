@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   __shared__ uint32_t s_minP;
   __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
-  uint32_t local_err = 0;
+  uint32_t local_err = 0, local_unal = 0;
   pdl_wait();
   pdl_trigger();
   if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x);
@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
       w.g->ntiles = (uint32_t)((pe + kWTile - 1) / kWTile);
       w.g->pool_end = pe;
     }
+    if (g && (base & 3ull)) local_unal = 1u;
     if (debug) {
       if (P == 0) local_err |= kErrPeriod;
       if (i + 1 < n && next < base + g) local_err |= kErrBase;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     }
   }
   if (local_err) atomicOr(&w.g->err, local_err);
+  if (__any_sync(0xffffffffu, local_unal) && (threadIdx.x & 31) == 0) atomicOr(&w.g->unal, 1u);
   if (!sched) return;
   for (int o = 16; o; o >>= 1) my_minP = min(my_minP, __shfl_xor_sync(0xffffffffu, my_minP, o));
   if ((threadIdx.x & 31) == 0) atomicMin(&s_minP, my_minP);
@@ -427,7 +429,7 @@ struct EntWin {
 
 template <bool kFinal, class Win>
 __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn, uint32_t t,
-                                          uint32_t mode, uint32_t cdirect) {
+                                          uint32_t mode, uint32_t cdirect, uint32_t swz_on) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
   const int32_t x0 = (int32_t)(lane * kScanItems);
@@ -441,7 +443,7 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
     }
     q0 = lo;
   }
-  const uint32_t rowb = tile_s + (lane << 7), rsw = lane & 7u;
+  const uint32_t rowb = tile_s + (lane << 7), rsw = swz_on ? (lane & 7u) : 0u;  // plain tiles: no XOR
   const Entry e0 = win.get(q0);
   const bool starts_here = e0.ls == x0;
   // Pieces that start in this row are final after one pass.  The row's first piece, when it
@@ -625,12 +627,180 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   }
 }
 
+// ---- aligned fast path: every request starting in the tile starts on a 16-byte boundary
+// (token index multiple of 4), so every 4-token group belongs to one request.  The tile's valid
+// tokens are cut into pieces (request ∩ tile, up to its valid end) and the pieces into
+// sub-ranges of SR tokens (SR chosen per tile so that <= 32 sub-ranges exist); lane u owns
+// sub-range u, so no lane ever meets a request boundary (no event path, no divergence):
+//   pass 1  zero-carry recurrence over the sub-range -> its lateness at the last token (tokens
+//           past the valid end read as d = 0, which keeps the lateness constant);
+//   scan    segmented max over the sub-ranges (flag = a piece that starts in the tile), seeded
+//           with the tile's carry-in -> every sub-range's exact carry;
+//   pass 2  the recurrence again from the carry: sum of T~ = min(A, t) over the valid tokens,
+//           the edge value at the request's last valid token, one 64-bit atomic per sub-range.
+// Returns false (nothing done) when the tile has too many pieces for one round.
+template <bool kFinal, class Win>
+__device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn,
+                                                  uint32_t t, uint32_t mode, uint32_t cdirect) {
+  const Work& w = A.w;
+  const uint32_t lane = threadIdx.x & 31;
+  if (wn > 24u) return false;
+  // lane q: window entry q -> its piece [ps, pe) of valid tokens inside the tile
+  const Entry e = lane < wn ? win.get(lane) : null_entry(true);
+  const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
+  const bool starts_in = e.ls >= 0 && e.ls < (int32_t)kWTile;
+  if (__any_sync(0xffffffffu, starts_in && (e.ls & 3))) return false;  // not 16-byte aligned
+  const uint32_t len = (uint32_t)(pe - ps);
+  const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
+  // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32)
+  // (an odd number of 16-byte chunks: sub-ranges of one piece hit distinct shared-memory banks)
+  const uint32_t SR = 4u * (((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u);
+  const uint32_t cnt = (len + SR - 1) / SR;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
+  }
+  const uint32_t U = __shfl_sync(0xffffffffu, incl, 31);
+  // sub-range u = lane: its piece q = first entry with incl[q] > u
+  const uint32_t u = lane;
+  uint32_t q = 0;
+#pragma unroll
+  for (uint32_t st = 16; st; st >>= 1) {
+    const uint32_t v = __shfl_sync(0xffffffffu, incl, q + st - 1);
+    if (v <= u) q += st;
+  }
+  q = min(q, 31u);
+  const bool active = u < U;
+  const int32_t q_ps = __shfl_sync(0xffffffffu, ps, q), q_pe = __shfl_sync(0xffffffffu, pe, q);
+  const uint32_t q_off = __shfl_sync(0xffffffffu, incl - cnt, q);
+  const uint32_t qA = __shfl_sync(0xffffffffu, e.A, q), qP = __shfl_sync(0xffffffffu, e.P, q);
+  const uint32_t qtrel = __shfl_sync(0xffffffffu, e.trel, q), qek = __shfl_sync(0xffffffffu, e.ek, q);
+  const uint32_t qridx = __shfl_sync(0xffffffffu, e.ridx, q);
+  const int32_t qvend = __shfl_sync(0xffffffffu, e.vend, q), qls = __shfl_sync(0xffffffffu, e.ls, q);
+  const uint32_t k = u - q_off;
+  const int32_t xs = active ? q_ps + (int32_t)(SR * k) : 0;
+  const int32_t xe = active ? min(xs + (int32_t)SR, q_pe) : 0;
+  const uint32_t P = active ? qP : 0u;
+  const uint32_t tcl = kFinal ? 0xFFFFFFFFu : qtrel;
+  // full 4-token groups of the sub-range, then at most one partial group (the valid end)
+  const uint32_t nfull = active ? (uint32_t)(xe - xs) >> 2 : 0u;
+  const uint32_t ntail = active ? (uint32_t)(xe - xs) & 3u : 0u;
+  const uint32_t gmax = __reduce_max_sync(0xffffffffu, nfull);
+  const uint32_t Is = qA + (uint32_t)xs * P;  // ideal time of the sub-range's first token
+  // the tile is in plain row-major layout here (no swizzle): chunk c at tile_s + 16 c
+  const uint32_t a0 = tile_s + (((uint32_t)xs >> 2) << 4);
+  // the tail group's tokens (loaded once, used by both passes); missing tokens read as 0
+  uint32_t t0 = 0, t1 = 0, t2 = 0;
+  if (ntail) {
+    const uint4 v = ld_shared_v4(a0 + (nfull << 4));
+    t0 = v.x;
+    t1 = ntail > 1 ? v.y : 0u;
+    t2 = ntail > 2 ? v.z : 0u;
+  }
+  // ---- pass 1: zero-carry lateness at the sub-range's end
+  uint32_t a = Is - P;
+#pragma unroll 2
+  for (uint32_t gi = 0; gi < gmax; ++gi) {
+    if (gi < nfull) {
+      const uint4 v = ld_shared_v4(a0 + (gi << 4));
+      a = max(a + P, v.x);
+      a = max(a + P, v.y);
+      a = max(a + P, v.z);
+      a = max(a + P, v.w);
+    }
+  }
+  if (ntail) {
+    a = max(a + P, t0);
+    a = max(a + P, t1);
+    a = max(a + P, t2);
+  }
+  const uint32_t nslots = 4u * nfull + (ntail ? 3u : 0u);  // processed token slots
+  const uint32_t dz = nslots ? a - (Is + (nslots - 1u) * P) : 0u;
+  // a request starts in this sub-range; idle lanes (after every sub-range) are the identity
+  const bool flag = active && k == 0 && qls >= 0;
+  const unsigned long long agg = (flag ? kFlagBit : 0ull) | dz;
+  unsigned long long sc = agg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, sc, o);
+    if (lane >= (uint32_t)o) sc = seg_combine(v, sc);
+  }
+  unsigned long long excl = __shfl_up_sync(0xffffffffu, sc, 1);
+  if (lane == 0) excl = 0ull;
+  const unsigned long long tile_agg = __shfl_sync(0xffffffffu, sc, 31);
+  // ---- the tile's carry-in (direct read or decoupled look-back), as in warp_tile; the aggregate
+  // is published first so that successors looking back never wait on this tile's second pass
+  if (lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
+  unsigned long long acc = 0ull;
+  if (mode == 2u) {
+    for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
+      const int64_t j = jhi - (int64_t)lane;
+      unsigned long long st = kStPrefix;
+      if (j >= 0) {
+        do {
+          st = ld_relaxed(&w.tile_status[j]);
+        } while ((st & kStMask) == 0ull);
+      }
+      const bool stop = (st & kStMask) == kStPrefix || (st & kFlagBit);
+      const uint32_t bal = __ballot_sync(0xffffffffu, stop);
+      const uint32_t kst = bal ? (uint32_t)(__ffs(bal) - 1) : 31u;
+      unsigned long long v = (lane <= kst) ? (st & ~kStMask) : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long uu = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = seg_combine(uu, v);
+      }
+      acc = seg_combine(__shfl_sync(0xffffffffu, v, 0), acc);
+      if (bal) break;
+    }
+  } else if (mode == 1u) {
+    acc = kFlagBit | cdirect;
+  }
+  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+  const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
+  // ---- pass 2: consumption times from the carry, sums, edge
+  uint32_t Ac = Is - P + carry;
+  unsigned long long sumT = 0ull;
+#pragma unroll 2
+  for (uint32_t gi = 0; gi < gmax; ++gi) {
+    if (gi < nfull) {
+      const uint4 v = ld_shared_v4(a0 + (gi << 4));
+      const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+      Ac = A3;
+      sumT += (unsigned long long)min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+    }
+  }
+  uint32_t A_last = Ac;  // consumption time of the last valid token
+  if (ntail) {
+    const uint32_t A0 = max(Ac + P, t0), A1 = max(A0 + P, t1), A2 = max(A1 + P, t2);
+    sumT += min(A0, tcl);
+    if (ntail > 1) sumT += min(A1, tcl);
+    if (ntail > 2) sumT += min(A2, tcl);
+    A_last = ntail == 1 ? A0 : ntail == 2 ? A1 : A2;
+  }
+  const int32_t xl = xe - 1;  // the sub-range's last valid token
+  if (active && xe > xs) {
+    const uint32_t nn = (uint32_t)(xe - xs);
+    const unsigned long long sumI =
+        (unsigned long long)nn * Is + (unsigned long long)P * (((unsigned long long)nn * (nn - 1)) >> 1);
+    const unsigned long long dsum = sumT - sumI;
+    if (dsum) atomicAdd(&w.spre[qridx], dsum);
+    if (qek && xe == qvend) {
+      const uint32_t Il = qA + (uint32_t)xl * P;
+      w.edge[qridx] = (qek == 1u) ? A_last - Il : min(A_last, tcl) - Il;
+    }
+  }
+  return true;
+}
+
 template <bool kFinal>
 __device__ __noinline__ void warp_tile_global(const ScanArgs& A, uint32_t tile_s, unsigned long long p0, uint32_t r0,
                                               uint32_t dummy, uint32_t wn, uint32_t t, uint32_t mode,
-                                              uint32_t cdirect) {
+                                              uint32_t cdirect, uint32_t swz_on) {
   RawWin win{A.w.srec + r0, p0, r0, dummy, wn};
-  warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect);
+  warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect, swz_on);
 }
 
 }  // namespace
@@ -643,7 +813,8 @@ __device__ __noinline__ void warp_tile_global(const ScanArgs& A, uint32_t tile_s
 // warp shuffles only: no CTA-wide barriers on the hot path.
 template <bool kFinal>
 __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant__ ScanArgs A,
-                                                           const __grid_constant__ CUtensorMap tmap) {
+                                                           const __grid_constant__ CUtensorMap tmap_swz,
+                                                           const __grid_constant__ CUtensorMap tmap_plain) {
   extern __shared__ unsigned char s_dyn_raw[];
   unsigned char* s_base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn_raw) + 1023) & ~uintptr_t(1023));
@@ -668,25 +839,33 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   const uint32_t ntiles = w.g->ntiles;
   const unsigned long long pool_end = w.g->pool_end;
   const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
+  // 16-byte aligned timelines (every request): plain tiles and the piece-parallel path; else
+  // 128B-swizzled tiles and the row-per-lane event path
+  const uint32_t swz_on = __ldcg(&w.g->unal) ? 1u : 0u;
+  const CUtensorMap* pmap = swz_on ? &tmap_swz : &tmap_plain;
   unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles + records
   Entry* const went_own = reinterpret_cast<Entry*>(wbase + 2 * kWTile * 4);
   Entry* const went_ovf = reinterpret_cast<Entry*>(s_base + (kScanThreads / 32) * kWarpSmem);
   uint64_t* bar = s_bar[wid];
 
-  uint32_t tcur = 0, tnext = 0;
+  // tiles are claimed in increasing order, one claim ahead of the refills (the atomic's latency
+  // hides behind a tile); a warp processes its claims in increasing order, so the smallest
+  // unfinished tile is always being processed and look-backs cannot deadlock
+  uint32_t tcur = 0, tnext = 0, tpend = 0;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tcur = atomicAdd(&w.g->tile_ctr, 1u);
     tnext = atomicAdd(&w.g->tile_ctr, 1u);
+    tpend = atomicAdd(&w.g->tile_ctr, 1u);
     if (tcur < ntiles) {
       mbar_expect_tx(&bar[0], kWTile * 4u);
-      tma_tile(&tmap, wbase, tcur * (kWTile / 32), &bar[0]);
+      tma_tile(pmap, wbase, tcur * (kWTile / 32), &bar[0]);
     }
     if (tnext < ntiles) {
       mbar_expect_tx(&bar[1], kWTile * 4u);
-      tma_tile(&tmap, wbase + kWTile * 4, tnext * (kWTile / 32), &bar[1]);
+      tma_tile(pmap, wbase + kWTile * 4, tnext * (kWTile / 32), &bar[1]);
     }
   }
   __syncwarp();
@@ -772,16 +951,18 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
       if (pe > full_rows_end) {
         const unsigned long long lo = max(p0, full_rows_end);
         for (unsigned long long p = lo + lane; p < pe; p += 32)
-          *reinterpret_cast<uint32_t*>(tile + swz((uint32_t)(p - p0))) = r.tl_pool[p];
+          *reinterpret_cast<uint32_t*>(tile + (swz_on ? swz((uint32_t)(p - p0)) : (uint32_t)(p - p0) * 4u)) =
+              r.tl_pool[p];
       }
     }
     __syncwarp();
     const unsigned long long t_body = (w.trace && tcur < 16384) ? gtimer() : 0ull;
     if (win_ok) {
       EntWin win{smem_u32(went)};
-      warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm);
+      if (swz_on || !warp_tile_aligned<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm))
+        warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm, swz_on);
     } else {
-      warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm);
+      warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
     }
     // refill this buffer with a newly claimed warp-tile (two ahead)
     __syncwarp();
@@ -792,11 +973,12 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     }
     uint32_t tt = 0;
     if (lane == 0) {
-      tt = atomicAdd(&w.g->tile_ctr, 1u);
+      tt = tpend;
       if (tt < ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[buf], kWTile * 4u);
-        tma_tile(&tmap, tile, tt * (kWTile / 32), &bar[buf]);
+        tma_tile(pmap, tile, tt * (kWTile / 32), &bar[buf]);
+        tpend = atomicAdd(&w.g->tile_ctr, 1u);
       }
     }
     tt = __shfl_sync(0xffffffffu, tt, 0);
@@ -906,9 +1088,9 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
   ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags};
   const uint32_t grid = r.n ? L.scan_grid : 1u;
   if (final_mode)
-    launch_pdl(k_qoe_scan<true>, grid, kScanThreads, kScanDynSmem, L.stream, A, *tmap);
+    launch_pdl(k_qoe_scan<true>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
   else
-    launch_pdl(k_qoe_scan<false>, grid, kScanThreads, kScanDynSmem, L.stream, A, *tmap);
+    launch_pdl(k_qoe_scan<false>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,

@@ -53,7 +53,8 @@ def _check_qoe(A, ctx, orc, snap, eval_time, final):
 
 @pytest.mark.parametrize("seed", range(30))
 def test_qoe_random_small(A, ctx, orc, seed):
-    snap = W.random_small(seed, n=int(np.random.default_rng(seed).integers(1, 40)), max_tokens=300)
+    # odd seeds: unaligned pools (the scan's general path); even seeds: 16-byte aligned timelines
+    snap = W.random_small(seed, align=[4, 1][seed % 2], n=int(np.random.default_rng(seed).integers(1, 40)), max_tokens=300)
     for final in (False, True):
         _check_qoe(A, ctx, orc, snap, snap.now_us + snap.horizon_us, final)
         _check_qoe(A, ctx, orc, snap, snap.now_us, final)
@@ -63,8 +64,9 @@ def test_qoe_many_tiles_ragged(A, ctx, orc):
     # ~4.7 tiles of tokens, a 100k-token request spanning many tiles, empty requests, a ragged tail
     rng = np.random.default_rng(99)
     snap = W.random_small(7, n=60, max_tokens=2000)
+    snap_u = W.random_small(7, n=60, max_tokens=2000, align=1)
     long = W.snapshot(300, seed=3)
-    for s in (snap, long):
+    for s in (snap, snap_u, long):
         _check_qoe(A, ctx, orc, s, s.now_us + s.horizon_us, False)
         _check_qoe(A, ctx, orc, s, s.now_us, True)
     # one request with 100,003 tokens on time then late, plus neighbours with 0 and 1 tokens
@@ -73,7 +75,12 @@ def test_qoe_many_tiles_ragged(A, ctx, orc):
     d = ttft + np.arange(g, dtype=np.int64) * P + np.where(np.arange(g) > 50_000, 7_777, 0)
     d = np.maximum.accumulate(d + rng.integers(-900, 900, g)).astype(np.uint32)
     tl = [np.zeros(0, np.uint32), d, np.array([12], np.uint32), np.zeros(0, np.uint32)]
-    gg, base, pool = W._pack(tl)
+    for align in (4, 1):
+        _check_long_request(A, ctx, orc, tl, ttft, P, d, align)
+
+
+def _check_long_request(A, ctx, orc, tl, ttft, P, d, align):
+    gg, base, pool = W._pack(tl, align)
     n = 4
     big = W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, ttft, np.uint32),
                      period_us=np.full(n, P, np.uint32), ctx_len=np.ones(n, np.uint32), n_deliv=gg,
@@ -108,7 +115,8 @@ def _check_gains(A, ctx, orc, snap, B_list, sub=None):
 
 @pytest.mark.parametrize("seed", range(40))
 def test_gains_random_small(A, ctx, orc, seed):
-    snap = W.random_small(seed, n=int(np.random.default_rng(seed + 1).integers(1, 30)), max_tokens=200)
+    snap = W.random_small(seed, n=int(np.random.default_rng(seed + 1).integers(1, 30)), max_tokens=200,
+                          align=[4, 1][seed % 2])
     _check_gains(A, ctx, orc, snap, np.arange(1, snap.tau_us.size + 1))
 
 
@@ -166,7 +174,7 @@ def test_golden_g1_on_gpu(A, ctx, orc):
 
 @pytest.mark.parametrize("seed", range(60))
 def test_schedule_random_small(A, ctx, orc, seed):
-    snap = W.random_small(seed, B_cap=int(np.random.default_rng(seed).integers(1, 20)))
+    snap = W.random_small(seed, B_cap=int(np.random.default_rng(seed).integers(1, 20)), align=[4, 1][seed % 2])
     flags = [1, 3, 0, 2][seed % 4]
     _check_sched(A, ctx, orc, snap, flags=flags, cur_latency=[0, 400_000][seed % 2])
 

@@ -72,15 +72,11 @@ class Snapshot:
     def n_tokens(self) -> int:
         return int(self.tl_pool.shape[0])
 
-    def subset(self, idx) -> "Snapshot":
+    def subset(self, idx, align: int = 4) -> "Snapshot":
         """Requests idx (re-packed pool), same parameters."""
         idx = np.asarray(idx, dtype=np.int64)
-        g = self.n_deliv[idx]
         parts = [self.tl_pool[int(self.tl_base[i]):int(self.tl_base[i]) + int(self.n_deliv[i])] for i in idx]
-        pool = np.concatenate(parts).astype(np.uint32) if len(parts) else np.zeros(0, np.uint32)
-        base = np.zeros(len(idx), np.uint64)
-        if len(idx):
-            base[1:] = np.cumsum(g[:-1].astype(np.uint64))
+        g, base, pool = _pack(parts, align)
         return replace(self, arrival_us=self.arrival_us[idx].copy(), ttft_us=self.ttft_us[idx].copy(),
                        period_us=self.period_us[idx].copy(), ctx_len=self.ctx_len[idx].copy(),
                        n_deliv=g.copy(), max_total=self.max_total[idx].copy(),
@@ -88,12 +84,24 @@ class Snapshot:
                        running=self.running[idx].copy(), tl_base=base, tl_pool=pool)
 
 
-def _pack(timelines):
+POOL_ALIGN = 4  # tokens: every timeline starts on a 16-byte boundary (the scan's aligned fast path)
+
+
+def _pack(timelines, align: int = POOL_ALIGN):
+    """Pack per-request timelines into one pool, request order; each timeline starts at a
+    multiple of `align` tokens (padding repeats the previous value; it is never a valid token)."""
     g = np.array([len(t) for t in timelines], dtype=np.uint32)
+    span = ((g.astype(np.uint64) + np.uint64(align - 1)) // np.uint64(align)) * np.uint64(align)
     base = np.zeros(len(timelines), np.uint64)
     if len(timelines):
-        base[1:] = np.cumsum(g[:-1].astype(np.uint64))
-    pool = np.concatenate([np.asarray(t, np.uint32) for t in timelines]) if int(g.sum()) else np.zeros(0, np.uint32)
+        base[1:] = np.cumsum(span[:-1])
+    total = int(span.sum())
+    pool = np.zeros(total, np.uint32)
+    for i, t in enumerate(timelines):
+        if len(t):
+            b = int(base[i])
+            pool[b:b + len(t)] = np.asarray(t, np.uint32)
+            pool[b + len(t):b + int(span[i])] = pool[b + len(t) - 1]
     return g, base, pool
 
 
@@ -271,8 +279,14 @@ def sweep(scenarios, n_base: int = 2000) -> tuple[Snapshot, np.ndarray]:
     request offsets u32[S+1] of the scenarios (BASELINE config 5: 32 seeds x SWEEP_RHOS)."""
     parts = [sweep_scenario(sd, rho, n_base) for sd, rho in scenarios]
     cat = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
-    g = cat["n_deliv"].astype(np.uint64)
-    base = np.concatenate([[0], np.cumsum(g)[:-1]]).astype(np.uint64)
+    g = cat["n_deliv"].astype(np.int64)
+    span = (g + POOL_ALIGN - 1) // POOL_ALIGN * POOL_ALIGN  # 16-byte aligned timelines
+    base = np.concatenate([[0], np.cumsum(span)[:-1]]).astype(np.int64)
+    src = np.concatenate([[0], np.cumsum(g)[:-1]])
+    pool = np.zeros(int(span.sum()), np.uint32)
+    pool[np.repeat(base - src, g) + np.arange(int(g.sum()))] = cat["tl_pool"]
+    cat["tl_pool"] = pool
+    base = base.astype(np.uint64)
     n = int(g.size)
     off = np.concatenate([[0], np.cumsum([p["n_deliv"].size for p in parts])]).astype(np.uint32)
     snap = Snapshot(arrival_us=cat["arrival_us"], ttft_us=cat["ttft_us"], period_us=cat["period_us"],
@@ -288,7 +302,7 @@ def config5_scenarios(seeds: int = 32, rhos=SWEEP_RHOS):
     return [(sd, rho) for sd in range(1, seeds + 1) for rho in rhos]
 
 
-def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True) -> Snapshot:
+def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True, align: int = POOL_ALIGN) -> Snapshot:
     """Small adversarial instances for parity: arbitrary periods, ttft, offsets,
     max_total caps, deliveries ahead of / behind schedule, pauses, ties."""
     rng = np.random.default_rng(seed)
@@ -310,7 +324,7 @@ def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True) -> Snapshot:
             ts = np.minimum(ts, ttft[i] + np.arange(g) * int(period[i]))  # on/ahead of schedule
             ts = np.sort(np.minimum(ts, age))
         timelines.append(ts.astype(np.uint32))
-    g, base, pool = _pack(timelines)
+    g, base, pool = _pack(timelines, align)
     ctx = rng.integers(1, 60, n).astype(np.uint32)
     mt = np.where(rng.random(n) < 0.2, g + rng.integers(0, 5, n), UINT32_MAX).astype(np.uint32)
     off = np.where(rng.random(n) < 0.3, rng.integers(0, 3_000_000, n), 0).astype(np.uint32)
