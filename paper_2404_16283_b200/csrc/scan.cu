@@ -428,8 +428,8 @@ struct EntWin {
 };
 
 template <bool kFinal, class Win>
-__device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn, uint32_t t,
-                                          uint32_t mode, uint32_t cdirect, uint32_t swz_on) {
+__device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn,
+                                                        uint32_t t, uint32_t mode, uint32_t cdirect, uint32_t swz_on) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
   const int32_t x0 = (int32_t)(lane * kScanItems);
@@ -596,7 +596,8 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
   } else if (mode == 1u) {
     acc = kFlagBit | cdirect;
   }
-  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+  const unsigned long long prefix = seg_combine(acc, tile_agg);
+  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
   const uint32_t carry = (uint32_t)seg_combine(acc, excl);
 
   // ---- the held first piece, now that its carry-in is known
@@ -625,6 +626,7 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
     flush(e0, x0, h_xe, h_sum);
     if (h_has_edge) w.edge[e0.ridx] = h_edge;
   }
+  return prefix;
 }
 
 // ---- aligned fast path: every request starting in the tile starts on a 16-byte boundary
@@ -639,14 +641,15 @@ __device__ __forceinline__ void warp_tile(const ScanArgs& A, const Win& win, uin
 //   pass 2  the recurrence again from the carry: sum of T~ = min(A, t) over the valid tokens,
 //           the edge value at the request's last valid token, one 64-bit atomic per sub-range.
 // Returns false (nothing done) when the tile has too many pieces for one round.
-template <bool kFinal, class Win>
-__device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn,
-                                                  uint32_t t, uint32_t mode, uint32_t cdirect) {
+// e: this lane's request of the tile (lane q = request r0 + q, q < wn <= 24, zero-length ones
+// included), in tile-local coordinates.
+template <bool kFinal>
+__device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t wn,
+                                                  uint32_t t, uint32_t mode, uint32_t cdirect,
+                                                  unsigned long long& prefix) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
-  if (wn > 24u) return false;
-  // lane q: window entry q -> its piece [ps, pe) of valid tokens inside the tile
-  const Entry e = lane < wn ? win.get(lane) : null_entry(true);
+  (void)wn;
   const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
   const bool starts_in = e.ls >= 0 && e.ls < (int32_t)kWTile;
   if (__any_sync(0xffffffffu, starts_in && (e.ls & 3))) return false;  // not 16-byte aligned
@@ -758,7 +761,8 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Win& 
   } else if (mode == 1u) {
     acc = kFlagBit | cdirect;
   }
-  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | seg_combine(acc, tile_agg));
+  prefix = seg_combine(acc, tile_agg);
+  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
@@ -796,11 +800,11 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Win& 
 }
 
 template <bool kFinal>
-__device__ __noinline__ void warp_tile_global(const ScanArgs& A, uint32_t tile_s, unsigned long long p0, uint32_t r0,
-                                              uint32_t dummy, uint32_t wn, uint32_t t, uint32_t mode,
-                                              uint32_t cdirect, uint32_t swz_on) {
+__device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, uint32_t tile_s, unsigned long long p0,
+                                                            uint32_t r0, uint32_t dummy, uint32_t wn, uint32_t t,
+                                                            uint32_t mode, uint32_t cdirect, uint32_t swz_on) {
   RawWin win{A.w.srec + r0, p0, r0, dummy, wn};
-  warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect, swz_on);
+  return warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect, swz_on);
 }
 
 }  // namespace
@@ -848,84 +852,129 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   Entry* const went_ovf = reinterpret_cast<Entry*>(s_base + (kScanThreads / 32) * kWarpSmem);
   uint64_t* bar = s_bar[wid];
 
-  // tiles are claimed in increasing order, one claim ahead of the refills (the atomic's latency
-  // hides behind a tile); a warp processes its claims in increasing order, so the smallest
-  // unfinished tile is always being processed and look-backs cannot deadlock
-  uint32_t tcur = 0, tnext = 0, tpend = 0;
+  // Chunks of CH consecutive warp-tiles are claimed in increasing order (lane 0 runs the tile
+  // sequence two tiles ahead of the processing, for the TMA double buffer, and holds the next
+  // chunk's claim one chunk ahead).  Inside a chunk the carry passes from tile to tile in
+  // registers; a chunk's first tile takes it from the head request's earlier tokens (direct read)
+  // or by look-back.  A warp processes its tiles in increasing order, so the smallest unfinished
+  // tile is always being processed and look-backs cannot deadlock.
+  constexpr uint32_t kNone = 0xFFFFFFFFu, kStart = 0x80000000u;
+  const uint32_t KW = gridDim.x * (kScanThreads / 32);
+  const uint32_t CH = min(8u, max(1u, ntiles / (8u * KW)));
+  const uint32_t nchunks = (ntiles + CH - 1) / CH;
+  uint32_t g_t = kNone, g_hi = 0, g_nxt = 0;  // lane 0: generator position, chunk end, claimed chunk
+  auto gen = [&]() -> uint32_t {
+    if (g_t + 1 < g_hi) return ++g_t;
+    if (g_nxt >= nchunks) return kNone;
+    g_t = g_nxt * CH;
+    g_hi = min(g_t + CH, ntiles);
+    g_nxt = atomicAdd(&w.g->tile_ctr, 1u);
+    return g_t | kStart;
+  };
+  uint32_t cur = kNone, s1 = kNone;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    tcur = atomicAdd(&w.g->tile_ctr, 1u);
-    tnext = atomicAdd(&w.g->tile_ctr, 1u);
-    tpend = atomicAdd(&w.g->tile_ctr, 1u);
-    if (tcur < ntiles) {
+    g_nxt = atomicAdd(&w.g->tile_ctr, 1u);
+    cur = gen();
+    s1 = gen();
+    if (cur != kNone) {
       mbar_expect_tx(&bar[0], kWTile * 4u);
-      tma_tile(pmap, wbase, tcur * (kWTile / 32), &bar[0]);
+      tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), &bar[0]);
     }
-    if (tnext < ntiles) {
+    if (s1 != kNone) {
       mbar_expect_tx(&bar[1], kWTile * 4u);
-      tma_tile(pmap, wbase + kWTile * 4, tnext * (kWTile / 32), &bar[1]);
+      tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), &bar[1]);
     }
   }
   __syncwarp();
-  tcur = __shfl_sync(0xffffffffu, tcur, 0);
-  tnext = __shfl_sync(0xffffffffu, tnext, 0);
+  cur = __shfl_sync(0xffffffffu, cur, 0);
+  unsigned long long acc_reg = 0ull;  // carry out of the previous tile of the chunk
   uint32_t buf = 0, ph0 = 0, ph1 = 0;
-  while (tcur < ntiles) {
-    const unsigned long long p0 = (unsigned long long)tcur * kWTile;
-    // tile descriptor (prep) and the window's request records
-    TileMeta tm;
-    uint32_t r_end = 0;
+  // the current tile's descriptor (lane 0) and request records (lane k: request r0 + k), loaded
+  // one tile ahead: within a chunk the next tile's first request is this tile's last one, so its
+  // records are requested before this tile is computed
+  TileMeta tm;
+  uint32_t r_end = 0;
+  ScanRec rec;
+  rec.lim = 0;
+  auto load_meta = [&](uint32_t tt, TileMeta& m, uint32_t& re) {
     if (lane == 0) {
-      tm = w.tile_meta[tcur];
-      r_end = (tcur + 1 < ntiles) ? w.tile_meta[tcur + 1].r0 : n - 1;
+      m = w.tile_meta[tt];
+      re = (tt + 1 < ntiles) ? w.tile_meta[tt + 1].r0 : n - 1;
     }
+  };
+  auto load_rec = [&](uint32_t rr, ScanRec& sr) {
+    sr.lim = 0;
+    if (rr + lane < n) sr = w.srec[rr + lane];
+  };
+  if (cur != kNone) {
+    load_meta(cur & ~kStart, tm, r_end);
+    load_rec(__shfl_sync(0xffffffffu, tm.r0, 0), rec);
+  }
+  while (cur != kNone) {
+    const uint32_t tcur = cur & ~kStart;
+    const bool chunk_start = (cur & kStart) != 0u;
+    const unsigned long long p0 = (unsigned long long)tcur * kWTile;
     const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
     const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
     const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
     const uint32_t httft = __shfl_sync(0xffffffffu, tm.httft, 0);
     const uint32_t hP = __shfl_sync(0xffffffffu, tm.hP, 0);
     const unsigned long long hbase = __shfl_sync(0xffffffffu, tm.hbase, 0);
-    r_end = __shfl_sync(0xffffffffu, r_end, 0);
-    const uint32_t dummy = flags & 1u, mode = (flags >> 1) & 3u;
-    const uint32_t wn = r_end - r0 + 1 + dummy;
+    const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
+    // ---- prefetch of the next tile
+    const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
+    TileMeta tmn;
+    uint32_t r_endn = 0;
+    ScanRec recn;
+    recn.lim = 0;
+    const bool seq = nxt != kNone && (nxt & ~kStart) == tcur + 1u;
+    if (nxt != kNone) load_meta(nxt & ~kStart, tmn, r_endn);
+    if (seq) load_rec(re, recn);
+    const uint32_t dummy = flags & 1u;
+    // inside a chunk the carry comes from the previous tile (mode 1 with that value)
+    const uint32_t mode = chunk_start ? (flags >> 1) & 3u : 1u;
+    const uint32_t wn = re - r0 + 1 + dummy;
     const uint32_t nrec = wn - dummy;
-    // tile-local entries of the window, without requests that have no valid token here
-    // (lim == 0: their pool span is dead either way); the owner r0 is always kept
-    // (a dense tile borrows the CTA's larger overflow window when it is free)
+    const bool fast = !swz_on && nrec <= 24u;
+    // old path: tile-local entries of the window in shared memory, without requests that have no
+    // valid token here (lim == 0); the owner r0 is always kept (a dense tile borrows the CTA's
+    // larger overflow window when it is free)
     Entry* went = went_own;
-    uint32_t cap = kWWinCap;
+    uint32_t cap = kWWinCap, wc = dummy;
     bool ovf = false;
-    if (wn >= (uint32_t)kWWinCap) {
-      uint32_t got = 0;
-      if (lane == 0) got = atomicCAS(&s_ovf_owner, 0u, wid + 1u) == 0u;
-      ovf = __shfl_sync(0xffffffffu, got, 0) != 0u;
-      if (ovf) {
-        went = went_ovf;
-        cap = kOvfCap;
+    if (!fast) {
+      if (wn >= (uint32_t)kWWinCap) {
+        uint32_t got = 0;
+        if (lane == 0) got = atomicCAS(&s_ovf_owner, 0u, wid + 1u) == 0u;
+        ovf = __shfl_sync(0xffffffffu, got, 0) != 0u;
+        if (ovf) {
+          went = went_ovf;
+          cap = kOvfCap;
+        }
       }
-    }
-    uint32_t wc = dummy;
-    if (dummy && lane == 0) went[0] = null_entry(false);
-    for (uint32_t c0 = 0; c0 < nrec && wc < cap; c0 += 32) {
-      const uint32_t k = c0 + lane;
-      ScanRec sr;
-      bool keep = false;
-      if (k < nrec) {
-        sr = w.srec[r0 + k];
-        keep = k == 0 || sr.lim != 0u;
+      if (dummy && lane == 0) went[0] = null_entry(false);
+      for (uint32_t c0 = 0; c0 < nrec && wc < cap; c0 += 32) {
+        const uint32_t k = c0 + lane;
+        ScanRec sr = rec;
+        bool keep = false;
+        if (k < nrec) {
+          if (c0) sr = w.srec[r0 + k];
+          keep = k == 0 || sr.lim != 0u;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        const uint32_t pos = wc + __popc(bal & ((1u << lane) - 1u));
+        if (keep && pos < cap) went[pos] = entry_of(sr, r0 + k, p0);
+        wc += __popc(bal);
       }
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-      const uint32_t pos = wc + __popc(bal & ((1u << lane) - 1u));
-      if (keep && pos < cap) went[pos] = entry_of(sr, r0 + k, p0);
-      wc += __popc(bal);
+      if (wc < cap && lane == 0) went[wc] = null_entry(true);
     }
     const bool win_ok = wc < cap;  // entries + sentinel fit the window
-    if (win_ok && lane == 0) went[wc] = null_entry(true);
     // direct head carry
-    uint32_t cm = 0;
-    if (mode == 1u) {
+    uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
+    if (chunk_start && mode == 1u) {
       for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
         uint32_t d[8];
 #pragma unroll
@@ -957,34 +1006,56 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     }
     __syncwarp();
     const unsigned long long t_body = (w.trace && tcur < 16384) ? gtimer() : 0ull;
-    if (win_ok) {
-      EntWin win{smem_u32(went)};
-      if (swz_on || !warp_tile_aligned<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm))
-        warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm, swz_on);
-    } else {
-      warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+    bool done = false;
+    if (fast) {
+      const Entry e = lane < nrec ? entry_of(rec, r0 + lane, p0) : null_entry(true);
+      done = warp_tile_aligned<kFinal>(A, e, smem_u32(tile), nrec, tcur, mode, cm, acc_reg);
     }
-    // refill this buffer with a newly claimed warp-tile (two ahead)
+    if (!done) {
+      if (fast) {  // fall back: stage the window now
+        if (dummy && lane == 0) went[0] = null_entry(false);
+        wc = dummy;
+        {
+          const bool keep = lane < nrec && (lane == 0 || rec.lim != 0u);
+          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) went[wc + __popc(bal & ((1u << lane) - 1u))] = entry_of(rec, r0 + lane, p0);
+          wc += __popc(bal);
+        }
+        if (lane == 0) went[wc] = null_entry(true);
+        __syncwarp();
+      }
+      if (fast || win_ok) {
+        EntWin win{smem_u32(went)};
+        acc_reg = warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm, swz_on);
+      } else {
+        acc_reg = warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+      }
+    }
+    // refill this buffer with the tile two ahead in the warp's sequence
     __syncwarp();
     if (ovf && lane == 0) atomicExch(&s_ovf_owner, 0u);
     if (t_body && lane == 0) {
       w.trace[16384 + 2 * tcur] = t_body;
       w.trace[16384 + 2 * tcur + 1] = gtimer();
     }
-    uint32_t tt = 0;
+    uint32_t nx = kNone;
     if (lane == 0) {
-      tt = tpend;
-      if (tt < ntiles) {
+      const uint32_t s2 = gen();
+      if (s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[buf], kWTile * 4u);
-        tma_tile(pmap, tile, tt * (kWTile / 32), &bar[buf]);
-        tpend = atomicAdd(&w.g->tile_ctr, 1u);
+        tma_tile(pmap, tile, (s2 & ~kStart) * (kWTile / 32), &bar[buf]);
       }
+      nx = s1;
+      s1 = s2;
     }
-    tt = __shfl_sync(0xffffffffu, tt, 0);
-    tcur = tnext;
-    tnext = tt;
+    cur = __shfl_sync(0xffffffffu, nx, 0);
     buf ^= 1u;
+    // the next tile's records (requested earlier when it follows this one)
+    if (cur != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tmn.r0, 0), recn);
+    tm = tmn;
+    r_end = r_endn;
+    rec = recn;
   }
   if (w.trace && blockIdx.x < 1000 && lane == 0) atomicMax(&w.trace[5000 + 2 * blockIdx.x + 1], gtimer());
 }
