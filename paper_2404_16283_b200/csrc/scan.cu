@@ -657,8 +657,30 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry
   const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
   // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32)
   // (an odd number of 16-byte chunks: sub-ranges of one piece hit distinct shared-memory banks)
-  const uint32_t SR = 4u * (((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u);
-  const uint32_t cnt = (len + SR - 1) / SR;
+  // ceil(len / (4 s4)) for len <= kWTile, s4 <= 256: fp32 estimate + one exact fix-up
+  auto nsub = [&](uint32_t s4) -> uint32_t {
+    const uint32_t sr = 4u * s4;
+    uint32_t c = (uint32_t)__fmul_rn((float)(len + sr - 1), __frcp_rn((float)sr));
+    if (c * sr < len) ++c;
+    else if (c && (c - 1) * sr >= len) --c;
+    return c;
+  };
+  // the shortest odd s4 with sum ceil(len / 4 s4) <= 32 (odd: the sub-ranges of one piece start
+  // in distinct shared-memory banks), between the volume bound and the always-feasible bound
+  uint32_t s_hi = ((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u;
+  uint32_t s_lo = 1u;
+  {
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, len);
+    s_lo = max(1u, (tot + 127u) / 128u) | 1u;
+  }
+  while (s_lo < s_hi) {  // warp-uniform bisection over odd values
+    const uint32_t mid = ((s_lo + s_hi) >> 1) | 1u;
+    const uint32_t m = mid >= s_hi ? s_lo : mid;
+    if (__reduce_add_sync(0xffffffffu, nsub(m)) <= 32u) s_hi = m;
+    else s_lo = m + 2u;
+  }
+  const uint32_t SR = 4u * s_hi;
+  const uint32_t cnt = nsub(s_hi);
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
