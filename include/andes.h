@@ -94,6 +94,8 @@ typedef struct {
 #define ANDES_FORCE 1u        /* run the solver even if the trigger does not fire            */
 #define ANDES_PRUNE 2u        /* restrict B to [B_min, B_max]; default [1, B_max] */
 #define ANDES_DEBUG_CHECKS 4u /* device-side data precondition checks                         */
+#define ANDES_LQSF 16u        /* priority = the raw gain (Least QoE Slack First; reading
+                                 R21) instead of gain / l (Eq. 6); everything else unchanged  */
 
 /* Decision-time parameters. */
 typedef struct {
@@ -104,7 +106,7 @@ typedef struct {
     uint64_t kv_capacity;    /* M: KV-cache capacity in tokens (Eq. 5)                          */
     uint32_t preempt_cap;    /* max preemptions per decision; UINT32_MAX = off (reading R18)    */
     uint32_t cur_latency_us; /* current iteration latency (trigger)                     */
-    uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS                  */
+    uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS | ANDES_LQSF     */
 } AndesSchedParams;
 
 /* scalars[] layout of AndesDecision */

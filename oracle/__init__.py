@@ -24,6 +24,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 ORC_FORCE = 1
 ORC_PRUNE = 2
+ORC_LQSF = 16
 UINT32_MAX = 0xFFFFFFFF
 INT64_MIN = -(1 << 63)
 

@@ -47,6 +47,7 @@
 
 #define ORC_FORCE 1u
 #define ORC_PRUNE 2u
+#define ORC_LQSF 16u /* priority = the raw gain (Least QoE Slack First; SPEC lqsf_policy) */
 
 #define ORC_FLAG_TRIGGERED 1u
 #define ORC_FLAG_CAP_HIT 2u
@@ -274,6 +275,16 @@ static float priority_key(double gain, uint32_t l)
     return key;
 }
 
+/* LQSF reading (R21): the same decision with the raw gain (Eq. 4) as the priority
+ * instead of gain / l (Eq. 6): key = float(gain), -0 canonicalised to +0. */
+static float lqsf_key(double gain)
+{
+    float key = (float)gain;
+    if (key == 0.0f)
+        key = 0.0f;
+    return key;
+}
+
 static int64_t gain_fixed(double gain)
 {
     return llrint(gain * 4294967296.0);
@@ -473,7 +484,7 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
             gain[i] = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s) - qw[i];
             items[i].idx = i;
             items[i].rank = r->rank[i];
-            items[i].key = priority_key(gain[i], r->ctx_len[i]);
+            items[i].key = (p->flags & ORC_LQSF) ? lqsf_key(gain[i]) : priority_key(gain[i], r->ctx_len[i]);
         }
         qsort(items, n, sizeof(item_t), cmp_greedy);
         /* Algorithm 1: take while within M and B, else break. */

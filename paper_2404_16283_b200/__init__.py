@@ -31,6 +31,7 @@ ANDES_EVAL_FINAL = 1
 ANDES_FORCE = 1
 ANDES_PRUNE = 2
 ANDES_DEBUG_CHECKS = 4
+ANDES_LQSF = 16
 ANDES_F_TRIGGERED = 1
 ANDES_F_CAP_HIT = 2
 ANDES_F_CAP_OVERRIDDEN = 4

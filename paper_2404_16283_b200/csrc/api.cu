@@ -483,7 +483,8 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LaunchCfg L = cfg_of(c, stream);
   const ReqView r = view_of(req);
-  const Work w = work_of(c, r.n);
+  Work w = work_of(c, r.n);
+  w.lqsf = (p->flags & ANDES_LQSF) ? 1u : 0u;
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
@@ -548,7 +549,8 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LaunchCfg L = cfg_of(c, stream);
   const ReqView r = view_of(req);
-  const Work w = work_of(c, r.n);
+  Work w = work_of(c, r.n);
+  w.lqsf = (p->flags & ANDES_LQSF) ? 1u : 0u;
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};

@@ -11,12 +11,12 @@ constexpr int kSortCap = kMaxB;
 constexpr int kVictCap = kMaxRunning;
 
 // ---------------------------------------------------------------- block helpers
-__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau) {
-  return ordered_key(prio_key(gain_at(unpack_state(p), tau), p.l));
+__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau, uint32_t lqsf) {
+  return ordered_key(prio_key(gain_at(unpack_state(p), tau), p.l, lqsf));
 }
 
-__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau) {
-  return composite(okey_of(p, tau), p.rank);
+__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau, uint32_t lqsf) {
+  return composite(okey_of(p, tau, lqsf), p.rank);
 }
 
 template <int NT>

@@ -170,6 +170,7 @@ struct Work {
   uint32_t N_cap;            // row stride of keyrow
   uint32_t tiles_cap;        // capacity of tile_owner / tile_status
   uint32_t S_cap;            // survivor capacity of cand_idx
+  uint32_t lqsf;             // this call's priority: 0 gain / l (Eq. 6), 1 raw gain (ANDES_LQSF)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -318,9 +319,10 @@ __device__ __forceinline__ double gain_at(const GainState& s, uint32_t tau) {
   return __dsub_rn(qoe_value(sd, sw), s.qw);
 }
 
-// priority key (Eq. 6, reading R9): float(gain / l), -0 -> +0
-__device__ __forceinline__ float prio_key(double gain, uint32_t l) {
-  float k = __double2float_rn(__ddiv_rn(gain, (double)l));
+// priority key (Eq. 6, reading R9): float(gain / l), -0 -> +0; with the LQSF objective (reading
+// R21) the raw gain (Eq. 4) is the priority: float(gain)
+__device__ __forceinline__ float prio_key(double gain, uint32_t l, uint32_t lqsf = 0u) {
+  float k = lqsf ? __double2float_rn(gain) : __double2float_rn(__ddiv_rn(gain, (double)l));
   return (__float_as_uint(k) << 1) == 0u ? 0.0f : k;
 }
 

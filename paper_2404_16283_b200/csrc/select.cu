@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
       serve_area(s, thi, sd_hi, sw_hi);
       const double q_ub = qoe_value(sd_lo, sw_hi);
       const double q_lb = (sw_lo == 0) ? 0.0 : qoe_value(sd_hi, sw_lo);
-      ub = ordered_key(prio_key(__dsub_rn(q_ub, s.qw), p.l));
-      lb = ordered_key(prio_key(__dsub_rn(q_lb, s.qw), p.l));
+      ub = ordered_key(prio_key(__dsub_rn(q_ub, s.qw), p.l, w.lqsf));
+      lb = ordered_key(prio_key(__dsub_rn(q_lb, s.qw), p.l, w.lqsf));
     }
     w.ub[i] = ub;
     atomicAdd(&s_hlb[lb >> 20], 1u);
@@ -296,7 +296,7 @@ __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
     for (uint32_t q = tid; q < n_run; q += kSelThreads) {
       const uint32_t i = w.run_list[q];
       wl += r.ctx_len[i];
-      const unsigned long long c = Bs ? comp_of(w.st[i], tB) : 0ull;
+      const unsigned long long c = Bs ? comp_of(w.st[i], tB, w.lqsf) : 0ull;
       if (ks == 0 || c < thr) {
         const uint32_t slot = atomicAdd(&s_nv, 1u);
         s_key[slot] = ~c;  // descending of ~ = ascending of the composite
@@ -443,7 +443,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
       const uint32_t i = __ldcg(w.run_list + q);
       const PackedState st = w.st[i];
       wl += st.l;
-      const unsigned long long c = comp_of(st, tB);
+      const unsigned long long c = comp_of(st, tB, w.lqsf);
       if (kstar == 0 || c < thr) {
         const uint32_t slot = atomicAdd(&s_nv, 1u);
         vkey[slot] = ~c;  // descending of ~c = ascending composite
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     if (ovf) {
       // overflow fallback: exact keys of every request at B (row B of keyrow), radix select
       uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
-      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB);
+      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB, w.lqsf);
       __syncthreads();
       cnt = select_top_k(
           n, k,
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
         const uint32_t i = __ldcg(w.cand_idx + e);
         const PackedState p = w.st[i];
         const double gn = gain_at(unpack_state(p), tB);
-        s_all[e] = composite(ordered_key(prio_key(gn, p.l)), p.rank);
+        s_all[e] = composite(ordered_key(prio_key(gn, p.l, w.lqsf)), p.rank);
         s_gall[e] = gain_fixed(gn);
         s_ri[e] = i;
       }

@@ -337,3 +337,17 @@ def test_scenario_means_match_oracle(A, ctx, orc):
         assert int(cnt[s]) == sel.size
         exact = math.fsum(q[sel]) / sel.size if sel.size else 0.0
         assert abs(mean[s] - exact) <= 1e-12 * max(1.0, abs(exact)), (s, mean[s], exact)
+
+
+# ---------------------------------------------------------------- LQSF priority (NEXT-2, reading R21)
+@pytest.mark.parametrize("seed", range(20))
+def test_schedule_lqsf_random_small(A, ctx, orc, seed):
+    snap = W.random_small(seed + 100, B_cap=int(np.random.default_rng(seed).integers(1, 20)), align=[4, 1][seed % 2])
+    _check_sched(A, ctx, orc, snap, flags=[1 | 16, 3 | 16][seed % 2], cap=[W.UINT32_MAX, 1][seed % 2])
+
+
+def test_schedule_lqsf_config2(A, ctx, orc):
+    snap = W.config2()
+    g, o = _check_sched(A, ctx, orc, snap, flags=1 | 16, cap=16)
+    g2, o2 = _check_sched(A, ctx, orc, snap, flags=1, cap=16)
+    assert not np.array_equal(g["V"], g2["V"])  # the priority changed the decision

@@ -144,3 +144,9 @@ def test_shard_long_contexts_reach_the_long_bucket(A):
     snap.kv_capacity = 60_000
     check(A, snap, 3)
     check(A, snap, 5, cap=1)
+
+
+def test_shard_lqsf(A):
+    snap = W.config2()
+    check(A, snap, 3, flags=1 | 16, cap=16)
+    check(A, W.random_small(5, B_cap=9), 2, flags=1 | 16)

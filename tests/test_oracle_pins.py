@@ -436,3 +436,30 @@ def test_cap_memory_override(orc):
     dec = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, 100, preempt_cap=0)
     assert dec.flags & 4 and dec.admit.size == 0
     assert sum(int(snap.ctx_len[i]) for i in range(3) if dec.serve_mask[i]) <= 100
+
+
+def test_lqsf_priority_is_the_raw_gain(orc):
+    """LQSF (SPEC lqsf_policy; reading R21): the priority is the raw gain (Eq. 4) instead
+    of gain / l (Eq. 6).  On G1 at B = 1 the raw-gain order puts R3 first: its gain is exactly 1
+    (Q_serve = 1, Q_wait = 0 by the hand check), so V(1) = 2^32; Eq. 6 keeps R1 (gain 10/11 on
+    l = 100 beats 1 on l = 800), V(1) = 3904515724 = llrint(10/11 * 2^32)."""
+    snap, d = g1_snapshot()
+    andes = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity)
+    lqsf = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                        flags=orc.ORC_FORCE | orc.ORC_LQSF)
+    assert int(andes.V[0]) == 3904515724 == round(10 / 11 * 2 ** 32)
+    assert int(lqsf.V[0]) == 2 ** 32
+    # every B: the LQSF prefix is Algorithm 1 over the raw-gain order (key desc, rank asc)
+    gain, key, qw = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, [1, 2, 3])
+    for B in range(1, 4):
+        g = gain[B - 1].astype(np.float32).astype(np.float64)
+        order = sorted(range(snap.n), key=lambda i: (-g[i], int(snap.rank[i])))
+        W_, c, V = 0, 0, 0
+        for i in order:
+            if W_ + int(snap.ctx_len[i]) <= snap.kv_capacity and c + 1 <= B:
+                W_ += int(snap.ctx_len[i])
+                c += 1
+                V += int(np.rint(gain[B - 1][i] * 2.0 ** 32))
+            else:
+                break
+        assert int(lqsf.V[B - 1]) == V and int(lqsf.kstar[B - 1]) == c
