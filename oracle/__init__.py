@@ -25,6 +25,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 ORC_FORCE = 1
 ORC_PRUNE = 2
 ORC_LQSF = 16
+ORC_MAXMIN = 32
+ORC_PERFECT = 64
 UINT32_MAX = 0xFFFFFFFF
 INT64_MIN = -(1 << 63)
 

@@ -48,6 +48,12 @@
 #define ORC_FORCE 1u
 #define ORC_PRUNE 2u
 #define ORC_LQSF 16u /* priority = the raw gain (Least QoE Slack First; SPEC lqsf_policy) */
+/* Appendix A objectives, readings R22-R23: the item value (gain) of request i is
+ *   MAXMIN : max(Q_min - Q_wait,i, 0), Q_min = min over the live requests of their QoE now;
+ *   PERFECT: [1(Q_serve,i = 1) - 1(Q_wait,i = 1)] * 1(Q_now,i = 1);
+ * Q_now,i = the in-flight QoE at the decision time (O1-O2 with t = now - a_i, reading R3). */
+#define ORC_MAXMIN 32u
+#define ORC_PERFECT 64u
 
 #define ORC_FLAG_TRIGGERED 1u
 #define ORC_FLAG_CAP_HIT 2u
@@ -384,7 +390,7 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
     int64_t best_V = INT64_MIN;
     item_t *items = NULL, *best_items = NULL, *vict = NULL;
     uint32_t *sorted_l = NULL;
-    double *qw = NULL, *gain = NULL, *best_gain = NULL;
+    double *qw = NULL, *gain = NULL, *best_gain = NULL, *qnow = NULL, qmin = 1.0;
     uint8_t *in_S = NULL;
     scratch_t s = {NULL, NULL};
     int rc = ORC_OK;
@@ -474,6 +480,18 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
     }
     for (i = 0; i < n; i++)
         qw[i] = q_wait(r, i, p->now_us, p->horizon_us, &s);
+    if (p->flags & (ORC_MAXMIN | ORC_PERFECT)) {
+        qnow = (double *)malloc(sizeof(double) * (n ? n : 1));
+        if (!qnow) {
+            rc = ORC_E_NOMEM;
+            goto done;
+        }
+        for (i = 0; i < n; i++) {
+            qnow[i] = q_wait(r, i, p->now_us, 0, &s); /* Q at t = now - a_i (no new token) */
+            if (i == 0 || qnow[i] < qmin)
+                qmin = qnow[i];
+        }
+    }
 
     /* S3/S4 for every candidate B: gains, priorities, Algorithm 1. */
     for (B = B_lo; B <= B_hi; B++) {
@@ -481,7 +499,15 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
         uint32_t c = 0;
         int64_t V = 0;
         for (i = 0; i < n; i++) {
-            gain[i] = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s) - qw[i];
+            if (p->flags & ORC_MAXMIN) {
+                double v = qmin - qw[i];
+                gain[i] = v > 0.0 ? v : 0.0;
+            } else if (p->flags & ORC_PERFECT) {
+                double qs = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s);
+                gain[i] = ((qs == 1.0 ? 1.0 : 0.0) - (qw[i] == 1.0 ? 1.0 : 0.0)) * (qnow[i] == 1.0 ? 1.0 : 0.0);
+            } else {
+                gain[i] = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s) - qw[i];
+            }
             items[i].idx = i;
             items[i].rank = r->rank[i];
             items[i].key = (p->flags & ORC_LQSF) ? lqsf_key(gain[i]) : priority_key(gain[i], r->ctx_len[i]);
@@ -589,6 +615,7 @@ done:
     free(best_items);
     free(vict);
     free(qw);
+    free(qnow);
     free(gain);
     free(best_gain);
     free(in_S);

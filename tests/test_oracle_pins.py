@@ -463,3 +463,44 @@ def test_lqsf_priority_is_the_raw_gain(orc):
             else:
                 break
         assert int(lqsf.V[B - 1]) == V and int(lqsf.kstar[B - 1]) == c
+
+
+def test_maxmin_objective_on_g1(orc):
+    """Max-min objective (Appendix A; reading R22): gain = max(Q_min - Q_wait, 0),
+    Q_min = the smallest QoE now.  On G1 every request is perfect now (R0 on time; R1's only due
+    token is due exactly at t; R2 ahead; R3 has nothing due), so Q_min = 1 and the gains are
+    1 - Q_wait = 11/24, 1, 0, 1 for every B.  Priority gain / l orders R1 (1/100), R0
+    (11/24/300), R3 (1/800), R2; M = 1000 admits R1 and R0, R3 breaks the walk."""
+    snap, d = g1_snapshot()
+    o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                     flags=orc.ORC_FORCE | orc.ORC_MAXMIN)
+    two32 = 2 ** 32
+    v1 = two32
+    v2 = two32 + round(11 / 24 * two32)
+    assert [int(x) for x in o.V[:3]] == [v1, v2, v2]
+    assert [int(x) for x in o.kstar[:3]] == [1, 2, 2]
+    assert o.B_star == 3 and o.k_star == 2  # V ties between B = 2 and 3: the larger B (R13)
+
+
+def test_perfect_count_objective_on_g1(orc):
+    """Perfect-count objective (Appendix A; reading R23): gain =
+    [1(Q_serve = 1) - 1(Q_wait = 1)] * 1(Q_now = 1).  On G1 all are perfect now; only R3 is
+    perfect if served at B = 1 (Q_serve = 1, G1 table) and not when waiting, so its gain is 1 at
+    B = 1 and 0 at B >= 2 (Q_serve(2) = 0.9765625); R2 is perfect either way (gain 0)."""
+    snap, d = g1_snapshot()
+    o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                     flags=orc.ORC_FORCE | orc.ORC_PERFECT)
+    assert int(o.V[0]) == 2 ** 32 and int(o.V[1]) == 0 and int(o.V[2]) == 0
+    assert o.B_star == 1 and o.k_star == 1 and list(o.admit) == [3]
+
+
+def test_objectives_reduce_to_zero_when_all_perfect(orc):
+    """SPEC gain_maxmin / gain_perfect_count examples: every request perfect and staying perfect
+    (deliveries far ahead) -> every gain 0 under both objectives."""
+    snap = W.random_small(3, n=6)
+    snap.now_us = 1_000_000
+    snap.horizon_us = 1
+    snap.ttft_us[:] = 10_000_000  # nothing due yet: Q = 1 now, waiting and serving (R4)
+    for f in (orc.ORC_MAXMIN, orc.ORC_PERFECT):
+        o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity, flags=orc.ORC_FORCE | f)
+        assert all(int(v) in (0, -(1 << 63)) for v in o.V)
