@@ -96,6 +96,14 @@ typedef struct {
 #define ANDES_DEBUG_CHECKS 4u /* device-side data precondition checks                         */
 #define ANDES_LQSF 16u        /* priority = the raw gain (Least QoE Slack First; reading
                                  R21) instead of gain / l (Eq. 6); everything else unchanged  */
+/* Appendix-A objectives (readings R22-R23; single-GPU andes_schedule only): the
+ * item value of request i becomes
+ *   ANDES_OBJ_MAXMIN : max(Q_min - Q_wait,i, 0), Q_min = min over the requests of their QoE now
+ *   ANDES_OBJ_PERFECT: [1(Q_serve,i = 1) - 1(Q_wait,i = 1)] * 1(Q_now,i = 1)
+ * where Q_now,i is the in-flight QoE at now (R3).  The call then runs a second timeline scan
+ * (eval = now) before the decision.  At most one of the two. */
+#define ANDES_OBJ_MAXMIN 32u
+#define ANDES_OBJ_PERFECT 64u
 
 /* Decision-time parameters. */
 typedef struct {
@@ -106,7 +114,8 @@ typedef struct {
     uint64_t kv_capacity;    /* M: KV-cache capacity in tokens (Eq. 5)                          */
     uint32_t preempt_cap;    /* max preemptions per decision; UINT32_MAX = off (reading R18)    */
     uint32_t cur_latency_us; /* current iteration latency (trigger)                     */
-    uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS | ANDES_LQSF     */
+    uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS | ANDES_LQSF |
+                                ANDES_OBJ_MAXMIN | ANDES_OBJ_PERFECT                            */
 } AndesSchedParams;
 
 /* scalars[] layout of AndesDecision */

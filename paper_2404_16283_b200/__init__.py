@@ -32,6 +32,8 @@ ANDES_FORCE = 1
 ANDES_PRUNE = 2
 ANDES_DEBUG_CHECKS = 4
 ANDES_LQSF = 16
+ANDES_OBJ_MAXMIN = 32
+ANDES_OBJ_PERFECT = 64
 ANDES_F_TRIGGERED = 1
 ANDES_F_CAP_HIT = 2
 ANDES_F_CAP_OVERRIDDEN = 4

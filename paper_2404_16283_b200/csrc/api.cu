@@ -266,6 +266,9 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.stage_adm, (size_t)lim->max_B * kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.stage_sc, (size_t)lim->max_B)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.xm, tri_off(lim->max_B + 1))) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.m_now, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre_now, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.edge_now, N)) != cudaSuccess || (e = ctx_alloc(c, &w.srec_now, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.qnow, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
@@ -485,6 +488,9 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   const ReqView r = view_of(req);
   Work w = work_of(c, r.n);
   w.lqsf = (p->flags & ANDES_LQSF) ? 1u : 0u;
+  if ((p->flags & ANDES_OBJ_MAXMIN) && (p->flags & ANDES_OBJ_PERFECT))
+    return set_err(c, ANDES_E_INVAL, "at most one objective flag%s");
+  w.obj = (p->flags & ANDES_OBJ_MAXMIN) ? kObjMaxMin : (p->flags & ANDES_OBJ_PERFECT) ? kObjPerfect : kObjAndes;
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
@@ -492,6 +498,22 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   // bounds (S3a), [3] candidate keys (S3b), [4] Algorithm 1 per B + best B + cap + mask (S4-S6)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
+  if (w.obj != kObjAndes && r.n) {
+    // Appendix-A objectives need every request's QoE now: a first scan at eval = now into the
+    // *_now arrays, then Q_now (and its minimum); the tile counter is reset for the main scan
+    Work wn = w;
+    wn.m = w.m_now;
+    wn.spre = w.spre_now;
+    wn.edge = w.edge_now;
+    wn.srec = w.srec_now;
+    launch_prep(L, r, wn, p->now_us, false, false, 0, false);
+    const CUtensorMap* tmn = c->pool_map;
+    if ((rc = pool_map(c, r.tl_pool, r.tl_len, &tmn))) return rc;
+    launch_scan(L, r, wn, p->now_us, false, tmn);
+    launch_qnow(L, r, wn, p->now_us);
+    cudaError_t e = cudaMemsetAsync(&c->w.g->tile_ctr, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return cuda_check(c, e, "memset");
+  }
   launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
   mark(c, 1, s);
   {
@@ -551,6 +573,8 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
   const ReqView r = view_of(req);
   Work w = work_of(c, r.n);
   w.lqsf = (p->flags & ANDES_LQSF) ? 1u : 0u;
+  if (p->flags & (ANDES_OBJ_MAXMIN | ANDES_OBJ_PERFECT))
+    return set_err(c, ANDES_E_INVAL, "the Appendix-A objectives are single-GPU only%s");
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};

@@ -11,12 +11,17 @@ constexpr int kSortCap = kMaxB;
 constexpr int kVictCap = kMaxRunning;
 
 // ---------------------------------------------------------------- block helpers
-__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau, uint32_t lqsf) {
-  return ordered_key(prio_key(gain_at(unpack_state(p), tau), p.l, lqsf));
+__device__ __forceinline__ double gain_of(const PackedState& p, uint32_t tau, uint32_t obj) {
+  return gain_obj(unpack_state(p), p.qx, tau, obj);
 }
 
-__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau, uint32_t lqsf) {
-  return composite(okey_of(p, tau, lqsf), p.rank);
+__device__ __forceinline__ uint32_t okey_of(const PackedState& p, uint32_t tau, uint32_t lqsf, uint32_t obj) {
+  return ordered_key(prio_key(gain_of(p, tau, obj), p.l, lqsf));
+}
+
+__device__ __forceinline__ unsigned long long comp_of(const PackedState& p, uint32_t tau, uint32_t lqsf,
+                                                     uint32_t obj) {
+  return composite(okey_of(p, tau, lqsf, obj), p.rank);
 }
 
 template <int NT>

@@ -104,7 +104,9 @@ struct Globals {
   uint32_t n_run_global;         // running requests over all ranks
   uint32_t shard_Bstar;          // B* (step 3 -> step 4)
   uint32_t unal;                 // prep: some timeline does not start on a 16-byte boundary
-  uint32_t pad_[3];
+  uint32_t pad_;
+  unsigned long long qmin_bits;  // max-min objective: ~(fp64 bits of min_i Q_now,i) (Q >= 0: the bit
+                                 // patterns are ordered; inverted so that the zeroed word is "none")
 };
 
 // B-independent per-request state for the gain closed form,
@@ -113,8 +115,12 @@ struct alignas(16) PackedState {
   long long w0, c0, spre, cw, dto;
   double qw;
   uint32_t m, K, P, h0, l, rank;
-  uint32_t pad[2];
+  double qx;  // objective scalar: max-min -> its (B-independent) gain; perfect-count -> Q_now
 };
+static_assert(sizeof(PackedState) == 80, "PackedState layout");
+
+// objectives (include/andes.h ANDES_OBJ_*): 0 = Andes (Eq. 4), 1 = max-min, 2 = perfect count
+constexpr uint32_t kObjAndes = 0, kObjMaxMin = 1, kObjPerfect = 2;
 
 // ---------------------------------------------------------------- multi-GPU exchange blocks
 // Round 0: one rank's trigger / batch-size-range inputs.
@@ -171,6 +177,13 @@ struct Work {
   uint32_t tiles_cap;        // capacity of tile_owner / tile_status
   uint32_t S_cap;            // survivor capacity of cand_idx
   uint32_t lqsf;             // this call's priority: 0 gain / l (Eq. 6), 1 raw gain (ANDES_LQSF)
+  uint32_t obj;              // this call's objective (kObj*)
+  // objectives that need the QoE now (Appendix A): the decision-time scan's outputs
+  uint32_t* m_now;           // [N]
+  unsigned long long* spre_now;  // [N]
+  uint32_t* edge_now;        // [N]
+  ScanRec* srec_now;         // [N]
+  double* qnow;              // [N] QoE at the decision time
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -317,6 +330,26 @@ __device__ __forceinline__ double gain_at(const GainState& s, uint32_t tau) {
   int64_t sd, sw;
   serve_area(s, tau, sd, sw);
   return __dsub_rn(qoe_value(sd, sw), s.qw);
+}
+
+// Q_serve(tau) == 1 exactly (S_delay = 0; Eq. 3): for the perfect-count objective
+__device__ __forceinline__ bool serve_perfect(const GainState& s, uint32_t tau) {
+  if (s.K == 0) return s.qw == 1.0;
+  int64_t sd, sw;
+  serve_area(s, tau, sd, sw);
+  return qoe_value(sd, sw) == 1.0;
+}
+
+// the item value (knapsack gain) of the call's objective at tau(B) (Appendix A, P:L1160-1177;
+// readings R22-R23): Andes Q_serve - Q_wait (Eq. 4); max-min max(Q_min - Q_wait, 0) (stored in
+// qx); perfect count [1(Q_serve = 1) - 1(Q_wait = 1)] * 1(Q_now = 1) (Q_now stored in qx)
+__device__ __forceinline__ double gain_obj(const GainState& s, double qx, uint32_t tau, uint32_t obj) {
+  if (obj == kObjMaxMin) return qx;
+  if (obj == kObjPerfect) {
+    if (qx != 1.0) return 0.0;
+    return (serve_perfect(s, tau) ? 1.0 : 0.0) - (s.qw == 1.0 ? 1.0 : 0.0);
+  }
+  return gain_at(s, tau);
 }
 
 // priority key (Eq. 6, reading R9): float(gain / l), -0 -> +0; with the LQSF objective (reading

@@ -43,6 +43,7 @@ void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
 void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* off, uint32_t S,
                           double* mean_out, uint32_t* count_out);
+void launch_qnow(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now);
 int scan_blocks_per_sm();
 void init_scan_kernels();
 

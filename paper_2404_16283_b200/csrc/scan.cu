@@ -1117,6 +1117,49 @@ __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_
   (void)final_mode;
 }
 
+// ---------------------------------------------------------------- QoE now (Appendix-A objectives)
+// Q_now,i from the decision-time scan (eval = now; reading R3) into w.qnow, and min_i Q_now,i
+// (max-min objective, reading R22) into g->qmin_bits as the inverted fp64 bit pattern.
+__global__ void __launch_bounds__(256) k_qnow(ReqView r, Work w, int64_t now) {
+  __shared__ unsigned long long s_best;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) s_best = 0ull;
+  __syncthreads();
+  unsigned long long best = 0ull;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
+    const uint32_t g = r.n_deliv[i], m = w.m_now[i];
+    const int64_t P = r.period[i];
+    const int64_t spre = (int64_t)w.spre_now[i];
+    const int64_t cw = P * (((int64_t)m * ((int64_t)m - 1)) >> 1);
+    int64_t sd = 0, sw = 0;
+    if (m == 0) {
+      sd = sw = 0;
+    } else if (g >= m) {
+      sd = spre;
+      sw = (int64_t)m * (int64_t)w.edge_now[i] + cw;
+    } else {
+      const int64_t t = now - r.arrival[i];
+      const int64_t K = m - g;
+      const int64_t w0 = t - (int64_t)r.ttft[i] - ((int64_t)g - 1) * P;
+      sd = spre + sum_down(0, K, w0, P);
+      sw = (int64_t)m * (w0 - K * P) + cw;
+    }
+    const double q = qoe_value(sd, sw);
+    w.qnow[i] = q;
+    best = max(best, ~(unsigned long long)__double_as_longlong(q));
+  }
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(&s_best, best);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_best) atomicMax(&w.g->qmin_bits, s_best);
+}
+
+void launch_qnow(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now) {
+  if (r.n == 0) return;
+  launch_pdl(k_qnow, umin32((r.n + 255) / 256, L.sm_count * 8), 256, 0, L.stream, r, w, now);
+}
+
 // ---------------------------------------------------------------- config-5 sweep: scenario means
 // One CTA per scenario s: QoE of its requests [off[s], off[s+1]) in FINAL mode (m = g, Eq. 1-3,
 // reading R19) and their mean over the requests with g >= 1 ("averaged across all

@@ -63,10 +63,21 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
     PackedState p;
     p.w0 = s.w0; p.c0 = s.c0; p.spre = s.spre; p.cw = s.cw; p.dto = s.dto; p.qw = s.qw;
     p.m = s.m; p.K = s.K; p.P = s.P; p.h0 = s.h0; p.l = r.ctx_len[i]; p.rank = r.rank[i];
-    p.pad[0] = p.pad[1] = 0;
+    p.qx = 0.0;
+    if (w.obj == kObjMaxMin) {
+      const double qmin = __longlong_as_double((long long)~__ldcg(&w.g->qmin_bits));  // stored inverted
+      const double v = __dsub_rn(qmin, s.qw);
+      p.qx = v > 0.0 ? v : 0.0;
+    } else if (w.obj == kObjPerfect) {
+      p.qx = w.qnow[i];
+    }
     w.st[i] = p;
     uint32_t lb, ub;
-    if (s.K == 0) {
+    if (w.obj != kObjAndes) {
+      // max-min: one gain for every B; perfect count: 1(Q_serve = 1) is nonincreasing in tau
+      lb = ordered_key(prio_key(gain_obj(s, p.qx, thi, w.obj), p.l, w.lqsf));
+      ub = ordered_key(prio_key(gain_obj(s, p.qx, tlo, w.obj), p.l, w.lqsf));
+    } else if (s.K == 0) {
       lb = ub = ordered_key(0.0f);  // gain exactly 0 for every B
     } else {
       int64_t sd_lo, sw_lo, sd_hi, sw_hi;
@@ -296,7 +307,7 @@ __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
     for (uint32_t q = tid; q < n_run; q += kSelThreads) {
       const uint32_t i = w.run_list[q];
       wl += r.ctx_len[i];
-      const unsigned long long c = Bs ? comp_of(w.st[i], tB, w.lqsf) : 0ull;
+      const unsigned long long c = Bs ? comp_of(w.st[i], tB, w.lqsf, w.obj) : 0ull;
       if (ks == 0 || c < thr) {
         const uint32_t slot = atomicAdd(&s_nv, 1u);
         s_key[slot] = ~c;  // descending of ~ = ascending of the composite
@@ -443,7 +454,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
       const uint32_t i = __ldcg(w.run_list + q);
       const PackedState st = w.st[i];
       wl += st.l;
-      const unsigned long long c = comp_of(st, tB, w.lqsf);
+      const unsigned long long c = comp_of(st, tB, w.lqsf, w.obj);
       if (kstar == 0 || c < thr) {
         const uint32_t slot = atomicAdd(&s_nv, 1u);
         vkey[slot] = ~c;  // descending of ~c = ascending composite
@@ -644,7 +655,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     if (ovf) {
       // overflow fallback: exact keys of every request at B (row B of keyrow), radix select
       uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
-      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB, w.lqsf);
+      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB, w.lqsf, w.obj);
       __syncthreads();
       cnt = select_top_k(
           n, k,
@@ -663,7 +674,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       for (uint32_t e = tid; e < ns; e += kSelThreads) {
         const uint32_t i = __ldcg(w.cand_idx + e);
         const PackedState p = w.st[i];
-        const double gn = gain_at(unpack_state(p), tB);
+        const double gn = gain_of(p, tB, w.obj);
         s_all[e] = composite(ordered_key(prio_key(gn, p.l, w.lqsf)), p.rank);
         s_gall[e] = gain_fixed(gn);
         s_ri[e] = i;
@@ -701,7 +712,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
         if (q < cnt) {
           const uint32_t i = s_idx[q];
           x.comp = s_key[q];
-          x.gfix = ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
+          x.gfix = ovf ? gain_fixed(gain_of(w.st[i], tB, w.obj)) : s_gf[q];
           x.l = r.ctx_len[i];
           x.gidx = (base + i) | (r.running[i] ? 0x80000000u : 0u);
         } else {
@@ -743,7 +754,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     long long v = 0;
     for (uint32_t q = tid; q < kstar; q += kSelThreads) {
       const uint32_t i = s_idx[q];
-      v += ovf ? gain_fixed(gain_at(unpack_state(w.st[i]), tB)) : s_gf[q];
+      v += ovf ? gain_fixed(gain_of(w.st[i], tB, w.obj)) : s_gf[q];
       w.sel[(size_t)(B - 1) * kMaxB + q] = i;
     }
     v = block_sum_ll<kSelThreads>(v, s_red);

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kSelThreads) k_shard_merge(MergeArgs A) {
     for (uint32_t q = tid; q < n_run; q += kSelThreads) {
       const uint32_t i = __ldcg(w.run_list + q);
       const PackedState st = w.st[i];
-      const unsigned long long c = comp_of(st, tB, w.lqsf);
+      const unsigned long long c = comp_of(st, tB, w.lqsf, w.obj);
       if (ks == 0 || c < thr) {
         const uint32_t slot = atomicAdd(&s_nv, 1u);
         VictimX x;

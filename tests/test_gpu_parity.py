@@ -351,3 +351,22 @@ def test_schedule_lqsf_config2(A, ctx, orc):
     g, o = _check_sched(A, ctx, orc, snap, flags=1 | 16, cap=16)
     g2, o2 = _check_sched(A, ctx, orc, snap, flags=1, cap=16)
     assert not np.array_equal(g["V"], g2["V"])  # the priority changed the decision
+
+
+# ---------------------------------------------------------------- Appendix-A objectives (R22-R23)
+@pytest.mark.parametrize("seed", range(24))
+def test_schedule_objectives_random_small(A, ctx, orc, seed):
+    snap = W.random_small(seed + 200, B_cap=int(np.random.default_rng(seed).integers(1, 20)), align=[4, 1][seed % 2])
+    obj = [32, 64][seed % 2]
+    extra = [0, 16, 2][seed % 3]  # plain, with the LQSF priority, with pruning
+    _check_sched(A, ctx, orc, snap, flags=1 | obj | extra, cap=[W.UINT32_MAX, 1, 0][seed % 3])
+
+
+def test_schedule_objectives_g1_and_config2(A, ctx, orc):
+    from test_oracle_pins import g1_snapshot
+    snap, d = g1_snapshot()
+    for obj in (32, 64):
+        _check_sched(A, ctx, orc, snap, flags=1 | obj)
+    snap = W.config2()
+    for obj in (32, 64):
+        _check_sched(A, ctx, orc, snap, flags=1 | obj, cap=16)
