@@ -490,6 +490,31 @@ def run_ours(args):
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
     del qctx, breq
 
+    # ---- the same decision under the LQSF priority and the Appendix-A objectives (NEXT-2)
+    objectives = {}
+    with torch.cuda.stream(stream):
+        for name, fl in (("lqsf", A.ANDES_LQSF), ("maxmin", A.ANDES_OBJ_MAXMIN), ("perfect", A.ANDES_OBJ_PERFECT)):
+            kwo = dict(preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE | fl)
+            for _ in range(2):
+                ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream, **kwo)
+            go = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(go, stream=stream):
+                ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream, **kwo)
+            ms_o = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                go.replay()
+                b.record(stream)
+                b.synchronize()
+                ms_o.append(a.elapsed_time(b))
+            sco = out.scalars.cpu().numpy().view(np.uint32)
+            objectives[name] = {"ms_per_decision": statistics.median(ms_o), "B_star": int(sco[0]),
+                                "realized": int(sco[1])}
+            del go
+
     # ---- config 4: the 2^20-request population sharded over the ranks (multi-GPU decision)
     config4 = None if args.no_sharded else sharded_decision(args, dist, rank, ws, lr, stream, flush)
 
@@ -532,6 +557,7 @@ def run_ours(args):
                    "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}},
         "roofline": roof,
         "qoe_eval": qoe_eval,
+        "objectives": objectives,
         "config4_sharded": config4,
         "config5_sweep": sweep,
         "e2e": {"value": ws * e2e_steps / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
