@@ -27,6 +27,8 @@ ORC_PRUNE = 2
 ORC_LQSF = 16
 ORC_MAXMIN = 32
 ORC_PERFECT = 64
+ORC_REFINE = 128
+ORC_FLAG_REFINED = 16
 UINT32_MAX = 0xFFFFFFFF
 INT64_MIN = -(1 << 63)
 
@@ -56,6 +58,7 @@ class _Params(C.Structure):
         ("now_us", C.c_int64), ("horizon_us", C.c_uint32), ("tau_us", C.c_void_p),
         ("B_cap", C.c_uint32), ("kv_capacity", C.c_uint64), ("preempt_cap", C.c_uint32),
         ("cur_latency_us", C.c_uint32), ("flags", C.c_uint32),
+        ("prefill_tok_s", C.c_uint32), ("swap_tok_s", C.c_uint32),
     ]
 
 
@@ -174,13 +177,13 @@ class Decision:
 
 
 def schedule(req, now_us, horizon_us, tau_us, kv_capacity, preempt_cap=UINT32_MAX,
-             cur_latency_us=0, flags=ORC_FORCE, B_cap=None):
+             cur_latency_us=0, flags=ORC_FORCE, B_cap=None, prefill_tok_s=5000, swap_tok_s=0):
     s, keep = _req_struct(req)
     tau = np.ascontiguousarray(tau_us, dtype=np.uint32)
     B_cap = tau.size if B_cap is None else B_cap
     n = s.n
     p = _Params(int(now_us), int(horizon_us), _p(tau), int(B_cap), int(kv_capacity), int(preempt_cap),
-                int(cur_latency_us), int(flags))
+                int(cur_latency_us), int(flags), int(prefill_tok_s), int(swap_tok_s))
     mask = np.zeros(max(n, 1), np.uint8)
     adm = np.zeros(max(n, 1), np.uint32)
     pre = np.zeros(max(n, 1), np.uint32)

@@ -54,6 +54,9 @@
  * Q_now,i = the in-flight QoE at the decision time (O1-O2 with t = now - a_i, reading R3). */
 #define ORC_MAXMIN 32u
 #define ORC_PERFECT 64u
+/* Overhead-aware refiner (readings R24-R27), applied to the decision after S6. */
+#define ORC_REFINE 128u
+#define ORC_FLAG_REFINED 16u
 
 #define ORC_FLAG_TRIGGERED 1u
 #define ORC_FLAG_CAP_HIT 2u
@@ -82,7 +85,9 @@ typedef struct {
     uint64_t kv_capacity;    /* M */
     uint32_t preempt_cap;    /* UINT32_MAX = off */
     uint32_t cur_latency_us; /* current iteration latency (trigger) */
-    uint32_t flags;          /* ORC_FORCE | ORC_PRUNE */
+    uint32_t flags;          /* ORC_FORCE | ORC_PRUNE | ORC_LQSF | ORC_MAXMIN | ORC_PERFECT | ORC_REFINE */
+    uint32_t prefill_tok_s;  /* refiner: recomputation / prefill throughput, tokens per second */
+    uint32_t swap_tok_s;     /* refiner: swap bandwidth, tokens per second (0 = no swapping) */
 } orc_params;
 
 typedef struct {
@@ -380,6 +385,133 @@ static int cmp_u32(const void *pa, const void *pb)
     return a < b ? -1 : (a > b ? 1 : 0);
 }
 
+/* ------------------------------------------------------------------ refiner (NEXT-1) */
+/* R24 overhead model (SPEC preemption_overhead / select_mechanism), integer us:
+ *   recompute: preempt 0, resume l * 1e6 / prefill_tok_s (one prefill of the context);
+ *   swap     : preempt = resume = l * 1e6 / swap_tok_s;
+ * the mechanism with the smaller round trip, ties to swap.  A queued request's admission costs
+ * its prefill (recompute resume). */
+static void overhead_us(const orc_params *p, uint32_t l, int queued, int64_t *pre, int64_t *res)
+{
+    int64_t rc = p->prefill_tok_s ? (int64_t)l * 1000000 / p->prefill_tok_s : 0;
+    int64_t sw = p->swap_tok_s ? (int64_t)l * 1000000 / p->swap_tok_s : -1;
+    if (queued || sw < 0 || rc < 2 * sw) {
+        *pre = 0;
+        *res = rc;
+    } else {
+        *pre = sw;
+        *res = sw;
+    }
+}
+
+/* R25-R27: walk the admits (greedy order); each takes the minimal prefix of the remaining
+ * victims (victim order) that makes room in M; its stall D = the victims' preempt costs + its
+ * own resume cost; loss = sum over the requests still running after the pair of
+ * llrint((Q_now - Q(now + D)) 2^32), Q(now + D) = the in-flight QoE at now + D with no new
+ * token (Q_wait with Delta t = D); keep the pair iff llrint(gain 2^32) > loss; the first
+ * rejected pair cancels it and every later one.  Identity when the running set alone exceeds M. */
+static int refine(const orc_requests *r, const orc_params *p, const double *gain, orc_decision *out)
+{
+    scratch_t sc = {NULL, NULL}, *s = &sc;
+    int64_t Dmax = 0, c_pre, c_res;
+    uint32_t n = r->n, i, k, n_adm = out->scalars[2], n_pre = out->scalars[3];
+    uint32_t *adm = NULL, *pre = NULL, vp = 0, na = 0, nv = 0;
+    uint8_t *kept = NULL;
+    double *qnow = NULL;
+    uint64_t W = 0, M = p->kv_capacity;
+    int rc = ORC_OK;
+    for (i = 0; i < n; i++)
+        if (r->running[i])
+            W += r->ctx_len[i];
+    if (W > M)
+        return ORC_OK;
+    adm = (uint32_t *)malloc(sizeof(uint32_t) * (n_adm + 1));
+    pre = (uint32_t *)malloc(sizeof(uint32_t) * (n_pre + 1));
+    kept = (uint8_t *)calloc(n ? n : 1, 1);
+    qnow = (double *)malloc(sizeof(double) * (n ? n : 1));
+    if (!adm || !pre || !kept || !qnow) {
+        rc = ORC_E_NOMEM;
+        goto out;
+    }
+    memcpy(adm, out->admit_idx, sizeof(uint32_t) * n_adm);
+    memcpy(pre, out->preempt_idx, sizeof(uint32_t) * n_pre);
+    /* every pair's stall is at most the sum of all the costs: scratch for that horizon */
+    for (k = 0; k < n_adm; k++) {
+        overhead_us(p, r->ctx_len[adm[k]], r->n_deliv[adm[k]] == 0, &c_pre, &c_res);
+        Dmax += c_res;
+    }
+    for (k = 0; k < n_pre; k++) {
+        overhead_us(p, r->ctx_len[pre[k]], 0, &c_pre, &c_res);
+        Dmax += c_pre;
+    }
+    if (Dmax > 0xFFFFFFFFll || alloc_scratch(r, p->now_us, (uint32_t)Dmax, s) != ORC_OK) {
+        rc = Dmax > 0xFFFFFFFFll ? ORC_E_INVAL : ORC_E_NOMEM;
+        goto out;
+    }
+    for (i = 0; i < n; i++) {
+        kept[i] = r->running[i];
+        if (kept[i])
+            qnow[i] = q_wait(r, i, p->now_us, 0, s);
+    }
+    for (k = 0; k < n_adm; k++) {
+        uint32_t a = adm[k], v0 = vp, v;
+        uint64_t Wk = W;
+        int64_t D, c_pre, c_res, loss = 0;
+        while (Wk + r->ctx_len[a] > M && vp < n_pre)
+            Wk -= r->ctx_len[pre[vp++]];
+        if (Wk + r->ctx_len[a] > M) /* no room even with every remaining victim */
+            break;
+        overhead_us(p, r->ctx_len[a], r->n_deliv[a] == 0, &c_pre, &c_res);
+        D = c_res;
+        for (v = v0; v < vp; v++) {
+            overhead_us(p, r->ctx_len[pre[v]], 0, &c_pre, &c_res);
+            D += c_pre;
+            kept[pre[v]] = 0;
+        }
+        for (i = 0; i < n; i++)
+            if (kept[i])
+                loss += gain_fixed(qnow[i] - q_wait(r, i, p->now_us, (uint32_t)D, s));
+        if (gain_fixed(gain[a]) > loss) {
+            W = Wk + r->ctx_len[a];
+            na = k + 1;
+            nv = vp;
+        } else {
+            for (v = v0; v < vp; v++)
+                kept[pre[v]] = 1;
+            break;
+        }
+    }
+    /* outputs: accepted admits and victims; everything else stays as the status quo */
+    for (i = 0; i < n; i++)
+        out->serve_mask[i] = r->running[i] ? 1 : 0;
+    for (k = 0; k < nv; k++) {
+        out->serve_mask[pre[k]] = 0;
+        out->preempt_idx[k] = pre[k];
+    }
+    for (k = 0; k < na; k++) {
+        out->serve_mask[adm[k]] = 1;
+        out->admit_idx[k] = adm[k];
+    }
+    {
+        uint32_t realized = 0;
+        for (i = 0; i < n; i++)
+            realized += out->serve_mask[i];
+        out->scalars[1] = realized;
+    }
+    out->scalars[2] = na;
+    out->scalars[3] = nv;
+    out->scalars[6] |= ORC_FLAG_REFINED;
+out:
+    free(adm);
+    free(pre);
+    free(kept);
+    free(qnow);
+    free(sc.D);
+    free(sc.T);
+    return rc;
+}
+
+
 int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *out)
 {
     uint32_t n = r->n, i, B, k;
@@ -608,6 +740,8 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
         out->scalars[2] = n_adm;
         out->scalars[3] = n_pre;
     }
+    if ((p->flags & ORC_REFINE) && B_star)
+        rc = refine(r, p, best_gain, out);
 
 done:
     free(sorted_l);

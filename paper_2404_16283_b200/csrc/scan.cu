@@ -698,12 +698,16 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry
   }
   q = min(q, 31u);
   const bool active = u < U;
-  const int32_t q_ps = __shfl_sync(0xffffffffu, ps, q), q_pe = __shfl_sync(0xffffffffu, pe, q);
+  // the piece's parameters from its lane (ls and the edge kind share one word)
   const uint32_t q_off = __shfl_sync(0xffffffffu, incl - cnt, q);
   const uint32_t qA = __shfl_sync(0xffffffffu, e.A, q), qP = __shfl_sync(0xffffffffu, e.P, q);
-  const uint32_t qtrel = __shfl_sync(0xffffffffu, e.trel, q), qek = __shfl_sync(0xffffffffu, e.ek, q);
+  const uint32_t qtrel = __shfl_sync(0xffffffffu, e.trel, q);
   const uint32_t qridx = __shfl_sync(0xffffffffu, e.ridx, q);
-  const int32_t qvend = __shfl_sync(0xffffffffu, e.vend, q), qls = __shfl_sync(0xffffffffu, e.ls, q);
+  const int32_t qvend = __shfl_sync(0xffffffffu, e.vend, q);
+  const uint32_t lsek = __shfl_sync(0xffffffffu, ((uint32_t)(e.ls + 1) << 2) | e.ek, q);
+  const int32_t qls = (int32_t)(lsek >> 2) - 1;
+  const uint32_t qek = lsek & 3u;
+  const int32_t q_ps = max(qls, 0), q_pe = max(q_ps, min(qvend, (int32_t)kWTile));
   const uint32_t k = u - q_off;
   const int32_t xs = active ? q_ps + (int32_t)(SR * k) : 0;
   const int32_t xe = active ? min(xs + (int32_t)SR, q_pe) : 0;
@@ -941,10 +945,6 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     const unsigned long long p0 = (unsigned long long)tcur * kWTile;
     const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
     const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
-    const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
-    const uint32_t httft = __shfl_sync(0xffffffffu, tm.httft, 0);
-    const uint32_t hP = __shfl_sync(0xffffffffu, tm.hP, 0);
-    const unsigned long long hbase = __shfl_sync(0xffffffffu, tm.hbase, 0);
     const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
     // ---- prefetch of the next tile
     const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
@@ -997,6 +997,10 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     // direct head carry
     uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
     if (chunk_start && mode == 1u) {
+      const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
+      const uint32_t httft = __shfl_sync(0xffffffffu, tm.httft, 0);
+      const uint32_t hP = __shfl_sync(0xffffffffu, tm.hP, 0);
+      const unsigned long long hbase = __shfl_sync(0xffffffffu, tm.hbase, 0);
       for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
         uint32_t d[8];
 #pragma unroll

@@ -504,3 +504,38 @@ def test_objectives_reduce_to_zero_when_all_perfect(orc):
     for f in (orc.ORC_MAXMIN, orc.ORC_PERFECT):
         o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity, flags=orc.ORC_FORCE | f)
         assert all(int(v) in (0, -(1 << 63)) for v in o.V)
+
+
+def test_refiner_on_g1(orc):
+    """Overhead-aware refiner (readings R24-R27) on G1 (B* = 2, admits [R1, R3],
+    victims [R2, R0], running R0 and R2).  Pair 1 = R1 alone (800 + 100 <= M): its stall is R1's
+    prefill, 100 tokens / rate.  At rate 20 tok/s the stall is 5 s: R0 (on time so far) then has
+    31 tokens due at t' = 7 s, 26 undelivered, S_delay = sum_{k=5..30} (6 - 0.2k) = 65 s,
+    S_whole = 0.2 * 465 = 93 s, so its QoE drops 1 -> 28/93 (R2 stays perfect: 40 tokens far
+    ahead); the loss 65/93 exceeds R1's gain 7/11, the pair is rejected and with it the rest:
+    the status quo.  At 40 tok/s (2.5 s) R0 drops by 16.9/30.6 < 7/11: R1 is kept; R3's pair
+    preempts R2 and R0 and leaves nobody running (loss 0): the decision is unchanged."""
+    snap, d = g1_snapshot()
+    base = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity)
+    assert list(base.admit) == [1, 3] and list(base.preempt) == [2, 0]
+    two32 = 2 ** 32
+    assert round(65 / 93 * two32) > round(7 / 11 * two32) > round(16.9 / 30.6 * two32)
+    slow = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                        flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=20)
+    assert slow.flags & orc.ORC_FLAG_REFINED
+    assert list(slow.admit) == [] and list(slow.preempt) == []
+    assert slow.serve_mask.tolist() == [1, 0, 1, 0] and slow.realized == 2
+    fast = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                        flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=40)
+    assert list(fast.admit) == [1, 3] and list(fast.preempt) == [2, 0]
+    assert fast.serve_mask.tolist() == base.serve_mask.tolist()
+
+
+def test_refiner_zero_overhead_is_identity(orc):
+    """SPEC refine: a zero-overhead profile (no prefill or swap cost) makes every stall 0, so
+    the loss is 0 and every positive-gain admission is kept (G1's admits both gain > 0)."""
+    snap, d = g1_snapshot()
+    base = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity)
+    z = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                     flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=0)
+    assert list(z.admit) == list(base.admit) and list(z.preempt) == list(base.preempt)
