@@ -104,6 +104,14 @@ typedef struct {
  * (eval = now) before the decision.  At most one of the two. */
 #define ANDES_OBJ_MAXMIN 32u
 #define ANDES_OBJ_PERFECT 64u
+/* Overhead-aware refiner (readings R24-R27), applied after the preemption cap: the
+ * admits (greedy order) are paired with the minimal prefix of the remaining victims that makes
+ * room in M; a pair's stall is its victims' preemption costs plus the admit's resumption cost
+ * (recompute = prefill of l at prefill_tok_s, swap = l / swap_tok_s each way, the faster round
+ * trip); the pair is kept iff the admit's gain exceeds the QoE the still-running requests lose
+ * under that stall (in 2^-32 units); the first rejected pair cancels itself and the rest
+ * (ANDES_F_REFINED in the flags).  The identity when the running set alone exceeds M. */
+#define ANDES_REFINE 128u
 
 /* Decision-time parameters. */
 typedef struct {
@@ -115,7 +123,9 @@ typedef struct {
     uint32_t preempt_cap;    /* max preemptions per decision; UINT32_MAX = off (reading R18)    */
     uint32_t cur_latency_us; /* current iteration latency (trigger)                     */
     uint32_t flags;          /* ANDES_FORCE | ANDES_PRUNE | ANDES_DEBUG_CHECKS | ANDES_LQSF |
-                                ANDES_OBJ_MAXMIN | ANDES_OBJ_PERFECT                            */
+                                ANDES_OBJ_MAXMIN | ANDES_OBJ_PERFECT | ANDES_REFINE            */
+    uint32_t prefill_tok_s;  /* refiner: prefill / recomputation throughput (tokens/s; 0 = free) */
+    uint32_t swap_tok_s;     /* refiner: swap bandwidth (tokens/s; 0 = no swapping)             */
 } AndesSchedParams;
 
 /* scalars[] layout of AndesDecision */
@@ -132,6 +142,7 @@ typedef struct {
 #define ANDES_F_CAP_HIT 2u
 #define ANDES_F_CAP_OVERRIDDEN 4u
 #define ANDES_F_SLOW_PATH 8u /* informational: a capacity fallback path ran */
+#define ANDES_F_REFINED 32u  /* the overhead-aware refiner rewrote the decision (ANDES_REFINE)   */
 
 /* Decision outputs (DEVICE memory owned by the caller). */
 typedef struct {

@@ -28,7 +28,7 @@ ORC_LQSF = 16
 ORC_MAXMIN = 32
 ORC_PERFECT = 64
 ORC_REFINE = 128
-ORC_FLAG_REFINED = 16
+ORC_FLAG_REFINED = 32
 UINT32_MAX = 0xFFFFFFFF
 INT64_MIN = -(1 << 63)
 

@@ -56,7 +56,7 @@
 #define ORC_PERFECT 64u
 /* Overhead-aware refiner (readings R24-R27), applied to the decision after S6. */
 #define ORC_REFINE 128u
-#define ORC_FLAG_REFINED 16u
+#define ORC_FLAG_REFINED 32u
 
 #define ORC_FLAG_TRIGGERED 1u
 #define ORC_FLAG_CAP_HIT 2u

@@ -34,6 +34,8 @@ ANDES_DEBUG_CHECKS = 4
 ANDES_LQSF = 16
 ANDES_OBJ_MAXMIN = 32
 ANDES_OBJ_PERFECT = 64
+ANDES_REFINE = 128
+ANDES_F_REFINED = 32
 ANDES_F_TRIGGERED = 1
 ANDES_F_CAP_HIT = 2
 ANDES_F_CAP_OVERRIDDEN = 4
@@ -71,7 +73,8 @@ class Requests(C.Structure):
 class SchedParams(C.Structure):
     _fields_ = [("now_us", C.c_int64), ("horizon_us", C.c_uint32), ("B_cap", C.c_uint32),
                 ("tau_us", C.c_void_p), ("kv_capacity", C.c_uint64), ("preempt_cap", C.c_uint32),
-                ("cur_latency_us", C.c_uint32), ("flags", C.c_uint32)]
+                ("cur_latency_us", C.c_uint32), ("flags", C.c_uint32), ("prefill_tok_s", C.c_uint32),
+                ("swap_tok_s", C.c_uint32)]
 
 
 class DecisionPtrs(C.Structure):
@@ -284,11 +287,11 @@ class Context:
 
     def schedule(self, req: dict, n: int, now_us: int, horizon_us: int, tau, kv_capacity: int,
                  preempt_cap=UINT32_MAX, cur_latency_us=0, flags=ANDES_FORCE, out: Decision | None = None,
-                 stream=None) -> Decision:
+                 stream=None, prefill_tok_s=5000, swap_tok_s=0) -> Decision:
         B_cap = int(tau.numel())
         out = out or self.alloc_decision(n, B_cap)
         p = SchedParams(int(now_us), int(horizon_us), B_cap, _ptr(tau), int(kv_capacity), int(preempt_cap),
-                        int(cur_latency_us), int(flags))
+                        int(cur_latency_us), int(flags), int(prefill_tok_s), int(swap_tok_s))
         d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
                          _ptr(out.V), _ptr(out.kstar))
         self._check(lib().andes_schedule(self._h, C.byref(_req_struct(req, n)), C.byref(p), C.byref(d),
@@ -302,7 +305,7 @@ class Context:
         B_cap = int(tau_host.numel())
         out = out or self.alloc_decision(n, B_cap, pin=True)
         p = SchedParams(int(now_us), int(horizon_us), B_cap, _ptr(tau_host), int(kv_capacity), int(preempt_cap),
-                        int(cur_latency_us), int(flags))
+                        int(cur_latency_us), int(flags), 5000, 0)
         d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
                          _ptr(out.V), _ptr(out.kstar))
         rc = self._check(lib().andes_schedule_host(self._h, C.byref(_req_struct(req_host, n)), C.byref(p),
@@ -328,7 +331,7 @@ class Context:
                        kv_capacity: int, out: Decision, recv=None, send=None, preempt_cap=UINT32_MAX,
                        cur_latency_us=0, flags=ANDES_FORCE, stream=None):
         p = SchedParams(int(now_us), int(horizon_us), int(tau.numel()), _ptr(tau), int(kv_capacity),
-                        int(preempt_cap), int(cur_latency_us), int(flags))
+                        int(preempt_cap), int(cur_latency_us), int(flags), 5000, 0)
         d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
                          _ptr(out.V), _ptr(out.kstar))
         self._check(lib().andes_schedule_shard(self._h, C.byref(sh), int(step), C.byref(_req_struct(req, n)),

@@ -268,13 +268,16 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.xm, tri_off(lim->max_B + 1))) != cudaSuccess ||
       (e = ctx_alloc(c, &w.m_now, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre_now, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.edge_now, N)) != cudaSuccess || (e = ctx_alloc(c, &w.srec_now, N)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.qnow, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.qnow, N)) != cudaSuccess || (e = ctx_alloc(c, &w.vmark, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.rf_vend, kMaxB)) != cudaSuccess || (e = ctx_alloc(c, &w.rf_D, kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.rf_loss, kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
     return rc;
   }
   cudaMemset(w.hist_l, 0, sizeof(uint32_t) * kHistL);
+  cudaMemset(w.vmark, 0, sizeof(uint32_t) * N);
   cudaMemset(c->zero_rows, 0, 128);
   cudaMemset(w.hist_lb, 0, sizeof(uint32_t) * kHistK);
   cudaMemset(w.hist_ub, 0, sizeof(uint32_t) * kHistK);
@@ -527,6 +530,8 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   launch_compact(L, r, w, nullptr, 1u);
   mark(c, 4, s);
   launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
+  if (p->flags & ANDES_REFINE)
+    launch_refine(L, r, w, o, p->now_us, p->tau_us, p->kv_capacity, p->prefill_tok_s, p->swap_tok_s);
   mark(c, 5, s);
   mark(c, 6, s);
   if (c->prof) c->prof_recorded = true;

@@ -107,6 +107,8 @@ struct Globals {
   uint32_t pad_;
   unsigned long long qmin_bits;  // max-min objective: ~(fp64 bits of min_i Q_now,i) (Q >= 0: the bit
                                  // patterns are ordered; inverted so that the zeroed word is "none")
+  uint32_t rf_npairs;            // refiner: feasible admit/victim pairs
+  uint32_t pad2_;
 };
 
 // B-independent per-request state for the gain closed form,
@@ -184,6 +186,11 @@ struct Work {
   uint32_t* edge_now;        // [N]
   ScanRec* srec_now;         // [N]
   double* qnow;              // [N] QoE at the decision time
+  // overhead-aware refiner (refine.cu)
+  uint32_t* vmark;           // [N] 1 + victim position of a preempted request, else 0
+  uint32_t* rf_vend;         // [kMaxB] victims consumed after pair k
+  long long* rf_D;           // [kMaxB] stall of pair k (us)
+  long long* rf_loss;        // [kMaxB] QoE loss of pair k in units of 2^-32
 };
 
 // ---------------------------------------------------------------- small helpers

@@ -133,10 +133,11 @@ def test_gains_config3_sampled(A, ctx, orc):
 
 
 # ---------------------------------------------------------------- S0-S6 decisions
-def _run_sched(A, ctx, snap, flags=1, cap=None, cur_latency=0):
+def _run_sched(A, ctx, snap, flags=1, cap=None, cur_latency=0, prefill=5000, swap=0):
     cap = snap.preempt_cap if cap is None else cap
     d = ctx.schedule(_dev(A, snap), snap.n, snap.now_us, snap.horizon_us, _tau(snap), snap.kv_capacity,
-                     preempt_cap=cap, cur_latency_us=cur_latency, flags=flags)
+                     preempt_cap=cap, cur_latency_us=cur_latency, flags=flags, prefill_tok_s=prefill,
+                     swap_tok_s=swap)
     torch.cuda.synchronize()
     sc = d.scalars.cpu().numpy().view(np.uint32)
     return dict(mask=d.serve_mask.cpu().numpy()[:snap.n], admit=d.admit.cpu().numpy().view(np.uint32)[:sc[2]],
@@ -144,18 +145,18 @@ def _run_sched(A, ctx, snap, flags=1, cap=None, cur_latency=0):
                 kstar=d.kstar.cpu().numpy().view(np.uint32))
 
 
-def _check_sched(A, ctx, orc, snap, flags=1, cap=None, cur_latency=0):
+def _check_sched(A, ctx, orc, snap, flags=1, cap=None, cur_latency=0, prefill=5000, swap=0):
     cap = snap.preempt_cap if cap is None else cap
-    g = _run_sched(A, ctx, snap, flags, cap, cur_latency)
+    g = _run_sched(A, ctx, snap, flags, cap, cur_latency, prefill, swap)
     o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity, preempt_cap=cap,
-                     cur_latency_us=cur_latency, flags=flags)
+                     cur_latency_us=cur_latency, flags=flags, prefill_tok_s=prefill, swap_tok_s=swap)
     trig = bool(g["sc"][6] & 1)
     assert trig == (o.status == 0)
     np.testing.assert_array_equal(g["mask"], o.serve_mask)
     if trig:
         assert [int(x) for x in g["sc"][[0, 1, 2, 3, 4, 5, 7]]] == [o.B_star, o.realized, o.admit.size,
                                                                     o.preempt.size, o.B_lo, o.B_hi, o.k_star]
-        assert int(g["sc"][6]) & 7 == o.flags & 7
+        assert int(g["sc"][6]) & 39 == o.flags & 39  # triggered, cap hit, cap overridden, refined
         np.testing.assert_array_equal(g["admit"], o.admit)
         np.testing.assert_array_equal(g["preempt"], o.preempt)
         np.testing.assert_array_equal(g["V"], o.V)
@@ -370,3 +371,30 @@ def test_schedule_objectives_g1_and_config2(A, ctx, orc):
     snap = W.config2()
     for obj in (32, 64):
         _check_sched(A, ctx, orc, snap, flags=1 | obj, cap=16)
+
+
+# ---------------------------------------------------------------- overhead-aware refiner (NEXT-1)
+def test_refiner_g1_on_gpu(A, ctx, orc):
+    from test_oracle_pins import g1_snapshot
+    snap, d = g1_snapshot()
+    for prefill in (20, 40, 0):
+        g, o = _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=prefill)
+    g, o = _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=20)
+    assert g["admit"].tolist() == [] and g["preempt"].tolist() == [] and g["sc"][6] & 32
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_refiner_random_small(A, ctx, orc, seed):
+    rng = np.random.default_rng(seed + 7)
+    snap = W.random_small(seed + 300, B_cap=int(rng.integers(1, 20)), align=[4, 1][seed % 2])
+    prefill = int([0, 30, 200, 5000, 100000][seed % 5])
+    swap = int([0, 0, 400, 0, 50][seed % 5])
+    extra = [0, 16, 32][seed % 3]
+    _check_sched(A, ctx, orc, snap, flags=1 | 128 | extra, cap=[W.UINT32_MAX, 2][seed % 2], prefill=prefill,
+                 swap=swap)
+
+
+def test_refiner_config2(A, ctx, orc):
+    snap = W.config2()
+    for prefill, swap in ((5000, 0), (500, 20000), (50_000, 0)):
+        _check_sched(A, ctx, orc, snap, flags=1 | 128, cap=16, prefill=prefill, swap=swap)
