@@ -490,10 +490,12 @@ def run_ours(args):
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
     del qctx, breq
 
-    # ---- the same decision under the LQSF priority and the Appendix-A objectives (NEXT-2)
+    # ---- the same decision under the LQSF priority, the Appendix-A objectives (NEXT-2) and with
+    # the overhead-aware refiner (NEXT-1; prefill 5000 tok/s, no swapping)
     objectives = {}
     with torch.cuda.stream(stream):
-        for name, fl in (("lqsf", A.ANDES_LQSF), ("maxmin", A.ANDES_OBJ_MAXMIN), ("perfect", A.ANDES_OBJ_PERFECT)):
+        for name, fl in (("lqsf", A.ANDES_LQSF), ("maxmin", A.ANDES_OBJ_MAXMIN), ("perfect", A.ANDES_OBJ_PERFECT),
+                         ("refine", A.ANDES_REFINE)):
             kwo = dict(preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE | fl)
             for _ in range(2):
                 ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream, **kwo)
@@ -512,7 +514,7 @@ def run_ours(args):
                 ms_o.append(a.elapsed_time(b))
             sco = out.scalars.cpu().numpy().view(np.uint32)
             objectives[name] = {"ms_per_decision": statistics.median(ms_o), "B_star": int(sco[0]),
-                                "realized": int(sco[1])}
+                                "realized": int(sco[1]), "n_admit": int(sco[2]), "n_preempt": int(sco[3])}
             del go
 
     # ---- config 4: the 2^20-request population sharded over the ranks (multi-GPU decision)
