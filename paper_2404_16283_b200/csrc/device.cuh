@@ -21,8 +21,8 @@ constexpr int kTile = kWTile;                     // tiling unit of tile_meta / 
 constexpr int kWWinCap = 32;                      // window entries (+ sentinel) per warp
 constexpr int kOvfCap = 128;                      // the CTA's shared overflow window (dense tiles)
 constexpr int kCarryDirect = 4096;                // head segments up to this long: carry read directly
-constexpr int kWarpSmem = 2 * kWTile * 4 + kWWinCap * 32;  // 2 tiles + records (1 KiB multiple)
-constexpr int kScanDynSmem = (kScanThreads / 32) * kWarpSmem + kOvfCap * 32 + 1024;  // + align slack
+constexpr int kWarpSmem = 2 * kWTile * 4;               // double-buffered warp-tile
+constexpr int kScanDynSmem = (kScanThreads / 32) * kWarpSmem + 1024;  // + 1 KiB alignment slack (swizzle)
 constexpr int kSelectThreads = 1024;
 constexpr int kMaxB = 1024;
 constexpr int kMaxRunning = 4096;

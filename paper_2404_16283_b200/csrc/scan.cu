@@ -409,23 +409,6 @@ struct RawWin {
 // time I(x) = e.A + x P; the actual consumption time follows A_x = max(d_x, A_{x-1} + P)
 // (reading R2) and is clamped at t (R3).  Pass 1 builds the segmented max of lat+ (the carry
 // monoid), pass 2 sums T~ per piece and subtracts the closed-form sum of I.
-// Window of precomputed tile-local entries in the warp's shared memory: entries 0..wn-1
-// (entry 0 the dummy when a gap precedes r0) and a sentinel at wn (start kWTile + 1).
-struct EntWin {
-  uint32_t base;  // shared address of entry 0
-  __device__ __forceinline__ int32_t start(uint32_t q) const {
-    int32_t v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(base + q * 32u));
-    return v;
-  }
-  __device__ __forceinline__ Entry get(uint32_t q) const {
-    const uint4 a = ld_shared_v4(base + q * 32u), b = ld_shared_v4(base + q * 32u + 16u);
-    Entry e;
-    e.ls = (int32_t)a.x; e.vend = (int32_t)a.y; e.A = a.z; e.trel = a.w;
-    e.P = b.x; e.ek = b.y; e.ridx = b.z; e.pad = b.w;
-    return e;
-  }
-};
 
 template <bool kFinal, class Win>
 __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const Win& win, uint32_t tile_s, uint32_t wn,
@@ -643,16 +626,16 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
 // Returns false (nothing done) when the tile has too many pieces for one round.
 // e: this lane's request of the tile (lane q = request r0 + q, q < wn <= 24, zero-length ones
 // included), in tile-local coordinates.
+// A dense tile is processed in batches of up to 31 requests (first_batch / last_batch): the
+// running prefix seeds the next batch (mode 1); only a single-batch tile publishes its aggregate
+// early or looks back (mode 2), and only the last batch publishes the tile's prefix.
 template <bool kFinal>
-__device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t wn,
-                                                  uint32_t t, uint32_t mode, uint32_t cdirect,
-                                                  unsigned long long& prefix) {
+__device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
+                                                  uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
+                                                  bool first_batch, bool last_batch) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
-  (void)wn;
   const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
-  const bool starts_in = e.ls >= 0 && e.ls < (int32_t)kWTile;
-  if (__any_sync(0xffffffffu, starts_in && (e.ls & 3))) return false;  // not 16-byte aligned
   const uint32_t len = (uint32_t)(pe - ps);
   const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
   // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32)
@@ -761,7 +744,7 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry
   const unsigned long long tile_agg = __shfl_sync(0xffffffffu, sc, 31);
   // ---- the tile's carry-in (direct read or decoupled look-back), as in warp_tile; the aggregate
   // is published first so that successors looking back never wait on this tile's second pass
-  if (lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
+  if (first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
   unsigned long long acc = 0ull;
   if (mode == 2u) {
     for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
@@ -788,7 +771,7 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry
     acc = kFlagBit | cdirect;
   }
   prefix = seg_combine(acc, tile_agg);
-  if (lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
+  if (last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
@@ -822,7 +805,6 @@ __device__ __forceinline__ bool warp_tile_aligned(const ScanArgs& A, const Entry
       w.edge[qridx] = (qek == 1u) ? A_last - Il : min(A_last, tcl) - Il;
     }
   }
-  return true;
 }
 
 template <bool kFinal>
@@ -842,23 +824,20 @@ __device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, u
 // before the tile (else decoupled look-back on per-warp-tile status words), and scans with
 // warp shuffles only: no CTA-wide barriers on the hot path.
 template <bool kFinal>
-__global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant__ ScanArgs A,
+__global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap_swz,
                                                            const __grid_constant__ CUtensorMap tmap_plain) {
   extern __shared__ unsigned char s_dyn_raw[];
   unsigned char* s_base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn_raw) + 1023) & ~uintptr_t(1023));
   __shared__ alignas(8) uint64_t s_bar[kScanThreads / 32][2];
-  __shared__ uint32_t s_ovf_owner;  // 0 free, else 1 + the warp using the CTA's overflow window
 
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t n = r.n;
-  if (tid == 0) s_ovf_owner = 0u;
   pdl_wait();
   pdl_trigger();
-  __syncthreads();
   if (blockIdx.x < 1000) ANDES_TRACE(w, 5000 + 2 * blockIdx.x);
   if (A.sched && blockIdx.x == 0) {
     bounds_block(r, w, A.tau, A.B_cap, A.M, A.cur_latency, A.flags);
@@ -873,9 +852,7 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
   // 128B-swizzled tiles and the row-per-lane event path
   const uint32_t swz_on = __ldcg(&w.g->unal) ? 1u : 0u;
   const CUtensorMap* pmap = swz_on ? &tmap_swz : &tmap_plain;
-  unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles + records
-  Entry* const went_own = reinterpret_cast<Entry*>(wbase + 2 * kWTile * 4);
-  Entry* const went_ovf = reinterpret_cast<Entry*>(s_base + (kScanThreads / 32) * kWarpSmem);
+  unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles
   uint64_t* bar = s_bar[wid];
 
   // Chunks of CH consecutive warp-tiles are claimed in increasing order (lane 0 runs the tile
@@ -960,40 +937,8 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     const uint32_t mode = chunk_start ? (flags >> 1) & 3u : 1u;
     const uint32_t wn = re - r0 + 1 + dummy;
     const uint32_t nrec = wn - dummy;
-    const bool fast = !swz_on && nrec <= 24u;
-    // old path: tile-local entries of the window in shared memory, without requests that have no
-    // valid token here (lim == 0); the owner r0 is always kept (a dense tile borrows the CTA's
-    // larger overflow window when it is free)
-    Entry* went = went_own;
-    uint32_t cap = kWWinCap, wc = dummy;
-    bool ovf = false;
-    if (!fast) {
-      if (wn >= (uint32_t)kWWinCap) {
-        uint32_t got = 0;
-        if (lane == 0) got = atomicCAS(&s_ovf_owner, 0u, wid + 1u) == 0u;
-        ovf = __shfl_sync(0xffffffffu, got, 0) != 0u;
-        if (ovf) {
-          went = went_ovf;
-          cap = kOvfCap;
-        }
-      }
-      if (dummy && lane == 0) went[0] = null_entry(false);
-      for (uint32_t c0 = 0; c0 < nrec && wc < cap; c0 += 32) {
-        const uint32_t k = c0 + lane;
-        ScanRec sr = rec;
-        bool keep = false;
-        if (k < nrec) {
-          if (c0) sr = w.srec[r0 + k];
-          keep = k == 0 || sr.lim != 0u;
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        const uint32_t pos = wc + __popc(bal & ((1u << lane) - 1u));
-        if (keep && pos < cap) went[pos] = entry_of(sr, r0 + k, p0);
-        wc += __popc(bal);
-      }
-      if (wc < cap && lane == 0) went[wc] = null_entry(true);
-    }
-    const bool win_ok = wc < cap;  // entries + sentinel fit the window
+    const uint32_t nbatch = (nrec + 30u) / 31u;
+    const bool fast = !swz_on && (nbatch == 1u || mode != 2u);
     // direct head carry
     uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
     if (chunk_start && mode == 1u) {
@@ -1032,34 +977,27 @@ __global__ void __launch_bounds__(kScanThreads) k_qoe_scan(const __grid_constant
     }
     __syncwarp();
     const unsigned long long t_body = (w.trace && tcur < 16384) ? gtimer() : 0ull;
-    bool done = false;
     if (fast) {
-      const Entry e = lane < nrec ? entry_of(rec, r0 + lane, p0) : null_entry(true);
-      done = warp_tile_aligned<kFinal>(A, e, smem_u32(tile), nrec, tcur, mode, cm, acc_reg);
-    }
-    if (!done) {
-      if (fast) {  // fall back: stage the window now
-        if (dummy && lane == 0) went[0] = null_entry(false);
-        wc = dummy;
-        {
-          const bool keep = lane < nrec && (lane == 0 || rec.lim != 0u);
-          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) went[wc + __popc(bal & ((1u << lane) - 1u))] = entry_of(rec, r0 + lane, p0);
-          wc += __popc(bal);
-        }
-        if (lane == 0) went[wc] = null_entry(true);
-        __syncwarp();
+      // piece-parallel path, batches of 31 requests (lane q of batch b = request r0 + 31 b + q)
+      unsigned long long pref = 0ull;
+      uint32_t mb = mode, cb = cm;
+      for (uint32_t b = 0; b < nbatch; ++b) {
+        const uint32_t nb_req = min(31u, nrec - 31u * b);
+        ScanRec rb = rec;
+        if (b && lane < nb_req) rb = w.srec[r0 + 31u * b + lane];
+        const Entry e = lane < nb_req ? entry_of(rb, r0 + 31u * b + lane, p0) : null_entry(true);
+        warp_tile_aligned<kFinal>(A, e, smem_u32(tile), tcur, mb, cb, pref, b == 0, b + 1 == nbatch);
+        mb = 1u;
+        cb = (uint32_t)pref;
       }
-      if (fast || win_ok) {
-        EntWin win{smem_u32(went)};
-        acc_reg = warp_tile<kFinal>(A, win, smem_u32(tile), wc, tcur, mode, cm, swz_on);
-      } else {
-        acc_reg = warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
-      }
+      acc_reg = pref;
+    } else {
+      // row-per-lane event path (unaligned pools, or a dense tile that must look back); the
+      // window's records are read from global memory
+      acc_reg = warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
     }
     // refill this buffer with the tile two ahead in the warp's sequence
     __syncwarp();
-    if (ovf && lane == 0) atomicExch(&s_ovf_owner, 0u);
     if (t_body && lane == 0) {
       w.trace[16384 + 2 * tcur] = t_body;
       w.trace[16384 + 2 * tcur + 1] = gtimer();
