@@ -640,30 +640,12 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
   // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32)
   // (an odd number of 16-byte chunks: sub-ranges of one piece hit distinct shared-memory banks)
-  // ceil(len / (4 s4)) for len <= kWTile, s4 <= 256: fp32 estimate + one exact fix-up
-  auto nsub = [&](uint32_t s4) -> uint32_t {
-    const uint32_t sr = 4u * s4;
-    uint32_t c = (uint32_t)__fmul_rn((float)(len + sr - 1), __frcp_rn((float)sr));
-    if (c * sr < len) ++c;
-    else if (c && (c - 1) * sr >= len) --c;
-    return c;
-  };
-  // the shortest odd s4 with sum ceil(len / 4 s4) <= 32 (odd: the sub-ranges of one piece start
-  // in distinct shared-memory banks), between the volume bound and the always-feasible bound
-  uint32_t s_hi = ((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u;
-  uint32_t s_lo = 1u;
-  {
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, len);
-    s_lo = max(1u, (tot + 127u) / 128u) | 1u;
-  }
-  while (s_lo < s_hi) {  // warp-uniform bisection over odd values
-    const uint32_t mid = ((s_lo + s_hi) >> 1) | 1u;
-    const uint32_t m = mid >= s_hi ? s_lo : mid;
-    if (__reduce_add_sync(0xffffffffu, nsub(m)) <= 32u) s_hi = m;
-    else s_lo = m + 2u;
-  }
-  const uint32_t SR = 4u * s_hi;
-  const uint32_t cnt = nsub(s_hi);
+  // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32), an odd
+  // number of 16-byte chunks (the sub-ranges of one piece then start in distinct banks)
+  const uint32_t SR = 4u * (((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u);
+  uint32_t cnt = (uint32_t)__fmul_rn((float)(len + SR - 1), __frcp_rn((float)SR));  // ceil(len/SR), fixed up
+  if (cnt * SR < len) ++cnt;
+  else if (cnt && (cnt - 1) * SR >= len) --cnt;
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -898,13 +880,19 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // the current tile's descriptor (lane 0) and request records (lane k: request r0 + k), loaded
   // one tile ahead: within a chunk the next tile's first request is this tile's last one, so its
   // records are requested before this tile is computed
-  TileMeta tm;
+  struct MetaLite {
+    uint32_t r0, flags, hcnt;
+  };
+  MetaLite tm{0u, 0u, 0u};
   uint32_t r_end = 0;
   ScanRec rec;
   rec.lim = 0;
-  auto load_meta = [&](uint32_t tt, TileMeta& m, uint32_t& re) {
+  auto load_meta = [&](uint32_t tt, MetaLite& m, uint32_t& re) {
     if (lane == 0) {
-      m = w.tile_meta[tt];
+      const TileMeta* tmp = w.tile_meta + tt;
+      m.r0 = tmp->r0;
+      m.flags = tmp->flags;
+      m.hcnt = tmp->hcnt;
       re = (tt + 1 < ntiles) ? w.tile_meta[tt + 1].r0 : n - 1;
     }
   };
@@ -925,7 +913,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
     // ---- prefetch of the next tile
     const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
-    TileMeta tmn;
+    MetaLite tmn{0u, 0u, 0u};
     uint32_t r_endn = 0;
     ScanRec recn;
     recn.lim = 0;
@@ -943,9 +931,9 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
     if (chunk_start && mode == 1u) {
       const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
-      const uint32_t httft = __shfl_sync(0xffffffffu, tm.httft, 0);
-      const uint32_t hP = __shfl_sync(0xffffffffu, tm.hP, 0);
-      const unsigned long long hbase = __shfl_sync(0xffffffffu, tm.hbase, 0);
+      const TileMeta* tmp = w.tile_meta + tcur;  // the head request's parameters (chunk starts only)
+      const uint32_t httft = tmp->httft, hP = tmp->hP;
+      const unsigned long long hbase = tmp->hbase;
       for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
         uint32_t d[8];
 #pragma unroll
