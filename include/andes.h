@@ -260,6 +260,21 @@ int andes_schedule_shard(AndesCtx *ctx, const AndesShard *shard, uint32_t step, 
                          const AndesSchedParams *p, AndesDecision *out, const void *recv, void *send,
                          void *stream);
 
+/* ---- Exact reference solver (NEXT-4; Algorithm 2) --------------------------
+ * The 3D dynamic program for Eq. 5 at target batch size B over n items with integer values
+ * value[i] (e.g. llrint(gain_i 2^32), reading R9, so that the optimum is exact) and weights
+ * weight[i] (context lengths l_i), capacity M: x[n] (u8) = Algorithm 2's solution (its line order:
+ * "not served" then "served" on strict improvement, the first maximum of dp[N][B][:], the
+ * backtracking), *best = its value (INT64_MIN when no B items fit), Vb[B+1] (optional) = the
+ * best value for every b <= B (max over m of dp[N][b][:]).  O(n (B+1)(M+1)) work in one CTA:
+ * meant for small instances (greedy-vs-exact quality checks), not for the decision path.
+ * All pointers DEVICE memory; workspace (8-byte aligned) of andes_knapsack_dp_workspace(n, B, M)
+ * bytes owned by the caller.  Asynchronous on stream.  Errors: ANDES_E_INVAL, ANDES_E_CAPACITY. */
+uint64_t andes_knapsack_dp_workspace(uint32_t n, uint32_t B, uint64_t M);
+int andes_knapsack_dp(AndesCtx *ctx, const int64_t *value, const uint32_t *weight, uint32_t n, uint32_t B,
+                      uint64_t M, void *workspace, uint64_t workspace_bytes, uint8_t *x, int64_t *best,
+                      int64_t *Vb, void *stream);
+
 /* Per-stage timing.  When enabled, andes_schedule records a CUDA event before its first
  * and after each of its kernels on the call's stream (also under stream capture, so a
  * captured CUDA graph of a decision carries the event-record nodes).  andes_profile_read

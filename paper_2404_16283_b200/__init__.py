@@ -45,7 +45,8 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
-           "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean"]
+           "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean", "andes_knapsack_dp",
+           "andes_knapsack_dp_workspace"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -121,6 +122,10 @@ def lib() -> C.CDLL:
                                           C.POINTER(DecisionPtrs), C.c_void_p]
         L.andes_qoe_scenario_mean.argtypes = [C.c_void_p, C.POINTER(Requests), C.c_void_p, C.c_uint32,
                                               C.c_void_p, C.c_void_p, C.c_void_p]
+        L.andes_knapsack_dp_workspace.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64]
+        L.andes_knapsack_dp_workspace.restype = C.c_uint64
+        L.andes_knapsack_dp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64,
+                                        C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.andes_shard_init.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Shard)]
         L.andes_schedule_shard.argtypes = [C.c_void_p, C.POINTER(Shard), C.c_uint32, C.POINTER(Requests),
                                            C.POINTER(SchedParams), C.POINTER(DecisionPtrs), C.c_void_p, C.c_void_p,
@@ -259,6 +264,20 @@ class Context:
                                                   _ptr(mean), _ptr(cnt), _stream_ptr(stream)),
                     "andes_qoe_scenario_mean")
         return mean[:S], cnt[:S]
+
+    # -- andes_knapsack_dp (Algorithm 2, exact reference for small instances)
+    def knapsack_dp(self, value, weight, B: int, M: int, stream=None):
+        """value: device int64 [n], weight: device int32 [n] -> (x u8 [n], best int, Vb int64 [B+1])."""
+        torch = _torch()
+        n = int(value.numel())
+        nb = int(lib().andes_knapsack_dp_workspace(n, int(B), int(M)))
+        ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=self.device)
+        x = torch.empty(max(n, 1), dtype=torch.uint8, device=self.device)
+        best = torch.empty(1, dtype=torch.int64, device=self.device)
+        Vb = torch.empty(int(B) + 1, dtype=torch.int64, device=self.device)
+        self._check(lib().andes_knapsack_dp(self._h, _ptr(value), _ptr(weight), n, int(B), int(M), _ptr(ws), nb,
+                                            _ptr(x), _ptr(best), _ptr(Vb), _stream_ptr(stream)), "andes_knapsack_dp")
+        return x[:n], best, Vb
 
     # -- andes_gain_estimate
     def gain_estimate(self, req: dict, n: int, now_us: int, horizon_us: int, tau, B_list, stream=None):

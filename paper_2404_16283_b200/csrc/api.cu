@@ -616,6 +616,24 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
   return finish_call(c, s, false);
 }
 
+uint64_t andes_knapsack_dp_workspace(uint32_t n, uint32_t B, uint64_t M) {
+  return (uint64_t)knapsack_dp_workspace(n, B, M);
+}
+
+int andes_knapsack_dp(AndesCtx* c, const int64_t* value, const uint32_t* weight, uint32_t n, uint32_t B,
+                      uint64_t M, void* workspace, uint64_t workspace_bytes, uint8_t* x, int64_t* best,
+                      int64_t* Vb, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  if ((n && (!value || !weight || !x)) || !best || !workspace) return set_err(c, ANDES_E_INVAL, "NULL argument%s");
+  if (M > 0xFFFFFFFEull || B > n + 1024u) return set_err(c, ANDES_E_INVAL, "M or B out of range%s");
+  if (workspace_bytes < knapsack_dp_workspace(n, B, M))
+    return set_err(c, ANDES_E_CAPACITY, "workspace smaller than andes_knapsack_dp_workspace()%s");
+  if (reinterpret_cast<uintptr_t>(workspace) & 7u) return set_err(c, ANDES_E_INVAL, "workspace must be 8-byte aligned%s");
+  launch_knapsack_dp(static_cast<cudaStream_t>(stream), reinterpret_cast<const long long*>(value), weight, n, B,
+                     (uint32_t)M, workspace, x, reinterpret_cast<long long*>(best), reinterpret_cast<long long*>(Vb));
+  return cuda_check(c, cudaGetLastError(), "kernel launch");
+}
+
 int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedParams* p, AndesDecision* out,
                         void* stream) {
   if (!c) return ANDES_E_INVAL;

@@ -398,3 +398,48 @@ def test_refiner_config2(A, ctx, orc):
     snap = W.config2()
     for prefill, swap in ((5000, 0), (500, 20000), (50_000, 0)):
         _check_sched(A, ctx, orc, snap, flags=1 | 128, cap=16, prefill=prefill, swap=swap)
+
+
+# ---------------------------------------------------------------- Algorithm 2 on the GPU (NEXT-4)
+@pytest.mark.parametrize("seed", range(16))
+def test_knapsack_dp_matches_algorithm2(A, ctx, seed):
+    """andes_knapsack_dp vs the oracle's line-by-line transcription of Algorithm 2 (exact integer
+    values): the same optimum, the same solution vector (tie rules included), and per-b optima
+    equal to brute force."""
+    from oracle import exact as X
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 12))
+    B = int(rng.integers(0, n + 2))
+    M = int(rng.integers(0, 60))
+    l = rng.integers(1, 25, n).tolist()
+    q = (rng.integers(-5, 12, n) * (2 ** 28 if seed % 2 else 1)).tolist()  # ties and negatives
+    if seed % 4 == 0:
+        q = [3] * n  # all tied
+    x, best, Vb = ctx.knapsack_dp(torch.tensor(q, dtype=torch.int64, device="cuda"),
+                                  torch.tensor(l, dtype=torch.int32, device="cuda"), B, M)
+    torch.cuda.synchronize()
+    qm, xo = X.dp_algorithm2(q, l, B, M)
+    if qm is None:
+        assert int(best.item()) == -(1 << 63)
+    else:
+        assert int(best.item()) == qm
+        assert x.cpu().numpy().tolist() == xo
+    for b in range(B + 1):
+        bf = X.brute_force(q, l, b, M)[0]
+        v = int(Vb[b].item())
+        assert (v == -(1 << 63) and bf is None) or v == bf, (b, v, bf)
+
+
+def test_knapsack_dp_bounds_the_greedy_on_a_snapshot(A, ctx, orc):
+    """Decision-quality reference: at every B the exact optimum of Eq. 5 (Algorithm 2 on the GPU
+    over the oracle's gains in 2^-32 units) is >= Algorithm 1's V(B) from andes_schedule."""
+    snap = W.random_small(21, n=14, B_cap=6)
+    g = _run_sched(A, ctx, snap, flags=1)
+    gain, key, qw = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, np.arange(1, 7))
+    l = torch.from_numpy(snap.ctx_len.astype(np.int32)).cuda()
+    for B in range(int(g["sc"][4]), int(g["sc"][5]) + 1):
+        q = torch.from_numpy(np.rint(gain[B - 1] * 2.0 ** 32).astype(np.int64)).cuda()
+        x, best, Vb = ctx.knapsack_dp(q, l, B, snap.kv_capacity)
+        torch.cuda.synchronize()
+        exact = max(int(v) for v in Vb.cpu().numpy()[: B + 1] if v != -(1 << 63))
+        assert exact >= int(g["V"][B - 1])
