@@ -851,7 +851,9 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   auto gen = [&]() -> uint32_t {
     if (g_t + 1 < g_hi) return ++g_t;
     if (g_nxt >= nchunks) return kNone;
-    g_t = g_nxt * CH;
+    // chunks from the pool's end first: arrival-ordered pools keep the newest, shortest
+    // timelines there (the densest tiles), which then do not form the tail
+    g_t = (nchunks - 1u - g_nxt) * CH;
     g_hi = min(g_t + CH, ntiles);
     g_nxt = atomicAdd(&w.g->tile_ctr, 1u);
     return g_t | kStart;

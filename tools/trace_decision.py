@@ -50,11 +50,7 @@ print("state CTAs", len(st), "start", us(st[:, 0].min()), "end", us(st[:, 1].max
 cp = span(8100, 9124)
 print("compact CTAs", len(cp), "start", us(cp[:, 0].min()), us(cp[:, 0].max()), "theta(CTA0)", us(tr[2210]),
       "end max", us(cp[:, 1].max()))
-cd = span(9200, 10400)
-print("cand CTAs", len(cd), "start", us(cd[:, 0].min()), us(cd[:, 0].max()), "end med/max", us(np.median(cd[:, 1])),
-      us(cd[:, 1].max()))
 print("select CTA255 phases", [us(tr[s]) for s in range(2400, 2406) if tr[s]])
-print("SM clock MHz (select CTA255 sort)", round((int(tr[2411]) - int(tr[2410])) / max(1, int(tr[2401]) - int(tr[2400])) * 1e3, 1))
 sel = span(0, 512)
 print("select CTAs", len(sel), "start", us(sel[:, 0].min()), us(sel[:, 0].max()), "end min/med/max",
       us(sel[:, 1].min()), us(np.median(sel[:, 1])), us(sel[:, 1].max()))
