@@ -902,9 +902,16 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     sr.lim = 0;
     if (rr + lane < n) sr = w.srec[rr + lane];
   };
+  // three-stage pipeline: the descriptor of the tile after next is requested when that tile is
+  // generated (end of an iteration), the records of the next tile once the current tile's data
+  // has arrived (its descriptor is in by then), both consumed one iteration later
+  MetaLite tm1{0u, 0u, 0u};
+  uint32_t r_end1 = 0;
   if (cur != kNone) {
     load_meta(cur & ~kStart, tm, r_end);
     load_rec(__shfl_sync(0xffffffffu, tm.r0, 0), rec);
+    const uint32_t n1 = __shfl_sync(0xffffffffu, s1, 0);
+    if (n1 != kNone) load_meta(n1 & ~kStart, tm1, r_end1);
   }
   while (cur != kNone) {
     const uint32_t tcur = cur & ~kStart;
@@ -913,14 +920,11 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
     const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
     const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
-    // ---- prefetch of the next tile
+    // ---- the next tile (its descriptor is in tm1)
     const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
-    MetaLite tmn{0u, 0u, 0u};
-    uint32_t r_endn = 0;
     ScanRec recn;
     recn.lim = 0;
     const bool seq = nxt != kNone && (nxt & ~kStart) == tcur + 1u;
-    if (nxt != kNone) load_meta(nxt & ~kStart, tmn, r_endn);
     if (seq) load_rec(re, recn);
     const uint32_t dummy = flags & 1u;
     // inside a chunk the carry comes from the previous tile (mode 1 with that value)
@@ -955,6 +959,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     // this tile's data
     if (buf == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
     else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+    if (nxt != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tm1.r0, 0), recn);
     unsigned char* tile = wbase + buf * (kWTile * 4);
     {
       const unsigned long long pe = min(p0 + (unsigned long long)kWTile, pool_end);
@@ -993,23 +998,26 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       w.trace[16384 + 2 * tcur + 1] = gtimer();
     }
     uint32_t nx = kNone;
+    MetaLite tm2{0u, 0u, 0u};
+    uint32_t r_end2 = 0;
     if (lane == 0) {
       const uint32_t s2 = gen();
       if (s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[buf], kWTile * 4u);
         tma_tile(pmap, tile, (s2 & ~kStart) * (kWTile / 32), &bar[buf]);
+        load_meta(s2 & ~kStart, tm2, r_end2);
       }
       nx = s1;
       s1 = s2;
     }
     cur = __shfl_sync(0xffffffffu, nx, 0);
     buf ^= 1u;
-    // the next tile's records (requested earlier when it follows this one)
-    if (cur != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tmn.r0, 0), recn);
-    tm = tmn;
-    r_end = r_endn;
+    tm = tm1;
+    r_end = r_end1;
     rec = recn;
+    tm1 = tm2;
+    r_end1 = r_end2;
   }
   if (w.trace && blockIdx.x < 1000 && lane == 0) atomicMax(&w.trace[5000 + 2 * blockIdx.x + 1], gtimer());
 }
