@@ -47,6 +47,15 @@ def _peaks():
         return {}
 
 
+def _ncu_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant
+    kernels from the committed `ncu --set full` captures (profiles/ncu_traffic.json), or {}."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
+
+
 def _hbm_peak():
     p = _peaks()
     if "hbm_gbs" in p:
@@ -446,21 +455,21 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     value = ws * args.steps / (total_ms / 1e3)
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline: the timeline scan (S1) is the path's one bandwidth-bound kernel; S3-S6
+    # (k_state, k_compact, k_select) are latency-bound stages (one CTA per B)
     hbm_peak, hbm_src = _hbm_peak()
     names = A.STAGES
     dom = max(range(len(stage_ms)), key=lambda i: stage_ms[i])
+    scan_i = names.index("scan")
     scan_bytes = 4 * snap.n_tokens + 44 * n  # one read of every timestamp + per-request SoA/state
-    alg_bytes = {"scan": scan_bytes}
-    dom_name = names[dom]
-    if dom_name in alg_bytes:
-        ach = alg_bytes[dom_name] / (stage_ms[dom] / 1e3) / 1e9
-        roof = {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None, "peak_source": hbm_src,
-                "algorithmic_bytes_per_launch": alg_bytes[dom_name]}
-    else:
-        roof = {"kernel": dom_name, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None}
+    ach = scan_bytes / (stage_ms[scan_i] / 1e3) / 1e9
+    roof = {"kernel": "k_qoe_scan (S1)", "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "traffic": _ncu_traffic().get("k_qoe_scan_config3"),
+            "traffic_source": _ncu_traffic().get("source"), "peak_source": hbm_src,
+            "algorithmic_bytes_per_launch": scan_bytes, "dominant_stage": names[dom],
+            "note": ("S3-S6 (state, compact, select: candidate keys, Algorithm 1 per B, cap) are "
+                     "latency-bound one-CTA-per-B stages without a throughput roofline; the scan is the "
+                     "HBM-bound kernel")}
     roof["stage_ms"] = dict(zip(names, stage_ms))
     roof["stage_share"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
 
@@ -486,7 +495,8 @@ def run_ours(args):
                 "unit": "token-events/s", "n_requests": big.n, "token_events": big_events,
                 "pool_tokens": big.n_tokens, "ms_per_eval": qoe_ms, "scan_ms": scan_ms,
                 "roofline": {"kernel": "k_qoe_scan", "bound": "hbm", "achieved": q_ach, "peak": hbm_peak,
-                             "unit": "GB/s", "frac": q_ach / hbm_peak, "traffic": None,
+                             "unit": "GB/s", "frac": q_ach / hbm_peak,
+                             "traffic": _ncu_traffic().get("k_qoe_scan_2p20"),
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
     del qctx, breq
 
