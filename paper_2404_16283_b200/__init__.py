@@ -22,7 +22,8 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libandes.so")
+# ANDES_LIB_PATH: load another build of the library (A/B timing of two builds; same ABI)
+LIB_PATH = os.environ.get("ANDES_LIB_PATH") or os.path.join(_HERE, "libandes.so")
 
 ANDES_OK = 0
 ANDES_NOT_TRIGGERED = 1

@@ -248,6 +248,11 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   c->tiles_cap = (uint32_t)((c->lim.max_tokens + kTile - 1) / kTile) + 2;
   Work& w = c->w;
   w.N_cap = N;
+  {
+    // look-back wait bound; 0 forces the direct head read on every look-back (a test hook)
+    const char* v = getenv("ANDES_LOOKBACK_NS");
+    w.lb_ns = v ? (uint32_t)strtoul(v, nullptr, 10) : 20000u;
+  }
   w.tiles_cap = c->tiles_cap;
   w.S_cap = N < kCandCap ? N : kCandCap;
   if ((e = ctx_alloc(c, &w.m, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre, N)) != cudaSuccess ||

@@ -10,6 +10,7 @@ constexpr int kSelThreads = 512;
 constexpr int kSortCap = kMaxB;
 constexpr int kVictCap = kMaxRunning;
 
+
 // ---------------------------------------------------------------- block helpers
 __device__ __forceinline__ double gain_of(const PackedState& p, uint32_t tau, uint32_t obj) {
   return gain_obj(unpack_state(p), p.qx, tau, obj);

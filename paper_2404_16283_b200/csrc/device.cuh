@@ -111,6 +111,17 @@ struct Globals {
   uint32_t pad2_;
 };
 
+static_assert(sizeof(Globals) == 128, "Globals: one 128-byte line, one warp snapshot");
+
+// Block snapshot of the Globals line: warp 0 loads it (one request per CTA) and the block reads
+// shared memory.  Every thread of a many-CTA grid loading the same global words instead queues
+// on one L2 slice; in k_select that skewed the CTA starts by 6 us.  Ends with __syncthreads().
+__device__ __forceinline__ void snap_globals(const Globals* g, Globals* s) {
+  if (threadIdx.x < 32)
+    reinterpret_cast<uint32_t*>(s)[threadIdx.x] = __ldcg(reinterpret_cast<const uint32_t*>(g) + threadIdx.x);
+  __syncthreads();
+}
+
 // B-independent per-request state for the gain closed form,
 // written once per decision by k_state and read by the candidate / select / cap kernels.
 struct alignas(16) PackedState {
@@ -180,6 +191,7 @@ struct Work {
   uint32_t S_cap;            // survivor capacity of cand_idx
   uint32_t lqsf;             // this call's priority: 0 gain / l (Eq. 6), 1 raw gain (ANDES_LQSF)
   uint32_t obj;              // this call's objective (kObj*)
+  uint32_t lb_ns;            // look-back wait bound (ns) before the direct head read (ANDES_LOOKBACK_NS)
   // objectives that need the QoE now (Appendix A): the decision-time scan's outputs
   uint32_t* m_now;           // [N]
   unsigned long long* spre_now;  // [N]

@@ -136,10 +136,12 @@ __device__ void walk_two(const ReqView& r, uint32_t i, long long t1, long long t
 }
 
 __global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work w, int64_t now) {
+  __shared__ Globals s_g;
   pdl_wait();
-  const uint32_t np = __ldcg(&w.g->rf_npairs);
+  snap_globals(w.g, &s_g);
+  const uint32_t np = s_g.rf_npairs;
   if (np == 0) return;
-  const uint32_t n_run = min(__ldcg(&w.g->n_run), (uint32_t)kMaxRunning);
+  const uint32_t n_run = min(s_g.n_run, (uint32_t)kMaxRunning);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t pr = gw; pr < n_run * np; pr += W) {

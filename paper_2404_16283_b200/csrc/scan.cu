@@ -332,6 +332,72 @@ __device__ __forceinline__ unsigned long long seg_combine(unsigned long long a, 
   return (a & kFlagBit) | v;
 }
 
+// The head request's carry read directly from its hcnt earlier tokens (tile descriptor mode 1,
+// and the look-back's fallback): max_j (d_j - I_j)^+ with I_j = ttft + j P (readings R1-R2).
+// Warp-wide; every lane returns the value.
+__device__ __noinline__ uint32_t head_carry(const uint32_t* __restrict__ pool, unsigned long long hbase,
+                                            uint32_t hcnt, uint32_t httft, uint32_t hP, uint32_t lane) {
+  uint32_t cm = 0u;
+  for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
+    uint32_t d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t kk = k0 + u * 32 + lane;
+      d[u] = kk < hcnt ? __ldg(&pool[hbase + kk]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t kk = k0 + u * 32 + lane;
+      const uint32_t I = httft + kk * hP;
+      if (kk < hcnt) cm = max(cm, max(d[u], I) - I);
+    }
+  }
+  for (int o = 16; o; o >>= 1) cm = max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+  return cm;
+}
+
+// Decoupled look-back for tile t (descriptor mode 2), 32 predecessors per step (lane k reads
+// tile t-1-k): stop at the newest inclusive prefix or segment head, combine older-to-newer with
+// a shuffle tree.  Only tiles from the one holding the head request's first token are read (that
+// tile's aggregate carries the segment flag, so the walk always stops there).  Predecessors are
+// claimed after t (chunks run from the pool's end), so a predecessor may belong to a warp that
+// is itself waiting, or to this warp's own next tile: a wait longer than w.lb_ns (20 us unless
+// ANDES_LOOKBACK_NS says otherwise) gives up and reads the head's earlier tokens directly (the
+// same value), so no wait blocks forever.
+__device__ __noinline__ unsigned long long lookback(const ReqView& r, const Work& w, uint32_t t, uint32_t lane) {
+  const TileMeta* tmp = w.tile_meta + t;
+  const unsigned long long hbase = tmp->hbase;
+  const int64_t hs = (int64_t)(hbase / (unsigned long long)kWTile);
+  const unsigned long long t0 = gtimer();
+  unsigned long long acc = 0ull;
+  for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
+    const int64_t j = jhi - (int64_t)lane;
+    unsigned long long s = kStPrefix;  // before the head's first tile: not needed (empty)
+    bool late = false;
+    if (j >= hs) {
+      while (((s = ld_relaxed(&w.tile_status[j])) & kStMask) == 0ull) {
+        if (gtimer() - t0 >= (unsigned long long)w.lb_ns) {
+          late = true;
+          break;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, late))
+      return kFlagBit | head_carry(r.tl_pool, hbase, tmp->hcnt, tmp->httft, tmp->hP, lane);
+    const bool stop = (s & kStMask) == kStPrefix || (s & kFlagBit);
+    const uint32_t bal = __ballot_sync(0xffffffffu, stop);
+    const uint32_t kst = bal ? (uint32_t)(__ffs(bal) - 1) : 31u;
+    unsigned long long v = (lane <= kst) ? (s & ~kStMask) : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_down_sync(0xffffffffu, v, o);
+      if (lane + o < 32) v = seg_combine(u, v);
+    }
+    acc = seg_combine(__shfl_sync(0xffffffffu, v, 0), acc);
+    if (bal) return acc;
+  }
+}
+
 // byte offset of tile-local token x in a 128B-swizzled [rows x 32] u32 tile
 __device__ __forceinline__ uint32_t swz(uint32_t x) {
   const uint32_t row = x >> 5, chunk = (x >> 2) & 7u;
@@ -556,26 +622,7 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
     // decoupled look-back, 32 predecessors per step (lane k reads tile t-1-k): stop at the
     // newest inclusive prefix or segment head; combine older-to-newer with a shuffle tree
     if (lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
-    for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
-      const int64_t j = jhi - (int64_t)lane;
-      unsigned long long s = kStPrefix;  // before the pool: empty prefix
-      if (j >= 0) {
-        do {
-          s = ld_relaxed(&w.tile_status[j]);
-        } while ((s & kStMask) == 0ull);
-      }
-      const bool stop = (s & kStMask) == kStPrefix || (s & kFlagBit);
-      const uint32_t bal = __ballot_sync(0xffffffffu, stop);
-      const uint32_t kst = bal ? (uint32_t)(__ffs(bal) - 1) : 31u;
-      unsigned long long v = (lane <= kst) ? (s & ~kStMask) : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long u = __shfl_down_sync(0xffffffffu, v, o);
-        if (lane + o < 32) v = seg_combine(u, v);
-      }
-      acc = seg_combine(__shfl_sync(0xffffffffu, v, 0), acc);
-      if (bal) break;
-    }
+    acc = lookback(A.r, w, t, lane);
   } else if (mode == 1u) {
     acc = kFlagBit | cdirect;
   }
@@ -628,7 +675,8 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
 // included), in tile-local coordinates.
 // A dense tile is processed in batches of up to 31 requests (first_batch / last_batch): the
 // running prefix seeds the next batch (mode 1); only a single-batch tile publishes its aggregate
-// early or looks back (mode 2), and only the last batch publishes the tile's prefix.
+// early, and only the last batch publishes the tile's prefix.  Modes 0 and 1 only: a tile that
+// looks back (mode 2) takes the row path.
 template <bool kFinal>
 __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
                                                   uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
@@ -728,30 +776,8 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   // is published first so that successors looking back never wait on this tile's second pass
   if (first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
   unsigned long long acc = 0ull;
-  if (mode == 2u) {
-    for (int64_t jhi = (int64_t)t - 1;; jhi -= 32) {
-      const int64_t j = jhi - (int64_t)lane;
-      unsigned long long st = kStPrefix;
-      if (j >= 0) {
-        do {
-          st = ld_relaxed(&w.tile_status[j]);
-        } while ((st & kStMask) == 0ull);
-      }
-      const bool stop = (st & kStMask) == kStPrefix || (st & kFlagBit);
-      const uint32_t bal = __ballot_sync(0xffffffffu, stop);
-      const uint32_t kst = bal ? (uint32_t)(__ffs(bal) - 1) : 31u;
-      unsigned long long v = (lane <= kst) ? (st & ~kStMask) : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long uu = __shfl_down_sync(0xffffffffu, v, o);
-        if (lane + o < 32) v = seg_combine(uu, v);
-      }
-      acc = seg_combine(__shfl_sync(0xffffffffu, v, 0), acc);
-      if (bal) break;
-    }
-  } else if (mode == 1u) {
-    acc = kFlagBit | cdirect;
-  }
+  // (a tile that looks back (mode 2) takes the row path: this one sees modes 0 and 1 only)
+  if (mode == 1u) acc = kFlagBit | cdirect;
   prefix = seg_combine(acc, tile_agg);
   if (last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
@@ -837,39 +863,51 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles
   uint64_t* bar = s_bar[wid];
 
-  // Chunks of CH consecutive warp-tiles are claimed in increasing order (lane 0 runs the tile
-  // sequence two tiles ahead of the processing, for the TMA double buffer, and holds the next
-  // chunk's claim one chunk ahead).  Inside a chunk the carry passes from tile to tile in
-  // registers; a chunk's first tile takes it from the head request's earlier tokens (direct read)
-  // or by look-back.  A warp processes its tiles in increasing order, so the smallest unfinished
-  // tile is always being processed and look-backs cannot deadlock.
+  // Chunks of CH consecutive warp-tiles: a warp's first chunk is static, the rest are claimed
+  // from a counter (lane 0 runs the tile sequence two tiles ahead of the processing, for the
+  // TMA double buffer, and holds the next chunk's claim one chunk ahead).  Chunks are taken from
+  // the pool's end first; inside a chunk the carry passes from tile to tile in registers; a
+  // chunk's first tile takes it from the head request's earlier tokens (direct read) or by
+  // look-back, whose waits are bounded (see lookback()).
   constexpr uint32_t kNone = 0xFFFFFFFFu, kStart = 0x80000000u;
   const uint32_t KW = gridDim.x * (kScanThreads / 32);
   const uint32_t CH = min(8u, max(1u, ntiles / (8u * KW)));
   const uint32_t nchunks = (ntiles + CH - 1) / CH;
-  uint32_t g_t = kNone, g_hi = 0, g_nxt = 0;  // lane 0: generator position, chunk end, claimed chunk
+  // lane 0's generator state (position, chunk end, claimed chunk) lives in shared memory: it is
+  // touched once per tile and would otherwise hold registers across the whole tile body
+  __shared__ uint32_t s_gen[kScanThreads / 32][3];
+  uint32_t* const gs = s_gen[wid];
   auto gen = [&]() -> uint32_t {
-    if (g_t + 1 < g_hi) return ++g_t;
+    const uint32_t g_t = gs[0], g_hi = gs[1], g_nxt = gs[2];
+    if (g_t + 1 < g_hi) {
+      gs[0] = g_t + 1;
+      return g_t + 1;
+    }
     if (g_nxt >= nchunks) return kNone;
     // chunks from the pool's end first: arrival-ordered pools keep the newest, shortest
     // timelines there (the densest tiles), which then do not form the tail
-    g_t = (nchunks - 1u - g_nxt) * CH;
-    g_hi = min(g_t + CH, ntiles);
-    g_nxt = atomicAdd(&w.g->tile_ctr, 1u);
-    return g_t | kStart;
+    const uint32_t t0 = (nchunks - 1u - g_nxt) * CH;
+    gs[0] = t0;
+    gs[1] = min(t0 + CH, ntiles);
+    gs[2] = atomicAdd(&w.g->tile_ctr, 1u) + KW;  // chunks [0, KW) are the warps' first claims
+    return t0 | kStart;
   };
   uint32_t cur = kNone, s1 = kNone;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    g_nxt = atomicAdd(&w.g->tile_ctr, 1u);
+    // the first chunk is static (chunk = global warp index): no start-up burst of KW atomics on
+    // one counter ahead of the first TMA copy
+    gs[0] = kNone;
+    gs[1] = 0u;
+    gs[2] = blockIdx.x * (kScanThreads / 32) + wid;
     cur = gen();
-    s1 = gen();
     if (cur != kNone) {
       mbar_expect_tx(&bar[0], kWTile * 4u);
       tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), &bar[0]);
     }
+    s1 = gen();
     if (s1 != kNone) {
       mbar_expect_tx(&bar[1], kWTile * 4u);
       tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), &bar[1]);
@@ -932,7 +970,8 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t wn = re - r0 + 1 + dummy;
     const uint32_t nrec = wn - dummy;
     const uint32_t nbatch = (nrec + 30u) / 31u;
-    const bool fast = !swz_on && (nbatch == 1u || mode != 2u);
+    // the aligned path never looks back: the look-back stays out of the hot loop's code
+    const bool fast = !swz_on && mode != 2u;
     // direct head carry
     uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
     if (chunk_start && mode == 1u) {

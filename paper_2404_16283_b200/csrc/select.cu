@@ -47,12 +47,14 @@ constexpr int kCandThreads = 256;
 
 __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
   __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
+  __shared__ Globals s_g;
   pdl_wait();
   pdl_trigger();
-  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
+  snap_globals(w.g, &s_g);
+  if (!s_g.triggered || s_g.B_hi == 0) return;
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
-  const uint32_t tlo = __ldcg(&w.g->tau_lo), thi = __ldcg(&w.g->tau_hi);
+  const uint32_t tlo = s_g.tau_lo, thi = s_g.tau_hi;
   for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
     s_hlb[q] = 0u;
     s_hub[q] = 0u;
@@ -172,10 +174,12 @@ __device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, 
 __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, const uint32_t* lb_src, uint32_t G) {
   pdl_wait();
   pdl_trigger();
+  __shared__ Globals s_g;
   if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
-  if (!__ldcg(&w.g->triggered) || __ldcg(&w.g->B_hi) == 0) return;
+  snap_globals(w.g, &s_g);
+  if (!s_g.triggered || s_g.B_hi == 0) return;
   uint32_t cut, ns;
-  theta_of(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, __ldcg(&w.g->B_hi), cut, ns);
+  theta_of(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, s_g.B_hi, cut, ns);
   if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
   const uint32_t theta = cut << 20;
   const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
@@ -433,14 +437,14 @@ __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
 // Requires n_run <= kStageRun (the last CTA falls back to finalize_decision otherwise).
 __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t kstar, unsigned long long thr,
                           const uint32_t* s_sel, unsigned long long* vkey, uint32_t* vidx, unsigned long long* vcum,
-                          unsigned long long* acum, uint32_t* aflag) {
+                          unsigned long long* acum, uint32_t* aflag, bool rpre, const unsigned long long* rk,
+                          const uint32_t* rx, const uint32_t* rlen, uint32_t n_run) {
   __shared__ uint32_t s_nv, s_na, s_e, s_a;
   __shared__ unsigned long long s_W0;
   __shared__ unsigned long long s_tmp[kSelThreads / 32];
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  const uint32_t n_run = __ldcg(&w.g->n_run);
   if (tid == 0) {
     s_nv = 0;
     s_W0 = 0;
@@ -450,21 +454,34 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
   __syncthreads();
   {
     unsigned long long wl = 0;
-    for (uint32_t q = tid; q < n_run; q += kSelThreads) {
-      const uint32_t i = __ldcg(w.run_list + q);
-      const PackedState st = w.st[i];
-      wl += st.l;
-      const unsigned long long c = comp_of(st, tB, w.lqsf, w.obj);
-      if (kstar == 0 || c < thr) {
-        const uint32_t slot = atomicAdd(&s_nv, 1u);
-        vkey[slot] = ~c;  // descending of ~c = ascending composite
-        vidx[slot] = i;
+    if (rpre) {
+      // composites precomputed by the caller in shared memory (n_run <= kSelThreads)
+      if (tid < n_run) {
+        wl = rlen[tid];
+        const unsigned long long c = rk[tid];
+        if (kstar == 0 || c < thr) {
+          const uint32_t slot = atomicAdd(&s_nv, 1u);
+          vkey[slot] = ~c;
+          vidx[slot] = rx[tid];
+        }
+      }
+    } else {
+      for (uint32_t q = tid; q < n_run; q += kSelThreads) {
+        const uint32_t i = __ldcg(w.run_list + q);
+        const PackedState st = w.st[i];
+        wl += st.l;
+        const unsigned long long c = comp_of(st, tB, w.lqsf, w.obj);
+        if (kstar == 0 || c < thr) {
+          const uint32_t slot = atomicAdd(&s_nv, 1u);
+          vkey[slot] = ~c;  // descending of ~c = ascending composite
+          vidx[slot] = i;
+        }
       }
     }
     for (int o = 16; o; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
     if (lane == 0 && wl) atomicAdd(&s_W0, wl);
   }
-  for (uint32_t q = tid; q < kstar; q += kSelThreads) acum[q] = r.running[s_sel[q]] ? 0ull : 1ull;
+  // acum[q] (q < kstar) = 1 for a waiting selected request, written by the caller's V loop
   __syncthreads();
   block_inclusive_scan(acum, kstar, s_tmp);
   for (uint32_t q = tid; q < kstar; q += kSelThreads)
@@ -622,12 +639,14 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   __shared__ long long s_gf[kSortCap];
   __shared__ uint32_t s_k, s_last;
   __shared__ long long s_red[32];
+  __shared__ Globals s_g;
 
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x;
-  const uint32_t B = blockIdx.x + 1;
+  const uint32_t B = gridDim.x - blockIdx.x;  // largest B (the longest walk) scheduled first
   const uint32_t n = r.n;
+  ANDES_TRACE(A.w, 9200 + B - 1);
   pdl_wait();
   pdl_trigger();
   // the key histograms were consumed by k_compact: self-clean them for the next call
@@ -635,12 +654,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     w.hist_lb[q] = 0u;
     w.hist_ub[q] = 0u;
   }
-  const bool trig = __ldcg(&w.g->triggered) != 0;
-  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
-  const bool ovf = __ldcg(&w.g->overflow) != 0;
-  const uint32_t ns = __ldcg(&w.g->n_surv);
-  const uint32_t n_run = __ldcg(&w.g->n_run);
-  ANDES_TRACE(w, 2 * blockIdx.x);
+  snap_globals(w.g, &s_g);
+  const bool trig = s_g.triggered != 0;
+  const uint32_t B_lo = s_g.B_lo, B_hi = s_g.B_hi;
+  const bool ovf = s_g.overflow != 0;
+  const uint32_t ns = s_g.n_surv;
+  const uint32_t n_run = s_g.n_run;
+  ANDES_TRACE(w, 2 * (B - 1));
 
   if (!trig || B < B_lo || B > B_hi) {
     if (tid == 0) {
@@ -649,6 +669,12 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     }
   } else {
     const uint32_t tB = A.tau[B - 1];
+    // running requests' composites at B, evaluated in the survivors' pass (stage_cap's fast
+    // path), in their own scratch past s_vc
+    const bool rpre = !A.xsend && !ovf && n_run <= (uint32_t)kSelThreads;
+    unsigned long long* const s_rk = s_vc + kVictCap;
+    uint32_t* const s_rx = reinterpret_cast<uint32_t*>(s_rk + kSelThreads);
+    uint32_t* const s_rl = s_rx + kSelThreads;
     // multi-GPU: a rank's local top list may be shorter than B (survivors are global)
     const uint32_t k = A.xsend ? min(B, ovf ? n : ns) : min(B, n);
     uint32_t cnt;
@@ -671,17 +697,31 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       unsigned long long* s_all = s_key + kSortCap;
       uint32_t* s_ri = s_idx + kSortCap;
       long long* s_gall = reinterpret_cast<long long*>(s_vc);
-      for (uint32_t e = tid; e < ns; e += kSelThreads) {
-        const uint32_t i = __ldcg(w.cand_idx + e);
+      // indices first (one coalesced round trip), then the states: each iteration of the second
+      // loop is independent, so its loads overlap instead of chaining behind the index load
+      const uint32_t nr = rpre ? n_run : 0u;
+      for (uint32_t e = tid; e < ns; e += kSelThreads) s_ri[e] = __ldcg(w.cand_idx + e);
+      for (uint32_t q = tid; q < nr; q += kSelThreads) s_rx[q] = __ldcg(w.run_list + q);
+      __syncthreads();
+#pragma unroll 2
+      for (uint32_t e = tid; e < ns + nr; e += kSelThreads) {
+        const bool sv = e < ns;
+        const uint32_t i = sv ? s_ri[e] : s_rx[e - ns];
         const PackedState p = w.st[i];
         const double gn = gain_of(p, tB, w.obj);
-        s_all[e] = composite(ordered_key(prio_key(gn, p.l, w.lqsf)), p.rank);
-        s_gall[e] = gain_fixed(gn);
-        s_ri[e] = i;
+        const unsigned long long c = composite(ordered_key(prio_key(gn, p.l, w.lqsf)), p.rank);
+        if (sv) {
+          s_all[e] = c;
+          s_gall[e] = gain_fixed(gn);
+        } else {
+          s_rk[e - ns] = c;
+          s_rl[e - ns] = p.l;
+        }
       }
       if (tid == 0) s_all[ns] = 0ull;
       __syncthreads();
-      if (blockIdx.x == 255) ANDES_TRACE(w, 2400);
+      if (B == 256) ANDES_TRACE(w, 2400);
+      if (B == 256 && w.trace && tid == 0) w.trace[2410] = ns;
       const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(s_all);
       const uint32_t np = (ns + 1) >> 1;
       for (uint32_t e = tid; e < ns; e += kSelThreads) {
@@ -699,13 +739,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
         }
       }
       __syncthreads();
-      if (blockIdx.x == 255) ANDES_TRACE(w, 2401);
+      if (B == 256) ANDES_TRACE(w, 2401);
       cnt = k;
     }
     if (A.xsend) {
       // multi-GPU step 2: publish this rank's top-k of B in order (padded to B); the merge of
       // all ranks' lists and Algorithm 1's walk run in k_shard_merge
-      const uint32_t base = __ldcg(&w.g->shard_base);
+      const uint32_t base = s_g.shard_base;
       XEntry* dst = A.xsend + tri_off(B);
       for (uint32_t q = tid; q < B; q += kSelThreads) {
         XEntry x;
@@ -727,10 +767,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     }
     // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
     // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
-    if (blockIdx.x == 255) ANDES_TRACE(w, 2402);
+    if (B == 256) ANDES_TRACE(w, 2402);
     for (uint32_t q = tid; q < cnt; q += kSelThreads) s_ps[q] = r.ctx_len[s_idx[q]];
     __syncthreads();
-    if (blockIdx.x == 255) ANDES_TRACE(w, 2403);
+    if (B == 256) ANDES_TRACE(w, 2403);
     if (tid < 32) {
       const uint32_t per = (cnt + 31) / 32, q0 = tid * per, q1 = min(cnt, q0 + per);
       unsigned long long part = 0;
@@ -756,6 +796,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       const uint32_t i = s_idx[q];
       v += ovf ? gain_fixed(gain_of(w.st[i], tB, w.obj)) : s_gf[q];
       w.sel[(size_t)(B - 1) * kMaxB + q] = i;
+      s_ps[q] = r.running[i] ? 0ull : 1ull;  // stage_cap's admit flags (s_ps is free after the walk)
     }
     v = block_sum_ll<kSelThreads>(v, s_red);
     const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
@@ -764,15 +805,15 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       A.o.kstar[B - 1] = kstar;
       w.sel_thr[B - 1] = thr;
     }
-    if (blockIdx.x == 255) ANDES_TRACE(w, 2404);
+    if (B == 256) ANDES_TRACE(w, 2404);
     if (n_run <= (uint32_t)kStageRun) {
       // victims and their prefix sums live past the first kStageRun slots of s_key / s_idx
       stage_cap(A, B, tB, kstar, thr, s_idx, s_key + kStageRun, s_idx + kStageRun, s_vc,
-                reinterpret_cast<unsigned long long*>(s_ps), reinterpret_cast<uint32_t*>(s_gf));
+                s_ps, reinterpret_cast<uint32_t*>(s_gf), rpre, s_rk, s_rx, s_rl, n_run);
     }
-    if (blockIdx.x == 255) ANDES_TRACE(w, 2405);
+    if (B == 256) ANDES_TRACE(w, 2405);
   }
-  ANDES_TRACE(w, 2 * blockIdx.x + 1);
+  ANDES_TRACE(w, 2 * (B - 1) + 1);
   if (A.xsend) return;
   // the last CTA to finish runs S5 + S6 (last-block pattern)
   __threadfence();
@@ -823,7 +864,11 @@ void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint
 }
 
 // victims keys + indices + prefix sums (the fused S5/S6 tail needs all three)
-static size_t select_smem() { return (2 * sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap; }
+// + the running requests' composites / indices / lengths (n_run <= kSelThreads)
+static size_t select_smem() {
+  return (2 * sizeof(unsigned long long) + sizeof(uint32_t)) * kVictCap +
+         (sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * kSelThreads;
+}
 
 void init_kernels() {
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());

@@ -250,9 +250,11 @@ __global__ void __launch_bounds__(kSelThreads) k_shard_merge(MergeArgs A) {
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t B = blockIdx.x + 1, G = A.G;
+  __shared__ Globals s_g;
   pdl_wait();
-  const bool trig = __ldcg(&w.g->triggered) != 0;
-  const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
+  snap_globals(w.g, &s_g);
+  const bool trig = s_g.triggered != 0;
+  const uint32_t B_lo = s_g.B_lo, B_hi = s_g.B_hi;
   const size_t stride = tri_off(A.B_cap + 1);
   if (!trig || B < B_lo || B > B_hi) {
     if (tid == 0) {

@@ -92,6 +92,19 @@ def _check_long_request(A, ctx, orc, tl, ttft, P, d, align):
         _check_qoe(A, ctx, orc, big, big.now_us - 40_000_000, final)
 
 
+@pytest.mark.parametrize("lb_ns", ["20000", "0", "1000"])
+def test_qoe_long_lookback(A, orc, lb_ns, monkeypatch):
+    # long requests: nearly every tile's carry comes by look-back; ANDES_LOOKBACK_NS=0 forces the
+    # direct fallback on every look-back, 1000 mixes both (whichever wins, the values are equal)
+    monkeypatch.setenv("ANDES_LOOKBACK_NS", lb_ns)
+    c2 = A.Context(max_requests=1024, max_B=256, max_tokens=1 << 23)
+    for align in (4, 1):
+        snap = W.long_requests(5, align=align)
+        for final in (False, True):
+            _check_qoe(A, c2, orc, snap, snap.now_us, final)
+            _check_qoe(A, c2, orc, snap, snap.now_us // 2, final)
+
+
 def test_qoe_config3_full(A, ctx, orc):
     snap = W.config3()
     # the oracle is fast enough for QoE (one walk per request)

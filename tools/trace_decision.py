@@ -54,6 +54,9 @@ print("select CTA255 phases", [us(tr[s]) for s in range(2400, 2406) if tr[s]])
 sel = span(0, 512)
 print("select CTAs", len(sel), "start", us(sel[:, 0].min()), us(sel[:, 0].max()), "end min/med/max",
       us(sel[:, 1].min()), us(np.median(sel[:, 1])), us(sel[:, 1].max()))
+ent = tr[9200:9456]
+print("select entry min/med/max", us(ent.min()), us(np.median(ent)), us(ent.max()), "n_surv", int(tr[2410]),
+      "late entries (B)", (np.argsort(-ent)[:8] + 1).tolist())
 print("finalize phases", [us(tr[s]) for s in range(2100, 2106) if tr[s]])
 
 tl = tr[16384:16384 + 2 * 16384].reshape(-1, 2)
@@ -71,3 +74,8 @@ ends = np.sort(tl[ok, 1])
 print("tile end percentiles us", [us(np.percentile(ends, p)) for p in (50, 90, 99, 99.9, 100)])
 last = ids[np.argsort(-tl[ok, 1])[:8]]
 print("last tiles to finish", [(int(t), us(tl[t, 0]), us(tl[t, 1])) for t in last])
+st0 = np.sort(tl[ok, 0])
+print("tile start percentiles us", [us(np.percentile(st0, p)) for p in (0, 1, 10, 50, 90, 99, 100)])
+grid = np.arange(int(us(st0[0])), int(us(ends[-1])) + 2, 2.0)
+live = [int(((tl[ok, 0] - t0) / 1e3 <= g).sum() - ((tl[ok, 1] - t0) / 1e3 <= g).sum()) for g in grid]
+print("tiles in flight every 2 us from", grid[0], ":", live)

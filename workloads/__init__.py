@@ -337,3 +337,33 @@ def random_small(seed, n=None, max_tokens=40, B_cap=16, edge=True, align: int = 
                     max_total=mt, start_off_us=off, rank=rank, running=running, tl_base=base, tl_pool=pool,
                     now_us=now, horizon_us=horizon, tau_us=tau, kv_capacity=M,
                     preempt_cap=int(rng.choice([UINT32_MAX, 0, 1, 2])), name=f"rand-s{seed}")
+
+
+def long_requests(seed, n=200, lo=5_000, hi=30_000, align: int = POOL_ALIGN) -> Snapshot:
+    """Long-output requests (5K-30K tokens each): nearly every tile's head request started more
+    than 4096 tokens earlier, so the scan's carry comes by look-back (or its direct fallback).
+    Deliveries follow the ideal schedule with jitter, stalls that make them late, and catch-ups;
+    a few requests are empty or tiny so that short segments sit between the long ones."""
+    rng = np.random.default_rng(seed)
+    P = rng.choice([20_000, 33_333, 50_000], n).astype(np.uint32)
+    ttft = rng.choice([0, 300_000, 1_000_000], n).astype(np.uint32)
+    timelines = []
+    span = 0
+    for i in range(n):
+        g = int(rng.integers(lo, hi + 1)) if rng.random() < 0.9 else int(rng.integers(0, 3))
+        j = np.arange(g, dtype=np.int64)
+        d = int(ttft[i]) + j * int(P[i]) + rng.integers(-int(P[i]) // 2, int(P[i]) // 2 + 1, g)
+        for _ in range(int(rng.integers(0, 4))):  # stalls: every later token shifted
+            if g:
+                d[int(rng.integers(0, g)):] += int(rng.integers(0, 40)) * int(P[i])
+        d = np.maximum.accumulate(np.maximum(d, 0))
+        timelines.append(d.astype(np.uint32))
+        span = max(span, int(d[-1]) if g else 0)
+    g, base, pool = _pack(timelines, align)
+    now = span + 1_000_000
+    return Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=ttft, period_us=P,
+                    ctx_len=rng.integers(1, 4096, n).astype(np.uint32), n_deliv=g,
+                    max_total=np.full(n, UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                    rank=rng.permutation(n).astype(np.uint32), running=(rng.random(n) < 0.5).astype(np.uint8),
+                    tl_base=base, tl_pool=pool, now_us=now, horizon_us=2_000_000, tau_us=tau_table(),
+                    kv_capacity=1 << 20, preempt_cap=UINT32_MAX, name=f"long-s{seed}")
