@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
   // 16-byte aligned timelines (every request): plain tiles and the piece-parallel path; else
   // 128B-swizzled tiles and the row-per-lane event path
-  const uint32_t swz_on = __ldcg(&w.g->unal) ? 1u : 0u;
+  const uint32_t swz_on = w.g->unal ? 1u : 0u;  // (L1: one L2 request per SM, not per warp)
   const CUtensorMap* pmap = swz_on ? &tmap_swz : &tmap_plain;
   unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles
   uint64_t* bar = s_bar[wid];
@@ -877,7 +877,13 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // touched once per tile and would otherwise hold registers across the whole tile body
   __shared__ uint32_t s_gen[kScanThreads / 32][3];
   uint32_t* const gs = s_gen[wid];
-  auto gen = [&]() -> uint32_t {
+  // claims: chunk sw then chunk KS + sw are static (sw: the warp's index among the KS static
+  // warps), later ones come from the counter (+ 2 KS); the counter's result is first needed a
+  // whole tile after it is asked.  CTA 0 of a decision computes the bounds first: its warps
+  // claim from the counter only (static chunks there would start last and form the tail).
+  const uint32_t cta0_dyn = (A.sched && blockIdx.x == 0) ? 1u : 0u;
+  const uint32_t KS = KW - (A.sched ? (kScanThreads / 32) : 0u);
+  auto gen = [&](bool static_next) -> uint32_t {
     const uint32_t g_t = gs[0], g_hi = gs[1], g_nxt = gs[2];
     if (g_t + 1 < g_hi) {
       gs[0] = g_t + 1;
@@ -889,7 +895,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t t0 = (nchunks - 1u - g_nxt) * CH;
     gs[0] = t0;
     gs[1] = min(t0 + CH, ntiles);
-    gs[2] = atomicAdd(&w.g->tile_ctr, 1u) + KW;  // chunks [0, KW) are the warps' first claims
+    gs[2] = static_next ? g_nxt + KS : atomicAdd(&w.g->tile_ctr, 1u) + 2u * KS;
     return t0 | kStart;
   };
   uint32_t cur = kNone, s1 = kNone;
@@ -897,17 +903,18 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the first chunk is static (chunk = global warp index): no start-up burst of KW atomics on
-    // one counter ahead of the first TMA copy
+    // static first claims: no start-up burst of KW atomics on one counter ahead of the first
+    // two TMA copies
     gs[0] = kNone;
     gs[1] = 0u;
-    gs[2] = blockIdx.x * (kScanThreads / 32) + wid;
-    cur = gen();
+    gs[2] = cta0_dyn ? atomicAdd(&w.g->tile_ctr, 1u) + 2u * KS
+                     : (blockIdx.x - (A.sched ? 1u : 0u)) * (kScanThreads / 32) + wid;
+    cur = gen(!cta0_dyn);
     if (cur != kNone) {
       mbar_expect_tx(&bar[0], kWTile * 4u);
       tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), &bar[0]);
     }
-    s1 = gen();
+    s1 = gen(false);
     if (s1 != kNone) {
       mbar_expect_tx(&bar[1], kWTile * 4u);
       tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), &bar[1]);
@@ -951,12 +958,21 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t n1 = __shfl_sync(0xffffffffu, s1, 0);
     if (n1 != kNone) load_meta(n1 & ~kStart, tm1, r_end1);
   }
+#ifdef ANDES_SCAN_PHASES
+  uint32_t ph_it = 0;
+  if (w.trace && blockIdx.x * 4 + wid < 4096 && lane == 0) w.trace[49152 + 4 * (blockIdx.x * 4 + wid)] = gtimer();
+#endif
   while (cur != kNone) {
     const uint32_t tcur = cur & ~kStart;
     const bool chunk_start = (cur & kStart) != 0u;
     const unsigned long long p0 = (unsigned long long)tcur * kWTile;
     const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
     const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
+#ifdef ANDES_SCAN_PHASES
+    const uint32_t gw_ = blockIdx.x * 4 + wid;
+    const bool ph_on = w.trace && gw_ < 4096 && ph_it == 0 && lane == 0;
+    if (ph_on) w.trace[49152 + 4 * gw_ + 1] = gtimer();
+#endif
     const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
     // ---- the next tile (its descriptor is in tm1)
     const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
@@ -996,8 +1012,15 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       for (int o = 16; o; o >>= 1) cm = max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
     }
     // this tile's data
+#ifdef ANDES_SCAN_PHASES
+    if (ph_on) w.trace[49152 + 4 * gw_ + 2] = gtimer();
+#endif
     if (buf == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
     else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+#ifdef ANDES_SCAN_PHASES
+    if (ph_on) w.trace[49152 + 4 * gw_ + 3] = gtimer();
+    ++ph_it;
+#endif
     if (nxt != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tm1.r0, 0), recn);
     unsigned char* tile = wbase + buf * (kWTile * 4);
     {
@@ -1040,7 +1063,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     MetaLite tm2{0u, 0u, 0u};
     uint32_t r_end2 = 0;
     if (lane == 0) {
-      const uint32_t s2 = gen();
+      const uint32_t s2 = gen(false);
       if (s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[buf], kWTile * 4u);

@@ -79,3 +79,9 @@ print("tile start percentiles us", [us(np.percentile(st0, p)) for p in (0, 1, 10
 grid = np.arange(int(us(st0[0])), int(us(ends[-1])) + 2, 2.0)
 live = [int(((tl[ok, 0] - t0) / 1e3 <= g).sum() - ((tl[ok, 1] - t0) / 1e3 <= g).sum()) for g in grid]
 print("tiles in flight every 2 us from", grid[0], ":", live)
+ph = tr[49152:65536].reshape(-1, 4)
+okp = ph[:, 0] > 0
+if okp.any():
+    ph = ph[okp]
+    for k, name in enumerate(["loop entry", "meta in", "carry done", "data in"]):
+        print(f"first tile {name:10s} us p0/p10/p50/p90/max", [us(np.percentile(ph[:, k], q)) for q in (0, 10, 50, 90, 100)])
