@@ -677,6 +677,26 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
 // running prefix seeds the next batch (mode 1); only a single-batch tile publishes its aggregate
 // early, and only the last batch publishes the tile's prefix.  Modes 0 and 1 only: a tile that
 // looks back (mode 2) takes the row path.
+// Sub-range length SR(np) of the aligned path for np pieces in a tile: sum ceil(len/SR) <=
+// kWTile/SR + np <= 32, and SR is an odd number of 16-byte chunks (the sub-ranges of one piece
+// then start in distinct shared-memory banks); mg = ceil(2^32 / SR), so that ceil(x / SR) =
+// umulhi(x + SR - 1, mg) exactly for x < 2^32 / SR (here x <= 2 kWTile).
+struct SubRangeTab {
+  uint32_t sr[33], mg[33];
+};
+constexpr SubRangeTab make_subrange_tab() {
+  SubRangeTab t{};
+  for (uint32_t np = 0; np <= 32; ++np) {
+    const uint32_t d = np < 32 ? 32u - np : 1u;
+    const uint32_t sr = 4u * (((kWTile / 4u + d - 1u) / d) | 1u);
+    t.sr[np] = sr;
+    t.mg[np] = (uint32_t)((0x100000000ull + sr - 1u) / sr);
+  }
+  return t;
+}
+__constant__ SubRangeTab kSubRange = make_subrange_tab();
+static_assert(make_subrange_tab().sr[31] <= 2 * kWTile && make_subrange_tab().sr[0] == 4u * 9u, "SR table");
+
 template <bool kFinal>
 __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
                                                   uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
@@ -686,14 +706,9 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
   const uint32_t len = (uint32_t)(pe - ps);
   const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
-  // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32)
-  // (an odd number of 16-byte chunks: sub-ranges of one piece hit distinct shared-memory banks)
-  // sub-range length: <= 32 sub-ranges in total (sum ceil(len/SR) <= kWTile/SR + np <= 32), an odd
-  // number of 16-byte chunks (the sub-ranges of one piece then start in distinct banks)
-  const uint32_t SR = 4u * (((kWTile / 4u + (32u - np) - 1u) / (32u - np)) | 1u);
-  uint32_t cnt = (uint32_t)__fmul_rn((float)(len + SR - 1), __frcp_rn((float)SR));  // ceil(len/SR), fixed up
-  if (cnt * SR < len) ++cnt;
-  else if (cnt && (cnt - 1) * SR >= len) --cnt;
+  // sub-range length from the table (no division on the hot path): <= 32 sub-ranges in total
+  const uint32_t SR = kSubRange.sr[np];
+  const uint32_t cnt = __umulhi(len + SR - 1u, kSubRange.mg[np]);  // ceil(len / SR), exact
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
