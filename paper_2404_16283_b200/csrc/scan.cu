@@ -300,6 +300,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// 32-bit shared-address forms (addresses computed once per warp; no generic->shared
+// conversions on the per-tile path)
+__device__ __forceinline__ void mbar_expect_tx_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -312,11 +331,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 // TMA: one [32 rows x 32 u32] box of the pool (one warp-tile), 128-byte swizzled
-__device__ __forceinline__ void tma_tile(const CUtensorMap* tmap, void* dst, uint32_t row0, uint64_t* bar) {
+__device__ __forceinline__ void tma_tile(const CUtensorMap* tmap, uint32_t dst, uint32_t row0, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(row0), "r"(smem_u32(bar))
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(row0), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
@@ -875,8 +894,9 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // 128B-swizzled tiles and the row-per-lane event path
   const uint32_t swz_on = w.g->unal ? 1u : 0u;  // (L1: one L2 request per SM, not per warp)
   const CUtensorMap* pmap = swz_on ? &tmap_swz : &tmap_plain;
-  unsigned char* wbase = s_base + wid * kWarpSmem;                      // [2][kWTile*4] tiles
+  const uint32_t wbase = smem_u32(s_base) + wid * kWarpSmem;  // [2][kWTile*4] tiles (shared address)
   uint64_t* bar = s_bar[wid];
+  const uint32_t bar_s = smem_u32(bar);  // bar[0]; bar[1] at + 8
 
   // Chunks of CH consecutive warp-tiles: a warp's first chunk is static, the rest are claimed
   // from a counter (lane 0 runs the tile sequence two tiles ahead of the processing, for the
@@ -926,13 +946,13 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
                      : (blockIdx.x - (A.sched ? 1u : 0u)) * (kScanThreads / 32) + wid;
     cur = gen(!cta0_dyn);
     if (cur != kNone) {
-      mbar_expect_tx(&bar[0], kWTile * 4u);
-      tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), &bar[0]);
+      mbar_expect_tx_s(bar_s, kWTile * 4u);
+      tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), bar_s);
     }
     s1 = gen(false);
     if (s1 != kNone) {
-      mbar_expect_tx(&bar[1], kWTile * 4u);
-      tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), &bar[1]);
+      mbar_expect_tx_s(bar_s + 8u, kWTile * 4u);
+      tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), bar_s + 8u);
     }
   }
   __syncwarp();
@@ -1030,25 +1050,26 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
 #ifdef ANDES_SCAN_PHASES
     if (ph_on) w.trace[49152 + 4 * gw_ + 2] = gtimer();
 #endif
-    if (buf == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
-    else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+    if (buf == 0) { mbar_wait_s(bar_s, ph0); ph0 ^= 1u; }
+    else { mbar_wait_s(bar_s + 8u, ph1); ph1 ^= 1u; }
 #ifdef ANDES_SCAN_PHASES
     if (ph_on) w.trace[49152 + 4 * gw_ + 3] = gtimer();
     ++ph_it;
 #endif
     if (nxt != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tm1.r0, 0), recn);
-    unsigned char* tile = wbase + buf * (kWTile * 4);
+    const uint32_t tile = wbase + buf * (kWTile * 4);
     {
       const unsigned long long pe = min(p0 + (unsigned long long)kWTile, pool_end);
       if (pe > full_rows_end) {
         const unsigned long long lo = max(p0, full_rows_end);
         for (unsigned long long p = lo + lane; p < pe; p += 32)
-          *reinterpret_cast<uint32_t*>(tile + (swz_on ? swz((uint32_t)(p - p0)) : (uint32_t)(p - p0) * 4u)) =
-              r.tl_pool[p];
+          st_shared_u32(tile + (swz_on ? swz((uint32_t)(p - p0)) : (uint32_t)(p - p0) * 4u), r.tl_pool[p]);
       }
     }
     __syncwarp();
+#ifdef ANDES_SCAN_PHASES
     const unsigned long long t_body = (w.trace && tcur < 16384) ? gtimer() : 0ull;
+#endif
     if (fast) {
       // piece-parallel path, batches of 31 requests (lane q of batch b = request r0 + 31 b + q)
       unsigned long long pref = 0ull;
@@ -1058,7 +1079,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
         ScanRec rb = rec;
         if (b && lane < nb_req) rb = w.srec[r0 + 31u * b + lane];
         const Entry e = lane < nb_req ? entry_of(rb, r0 + 31u * b + lane, p0) : null_entry(true);
-        warp_tile_aligned<kFinal>(A, e, smem_u32(tile), tcur, mb, cb, pref, b == 0, b + 1 == nbatch);
+        warp_tile_aligned<kFinal>(A, e, tile, tcur, mb, cb, pref, b == 0, b + 1 == nbatch);
         mb = 1u;
         cb = (uint32_t)pref;
       }
@@ -1066,14 +1087,16 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     } else {
       // row-per-lane event path (unaligned pools, or a dense tile that must look back); the
       // window's records are read from global memory
-      acc_reg = warp_tile_global<kFinal>(A, smem_u32(tile), p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+      acc_reg = warp_tile_global<kFinal>(A, tile, p0, r0, dummy, wn, tcur, mode, cm, swz_on);
     }
     // refill this buffer with the tile two ahead in the warp's sequence
     __syncwarp();
+#ifdef ANDES_SCAN_PHASES
     if (t_body && lane == 0) {
       w.trace[16384 + 2 * tcur] = t_body;
       w.trace[16384 + 2 * tcur + 1] = gtimer();
     }
+#endif
     uint32_t nx = kNone;
     MetaLite tm2{0u, 0u, 0u};
     uint32_t r_end2 = 0;
@@ -1081,8 +1104,8 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       const uint32_t s2 = gen(false);
       if (s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[buf], kWTile * 4u);
-        tma_tile(pmap, tile, (s2 & ~kStart) * (kWTile / 32), &bar[buf]);
+        mbar_expect_tx_s(bar_s + 8u * buf, kWTile * 4u);
+        tma_tile(pmap, tile, (s2 & ~kStart) * (kWTile / 32), bar_s + 8u * buf);
         load_meta(s2 & ~kStart, tm2, r_end2);
       }
       nx = s1;

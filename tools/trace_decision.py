@@ -1,4 +1,5 @@
 """Internal timeline of one config-3 decision from %globaltimer stamps (andes_debug_trace).
+Tile / first-tile stamps need a -DANDES_SCAN_PHASES build (ANDES_LIB_PATH).
 Slots: 7000+2b prep CTA b start/end; 5000+2b scan CTA b start/end; 2300 bounds end (scan CTA 0);
 3000+2b state CTA b; 2200/2201 state last block; 0+2b select CTA b; 2100.. finalize phases."""
 import ctypes as C
@@ -61,6 +62,8 @@ print("finalize phases", [us(tr[s]) for s in range(2100, 2106) if tr[s]])
 
 tl = tr[16384:16384 + 2 * 16384].reshape(-1, 2)
 ok = tl[:, 0] > 0
+if not ok.any():  # tile stamps only in a -DANDES_SCAN_PHASES build (tools/build_variant.py)
+    sys.exit(0)
 ids = np.where(ok)[0]
 dur = (tl[ok, 1] - tl[ok, 0]) / 1e3
 print("tiles traced", ok.sum(), "body us median/p90/p99/max", np.percentile(dur, [50, 90, 99, 100]).round(2))
