@@ -694,7 +694,8 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
 // included), in tile-local coordinates.
 // A dense tile is processed in batches of up to 31 requests (first_batch / last_batch): the
 // running prefix seeds the next batch (mode 1); only a single-batch tile publishes its aggregate
-// early, and only the last batch publishes the tile's prefix.  Modes 0 and 1 only: a tile that
+// early, and only the last batch publishes the tile's prefix (both only when pub: a look-back
+// can reach this tile).  Modes 0 and 1 only: a tile that
 // looks back (mode 2) takes the row path.
 // Sub-range length SR(np) of the aligned path for np pieces in a tile: sum ceil(len/SR) <=
 // kWTile/SR + np <= 32, and SR is an odd number of 16-byte chunks (the sub-ranges of one piece
@@ -719,7 +720,7 @@ static_assert(make_subrange_tab().sr[31] <= 2 * kWTile && make_subrange_tab().sr
 template <bool kFinal>
 __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
                                                   uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
-                                                  bool first_batch, bool last_batch) {
+                                                  bool first_batch, bool last_batch, bool pub) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
   const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
@@ -808,12 +809,12 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const unsigned long long tile_agg = __shfl_sync(0xffffffffu, sc, 31);
   // ---- the tile's carry-in (direct read or decoupled look-back), as in warp_tile; the aggregate
   // is published first so that successors looking back never wait on this tile's second pass
-  if (first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
+  if (pub && first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
   unsigned long long acc = 0ull;
   // (a tile that looks back (mode 2) takes the row path: this one sees modes 0 and 1 only)
   if (mode == 1u) acc = kFlagBit | cdirect;
   prefix = seg_combine(acc, tile_agg);
-  if (last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
+  if (pub && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
@@ -1079,7 +1080,10 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
         ScanRec rb = rec;
         if (b && lane < nb_req) rb = w.srec[r0 + 31u * b + lane];
         const Entry e = lane < nb_req ? entry_of(rb, r0 + 31u * b + lane, p0) : null_entry(true);
-        warp_tile_aligned<kFinal>(A, e, tile, tcur, mb, cb, pref, b == 0, b + 1 == nbatch);
+        // the status words are read only by look-backs, i.e. from inside a request longer than
+        // kCarryDirect: publish when the request crossing the tile's end (the last one) is such
+        const bool pub = __shfl_sync(0xffffffffu, rb.lim, nb_req - 1u) > (uint32_t)kCarryDirect;
+        warp_tile_aligned<kFinal>(A, e, tile, tcur, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
         mb = 1u;
         cb = (uint32_t)pref;
       }
