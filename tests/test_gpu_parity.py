@@ -105,6 +105,20 @@ def test_qoe_long_lookback(A, orc, lb_ns, monkeypatch):
             _check_qoe(A, c2, orc, snap, snap.now_us // 2, final)
 
 
+@pytest.mark.parametrize("lb_ns", ["20000", "0"])
+def test_schedule_long_requests(A, orc, lb_ns, monkeypatch):
+    # decisions over long-output requests (the scan's look-back and its direct fallback feed
+    # Q_wait and the gains): B = 1..16, M tight enough that Algorithm 1 stops early
+    import dataclasses
+    monkeypatch.setenv("ANDES_LOOKBACK_NS", lb_ns)
+    c2 = A.Context(max_requests=1024, max_B=16, max_tokens=1 << 22)
+    for seed, align in ((11, 4), (12, 1)):
+        snap = W.long_requests(seed, n=40, lo=5_000, hi=12_000, align=align)
+        snap = dataclasses.replace(snap, tau_us=W.tau_table(B_cap=16), kv_capacity=20_000,
+                                   now_us=snap.now_us // 2, preempt_cap=3)
+        _check_sched(A, c2, orc, snap)
+
+
 def test_qoe_config3_full(A, ctx, orc):
     snap = W.config3()
     # the oracle is fast enough for QoE (one walk per request)
