@@ -782,16 +782,22 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const uint32_t dz = nslots ? a - (Is + (nslots - 1u) * P) : 0u;
   // a request starts in this sub-range; idle lanes (after every sub-range) are the identity
   const bool flag = active && k == 0 && qls >= 0;
-  const unsigned long long agg = (flag ? kFlagBit : 0ull) | dz;
-  unsigned long long sc = agg;
+  // warp segmented max-scan on 32-bit values, the segment flags in a ballot: lane i's inclusive
+  // value is the max over lanes [s_i, i], s_i the last flagged lane <= i (0 if none)
+  const uint32_t F = __ballot_sync(0xffffffffu, flag);
+  const uint32_t fb = F & (0xFFFFFFFFu >> (31u - lane));  // flags of lanes 0..lane
+  const int32_t sgs = fb ? 31 - __clz(fb) : -1;
+  uint32_t sv = dz;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, sc, o);
-    if (lane >= (uint32_t)o) sc = seg_combine(v, sc);
+    const uint32_t u = __shfl_up_sync(0xffffffffu, sv, o);
+    if ((int32_t)lane - o >= sgs) sv = max(sv, u);
   }
-  unsigned long long excl = __shfl_up_sync(0xffffffffu, sc, 1);
-  if (lane == 0) excl = 0ull;
-  const unsigned long long tile_agg = __shfl_sync(0xffffffffu, sc, 31);
+  uint32_t excl_v = __shfl_up_sync(0xffffffffu, sv, 1);
+  if (lane == 0) excl_v = 0u;
+  const bool excl_flag = (F & ((1u << lane) - 1u)) != 0u;  // a segment starts in lanes 0..lane-1
+  const unsigned long long tile_agg =
+      (F ? kFlagBit : 0ull) | (unsigned long long)__shfl_sync(0xffffffffu, sv, 31);
   // ---- the tile's carry-in (direct read or decoupled look-back), as in warp_tile; the aggregate
   // is published first so that successors looking back never wait on this tile's second pass
   if (pub && first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
@@ -800,7 +806,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   if (mode == 1u) acc = kFlagBit | cdirect;
   prefix = seg_combine(acc, tile_agg);
   if (pub && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
-  const uint32_t carry = flag ? 0u : (uint32_t)seg_combine(acc, excl);
+  const uint32_t carry = flag ? 0u : excl_flag ? excl_v : max((uint32_t)acc, excl_v);
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
   unsigned long long sumT = 0ull;
