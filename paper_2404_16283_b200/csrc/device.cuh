@@ -104,7 +104,7 @@ struct Globals {
   uint32_t n_run_global;         // running requests over all ranks
   uint32_t shard_Bstar;          // B* (step 3 -> step 4)
   uint32_t unal;                 // prep: some timeline does not start on a 16-byte boundary
-  uint32_t pad_;
+  uint32_t sel_ready;            // k_select, B-independent keys: B_hi's sorted list is published
   unsigned long long qmin_bits;  // max-min objective: ~(fp64 bits of min_i Q_now,i) (Q >= 0: the bit
                                  // patterns are ordered; inverted so that the zeroed word is "none")
   uint32_t rf_npairs;            // refiner: feasible admit/victim pairs

@@ -204,6 +204,15 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, con
   if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x + 1);
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ---------------------------------------------------------------- S4: Algorithm 1 per B
 struct SelectArgs {
   ReqView r;
@@ -679,16 +688,54 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     const uint32_t k = A.xsend ? min(B, ovf ? n : ns) : min(B, n);
     uint32_t cnt;
     if (ovf) {
-      // overflow fallback: exact keys of every request at B (row B of keyrow), radix select
-      uint32_t* keys = w.keyrow + (size_t)(B - 1) * w.N_cap;
-      for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB, w.lqsf, w.obj);
+      // overflow fallback: exact keys of every request at B (row B of keyrow), radix select.
+      // Max-min keys do not depend on B (reading R22): k_state's upper bound is the exact key,
+      // so every CTA selects from it directly (4 B per request instead of the 80-byte states).
+      const bool bind = w.obj == kObjMaxMin;
+      uint32_t* keys = bind ? w.ub : w.keyrow + (size_t)(B - 1) * w.N_cap;
+      if (!bind)
+        for (uint32_t i = tid; i < n; i += kSelThreads) keys[i] = okey_of(w.st[i], tB, w.lqsf, w.obj);
       __syncthreads();
-      cnt = select_top_k(
-          n, k,
-          [&](uint32_t e, bool low) -> unsigned long long {
-            return low ? composite(keys[e], r.rank[e]) : ((unsigned long long)keys[e] << 32);
-          },
-          [&](uint32_t e) { return e; }, s_key, s_idx);
+      // B-independent keys: the order is the same for every B, so the CTA of B_hi selects once
+      // and publishes its sorted list (row B_hi of sel); the other CTAs take prefixes of it.  A
+      // CTA whose wait exceeds 200 us (the producer not yet resident: more CTAs than slots)
+      // selects for itself, so no wait can block forever.
+      uint32_t* const shared_list = w.sel + (size_t)(B_hi - 1) * kMaxB;
+      bool have = false;
+      if (bind && !A.xsend && B != B_hi) {
+        if (tid == 0) {
+          const unsigned long long t0 = gtimer();
+          uint32_t ready = 0;
+          while ((ready = ld_acquire_u32(&w.g->sel_ready)) == 0u && gtimer() - t0 < 200000ull) {
+          }
+          s_k = ready;
+        }
+        __syncthreads();
+        have = s_k != 0u;
+        if (have) {
+          for (uint32_t q = tid; q < k; q += kSelThreads) {
+            const uint32_t i = __ldcg(shared_list + q);
+            s_idx[q] = i;
+            s_key[q] = composite(keys[i], r.rank[i]);
+          }
+          __syncthreads();
+          cnt = k;
+        }
+      }
+      if (!have) {
+        cnt = select_top_k(
+            n, k,
+            [&](uint32_t e, bool low) -> unsigned long long {
+              return low ? composite(keys[e], r.rank[e]) : ((unsigned long long)keys[e] << 32);
+            },
+            [&](uint32_t e) { return e; }, s_key, s_idx);
+        if (bind && !A.xsend && B == B_hi) {
+          for (uint32_t q = tid; q < cnt; q += kSelThreads) shared_list[q] = s_idx[q];
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) st_release_u32(&w.g->sel_ready, 1u);
+        }
+      }
     } else {
       // exact keys of the survivors at B (S3 for this B), then their order by rank counting:
       // position = number of larger composites (unique); two composites per 16-byte load,

@@ -344,6 +344,10 @@ def test_schedule_survivor_overflow_fallback(A, ctx, orc):
                       tau_us=W.tau_table(48), kv_capacity=4000)
     gg, o = _check_sched(A, ctx, orc, snap, cap=5)
     assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
+    # the objectives' fallback (max-min selects from the B-independent key bounds directly)
+    for obj in (32, 64):
+        gg, o = _check_sched(A, ctx, orc, snap, flags=1 | obj, cap=5)
+        assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
 
 
 # ---------------------------------------------------------------- config-5 sweep: scenario means
