@@ -260,7 +260,8 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.tile_status, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess || (e = ctx_alloc(c, &w.hist_lb, kHistK)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess || (e = ctx_alloc(c, &w.zr, N)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.hist_zr, kHistK)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.srec, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &c->zero_rows, 32)) != cudaSuccess ||
@@ -286,6 +287,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   cudaMemset(c->zero_rows, 0, 128);
   cudaMemset(w.hist_lb, 0, sizeof(uint32_t) * kHistK);
   cudaMemset(w.hist_ub, 0, sizeof(uint32_t) * kHistK);
+  cudaMemset(w.hist_zr, 0, sizeof(uint32_t) * kHistK);
   if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess) {
     int rc = cuda_check(c, e, "pinned alloc");
     andes_destroy(c);

@@ -108,7 +108,7 @@ struct Globals {
   unsigned long long qmin_bits;  // max-min objective: ~(fp64 bits of min_i Q_now,i) (Q >= 0: the bit
                                  // patterns are ordered; inverted so that the zeroed word is "none")
   uint32_t rf_npairs;            // refiner: feasible admit/victim pairs
-  uint32_t pad2_;
+  uint32_t max_rank;             // prep (decisions): max_i rank_i (the exact-zero rank histogram's scale)
 };
 
 static_assert(sizeof(Globals) == 128, "Globals: one 128-byte line, one warp snapshot");
@@ -176,6 +176,8 @@ struct Work {
   ScanRec* srec;             // [N] timeline-scan records
   PackedState* st;           // [N]
   uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
+  uint32_t* zr;              // [N] rank bucket of a request whose key is exactly 0 for every B, else ~0
+  uint32_t* hist_zr;         // [kHistK] histogram of zr (self-cleaning)
   uint32_t* cand_idx;        // [S_cap] request index of candidate slot
   uint32_t* keyrow;          // [max_B][N] fallback: ordered keys of every request per B
   uint32_t* sel;             // [max_B][kMaxB] Algorithm 1 prefix per B, greedy order

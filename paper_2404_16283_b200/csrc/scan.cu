@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
                                                       uint32_t sched, uint64_t kv_cap, uint32_t debug,
                                                       uint8_t* __restrict__ serve_mask) {
   __shared__ uint32_t s_hl[kHistL];
-  __shared__ uint32_t s_minP;
+  __shared__ uint32_t s_minP, s_maxR;
   __shared__ unsigned long long s_runl;
   const uint32_t n = r.n;
   uint32_t local_err = 0, local_unal = 0;
@@ -182,11 +182,12 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
     if (threadIdx.x == 0) {
       s_minP = 0xFFFFFFFFu;
+      s_maxR = 0u;
       s_runl = 0;
     }
     __syncthreads();
   }
-  uint32_t my_minP = 0xFFFFFFFFu;
+  uint32_t my_minP = 0xFFFFFFFFu, my_maxR = 0u;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t g = r.n_deliv[i];
     const uint32_t P = r.period[i];
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     if (sched) {
       const uint32_t l = r.ctx_len[i];
       my_minP = min(my_minP, P);
+      my_maxR = max(my_maxR, r.rank[i]);
       serve_mask[i] = r.running[i] ? 1 : 0;  // status quo; the decision edits only the changes
       atomicAdd(&s_hl[l < kHistL - 1 ? l : kHistL - 1], 1u);
       if (r.running[i]) {
@@ -275,13 +277,20 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   if (local_err) atomicOr(&w.g->err, local_err);
   if (__any_sync(0xffffffffu, local_unal) && (threadIdx.x & 31) == 0) atomicOr(&w.g->unal, 1u);
   if (!sched) return;
-  for (int o = 16; o; o >>= 1) my_minP = min(my_minP, __shfl_xor_sync(0xffffffffu, my_minP, o));
-  if ((threadIdx.x & 31) == 0) atomicMin(&s_minP, my_minP);
+  for (int o = 16; o; o >>= 1) {
+    my_minP = min(my_minP, __shfl_xor_sync(0xffffffffu, my_minP, o));
+    my_maxR = max(my_maxR, __shfl_xor_sync(0xffffffffu, my_maxR, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&s_minP, my_minP);
+    atomicMax(&s_maxR, my_maxR);
+  }
   __syncthreads();
   for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x)
     if (s_hl[q]) atomicAdd(&w.hist_l[q], s_hl[q]);
   if (threadIdx.x == 0) {
     atomicMax(&w.g->inv_minP, 0xFFFFFFFFu - s_minP);
+    if (s_maxR) atomicMax(&w.g->max_rank, s_maxR);
     if (s_runl) atomicAdd(&w.g->run_l, s_runl);
   }
   if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x + 1);

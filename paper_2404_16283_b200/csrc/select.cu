@@ -45,6 +45,13 @@ __global__ void k_gain_estimate(ReqView r, Work w, int64_t now, uint32_t horizon
 constexpr int kStateThreads = 256;
 constexpr int kCandThreads = 256;
 
+// ordered key of a zero priority, and the shift that maps ranks to the 4096 buckets of hist_zr
+constexpr uint32_t kOKey0 = 0x80000000u;  // ordered_key(+0.0f)
+__device__ __forceinline__ uint32_t zr_shift(uint32_t max_rank) {
+  const uint32_t bits = 32u - __clz(max_rank | 1u);
+  return bits > 12u ? bits - 12u : 0u;
+}
+
 __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
   __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
   __shared__ Globals s_g;
@@ -55,6 +62,7 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
   const uint32_t tlo = s_g.tau_lo, thi = s_g.tau_hi;
+  const uint32_t zs = zr_shift(s_g.max_rank);
   for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
     s_hlb[q] = 0u;
     s_hub[q] = 0u;
@@ -91,6 +99,12 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
       lb = ordered_key(prio_key(__dsub_rn(q_lb, s.qw), p.l, w.lqsf));
     }
     w.ub[i] = ub;
+    // a key exactly 0 at every B of the range (reading R10: ties by rank): only the B_hi smallest
+    // ranks of these can ever be selected, so k_compact may prune the rest (rank histogram)
+    const bool zero = lb == kOKey0 && ub == kOKey0;
+    const uint32_t zb = zero ? p.rank >> zs : 0xFFFFFFFFu;
+    w.zr[i] = zb;
+    if (zero) atomicAdd(&w.hist_zr[zb], 1u);
     atomicAdd(&s_hlb[lb >> 20], 1u);
     atomicAdd(&s_hub[ub >> 20], 1u);
   }
@@ -170,6 +184,51 @@ __device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, 
   for (uint32_t k = 0; k < NT / 32; ++k) nsurv += s_sv[k];
 }
 
+// The exact-zero rank cut: the smallest bucket z* with #(exact zeros in buckets <= z*) >= need
+// (every exact zero beyond it is pruned; non-zeros carry zr = ~0 and are never pruned), and
+// the survivor count reduced by the pruned ones.  Computed redundantly by every CTA.
+__device__ __forceinline__ void zero_rank_cut(const Work& w, uint32_t need, uint32_t& zcut, uint32_t& nsurv) {
+  constexpr uint32_t NT = kCandThreads, kPer = kHistK / NT;  // 16 buckets per thread, ascending
+  __shared__ uint32_t s_w[NT / 32], s_zc, s_kept;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t h[kPer], cnt = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < kPer; ++q) {
+    h[q] = __ldcg(w.hist_zr + tid * kPer + q);
+    cnt += h[q];
+  }
+  uint32_t inc = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += v;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  if (tid == 0) s_zc = 0xFFFFFFFFu;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+  for (uint32_t k = 0; k < NT / 32; ++k) {
+    if (k < wid) wpre += s_w[k];
+    tot += s_w[k];
+  }
+  const uint32_t ex = wpre + inc - cnt;
+  if (ex < need && ex + cnt >= need) {
+    uint32_t c2 = ex;
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      c2 += h[q];
+      if (c2 >= need) {
+        s_zc = tid * kPer + q;
+        s_kept = c2;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  zcut = s_zc;
+  if (zcut != 0xFFFFFFFFu) nsurv -= tot - s_kept;
+  __syncthreads();
+}
+
 // Compaction of the survivors (UB >= theta) into cand_idx, warp-aggregated appends.
 __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, const uint32_t* lb_src, uint32_t G) {
   pdl_wait();
@@ -182,6 +241,10 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, con
   theta_of(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, s_g.B_hi, cut, ns);
   if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
   const uint32_t theta = cut << 20;
+  // exact zeros beyond the B_hi smallest ranks never make any top-B (single GPU only: the
+  // multi-GPU path has no global rank histogram)
+  uint32_t zcut = 0xFFFFFFFFu;
+  if (!lb_src && theta <= kOKey0) zero_rank_cut(w, s_g.B_hi, zcut, ns);
   const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     w.g->theta = theta;
@@ -193,7 +256,7 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, con
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < r.n; i0 += gridDim.x * blockDim.x) {
     const uint32_t i = i0 + threadIdx.x;
-    const bool surv = (i < r.n) && (w.ub[i] >= theta);
+    const bool surv = (i < r.n) && (w.ub[i] >= theta) && (zcut == 0xFFFFFFFFu || w.zr[i] == 0xFFFFFFFFu || w.zr[i] <= zcut);
     const uint32_t bal = __ballot_sync(0xffffffffu, surv);
     if (!bal) continue;
     uint32_t base = 0;
@@ -662,6 +725,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   for (uint32_t q = blockIdx.x * blockDim.x + tid; q < kHistK; q += gridDim.x * blockDim.x) {
     w.hist_lb[q] = 0u;
     w.hist_ub[q] = 0u;
+    w.hist_zr[q] = 0u;
   }
   snap_globals(w.g, &s_g);
   const bool trig = s_g.triggered != 0;

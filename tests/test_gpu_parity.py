@@ -344,10 +344,40 @@ def test_schedule_survivor_overflow_fallback(A, ctx, orc):
                       tau_us=W.tau_table(48), kv_capacity=4000)
     gg, o = _check_sched(A, ctx, orc, snap, cap=5)
     assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
-    # the objectives' fallback (max-min selects from the B-independent key bounds directly)
-    for obj in (32, 64):
-        gg, o = _check_sched(A, ctx, orc, snap, flags=1 | obj, cap=5)
-        assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
+    # max-min: every request has the same non-zero key (Q_min - Q_wait > 0, equal l): the
+    # fallback, with one sorted list shared by all B; perfect count: every gain is exactly 0,
+    # so the exact-zero rank cut keeps the pruned path
+    gg, o = _check_sched(A, ctx, orc, snap, flags=1 | 32, cap=5)
+    assert int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
+    gg, o = _check_sched(A, ctx, orc, snap, flags=1 | 64, cap=5)
+    assert not int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH
+
+
+def test_schedule_exact_zero_rank_pruning(A, ctx, orc):
+    """Most requests are ahead of schedule (no undelivered due token: gain exactly 0 at every B),
+    so the key bucket holding theta is the zero bucket; k_compact keeps only the B_hi smallest
+    ranks of the exact zeros (the survivors then fit: no slow path), and the decision, the
+    zero-gain requests it takes included (Algorithm 1 takes gain-0 requests while they fit),
+    must equal the oracle's."""
+    n, nz = 5000, 4880
+    rng = np.random.default_rng(5)
+    tl = []
+    for i in range(n):
+        if i < nz:  # 60 tokens delivered right after ttft: far ahead of the 208 ms schedule
+            tl.append((1_000_000 + np.arange(60, dtype=np.uint32) * 1_000).astype(np.uint32))
+        else:  # behind: 6 tokens, late
+            tl.append((np.arange(6, dtype=np.uint32) * 250_000 + 1_400_000 + rng.integers(0, 90_000)).astype(np.uint32))
+    g, base, pool = W._pack(tl)
+    perm = rng.permutation(n)
+    snap = W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, 1_000_000, np.uint32),
+                      period_us=np.full(n, 208_333, np.uint32), ctx_len=rng.integers(50, 400, n).astype(np.uint32),
+                      n_deliv=g, max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=perm.astype(np.uint32), running=(rng.random(n) < 0.01).astype(np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=3_000_000, horizon_us=2_000_000,
+                      tau_us=W.tau_table(200), kv_capacity=30_000)
+    for flags in (1, 1 | 16, 1 | 32):
+        gg, o = _check_sched(A, ctx, orc, snap, flags=flags, cap=4)
+        assert not (int(gg["sc"][6]) & A.ANDES_F_SLOW_PATH), flags
 
 
 # ---------------------------------------------------------------- config-5 sweep: scenario means
