@@ -262,7 +262,9 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess || (e = ctx_alloc(c, &w.zr, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_zr, kHistK)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.cand_idx, w.S_cap)) != cudaSuccess || (e = ctx_alloc(c, &w.cand_st, w.S_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.run_st, kMaxRunning)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.run_idx, kMaxRunning)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.run_list, kMaxRunning)) != cudaSuccess || (e = ctx_alloc(c, &w.srec, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &c->zero_rows, 32)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.keyrow, (size_t)lim->max_B * N)) != cudaSuccess ||

@@ -92,7 +92,7 @@ struct Globals {
   uint32_t slow;                 // slow-path flags
   uint32_t tile_ctr;             // dynamic tile counter of the timeline scan
   uint32_t prep_done;            // prep CTAs finished (last-block pattern)
-  uint32_t state_done;           // state CTAs finished
+  uint32_t run_ctr;              // k_state: running requests appended to run_st / run_idx
   uint32_t tau_lo, tau_hi;       // min / max tau(B) over the candidate range
   uint32_t theta;                // ordered-key threshold: >= B_hi requests have LB >= theta
   uint32_t n_surv;               // requests with UB >= theta (candidates)
@@ -178,7 +178,10 @@ struct Work {
   uint32_t* ub;              // [N] ordered upper-bound key over the candidate B range
   uint32_t* zr;              // [N] rank bucket of a request whose key is exactly 0 for every B, else ~0
   uint32_t* hist_zr;         // [kHistK] histogram of zr (self-cleaning)
-  uint32_t* cand_idx;        // [S_cap] request index of candidate slot
+  uint32_t* cand_idx;        // [S_cap] request index of candidate slot (bit 31: running)
+  PackedState* cand_st;      // [S_cap] the survivors' states, contiguous (one load in k_select)
+  PackedState* run_st;       // [kMaxRunning] the running requests' states (k_state, any order)
+  uint32_t* run_idx;         // [kMaxRunning] their request indices
   uint32_t* keyrow;          // [max_B][N] fallback: ordered keys of every request per B
   uint32_t* sel;             // [max_B][kMaxB] Algorithm 1 prefix per B, greedy order
   unsigned long long* sel_thr;  // [max_B] composite of the k*-th selected request per B

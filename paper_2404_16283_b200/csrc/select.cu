@@ -82,6 +82,13 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
       p.qx = w.qnow[i];
     }
     w.st[i] = p;
+    if (r.running[i]) {  // a contiguous copy for k_select's cap staging (order irrelevant)
+      const uint32_t slot = atomicAdd(&w.g->run_ctr, 1u);
+      if (slot < (uint32_t)kMaxRunning) {
+        w.run_st[slot] = p;
+        w.run_idx[slot] = i;
+      }
+    }
     uint32_t lb, ub;
     if (w.obj != kObjAndes) {
       // max-min: one gain for every B; perfect count: 1(Q_serve = 1) is nonincreasing in tau
@@ -262,7 +269,11 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, con
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(&w.g->cand_ctr, (uint32_t)__popc(bal));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (surv) w.cand_idx[base + __popc(bal & ((1u << lane) - 1u))] = i;
+    if (surv) {
+      const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+      w.cand_idx[slot] = i | (r.running[i] ? 0x80000000u : 0u);
+      w.cand_st[slot] = w.st[i];
+    }
   }
   if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x + 1);
 }
@@ -712,6 +723,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   __shared__ uint32_t s_k, s_last;
   __shared__ long long s_red[32];
   __shared__ Globals s_g;
+  __shared__ uint8_t s_run8[kSortCap];  // running flag of the ordered survivors (pruned path)
 
   const ReqView& r = A.r;
   const Work& w = A.w;
@@ -810,15 +822,16 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       long long* s_gall = reinterpret_cast<long long*>(s_vc);
       // indices first (one coalesced round trip), then the states: each iteration of the second
       // loop is independent, so its loads overlap instead of chaining behind the index load
+      // survivors and running requests from their contiguous copies (k_compact / k_state): one
+      // round trip, no index-then-state chain
       const uint32_t nr = rpre ? n_run : 0u;
-      for (uint32_t e = tid; e < ns; e += kSelThreads) s_ri[e] = __ldcg(w.cand_idx + e);
-      for (uint32_t q = tid; q < nr; q += kSelThreads) s_rx[q] = __ldcg(w.run_list + q);
-      __syncthreads();
 #pragma unroll 2
       for (uint32_t e = tid; e < ns + nr; e += kSelThreads) {
         const bool sv = e < ns;
-        const uint32_t i = sv ? s_ri[e] : s_rx[e - ns];
-        const PackedState p = w.st[i];
+        const uint32_t iv = sv ? __ldcg(w.cand_idx + e) : __ldcg(w.run_idx + (e - ns));
+        const PackedState p = *(sv ? w.cand_st + e : w.run_st + (e - ns));
+        if (sv) s_ri[e] = iv;
+        else s_rx[e - ns] = iv;
         const double gn = gain_of(p, tB, w.obj);
         const unsigned long long c = composite(ordered_key(prio_key(gn, p.l, w.lqsf)), p.rank);
         if (sv) {
@@ -845,7 +858,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
         }
         if (pos < k) {
           s_key[pos] = c;
-          s_idx[pos] = s_ri[e];
+          s_idx[pos] = s_ri[e] & 0x7FFFFFFFu;
+          s_run8[pos] = (uint8_t)(s_ri[e] >> 31);
           s_gf[pos] = s_gall[e];
         }
       }
@@ -907,7 +921,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       const uint32_t i = s_idx[q];
       v += ovf ? gain_fixed(gain_of(w.st[i], tB, w.obj)) : s_gf[q];
       w.sel[(size_t)(B - 1) * kMaxB + q] = i;
-      s_ps[q] = r.running[i] ? 0ull : 1ull;  // stage_cap's admit flags (s_ps is free after the walk)
+      // stage_cap's admit flags (s_ps is free after the walk)
+      s_ps[q] = (ovf ? r.running[i] != 0 : s_run8[q] != 0) ? 0ull : 1ull;
     }
     v = block_sum_ll<kSelThreads>(v, s_red);
     const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
