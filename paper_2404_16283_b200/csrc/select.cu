@@ -545,7 +545,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
         if (kstar == 0 || c < thr) {
           const uint32_t slot = atomicAdd(&s_nv, 1u);
           vkey[slot] = ~c;
-          vidx[slot] = rx[tid];
+          vidx[slot] = tid;  // the running slot: index rx[], length rlen[] (shared memory)
         }
       }
     } else {
@@ -595,7 +595,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
     realized = kstar;
   } else {
     flags |= 2u;
-    for (uint32_t q = tid; q < nv; q += kSelThreads) vcum[q] = r.ctx_len[vidx[q]];
+    for (uint32_t q = tid; q < nv; q += kSelThreads) vcum[q] = rpre ? rlen[vidx[q]] : r.ctx_len[vidx[q]];
     __syncthreads();
     block_inclusive_scan(vcum, nv, s_tmp);
     const unsigned long long W0a = s_W0;
@@ -627,7 +627,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
   }
   uint32_t* pre = w.stage_pre + (size_t)(B - 1) * kStageRun;
   uint32_t* adm = w.stage_adm + (size_t)(B - 1) * kMaxB;
-  for (uint32_t q = tid; q < n_pre; q += kSelThreads) pre[q] = vidx[q];
+  for (uint32_t q = tid; q < n_pre; q += kSelThreads) pre[q] = rpre ? rx[vidx[q]] : vidx[q];
   for (uint32_t q = tid; q < n_adm; q += kSelThreads) adm[q] = aflag[q];
   if (tid == 0) w.stage_sc[B - 1] = make_uint4(n_pre, n_adm, realized, flags);
 }
