@@ -442,17 +442,18 @@ struct Entry {
 };
 static_assert(sizeof(Entry) == 32, "Entry is two 16-byte shared-memory vectors");
 
+template <int kT = kWTile>
 __device__ __forceinline__ Entry entry_of(const ScanRec& s, uint32_t ri, unsigned long long p0) {
   Entry e;
   const long long ls = (long long)s.base - (long long)p0;
   const long long ve = ls + (long long)s.lim;
-  e.ls = (int32_t)max(-1ll, min(ls, (long long)kWTile + 1));
-  e.vend = (int32_t)max(-1ll, min(ve, (long long)kWTile));
+  e.ls = (int32_t)max(-1ll, min(ls, (long long)kT + 1));
+  e.vend = (int32_t)max(-1ll, min(ve, (long long)kT));
   e.A = s.ttft + (uint32_t)(unsigned long long)(-ls) * s.P;
   e.trel = s.trel;
   e.pad = 0;
   e.P = s.P;
-  e.ek = (ve >= 1 && ve <= (long long)kWTile) ? s.ek : 0u;
+  e.ek = (ve >= 1 && ve <= (long long)kT) ? s.ek : 0u;
   e.ridx = ri;
   return e;
 }
@@ -698,31 +699,34 @@ __device__ __forceinline__ unsigned long long warp_tile(const ScanArgs& A, const
 struct SubRangeTab {
   uint32_t sr[33], mg[33];
 };
-constexpr SubRangeTab make_subrange_tab() {
+constexpr SubRangeTab make_subrange_tab(uint32_t tokens = kWTile) {
   SubRangeTab t{};
   for (uint32_t np = 0; np <= 32; ++np) {
     const uint32_t d = np < 32 ? 32u - np : 1u;
-    const uint32_t sr = 4u * (((kWTile / 4u + d - 1u) / d) | 1u);
+    const uint32_t sr = 4u * (((tokens / 4u + d - 1u) / d) | 1u);
     t.sr[np] = sr;
     t.mg[np] = (uint32_t)((0x100000000ull + sr - 1u) / sr);
   }
   return t;
 }
 __constant__ SubRangeTab kSubRange = make_subrange_tab();
+__constant__ SubRangeTab kSubRange2 = make_subrange_tab(2 * kWTile);  // two-tile units
+static_assert(make_subrange_tab(2 * kWTile).sr[31] <= 4 * kWTile, "SR table (2 tiles)");
 static_assert(make_subrange_tab().sr[31] <= 2 * kWTile && make_subrange_tab().sr[0] == 4u * 9u, "SR table");
 
-template <bool kFinal>
+template <bool kFinal, int TW = 1>
 __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
                                                   uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
                                                   bool first_batch, bool last_batch, bool pub) {
   const Work& w = A.w;
   const uint32_t lane = threadIdx.x & 31;
-  const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, (int32_t)kWTile));
+  constexpr int32_t kT = TW * kWTile;  // tokens of the unit (TW warp-tiles)
+  const int32_t ps = max(e.ls, 0), pe = max(ps, min(e.vend, kT));
   const uint32_t len = (uint32_t)(pe - ps);
   const uint32_t np = __popc(__ballot_sync(0xffffffffu, len != 0u));
   // sub-range length from the table (no division on the hot path): <= 32 sub-ranges in total
-  const uint32_t SR = kSubRange.sr[np];
-  const uint32_t cnt = __umulhi(len + SR - 1u, kSubRange.mg[np]);  // ceil(len / SR), exact
+  const uint32_t SR = TW == 1 ? kSubRange.sr[np] : kSubRange2.sr[np];
+  const uint32_t cnt = __umulhi(len + SR - 1u, TW == 1 ? kSubRange.mg[np] : kSubRange2.mg[np]);  // ceil(len / SR)
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -749,7 +753,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const uint32_t lsek = __shfl_sync(0xffffffffu, ((uint32_t)(e.ls + 1) << 2) | e.ek, q);
   const int32_t qls = (int32_t)(lsek >> 2) - 1;
   const uint32_t qek = lsek & 3u;
-  const int32_t q_ps = max(qls, 0), q_pe = max(q_ps, min(qvend, (int32_t)kWTile));
+  const int32_t q_ps = max(qls, 0), q_pe = max(q_ps, min(qvend, kT));
   const uint32_t k = u - q_off;
   const int32_t xs = active ? q_ps + (int32_t)(SR * k) : 0;
   const int32_t xe = active ? min(xs + (int32_t)SR, q_pe) : 0;
@@ -809,12 +813,14 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
       (F ? kFlagBit : 0ull) | (unsigned long long)__shfl_sync(0xffffffffu, sv, 31);
   // ---- the tile's carry-in (direct read or decoupled look-back), as in warp_tile; the aggregate
   // is published first so that successors looking back never wait on this tile's second pass
-  if (pub && first_batch && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStAgg | tile_agg);
+  // (a unit of TW tiles publishes into each of its tiles' words: a look-back combines with max,
+  // so seeing the same unit twice is harmless)
+  if (pub && first_batch && last_batch && lane < (uint32_t)TW) st_relaxed(&w.tile_status[t + lane], kStAgg | tile_agg);
   unsigned long long acc = 0ull;
   // (a tile that looks back (mode 2) takes the row path: this one sees modes 0 and 1 only)
   if (mode == 1u) acc = kFlagBit | cdirect;
   prefix = seg_combine(acc, tile_agg);
-  if (pub && last_batch && lane == 0) st_relaxed(&w.tile_status[t], kStPrefix | prefix);
+  if (pub && last_batch && lane < (uint32_t)TW) st_relaxed(&w.tile_status[t + lane], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : excl_flag ? excl_v : max((uint32_t)acc, excl_v);
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
@@ -866,7 +872,7 @@ __device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, u
 // reads the head segment's earlier tokens directly when it started <= kCarryDirect tokens
 // before the tile (else decoupled look-back on per-warp-tile status words), and scans with
 // warp shuffles only: no CTA-wide barriers on the hot path.
-template <bool kFinal>
+template <bool kFinal, int TW>
 __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap_swz,
                                                            const __grid_constant__ CUtensorMap tmap_plain) {
@@ -907,8 +913,11 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // look-back, whose waits are bounded (see lookback()).
   constexpr uint32_t kNone = 0xFFFFFFFFu, kStart = 0x80000000u;
   const uint32_t KW = gridDim.x * (kScanThreads / 32);
-  const uint32_t CH = min(8u, max(1u, ntiles / (8u * KW)));
-  const uint32_t nchunks = (ntiles + CH - 1) / CH;
+  // work unit: TW consecutive warp-tiles (TW = 2 for large pools: one 2048-token unit fills
+  // both tile buffers, which halves the per-unit set-up per token; no TMA prefetch then)
+  const uint32_t nunits = (ntiles + TW - 1) / TW;
+  const uint32_t CH = min(8u, max(1u, nunits / (8u * KW)));
+  const uint32_t nchunks = (nunits + CH - 1) / CH;
   // lane 0's generator state (position, chunk end, claimed chunk) lives in shared memory: it is
   // touched once per tile and would otherwise hold registers across the whole tile body
   __shared__ uint32_t s_gen[kScanThreads / 32][3];
@@ -930,7 +939,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     // timelines there (the densest tiles), which then do not form the tail
     const uint32_t t0 = (nchunks - 1u - g_nxt) * CH;
     gs[0] = t0;
-    gs[1] = min(t0 + CH, ntiles);
+    gs[1] = min(t0 + CH, nunits);
     gs[2] = static_next ? g_nxt + KS : atomicAdd(&w.g->tile_ctr, 1u) + 2u * KS;
     return t0 | kStart;
   };
@@ -947,11 +956,13 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
                      : (blockIdx.x - (A.sched ? 1u : 0u)) * (kScanThreads / 32) + wid;
     cur = gen(!cta0_dyn);
     if (cur != kNone) {
-      mbar_expect_tx_s(bar_s, kWTile * 4u);
-      tma_tile(pmap, wbase, (cur & ~kStart) * (kWTile / 32), bar_s);
+      mbar_expect_tx_s(bar_s, TW * kWTile * 4u);
+#pragma unroll
+      for (int h = 0; h < TW; ++h)
+        tma_tile(pmap, wbase + h * kWTile * 4, ((cur & ~kStart) * TW + h) * (kWTile / 32), bar_s);
     }
     s1 = gen(false);
-    if (s1 != kNone) {
+    if (TW == 1 && s1 != kNone) {
       mbar_expect_tx_s(bar_s + 8u, kWTile * 4u);
       tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), bar_s + 8u);
     }
@@ -970,13 +981,13 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   uint32_t r_end = 0;
   ScanRec rec;
   rec.lim = 0;
-  auto load_meta = [&](uint32_t tt, MetaLite& m, uint32_t& re) {
+  auto load_meta = [&](uint32_t tt, MetaLite& m, uint32_t& re) {  // tt: unit index
     if (lane == 0) {
-      const TileMeta* tmp = w.tile_meta + tt;
+      const TileMeta* tmp = w.tile_meta + tt * TW;
       m.r0 = tmp->r0;
       m.flags = tmp->flags;
       m.hcnt = tmp->hcnt;
-      re = (tt + 1 < ntiles) ? w.tile_meta[tt + 1].r0 : n - 1;
+      re = (tt * TW + TW < ntiles) ? w.tile_meta[tt * TW + TW].r0 : n - 1;
     }
   };
   auto load_rec = [&](uint32_t rr, ScanRec& sr) {
@@ -1001,7 +1012,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   while (cur != kNone) {
     const uint32_t tcur = cur & ~kStart;
     const bool chunk_start = (cur & kStart) != 0u;
-    const unsigned long long p0 = (unsigned long long)tcur * kWTile;
+    const unsigned long long p0 = (unsigned long long)tcur * (TW * kWTile);
     const uint32_t r0 = __shfl_sync(0xffffffffu, tm.r0, 0);
     const uint32_t flags = __shfl_sync(0xffffffffu, tm.flags, 0);
 #ifdef ANDES_SCAN_PHASES
@@ -1028,7 +1039,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     uint32_t cm = chunk_start ? 0u : (uint32_t)acc_reg;
     if (chunk_start && mode == 1u) {
       const uint32_t hcnt = __shfl_sync(0xffffffffu, tm.hcnt, 0);
-      const TileMeta* tmp = w.tile_meta + tcur;  // the head request's parameters (chunk starts only)
+      const TileMeta* tmp = w.tile_meta + tcur * TW;  // the head request's parameters (chunk starts only)
       const uint32_t httft = tmp->httft, hP = tmp->hP;
       const unsigned long long hbase = tmp->hbase;
       for (uint32_t k0 = 0; k0 < hcnt; k0 += 8 * 32) {  // 8 independent loads in flight per lane
@@ -1052,7 +1063,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     if (ph_on) w.trace[49152 + 4 * gw_ + 2] = gtimer();
 #endif
     if (buf == 0) { mbar_wait_s(bar_s, ph0); ph0 ^= 1u; }
-    else { mbar_wait_s(bar_s + 8u, ph1); ph1 ^= 1u; }
+    else { mbar_wait_s(bar_s + 8u, ph1); ph1 ^= 1u; }  // (TW = 1 only)
 #ifdef ANDES_SCAN_PHASES
     if (ph_on) w.trace[49152 + 4 * gw_ + 3] = gtimer();
     ++ph_it;
@@ -1060,7 +1071,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     if (nxt != kNone && !seq) load_rec(__shfl_sync(0xffffffffu, tm1.r0, 0), recn);
     const uint32_t tile = wbase + buf * (kWTile * 4);
     {
-      const unsigned long long pe = min(p0 + (unsigned long long)kWTile, pool_end);
+      const unsigned long long pe = min(p0 + (unsigned long long)(TW * kWTile), pool_end);
       if (pe > full_rows_end) {
         const unsigned long long lo = max(p0, full_rows_end);
         for (unsigned long long p = lo + lane; p < pe; p += 32)
@@ -1079,11 +1090,11 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
         const uint32_t nb_req = min(31u, nrec - 31u * b);
         ScanRec rb = rec;
         if (b && lane < nb_req) rb = w.srec[r0 + 31u * b + lane];
-        const Entry e = lane < nb_req ? entry_of(rb, r0 + 31u * b + lane, p0) : null_entry(true);
+        const Entry e = lane < nb_req ? entry_of<TW * kWTile>(rb, r0 + 31u * b + lane, p0) : null_entry(true);
         // the status words are read only by look-backs, i.e. from inside a request longer than
         // kCarryDirect: publish when the request crossing the tile's end (the last one) is such
         const bool pub = __shfl_sync(0xffffffffu, rb.lim, nb_req - 1u) > (uint32_t)kCarryDirect;
-        warp_tile_aligned<kFinal>(A, e, tile, tcur, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
+        warp_tile_aligned<kFinal, TW>(A, e, tile, tcur * TW, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
         mb = 1u;
         cb = (uint32_t)pref;
       }
@@ -1091,7 +1102,33 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     } else {
       // row-per-lane event path (unaligned pools, or a dense tile that must look back); the
       // window's records are read from global memory
-      acc_reg = warp_tile_global<kFinal>(A, tile, p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+      if (TW == 1) {
+        acc_reg = warp_tile_global<kFinal>(A, tile, p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+      } else {
+        // a unit's warp-tiles one by one, each with its own descriptor; the second continues
+        // from the first's carry (the in-chunk rule)
+        unsigned long long a = cm;
+#pragma unroll 1
+        for (uint32_t h = 0; h < (uint32_t)TW; ++h) {
+          const uint32_t t = tcur * TW + h;
+          if (t >= ntiles) break;
+          uint32_t r0h = r0, fh = flags, reh = 0;
+          if (lane == 0) {
+            if (h) {
+              r0h = w.tile_meta[t].r0;
+              fh = w.tile_meta[t].flags;
+            }
+            reh = (t + 1 < ntiles) ? w.tile_meta[t + 1].r0 : n - 1;
+          }
+          r0h = __shfl_sync(0xffffffffu, r0h, 0);
+          fh = __shfl_sync(0xffffffffu, fh, 0);
+          reh = __shfl_sync(0xffffffffu, reh, 0);
+          const uint32_t dh = fh & 1u;
+          a = warp_tile_global<kFinal>(A, tile + h * (kWTile * 4), p0 + h * kWTile, r0h, dh, reh - r0h + 1 + dh, t,
+                                       h ? 1u : mode, (uint32_t)a, swz_on);
+        }
+        acc_reg = a;
+      }
     }
     // refill this buffer with the tile two ahead in the warp's sequence
     __syncwarp();
@@ -1106,17 +1143,25 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     uint32_t r_end2 = 0;
     if (lane == 0) {
       const uint32_t s2 = gen(false);
-      if (s2 != kNone) {
+      if (TW == 1 && s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx_s(bar_s + 8u * buf, kWTile * 4u);
         tma_tile(pmap, tile, (s2 & ~kStart) * (kWTile / 32), bar_s + 8u * buf);
-        load_meta(s2 & ~kStart, tm2, r_end2);
       }
+      if (TW > 1 && s1 != kNone) {
+        // the unit already claimed (s1) now gets the buffers this one has released
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx_s(bar_s, TW * kWTile * 4u);
+#pragma unroll
+        for (int h = 0; h < TW; ++h)
+          tma_tile(pmap, wbase + h * kWTile * 4, ((s1 & ~kStart) * TW + h) * (kWTile / 32), bar_s);
+      }
+      if (s2 != kNone) load_meta(s2 & ~kStart, tm2, r_end2);
       nx = s1;
       s1 = s2;
     }
     cur = __shfl_sync(0xffffffffu, nx, 0);
-    buf ^= 1u;
+    if (TW == 1) buf ^= 1u;
     tm = tm1;
     r_end = r_end1;
     rec = recn;
@@ -1267,10 +1312,20 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
   if (r.n == 0 && !sched) return;
   ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags};
   const uint32_t grid = r.n ? L.scan_grid : 1u;
-  if (final_mode)
-    launch_pdl(k_qoe_scan<true>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
-  else
-    launch_pdl(k_qoe_scan<false>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
+  // two-tile units for large pools (>= 16 M tokens: enough units per warp for balance);
+  // ANDES_SCAN_TW=1|2 forces one (tests)
+  static const int tw_env = [] {
+    const char* v = getenv("ANDES_SCAN_TW");
+    return v ? atoi(v) : 0;
+  }();
+  const bool tw2 = tw_env ? tw_env == 2 : r.tl_len >= (1ull << 24);
+  if (final_mode) {
+    if (tw2) launch_pdl(k_qoe_scan<true, 2>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
+    else launch_pdl(k_qoe_scan<true, 1>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
+  } else {
+    if (tw2) launch_pdl(k_qoe_scan<false, 2>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
+    else launch_pdl(k_qoe_scan<false, 1>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
+  }
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
@@ -1281,15 +1336,17 @@ void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64
 }
 
 void init_scan_kernels() {
-  cudaFuncSetAttribute(k_qoe_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
-  cudaFuncSetAttribute(k_qoe_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
 }
 
 int scan_blocks_per_sm() {
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_qoe_scan<false>, kScanThreads, kScanDynSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_qoe_scan<false, 1>, kScanThreads, kScanDynSmem);
   int b2 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_qoe_scan<true>, kScanThreads, kScanDynSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_qoe_scan<true, 2>, kScanThreads, kScanDynSmem);
   return b < b2 ? b : b2;
 }
 

@@ -504,3 +504,42 @@ def test_knapsack_dp_bounds_the_greedy_on_a_snapshot(A, ctx, orc):
         torch.cuda.synchronize()
         exact = max(int(v) for v in Vb.cpu().numpy()[: B + 1] if v != -(1 << 63))
         assert exact >= int(g["V"][B - 1])
+
+
+# ---------------------------------------------------------------- two-tile scan units
+_TW2_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_2404_16283_b200 as A, workloads as W, oracle
+from test_gpu_parity import _check_qoe, _check_sched
+oracle.build()
+ctx = A.Context(max_requests=1 << 17, max_B=256, max_tokens=1 << 24, max_running=4096)
+for seed in range(16):
+    snap = W.random_small(seed, align=[4, 1][seed % 2], n=int(np.random.default_rng(seed).integers(1, 40)), max_tokens=300)
+    for final in (False, True):
+        _check_qoe(A, ctx, oracle, snap, snap.now_us + snap.horizon_us, final)
+for align in (4, 1):
+    snap = W.long_requests(5, align=align)
+    for final in (False, True):
+        _check_qoe(A, ctx, oracle, snap, snap.now_us, final)
+snap = W.config3()
+_check_qoe(A, ctx, oracle, snap, snap.now_us + snap.horizon_us, False)
+_check_sched(A, ctx, oracle, W.config2(), cap=16)
+print("tw2 ok")
+"""
+
+
+@pytest.mark.parametrize("tw", ["2", "1"])
+def test_scan_unit_width_forced(tw):
+    """The scan's work unit is two warp-tiles (2048 tokens) on large pools and one on small ones;
+    ANDES_SCAN_TW forces either, so both are checked against the oracle on the same inputs
+    (aligned and unaligned pools, long requests, config 3, a config-2 decision)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ANDES_SCAN_TW=tw)
+    r = subprocess.run([sys.executable, "-c", _TW2_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "tw2 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
