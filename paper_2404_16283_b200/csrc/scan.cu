@@ -825,13 +825,32 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   // ---- pass 2: consumption times from the carry, sums, edge
   uint32_t Ac = Is - P + carry;
   unsigned long long sumT = 0ull;
+#ifndef ANDES_NO_NOCLAMP
+  // consumption times are nondecreasing, so the clamp min(A, t) is void for the whole warp when
+  // every lane's last one, I_last + max(L_end, carry), is <= t (warp-uniform loop choice)
+  const uint32_t A_hi = Is + (uint32_t)max(xe - xs - 1, 0) * P + max(dz, carry);
+  const bool noclamp = kFinal || __all_sync(0xffffffffu, !active || A_hi <= tcl);
+  if (noclamp) {
 #pragma unroll 2
-  for (uint32_t gi = 0; gi < gmax; ++gi) {
-    if (gi < nfull) {
-      const uint4 v = ld_shared_v4(a0 + (gi << 4));
-      const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
-      Ac = A3;
-      sumT += (unsigned long long)min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+    for (uint32_t gi = 0; gi < gmax; ++gi) {
+      if (gi < nfull) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+        Ac = A3;
+        sumT += (unsigned long long)A0 + A1 + A2 + A3;
+      }
+    }
+  } else
+#endif
+  {
+#pragma unroll 2
+    for (uint32_t gi = 0; gi < gmax; ++gi) {
+      if (gi < nfull) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+        Ac = A3;
+        sumT += (unsigned long long)min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+      }
     }
   }
   uint32_t A_last = Ac;  // consumption time of the last valid token
