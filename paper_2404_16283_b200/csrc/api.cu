@@ -258,6 +258,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   if ((e = ctx_alloc(c, &w.m, N)) != cudaSuccess || (e = ctx_alloc(c, &w.spre, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.edge, N)) != cudaSuccess || (e = ctx_alloc(c, &w.tile_meta, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.tile_status, c->tiles_cap)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.tile_status_now, c->tiles_cap)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_l, kHistL)) != cudaSuccess || (e = ctx_alloc(c, &w.hist_lb, kHistK)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.hist_ub, kHistK)) != cudaSuccess || (e = ctx_alloc(c, &w.st, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.ub, N)) != cudaSuccess || (e = ctx_alloc(c, &w.zr, N)) != cudaSuccess ||
@@ -510,15 +511,18 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   // bounds (S3a), [3] candidate keys (S3b), [4] Algorithm 1 per B + best B + cap + mask (S4-S6)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
-  if (w.obj != kObjAndes && r.n) {
-    // Appendix-A objectives need every request's QoE now: a first scan at eval = now into the
-    // *_now arrays, then Q_now (and its minimum); the tile counter is reset for the main scan
+  // Appendix-A objectives need every request's QoE now: prep also writes the records of an
+  // evaluation at now (dual), a first scan fills the *_now arrays (its own look-back status
+  // words), then Q_now (and its minimum); the tile counter is reset for the main scan
+  const bool dual = w.obj != kObjAndes && r.n;
+  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask, p->now_us, dual);
+  if (dual) {
     Work wn = w;
     wn.m = w.m_now;
     wn.spre = w.spre_now;
     wn.edge = w.edge_now;
     wn.srec = w.srec_now;
-    launch_prep(L, r, wn, p->now_us, false, false, 0, false);
+    wn.tile_status = w.tile_status_now;
     const CUtensorMap* tmn = c->pool_map;
     if ((rc = pool_map(c, r.tl_pool, r.tl_len, &tmn))) return rc;
     launch_scan(L, r, wn, p->now_us, false, tmn);
@@ -526,7 +530,6 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
     cudaError_t e = cudaMemsetAsync(&c->w.g->tile_ctr, 0, sizeof(uint32_t), s);
     if (e != cudaSuccess) return cuda_check(c, e, "memset");
   }
-  launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
   mark(c, 1, s);
   {
     const CUtensorMap* tm = c->pool_map;

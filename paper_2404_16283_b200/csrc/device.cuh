@@ -169,6 +169,7 @@ struct Work {
   uint32_t* edge;            // [N] delta_g (g < m) or delta~_m (g >= m)
   TileMeta* tile_meta;       // [tiles] per-tile descriptor
   unsigned long long* tile_status;  // [tiles]
+  unsigned long long* tile_status_now;  // [tiles] look-back status of the objectives' scan at now
   uint32_t* hist_l;          // [kHistL] histogram of min(l, kHistL-1) (self-cleaning)
   uint32_t* hist_lb;         // [kHistK] histogram of lower-bound keys (self-cleaning)
   uint32_t* hist_ub;         // [kHistK] histogram of upper-bound keys (self-cleaning)

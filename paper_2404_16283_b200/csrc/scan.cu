@@ -167,9 +167,13 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
 // One pass over the requests: m_i, zeroed accumulators, scan records, tile owners, and for a
 // decision the trigger inputs (sum of running l, min period), the l histogram for B_max,
 // the running list and the status-quo serve mask (bounds_block then runs in the scan's CTA 0).
+// dual: also the records of a second in-flight evaluation at now_abs (the Appendix-A objectives'
+// Q_now) into m_now / spre_now / edge_now / srec_now and tile_status_now; the tile descriptors
+// serve both scans (a head whose tokens due at now end before a tile contributes nothing there).
 __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
                                                       uint32_t sched, uint64_t kv_cap, uint32_t debug,
-                                                      uint8_t* __restrict__ serve_mask) {
+                                                      uint8_t* __restrict__ serve_mask, int64_t now_abs,
+                                                      uint32_t dual) {
   __shared__ uint32_t s_hl[kHistL];
   __shared__ uint32_t s_minP, s_maxR;
   __shared__ unsigned long long s_runl;
@@ -211,6 +215,16 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
       sr.ek = (!final_mode && g < m) ? 1u : 2u;
       sr.pad = 0u;
       w.srec[i] = sr;
+      if (dual) {
+        const uint32_t mn = due_count(now_abs - r.arrival[i], sr.ttft, P ? P : 1u, r.max_total[i]);
+        w.m_now[i] = mn;
+        w.spre_now[i] = 0ull;
+        w.edge_now[i] = 0u;
+        sr.lim = min(g, mn);
+        sr.trel = (uint32_t)(now_abs - r.arrival[i]);
+        sr.ek = g < mn ? 1u : 2u;
+        w.srec_now[i] = sr;
+      }
     }
     // tile ownership: tiles whose start position p satisfies base_i <= p < base_{i+1}
     const unsigned long long base = r.tl_base[i];
@@ -244,6 +258,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
       tm.pad = 0;
       w.tile_meta[t] = tm;
       w.tile_status[t] = 0ull;  // look-back status of this call (read only by the scan, after prep)
+      if (dual) w.tile_status_now[t] = 0ull;
     }
     if (i + 1 == n) {
       unsigned long long pe = min(base + g, (unsigned long long)w.tiles_cap * kWTile);
@@ -1318,11 +1333,11 @@ void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, c
 }
 
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask) {
+                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask, int64_t now_abs, bool dual) {
   if (r.n == 0) return;
   const uint32_t blocks = umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8);
   launch_pdl(k_prep, blocks, kPrepThreads, 0, L.stream, r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u,
-             kv_cap, debug ? 1u : 0u, serve_mask);
+             kv_cap, debug ? 1u : 0u, serve_mask, now_abs, dual ? 1u : 0u);
 }
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
