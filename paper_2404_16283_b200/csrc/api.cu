@@ -242,6 +242,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   init_kernels();
   init_scan_kernels();
   init_shard_kernels();
+  init_refine_kernels();
   const int bps = scan_blocks_per_sm();
   c->scan_grid = (uint32_t)(sms * (bps > 0 ? bps : 1));
   const uint32_t N = lim->max_requests;

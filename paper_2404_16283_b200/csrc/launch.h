@@ -77,6 +77,7 @@ void launch_shard_merge(const LaunchCfg& L, const ReqView& r, const Work& w, con
 void launch_shard_cap(const LaunchCfg& L, const ReqView& r, const Work& w, const ShardVictims* recv, uint32_t G,
                       uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
 void init_shard_kernels();
+void init_refine_kernels();
 size_t knapsack_dp_workspace(uint32_t n, uint32_t B, uint64_t M);
 void launch_knapsack_dp(cudaStream_t s, const long long* q, const uint32_t* l, uint32_t n, uint32_t B, uint32_t M,
                         void* ws, uint8_t* x, long long* best, long long* Vb);

@@ -34,10 +34,47 @@ __device__ __forceinline__ void overhead_us(uint32_t l, bool queued, uint32_t pr
   }
 }
 
+// In-place inclusive prefix sums of v[0..cnt) by a kRefineThreads CTA (contiguous runs per thread).
+template <class T>
+__device__ void refine_scan(T* v, uint32_t cnt, T* s_part) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (cnt + kRefineThreads - 1) / kRefineThreads;
+  const uint32_t lo = min(cnt, tid * per), hi = min(cnt, lo + per);
+  T part = 0;
+  for (uint32_t q = lo; q < hi; ++q) part += v[q];
+  T inc = part;
+  for (int o = 1; o < 32; o <<= 1) {
+    const T u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += u;
+  }
+  if (lane == 31) s_part[wid] = inc;
+  __syncthreads();
+  T off = 0;
+  for (uint32_t k = 0; k < wid; ++k) off += s_part[k];
+  T run = off + inc - part;
+  for (uint32_t q = lo; q < hi; ++q) {
+    run += v[q];
+    v[q] = run;
+  }
+  __syncthreads();
+}
+
+// The pairing of P:L565-598 (R24), in parallel: with AL = prefix sums of the admits' l and LV of
+// the victims' l (victim order), admit k needs the first vp(k) victims, vp(k) = the smallest j
+// with W0 + AL[k] - LV[j] <= M (monotone in k, so exactly the serial walk's victim pointer), and
+// is feasible iff LV[nv] suffices; the first infeasible admit ends the pairs.  Its stall D_k =
+// the preempt costs of victims vp(k-1) .. vp(k)-1 (prefix sums PV) + its own resume cost.
 __global__ void __launch_bounds__(kRefineThreads) k_refine_pairs(ReqView r, Work w, SchedOut o, uint64_t M,
                                                                  uint32_t prefill, uint32_t swap) {
-  __shared__ uint32_t s_la[kMaxB], s_qa[kMaxB];
-  __shared__ uint32_t s_lv[kMaxRunning];
+  extern __shared__ unsigned char s_dyn[];
+  unsigned long long* s_LV = reinterpret_cast<unsigned long long*>(s_dyn);  // [kMaxRunning + 1]
+  long long* s_PV = reinterpret_cast<long long*>(s_LV + kMaxRunning + 1);   // [kMaxRunning + 1]
+  __shared__ unsigned long long s_AL[kMaxB];
+  __shared__ long long s_res[kMaxB];
+  __shared__ uint32_t s_vp[kMaxB];
+  __shared__ unsigned long long s_pu[kRefineThreads / 32];
+  __shared__ long long s_pl[kRefineThreads / 32];
+  __shared__ uint32_t s_np;
   pdl_wait();
   const uint32_t tid = threadIdx.x;
   const bool trig = __ldcg(&w.g->triggered) != 0;
@@ -47,40 +84,54 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_pairs(ReqView r, Work
   for (uint32_t k = tid; k < kMaxB; k += kRefineThreads) w.rf_loss[k] = 0;
   for (uint32_t q = tid; q < na; q += kRefineThreads) {
     const uint32_t a = o.admit_idx[q];
-    s_la[q] = r.ctx_len[a];
-    s_qa[q] = r.n_deliv[a] == 0u ? 1u : 0u;
+    const uint32_t la = r.ctx_len[a];
+    long long pre, res;
+    overhead_us(la, r.n_deliv[a] == 0u, prefill, swap, pre, res);
+    s_AL[q] = la;
+    s_res[q] = res;
   }
   for (uint32_t v = tid; v < nv; v += kRefineThreads) {
     const uint32_t i = o.preempt_idx[v];
-    s_lv[v] = r.ctx_len[i];
+    const uint32_t lv = r.ctx_len[i];
+    long long pre, res;
+    overhead_us(lv, false, prefill, swap, pre, res);
+    s_LV[v + 1] = lv;
+    s_PV[v + 1] = pre;
     w.vmark[i] = v + 1u;  // 1 + victim position of request i (cleared by k_refine_final)
   }
-  __syncthreads();
   if (tid == 0) {
-    uint32_t vp = 0, npairs = 0;
-    unsigned long long Wc = W0;
-    if (W0 <= M) {  // identity when the running set alone exceeds M
-      for (uint32_t k = 0; k < na; ++k) {
-        unsigned long long Wk = Wc;
-        long long D = 0;
-        while (Wk + s_la[k] > M && vp < nv) {
-          long long pre, res;
-          overhead_us(s_lv[vp], false, prefill, swap, pre, res);
-          Wk -= s_lv[vp];
-          D += pre;
-          ++vp;
-        }
-        if (Wk + s_la[k] > M) break;  // no room even with every remaining victim
-        long long pre, res;
-        overhead_us(s_la[k], s_qa[k] != 0u, prefill, swap, pre, res);
-        w.rf_vend[k] = vp;
-        w.rf_D[k] = D + res;
-        Wc = Wk + s_la[k];
-        npairs = k + 1;
-      }
-    }
-    w.g->rf_npairs = npairs;
+    s_LV[0] = 0ull;
+    s_PV[0] = 0ll;
+    s_np = (W0 <= M) ? na : 0u;  // identity when the running set alone exceeds M
   }
+  __syncthreads();
+  refine_scan(s_AL, na, s_pu);
+  refine_scan(s_LV + 1, nv, s_pu);
+  refine_scan(s_PV + 1, nv, s_pl);
+  for (uint32_t k = tid; k < na; k += kRefineThreads) {
+    const unsigned long long need = W0 + s_AL[k];  // LV[j] >= need - M
+    uint32_t vp = 0;
+    if (need > M) {
+      const unsigned long long t = need - M;
+      uint32_t lo = 0, hi = nv + 1;  // first j in [0, nv] with LV[j] >= t, nv + 1 if none
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_LV[mid] >= t) hi = mid;
+        else lo = mid + 1;
+      }
+      vp = lo;
+    }
+    s_vp[k] = vp;
+    if (vp > nv) atomicMin(&s_np, k);
+  }
+  __syncthreads();
+  const uint32_t np = s_np;
+  for (uint32_t k = tid; k < np; k += kRefineThreads) {
+    const uint32_t vp = s_vp[k], vq = k ? s_vp[k - 1] : 0u;
+    w.rf_vend[k] = vp;
+    w.rf_D[k] = (s_PV[vp] - s_PV[vq]) + s_res[k];
+  }
+  if (tid == 0) w.g->rf_npairs = np;
 }
 
 // Q of request i at relative time t with its delivered timeline only (Eq. 1-3, readings R1-R3),
@@ -190,9 +241,15 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_final(ReqView r, Work
   }
 }
 
+static size_t refine_pairs_smem() { return 2 * sizeof(unsigned long long) * (kMaxRunning + 1); }
+
+void init_refine_kernels() {
+  cudaFuncSetAttribute(k_refine_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)refine_pairs_smem());
+}
+
 void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o, int64_t now,
                    const uint32_t* tau, uint64_t M, uint32_t prefill, uint32_t swap) {
-  launch_pdl(k_refine_pairs, 1, kRefineThreads, 0, L.stream, r, w, o, M, prefill, swap);
+  launch_pdl(k_refine_pairs, 1, kRefineThreads, refine_pairs_smem(), L.stream, r, w, o, M, prefill, swap);
   launch_pdl(k_refine_loss, L.sm_count * 4, kRefineThreads, 0, L.stream, r, w, now);
   launch_pdl(k_refine_final, 1, kRefineThreads, 0, L.stream, r, w, o, tau, M);
 }
