@@ -893,29 +893,32 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     // Algorithm 1 walk (greedy order): k* = number of leading prefix sums of l that stay <= M;
     // prefix sums strictly increase (l >= 1), so this is exactly the walk with `break`.
     if (B == 256) ANDES_TRACE(w, 2402);
-    for (uint32_t q = tid; q < cnt; q += kSelThreads) s_ps[q] = r.ctx_len[s_idx[q]];
-    __syncthreads();
-    if (B == 256) ANDES_TRACE(w, 2403);
-    if (tid < 32) {
-      const uint32_t per = (cnt + 31) / 32, q0 = tid * per, q1 = min(cnt, q0 + per);
-      unsigned long long part = 0;
-      for (uint32_t q = q0; q < q1; ++q) part += s_ps[q];
-      unsigned long long inc = part;
+    // the walk block-wide (one warp alone is starved by the SM's other CTA): thread t holds
+    // positions 2t, 2t+1 (cnt <= kSortCap = 2 kSelThreads); warp scan of l, warp totals through
+    // shared memory, and k* = the number of prefix sums <= M by two counting barriers
+    static_assert(kSortCap <= 2 * kSelThreads, "walk: two positions per thread");
+    uint32_t kstar;
+    {
+      const uint32_t lane = tid & 31, wid = tid >> 5, q0 = 2 * tid;
+      const unsigned long long l0 = q0 < cnt ? r.ctx_len[s_idx[q0]] : 0ull;
+      const unsigned long long l1 = q0 + 1 < cnt ? r.ctx_len[s_idx[q0 + 1]] : 0ull;
+      unsigned long long inc = l0 + l1;
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (tid >= (uint32_t)o) inc += v;
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += u;
       }
-      unsigned long long run = inc - part;
-      uint32_t mine = 0;
-      for (uint32_t q = q0; q < q1; ++q) {
-        run += s_ps[q];
-        mine += (run <= A.M) ? 1u : 0u;
-      }
-      for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-      if (tid == 0) s_k = mine;
+      unsigned long long* const s_wsum = reinterpret_cast<unsigned long long*>(s_red);
+      if (lane == 31) s_wsum[wid] = inc;
+      __syncthreads();
+      if (B == 256) ANDES_TRACE(w, 2403);
+      unsigned long long off = 0;
+      for (uint32_t k2 = 0; k2 < wid; ++k2) off += s_wsum[k2];
+      const unsigned long long p1 = off + inc, p0 = p1 - l1;
+      kstar = (uint32_t)__syncthreads_count(q0 < cnt && p0 <= A.M) +
+              (uint32_t)__syncthreads_count(q0 + 1 < cnt && p1 <= A.M);
     }
-    __syncthreads();
-    const uint32_t kstar = s_k;
+    if (B == 256) ANDES_TRACE(w, 2406);
     long long v = 0;
     for (uint32_t q = tid; q < kstar; q += kSelThreads) {
       const uint32_t i = s_idx[q];
@@ -924,7 +927,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       // stage_cap's admit flags (s_ps is free after the walk)
       s_ps[q] = (ovf ? r.running[i] != 0 : s_run8[q] != 0) ? 0ull : 1ull;
     }
+    if (B == 256) ANDES_TRACE(w, 2407);
     v = block_sum_ll<kSelThreads>(v, s_red);
+    if (B == 256) ANDES_TRACE(w, 2408);
     const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
     if (tid == 0) {
       A.o.V[B - 1] = v;

@@ -51,7 +51,7 @@ print("state CTAs", len(st), "start", us(st[:, 0].min()), "end", us(st[:, 1].max
 cp = span(8100, 9124)
 print("compact CTAs", len(cp), "start", us(cp[:, 0].min()), us(cp[:, 0].max()), "theta(CTA0)", us(tr[2210]),
       "end max", us(cp[:, 1].max()))
-print("select CTA255 phases", [us(tr[s]) for s in range(2400, 2406) if tr[s]])
+print("select CTA255 phases", [us(tr[s]) for s in range(2400, 2409) if tr[s]], "(2400 keys, 2401 rank, 2402-3 l loads, 2406 walk, 2407 V loop, 2408 block sum, 2404 V out, 2405 cap)")
 sel = span(0, 512)
 print("select CTAs", len(sel), "start", us(sel[:, 0].min()), us(sel[:, 0].max()), "end min/med/max",
       us(sel[:, 1].min()), us(np.median(sel[:, 1])), us(sel[:, 1].max()))
