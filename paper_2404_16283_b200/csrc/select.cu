@@ -521,7 +521,7 @@ __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
 __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t kstar, unsigned long long thr,
                           const uint32_t* s_sel, unsigned long long* vkey, uint32_t* vidx, unsigned long long* vcum,
                           unsigned long long* acum, uint32_t* aflag, bool rpre, const unsigned long long* rk,
-                          const uint32_t* rx, const uint32_t* rlen, uint32_t n_run) {
+                          const uint32_t* rx, const uint32_t* rlen, uint32_t n_run, const uint32_t* lsel) {
   __shared__ uint32_t s_nv, s_na, s_e, s_a;
   __shared__ unsigned long long s_W0;
   __shared__ unsigned long long s_tmp[kSelThreads / 32];
@@ -568,7 +568,10 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
   __syncthreads();
   block_inclusive_scan(acum, kstar, s_tmp);
   for (uint32_t q = tid; q < kstar; q += kSelThreads)
-    if (acum[q] != (q ? acum[q - 1] : 0ull)) aflag[acum[q] - 1] = s_sel[q];
+    if (acum[q] != (q ? acum[q - 1] : 0ull)) {
+      aflag[acum[q] - 1] = s_sel[q];
+      aflag[kSortCap + acum[q] - 1] = lsel[q];  // its l (upper half of aflag's 2 kSortCap words)
+    }
   if (tid == 0) s_na = kstar ? (uint32_t)acum[kstar - 1] : 0u;
   // victim order by rank counting (keys unique)
   const uint32_t nv = s_nv;
@@ -612,7 +615,7 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
       n_adm = 0;
       realized = n_run - n_pre;
     } else {
-      for (uint32_t q = tid; q < na; q += kSelThreads) acum[q] = r.ctx_len[aflag[q]];
+      for (uint32_t q = tid; q < na; q += kSelThreads) acum[q] = aflag[kSortCap + q];
       __syncthreads();
       block_inclusive_scan(acum, na, s_tmp);
       uint32_t mine = 0;
@@ -724,6 +727,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   __shared__ long long s_red[32];
   __shared__ Globals s_g;
   __shared__ uint8_t s_run8[kSortCap];  // running flag of the ordered survivors (pruned path)
+  __shared__ uint32_t s_lsel[kSortCap];  // l of the ordered candidates (the walk's loads)
 
   const ReqView& r = A.r;
   const Work& w = A.w;
@@ -902,6 +906,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
       const uint32_t lane = tid & 31, wid = tid >> 5, q0 = 2 * tid;
       const unsigned long long l0 = q0 < cnt ? r.ctx_len[s_idx[q0]] : 0ull;
       const unsigned long long l1 = q0 + 1 < cnt ? r.ctx_len[s_idx[q0 + 1]] : 0ull;
+      if (q0 < cnt) s_lsel[q0] = (uint32_t)l0;
+      if (q0 + 1 < cnt) s_lsel[q0 + 1] = (uint32_t)l1;
       unsigned long long inc = l0 + l1;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -940,7 +946,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     if (n_run <= (uint32_t)kStageRun) {
       // victims and their prefix sums live past the first kStageRun slots of s_key / s_idx
       stage_cap(A, B, tB, kstar, thr, s_idx, s_key + kStageRun, s_idx + kStageRun, s_vc,
-                s_ps, reinterpret_cast<uint32_t*>(s_gf), rpre, s_rk, s_rx, s_rl, n_run);
+                s_ps, reinterpret_cast<uint32_t*>(s_gf), rpre, s_rk, s_rx, s_rl, n_run, s_lsel);
     }
     if (B == 256) ANDES_TRACE(w, 2405);
   }
