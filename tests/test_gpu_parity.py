@@ -278,6 +278,41 @@ def test_not_triggered(A, ctx, orc):
     _check_sched(A, ctx, orc, snap, flags=0, cur_latency=0)
 
 
+def _snap_from(tl, *, P=208_333, ttft=1_000_000, l=None, running=None, now=3_000_000, horizon=2_000_000,
+               B_cap=8, M=10_000, rank=None, align=4):
+    n = len(tl)
+    g, base, pool = W._pack([np.asarray(t, np.uint32) for t in tl], align)
+    return W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, ttft, np.uint32),
+                      period_us=np.full(n, P, np.uint32),
+                      ctx_len=np.asarray(l if l is not None else np.full(n, 100), np.uint32), n_deliv=g,
+                      max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=np.asarray(rank if rank is not None else np.arange(n), np.uint32),
+                      running=np.asarray(running if running is not None else np.zeros(n), np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=now, horizon_us=horizon, tau_us=W.tau_table(B_cap),
+                      kv_capacity=M)
+
+
+def test_schedule_degenerate_cases(A, ctx, orc):
+    """The degenerate inputs of the decision, each against the oracle: one request; no request
+    has a token; B_cap = 1; every request running with the running set over M (the cap is
+    overridden by memory, O9); M fits exactly one request; a preemption cap of 0; identical
+    requests that differ only in rank (ties broken by rank, R10)."""
+    late = [np.arange(6) * 250_000 + 1_400_000]
+    cases = [
+        (_snap_from(late), {}),
+        (_snap_from(late, running=[1]), {}),
+        (_snap_from([[], [], []]), {}),
+        (_snap_from(late * 5, B_cap=1), {}),
+        (_snap_from(late * 6, running=[1] * 6, l=[3000] * 6, M=10_000), {"cap": 2}),
+        (_snap_from(late * 6, running=[1, 1, 0, 0, 0, 0], l=[5000] * 6, M=5000), {"cap": 0}),
+        (_snap_from(late * 7, rank=[6, 5, 4, 3, 2, 1, 0], B_cap=3), {"cap": 1}),
+        (_snap_from(late * 4 + [[]] * 4, running=[0, 1] * 4, l=[100, 200, 300, 400] * 2, B_cap=8), {"cap": 0}),
+    ]
+    for snap, kw in cases:
+        for flags in (1, 1 | 16, 1 | 2):
+            _check_sched(A, ctx, orc, snap, flags=flags, **kw)
+
+
 # ---------------------------------------------------------------- config 1: 200-iteration driver
 def _iterate(A, ctx, orc, iters=200, seed=1):
     """BASELINE config 1: 8 requests, ttft 1 s, 4.8 tok/s, M = 2048; each iteration the GPU
