@@ -469,7 +469,9 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": scan_bytes, "dominant_stage": names[dom],
             "note": ("S3-S6 (state, compact, select: candidate keys, Algorithm 1 per B, cap) are "
                      "latency-bound one-CTA-per-B stages without a throughput roofline; the scan is the "
-                     "HBM-bound kernel")}
+                     "HBM-bound kernel. At 64K requests (38 MB) its launch is latency-bound (ramp-up and "
+                     "tail of ~2.4 tiles per warp); its throughput roofline is qoe_eval.roofline (2^20 "
+                     "requests, the same kernel)")}
     roof["stage_ms"] = dict(zip(names, stage_ms))
     roof["stage_share"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
 
