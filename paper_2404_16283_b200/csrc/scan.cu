@@ -900,12 +900,14 @@ __device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, u
 
 }  // namespace
 
-// K1.  Persistent CTAs of independent warps.  Each warp claims 1024-token warp-tiles in
-// increasing order, double-buffers them with TMA tensor copies (32 rows x 128 B, 128B swizzle,
-// one mbarrier per buffer), stages the tile's request records in its own shared-memory window,
-// reads the head segment's earlier tokens directly when it started <= kCarryDirect tokens
-// before the tile (else decoupled look-back on per-warp-tile status words), and scans with
-// warp shuffles only: no CTA-wide barriers on the hot path.
+// K1.  Persistent CTAs of independent warps.  A warp's work unit is TW consecutive 1024-token
+// warp-tiles (TW = 1: double-buffered TMA prefetch; TW = 2 on large pools: one unit fills both
+// 4 KB buffers), claimed in chunks from the pool's end (the first two statically).  Each tile
+// arrives by a TMA tensor copy (32 rows x 128 B; 128B swizzle for unaligned pools) on an
+// mbarrier; the unit's request records come from global memory one unit ahead; the head
+// request's earlier tokens are read directly when it started <= kCarryDirect tokens before the
+// unit (else a bounded decoupled look-back on per-tile status words, on the row path); the
+// scan itself uses warp shuffles only: no CTA-wide barriers on the hot path.
 template <bool kFinal, int TW>
 __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap_swz,
