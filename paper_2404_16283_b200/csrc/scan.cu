@@ -21,6 +21,10 @@ namespace andes {
 
 // ---------------------------------------------------------------- prep (+ S0/S2 in the last CTA)
 constexpr int kPrepThreads = 256;
+#ifndef ANDES_TOK_UNROLL
+#define ANDES_TOK_UNROLL 4
+#endif
+constexpr int kTokUnroll = ANDES_TOK_UNROLL;  // unroll of the aligned path's token loops
 
 __device__ __forceinline__ void bounds_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kScanThreads) : "memory"); }
 
@@ -791,7 +795,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   }
   // ---- pass 1: zero-carry lateness at the sub-range's end
   uint32_t a = Is - P;
-#pragma unroll 2
+#pragma unroll kTokUnroll
   for (uint32_t gi = 0; gi < gmax; ++gi) {
     if (gi < nfull) {
       const uint4 v = ld_shared_v4(a0 + (gi << 4));
@@ -846,7 +850,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const uint32_t A_hi = Is + (uint32_t)max(xe - xs - 1, 0) * P + max(dz, carry);
   const bool noclamp = kFinal || __all_sync(0xffffffffu, !active || A_hi <= tcl);
   if (noclamp) {
-#pragma unroll 2
+#pragma unroll kTokUnroll
     for (uint32_t gi = 0; gi < gmax; ++gi) {
       if (gi < nfull) {
         const uint4 v = ld_shared_v4(a0 + (gi << 4));
@@ -858,7 +862,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   } else
 #endif
   {
-#pragma unroll 2
+#pragma unroll kTokUnroll
     for (uint32_t gi = 0; gi < gmax; ++gi) {
       if (gi < nfull) {
         const uint4 v = ld_shared_v4(a0 + (gi << 4));
