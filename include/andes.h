@@ -28,10 +28,18 @@
  *  - One context per stream; contexts are not thread-safe.
  *  - andes_qoe_eval / andes_gain_estimate / andes_schedule are stream-capture safe: a
  *    decision can be captured once into a CUDA graph and replayed (same pointers/params).
- *  - Data preconditions (timestamps nondecreasing, 1 <= l_i <= M, ranks unique,
- *    tl_base nondecreasing) are checked on the device only when
- *    ANDES_DEBUG_CHECKS is set; a violation sets the context's device error word
- *    and the NEXT call on that context returns ANDES_E_RANGE.
+ *  - Device-side errors go to the context's sticky error word (mapped pinned host memory the
+ *    kernels write; no copy or synchronisation is added to a call).  The first call on the
+ *    context that starts after the failing kernel has run returns the error and clears the
+ *    word (with back-to-back asynchronous calls that can be a later call than the next one):
+ *      ANDES_E_CAPACITY: a workspace capacity was exceeded on the device -- more running
+ *        requests than the decision holds (4096; 2048 per rank in the sharded decision), or a
+ *        timestamp pool longer than limits.max_tokens.  Always checked; the failing decision is
+ *        truncated and flags it with ANDES_F_TRUNCATED.
+ *      ANDES_E_RANGE: a data precondition failed.  Checked only under ANDES_DEBUG_CHECKS
+ *        (andes_schedule, andes_schedule_shard): period >= 1, 1 <= l_i <= M, tl_base
+ *        nondecreasing with room for n_deliv, delivery times nondecreasing and <= now - a_i,
+ *        ranks unique (exact), fewer than 2^20 tokens due per request.
  */
 #ifndef ANDES_H
 #define ANDES_H
@@ -59,7 +67,7 @@ typedef struct {
     uint32_t max_requests; /* largest n of any call                                     */
     uint32_t max_B;        /* largest B_cap (<= 1024)                                   */
     uint64_t max_tokens;   /* largest timestamp-pool span (tl_base[n-1] + n_deliv[n-1]) */
-    uint32_t max_running;  /* largest number of running requests (victim sort; <= 8192) */
+    uint32_t max_running;  /* largest number of running requests (<= 4096; 0 = 4096)    */
     int32_t device;        /* CUDA device ordinal                                       */
 } AndesLimits;
 
@@ -142,6 +150,8 @@ typedef struct {
 #define ANDES_F_CAP_HIT 2u
 #define ANDES_F_CAP_OVERRIDDEN 4u
 #define ANDES_F_SLOW_PATH 8u /* informational: a capacity fallback path ran */
+#define ANDES_F_TRUNCATED 16u /* the running set exceeded the decision's capacity (4096): the victim
+                                 list was truncated; the next call returns ANDES_E_CAPACITY        */
 #define ANDES_F_REFINED 32u  /* the overhead-aware refiner rewrote the decision (ANDES_REFINE)   */
 
 /* Decision outputs (DEVICE memory owned by the caller). */

@@ -37,8 +37,8 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc (IEEE binary64, no FP contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call([
-            "gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
-            "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm",
+            "gcc", "-O2", "-std=gnu99", "-pthread", "-ffp-contract=off", "-fno-fast-math",
+            "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm", "-lpthread",
         ])
     return _LIB
 
@@ -79,14 +79,15 @@ def lib():
         _lib.oracle_qoe_walk.restype = C.c_int
         _lib.oracle_qoe_walk.argtypes = [C.c_void_p, C.c_uint32, C.c_int64, C.c_int64, C.c_int64,
                                          C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
-        _lib.oracle_qoe_eval.restype = C.c_int
-        _lib.oracle_qoe_eval.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
-                                         C.c_void_p, C.c_void_p]
-        _lib.oracle_gain_estimate.restype = C.c_int
-        _lib.oracle_gain_estimate.argtypes = [C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_uint32,
-                                              C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
-        _lib.oracle_schedule.restype = C.c_int
-        _lib.oracle_schedule.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.oracle_qoe_eval_mt.restype = C.c_int
+        _lib.oracle_qoe_eval_mt.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_int]
+        _lib.oracle_gain_estimate_mt.restype = C.c_int
+        _lib.oracle_gain_estimate_mt.argtypes = [C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_uint32,
+                                                 C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                 C.c_int]
+        _lib.oracle_schedule_mt.restype = C.c_int
+        _lib.oracle_schedule_mt.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     return _lib
 
 
@@ -130,22 +131,32 @@ def qoe_walk(D_us, ttft, P, t, m, final=False):
     return sd.value, sw.value, q.value
 
 
-def qoe_eval(req, eval_time_us, final=False):
-    """Per-request (Q fp64, S_delay, S_whole, m)."""
+def nproc() -> int:
+    """Host threads available to this process (the threaded oracle's default)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def qoe_eval(req, eval_time_us, final=False, threads=1):
+    """Per-request (Q fp64, S_delay, S_whole, m).  threads > 1 splits the requests over threads."""
     s, keep = _req_struct(req)
     n = s.n
     q = np.zeros(n, np.float64)
     sd = np.zeros(n, np.int64)
     sw = np.zeros(n, np.int64)
     m = np.zeros(n, np.uint32)
-    rc = lib().oracle_qoe_eval(C.byref(s), int(eval_time_us), int(final), _p(q), _p(sd), _p(sw), _p(m))
+    rc = lib().oracle_qoe_eval_mt(C.byref(s), int(eval_time_us), int(final), _p(q), _p(sd), _p(sw), _p(m),
+                                  int(threads))
     if rc != 0:
         raise ValueError(f"oracle_qoe_eval rc={rc}")
     return q, sd, sw, m
 
 
-def gain_estimate(req, now_us, horizon_us, tau_us, B_list):
-    """gain f64[nB, n], key f32[nB, n], q_wait f64[n] (row b = B_list[b])."""
+def gain_estimate(req, now_us, horizon_us, tau_us, B_list, threads=1):
+    """gain f64[nB, n], key f32[nB, n], q_wait f64[n] (row b = B_list[b]).  threads > 1 splits
+    the requests over threads."""
     s, keep = _req_struct(req)
     tau = np.ascontiguousarray(tau_us, dtype=np.uint32)
     Bl = np.ascontiguousarray(B_list, dtype=np.uint32)
@@ -153,8 +164,8 @@ def gain_estimate(req, now_us, horizon_us, tau_us, B_list):
     gain = np.zeros((Bl.size, n), np.float64)
     key = np.zeros((Bl.size, n), np.float32)
     qw = np.zeros(n, np.float64)
-    rc = lib().oracle_gain_estimate(C.byref(s), int(now_us), int(horizon_us), _p(tau), tau.size,
-                                    _p(Bl), Bl.size, _p(gain), _p(key), _p(qw))
+    rc = lib().oracle_gain_estimate_mt(C.byref(s), int(now_us), int(horizon_us), _p(tau), tau.size,
+                                       _p(Bl), Bl.size, _p(gain), _p(key), _p(qw), int(threads))
     if rc != 0:
         raise ValueError(f"oracle_gain_estimate rc={rc}")
     return gain, key, qw
@@ -177,7 +188,9 @@ class Decision:
 
 
 def schedule(req, now_us, horizon_us, tau_us, kv_capacity, preempt_cap=UINT32_MAX,
-             cur_latency_us=0, flags=ORC_FORCE, B_cap=None, prefill_tok_s=5000, swap_tok_s=0):
+             cur_latency_us=0, flags=ORC_FORCE, B_cap=None, prefill_tok_s=5000, swap_tok_s=0, threads=1):
+    """One decision (O6-O9).  threads > 1 splits the independent per-B walks (S3/S4) over
+    threads; every output is identical for any thread count."""
     s, keep = _req_struct(req)
     tau = np.ascontiguousarray(tau_us, dtype=np.uint32)
     B_cap = tau.size if B_cap is None else B_cap
@@ -191,7 +204,7 @@ def schedule(req, now_us, horizon_us, tau_us, kv_capacity, preempt_cap=UINT32_MA
     V = np.zeros(max(B_cap, 1), np.int64)
     ks = np.zeros(max(B_cap, 1), np.uint32)
     d = _Dec(_p(mask), _p(adm), _p(pre), _p(sc), _p(V), _p(ks))
-    rc = lib().oracle_schedule(C.byref(s), C.byref(p), C.byref(d))
+    rc = lib().oracle_schedule_mt(C.byref(s), C.byref(p), C.byref(d), int(threads))
     if rc < 0:
         raise ValueError(f"oracle_schedule rc={rc}")
     return Decision(rc, mask[:n].copy(), adm[:sc[2]].copy(), pre[:sc[3]].copy(), int(sc[0]), int(sc[1]),

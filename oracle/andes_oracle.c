@@ -39,6 +39,9 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <pthread.h>
+
+#define ORC_MAX_THREADS 256
 
 #define ORC_OK 0
 #define ORC_E_INVAL (-1)
@@ -187,18 +190,17 @@ int oracle_qoe_walk(const uint32_t *D_us, uint32_t n, int64_t ttft, int64_t P, i
 
 /* QoE of every request at absolute time eval_time_us (O1+O2), or of its whole
  * delivered timeline (final_mode, reading R19). Outputs may be NULL. */
-int oracle_qoe_eval(const orc_requests *r, int64_t eval_time_us, int final_mode,
-                    double *q_out, int64_t *sd_out, int64_t *sw_out, uint32_t *m_out)
+/* O1+O2 for requests [lo, hi). */
+static int qoe_eval_range(const orc_requests *r, uint32_t lo, uint32_t hi, int64_t eval_time_us, int final_mode,
+                          double *q_out, int64_t *sd_out, int64_t *sw_out, uint32_t *m_out)
 {
     uint32_t i;
     uint64_t maxg = 1;
     int64_t maxm = 1;
     int64_t *D, *T;
-    for (i = 0; i < r->n; i++) {
+    for (i = lo; i < hi; i++) {
         int64_t t = eval_time_us - r->arrival_us[i];
         int64_t m = final_mode ? r->n_deliv[i] : due_count(t, r->ttft_us[i], r->period_us[i], r->max_total[i]);
-        if (r->period_us[i] < 1)
-            return ORC_E_INVAL;
         if (r->n_deliv[i] > maxg)
             maxg = r->n_deliv[i];
         if (m > maxm)
@@ -211,7 +213,7 @@ int oracle_qoe_eval(const orc_requests *r, int64_t eval_time_us, int final_mode,
         free(T);
         return ORC_E_NOMEM;
     }
-    for (i = 0; i < r->n; i++) {
+    for (i = lo; i < hi; i++) {
         int64_t t = eval_time_us - r->arrival_us[i];
         int64_t g = r->n_deliv[i], j, sd, sw;
         int64_t m = final_mode ? g : due_count(t, r->ttft_us[i], r->period_us[i], r->max_total[i]);
@@ -230,6 +232,69 @@ int oracle_qoe_eval(const orc_requests *r, int64_t eval_time_us, int final_mode,
     free(D);
     free(T);
     return ORC_OK;
+}
+
+typedef struct {
+    const orc_requests *r;
+    uint32_t lo, hi;
+    int64_t eval_time_us;
+    int final_mode, rc;
+    double *q;
+    int64_t *sd, *sw;
+    uint32_t *m;
+} qrange_t;
+
+static void *qrange_worker(void *arg)
+{
+    qrange_t *a = (qrange_t *)arg;
+    a->rc = qoe_eval_range(a->r, a->lo, a->hi, a->eval_time_us, a->final_mode, a->q, a->sd, a->sw, a->m);
+    return NULL;
+}
+
+/* QoE of every request at absolute time eval_time_us (O1+O2), or of its whole delivered
+ * timeline (final_mode, reading R19).  Outputs may be NULL.  The requests are independent;
+ * nthreads > 1 splits them into contiguous ranges over threads (same per-request values). */
+int oracle_qoe_eval_mt(const orc_requests *r, int64_t eval_time_us, int final_mode, double *q_out,
+                       int64_t *sd_out, int64_t *sw_out, uint32_t *m_out, int nthreads)
+{
+    qrange_t a[ORC_MAX_THREADS];
+    pthread_t th[ORC_MAX_THREADS];
+    uint32_t i;
+    int t, nt = nthreads < 1 ? 1 : (nthreads > ORC_MAX_THREADS ? ORC_MAX_THREADS : nthreads);
+    for (i = 0; i < r->n; i++)
+        if (r->period_us[i] < 1)
+            return ORC_E_INVAL;
+    if ((uint32_t)nt > r->n)
+        nt = r->n ? (int)r->n : 1;
+    for (t = 0; t < nt; t++) {
+        a[t].r = r;
+        a[t].lo = (uint32_t)((uint64_t)r->n * t / nt);
+        a[t].hi = (uint32_t)((uint64_t)r->n * (t + 1) / nt);
+        a[t].eval_time_us = eval_time_us;
+        a[t].final_mode = final_mode;
+        a[t].q = q_out;
+        a[t].sd = sd_out;
+        a[t].sw = sw_out;
+        a[t].m = m_out;
+        th[t] = 0;
+        if (nt == 1 || pthread_create(&th[t], NULL, qrange_worker, &a[t]) != 0) {
+            th[t] = 0;
+            qrange_worker(&a[t]);
+        }
+    }
+    for (t = 0; t < nt; t++)
+        if (th[t])
+            pthread_join(th[t], NULL);
+    for (t = 0; t < nt; t++)
+        if (a[t].rc != ORC_OK)
+            return a[t].rc;
+    return ORC_OK;
+}
+
+int oracle_qoe_eval(const orc_requests *r, int64_t eval_time_us, int final_mode,
+                    double *q_out, int64_t *sd_out, int64_t *sw_out, uint32_t *m_out)
+{
+    return oracle_qoe_eval_mt(r, eval_time_us, final_mode, q_out, sd_out, sw_out, m_out, 1);
 }
 
 /* ------------------------------------------------------------------ O3-O5 */
@@ -323,32 +388,92 @@ static int alloc_scratch(const orc_requests *r, int64_t now, uint32_t horizon, s
 }
 
 /* Gains and keys for an explicit list of B (row b of the outputs = B_list[b]). */
-int oracle_gain_estimate(const orc_requests *r, int64_t now, uint32_t horizon, const uint32_t *tau_us,
-                         uint32_t B_cap, const uint32_t *B_list, uint32_t nB, double *gain_out,
-                         float *key_out, double *qwait_out)
+typedef struct {
+    const orc_requests *r;
+    int64_t now;
+    uint32_t horizon, lo, hi, nB;
+    const uint32_t *tau_us, *B_list;
+    double *gain_out, *qwait_out;
+    float *key_out;
+    int rc;
+} grange_t;
+
+/* Gains and keys of requests [lo, hi) (O3-O5). */
+static void *grange_worker(void *arg)
 {
+    grange_t *a = (grange_t *)arg;
+    const orc_requests *r = a->r;
     uint32_t i, b;
     scratch_t s;
-    for (b = 0; b < nB; b++)
-        if (B_list[b] < 1 || B_list[b] > B_cap)
-            return ORC_E_INVAL;
-    if (alloc_scratch(r, now, horizon, &s) != ORC_OK)
-        return ORC_E_NOMEM;
-    for (i = 0; i < r->n; i++) {
-        double qw = q_wait(r, i, now, horizon, &s);
-        if (qwait_out)
-            qwait_out[i] = qw;
-        for (b = 0; b < nB; b++) {
-            double gain = q_serve(r, i, now, horizon, tau_us[B_list[b] - 1], &s) - qw;
-            if (gain_out)
-                gain_out[(size_t)b * r->n + i] = gain;
-            if (key_out)
-                key_out[(size_t)b * r->n + i] = priority_key(gain, r->ctx_len[i]);
+    a->rc = ORC_OK;
+    if (alloc_scratch(r, a->now, a->horizon, &s) != ORC_OK) {
+        a->rc = ORC_E_NOMEM;
+        return NULL;
+    }
+    for (i = a->lo; i < a->hi; i++) {
+        double qw = q_wait(r, i, a->now, a->horizon, &s);
+        if (a->qwait_out)
+            a->qwait_out[i] = qw;
+        for (b = 0; b < a->nB; b++) {
+            double gain = q_serve(r, i, a->now, a->horizon, a->tau_us[a->B_list[b] - 1], &s) - qw;
+            if (a->gain_out)
+                a->gain_out[(size_t)b * r->n + i] = gain;
+            if (a->key_out)
+                a->key_out[(size_t)b * r->n + i] = priority_key(gain, r->ctx_len[i]);
         }
     }
     free(s.D);
     free(s.T);
+    return NULL;
+}
+
+/* Gains and keys for an explicit list of B (row b of the outputs = B_list[b]).  The requests
+ * are independent; nthreads > 1 splits them into contiguous ranges over threads. */
+int oracle_gain_estimate_mt(const orc_requests *r, int64_t now, uint32_t horizon, const uint32_t *tau_us,
+                            uint32_t B_cap, const uint32_t *B_list, uint32_t nB, double *gain_out,
+                            float *key_out, double *qwait_out, int nthreads)
+{
+    grange_t a[ORC_MAX_THREADS];
+    pthread_t th[ORC_MAX_THREADS];
+    uint32_t b;
+    int t, nt = nthreads < 1 ? 1 : (nthreads > ORC_MAX_THREADS ? ORC_MAX_THREADS : nthreads);
+    for (b = 0; b < nB; b++)
+        if (B_list[b] < 1 || B_list[b] > B_cap)
+            return ORC_E_INVAL;
+    if ((uint32_t)nt > r->n)
+        nt = r->n ? (int)r->n : 1;
+    for (t = 0; t < nt; t++) {
+        a[t].r = r;
+        a[t].now = now;
+        a[t].horizon = horizon;
+        a[t].lo = (uint32_t)((uint64_t)r->n * t / nt);
+        a[t].hi = (uint32_t)((uint64_t)r->n * (t + 1) / nt);
+        a[t].nB = nB;
+        a[t].tau_us = tau_us;
+        a[t].B_list = B_list;
+        a[t].gain_out = gain_out;
+        a[t].qwait_out = qwait_out;
+        a[t].key_out = key_out;
+        th[t] = 0;
+        if (nt == 1 || pthread_create(&th[t], NULL, grange_worker, &a[t]) != 0) {
+            th[t] = 0;
+            grange_worker(&a[t]);
+        }
+    }
+    for (t = 0; t < nt; t++)
+        if (th[t])
+            pthread_join(th[t], NULL);
+    for (t = 0; t < nt; t++)
+        if (a[t].rc != ORC_OK)
+            return a[t].rc;
     return ORC_OK;
+}
+
+int oracle_gain_estimate(const orc_requests *r, int64_t now, uint32_t horizon, const uint32_t *tau_us,
+                         uint32_t B_cap, const uint32_t *B_list, uint32_t nB, double *gain_out,
+                         float *key_out, double *qwait_out)
+{
+    return oracle_gain_estimate_mt(r, now, horizon, tau_us, B_cap, B_list, nB, gain_out, key_out, qwait_out, 1);
 }
 
 /* ------------------------------------------------------------------ O6-O9 */
@@ -512,7 +637,132 @@ out:
 }
 
 
+/* S3 + S4 at one candidate B: every request's gain (O4/O5 or the objective's item value,
+ * readings R21-R23), its priority key, the full comparison sort in greedy order (R10) and
+ * Algorithm 1's walk with `break` (R11).  items[] / gain[] receive the sorted order
+ * and the gains; *V_out = sum of llrint(gain 2^32) over S_B, *c_out = |S_B|. */
+static void per_B(const orc_requests *r, const orc_params *p, uint32_t B, const double *qw,
+                  const double *qnow, double qmin, scratch_t *s, item_t *items, double *gain,
+                  int64_t *V_out, uint32_t *c_out)
+{
+    uint32_t n = r->n, i, k, c = 0;
+    uint64_t W = 0, M = p->kv_capacity;
+    int64_t V = 0;
+    for (i = 0; i < n; i++) {
+        if (p->flags & ORC_MAXMIN) {
+            double v = qmin - qw[i];
+            gain[i] = v > 0.0 ? v : 0.0;
+        } else if (p->flags & ORC_PERFECT) {
+            double qs = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], s);
+            gain[i] = ((qs == 1.0 ? 1.0 : 0.0) - (qw[i] == 1.0 ? 1.0 : 0.0)) * (qnow[i] == 1.0 ? 1.0 : 0.0);
+        } else {
+            gain[i] = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], s) - qw[i];
+        }
+        items[i].idx = i;
+        items[i].rank = r->rank[i];
+        items[i].key = (p->flags & ORC_LQSF) ? lqsf_key(gain[i]) : priority_key(gain[i], r->ctx_len[i]);
+    }
+    qsort(items, n, sizeof(item_t), cmp_greedy);
+    /* Algorithm 1: take while within M and B, else break. */
+    for (k = 0; k < n; k++) {
+        uint32_t l = r->ctx_len[items[k].idx];
+        if (W + l <= M && c + 1 <= B) {
+            W += l;
+            c += 1;
+            V += gain_fixed(gain[items[k].idx]);
+        } else {
+            break;
+        }
+    }
+    *V_out = V;
+    *c_out = c;
+}
+
+typedef struct {
+    const orc_requests *r;
+    const orc_params *p;
+    const double *qw, *qnow;
+    double qmin;
+    orc_decision *out;
+    uint32_t B_lo, B_hi, stride, first;
+    int rc;
+} bloop_t;
+
+/* One worker: B = B_lo + first, + stride, ... (its own scratch; writes only V[B-1], kstar[B-1]). */
+static void *bloop_worker(void *arg)
+{
+    bloop_t *a = (bloop_t *)arg;
+    uint32_t n = a->r->n, B;
+    scratch_t s = {NULL, NULL};
+    item_t *items = (item_t *)malloc(sizeof(item_t) * n);
+    double *gain = (double *)malloc(sizeof(double) * n);
+    a->rc = ORC_OK;
+    if (!items || !gain || alloc_scratch(a->r, a->p->now_us, a->p->horizon_us, &s) != ORC_OK) {
+        a->rc = ORC_E_NOMEM;
+    } else {
+        for (B = a->B_lo + a->first; B <= a->B_hi; B += a->stride) {
+            int64_t V;
+            uint32_t c;
+            per_B(a->r, a->p, B, a->qw, a->qnow, a->qmin, &s, items, gain, &V, &c);
+            a->out->V[B - 1] = V;
+            a->out->kstar[B - 1] = c;
+        }
+    }
+    free(items);
+    free(gain);
+    free(s.D);
+    free(s.T);
+    return NULL;
+}
+
+static int run_B_loop(const orc_requests *r, const orc_params *p, uint32_t B_lo, uint32_t B_hi,
+                      const double *qw, const double *qnow, double qmin, orc_decision *out, int nthreads)
+{
+    bloop_t a[ORC_MAX_THREADS];
+    pthread_t th[ORC_MAX_THREADS];
+    int t, nt = nthreads < 1 ? 1 : (nthreads > ORC_MAX_THREADS ? ORC_MAX_THREADS : nthreads);
+    if ((uint32_t)nt > B_hi - B_lo + 1)
+        nt = (int)(B_hi - B_lo + 1);
+    for (t = 0; t < nt; t++) {
+        a[t].r = r;
+        a[t].p = p;
+        a[t].qw = qw;
+        a[t].qnow = qnow;
+        a[t].qmin = qmin;
+        a[t].out = out;
+        a[t].B_lo = B_lo;
+        a[t].B_hi = B_hi;
+        a[t].stride = (uint32_t)nt;
+        a[t].first = (uint32_t)t;
+    }
+    if (nt == 1) {
+        bloop_worker(&a[0]);
+        return a[0].rc;
+    }
+    for (t = 0; t < nt; t++)
+        if (pthread_create(&th[t], NULL, bloop_worker, &a[t]) != 0) {
+            a[t].rc = ORC_E_NOMEM;
+            bloop_worker(&a[t]); /* run it here instead */
+            th[t] = 0;
+        }
+    for (t = 0; t < nt; t++)
+        if (th[t])
+            pthread_join(th[t], NULL);
+    for (t = 0; t < nt; t++)
+        if (a[t].rc != ORC_OK)
+            return a[t].rc;
+    return ORC_OK;
+}
+
+int oracle_schedule_mt(const orc_requests *r, const orc_params *p, orc_decision *out, int nthreads);
+
 int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *out)
+{
+    return oracle_schedule_mt(r, p, out, 1);
+}
+
+/* The decision (O6-O9).  nthreads > 1 splits the independent per-B walks over threads. */
+int oracle_schedule_mt(const orc_requests *r, const orc_params *p, orc_decision *out, int nthreads)
 {
     uint32_t n = r->n, i, B, k;
     uint64_t run_l = 0, M = p->kv_capacity;
@@ -520,9 +770,9 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
     int triggered;
     uint32_t B_lo, B_hi, k_M, B_star = 0, best_k = 0;
     int64_t best_V = INT64_MIN;
-    item_t *items = NULL, *best_items = NULL, *vict = NULL;
+    item_t *best_items = NULL, *vict = NULL;
     uint32_t *sorted_l = NULL;
-    double *qw = NULL, *gain = NULL, *best_gain = NULL, *qnow = NULL, qmin = 1.0;
+    double *qw = NULL, *best_gain = NULL, *qnow = NULL, qmin = 1.0;
     uint8_t *in_S = NULL;
     scratch_t s = {NULL, NULL};
     int rc = ORC_OK;
@@ -565,14 +815,12 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
     /* S2 batch-size range (readings R16/R17). B_max: add the shortest
      * contexts until M is reached. */
     sorted_l = (uint32_t *)malloc(sizeof(uint32_t) * n);
-    items = (item_t *)malloc(sizeof(item_t) * n);
     best_items = (item_t *)malloc(sizeof(item_t) * n);
     vict = (item_t *)malloc(sizeof(item_t) * n);
     qw = (double *)malloc(sizeof(double) * n);
-    gain = (double *)malloc(sizeof(double) * n);
     best_gain = (double *)malloc(sizeof(double) * n);
     in_S = (uint8_t *)calloc(n, 1);
-    if (!sorted_l || !items || !best_items || !vict || !qw || !gain || !best_gain || !in_S) {
+    if (!sorted_l || !best_items || !vict || !qw || !best_gain || !in_S) {
         rc = ORC_E_NOMEM;
         goto done;
     }
@@ -625,47 +873,25 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
         }
     }
 
-    /* S3/S4 for every candidate B: gains, priorities, Algorithm 1. */
-    for (B = B_lo; B <= B_hi; B++) {
-        uint64_t W = 0;
-        uint32_t c = 0;
-        int64_t V = 0;
-        for (i = 0; i < n; i++) {
-            if (p->flags & ORC_MAXMIN) {
-                double v = qmin - qw[i];
-                gain[i] = v > 0.0 ? v : 0.0;
-            } else if (p->flags & ORC_PERFECT) {
-                double qs = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s);
-                gain[i] = ((qs == 1.0 ? 1.0 : 0.0) - (qw[i] == 1.0 ? 1.0 : 0.0)) * (qnow[i] == 1.0 ? 1.0 : 0.0);
-            } else {
-                gain[i] = q_serve(r, i, p->now_us, p->horizon_us, p->tau_us[B - 1], &s) - qw[i];
-            }
-            items[i].idx = i;
-            items[i].rank = r->rank[i];
-            items[i].key = (p->flags & ORC_LQSF) ? lqsf_key(gain[i]) : priority_key(gain[i], r->ctx_len[i]);
-        }
-        qsort(items, n, sizeof(item_t), cmp_greedy);
-        /* Algorithm 1: take while within M and B, else break. */
-        for (k = 0; k < n; k++) {
-            uint32_t l = r->ctx_len[items[k].idx];
-            if (W + l <= M && c + 1 <= B) {
-                W += l;
-                c += 1;
-                V += gain_fixed(gain[items[k].idx]);
-            } else {
-                break;
-            }
-        }
-        out->V[B - 1] = V;
-        out->kstar[B - 1] = c;
-        /* S5 best B; ties go to the larger B (reading R13): B ascends, so >=. */
-        if (V >= best_V) {
-            best_V = V;
+    /* S3/S4 for every candidate B: gains, priorities, Algorithm 1 (per_B below).  The B
+     * values are independent; with nthreads > 1 they are split over threads (SURVEY.md 8(d)(ii):
+     * the integer outputs V(B), k*(B) do not depend on the split). */
+    if (run_B_loop(r, p, B_lo, B_hi, qw, qnow, qmin, out, nthreads) != ORC_OK) {
+        rc = ORC_E_NOMEM;
+        goto done;
+    }
+    /* S5 best B; ties go to the larger B (reading R13): B ascends, so >=. */
+    for (B = B_lo; B <= B_hi; B++)
+        if (out->V[B - 1] >= best_V) {
+            best_V = out->V[B - 1];
             B_star = B;
-            best_k = c;
-            memcpy(best_items, items, sizeof(item_t) * n);
-            memcpy(best_gain, gain, sizeof(double) * n);
         }
+    /* S_{B*}: the greedy order and gains at B* (the same per_B walk, recomputed once) */
+    {
+        int64_t Vb;
+        uint32_t cb;
+        per_B(r, p, B_star, qw, qnow, qmin, &s, best_items, best_gain, &Vb, &cb);
+        best_k = cb;
     }
     out->scalars[0] = B_star;
     out->scalars[7] = best_k;
@@ -745,12 +971,10 @@ int oracle_schedule(const orc_requests *r, const orc_params *p, orc_decision *ou
 
 done:
     free(sorted_l);
-    free(items);
     free(best_items);
     free(vict);
     free(qw);
     free(qnow);
-    free(gain);
     free(best_gain);
     free(in_S);
     free(s.D);

@@ -41,6 +41,11 @@ ANDES_F_TRIGGERED = 1
 ANDES_F_CAP_HIT = 2
 ANDES_F_CAP_OVERRIDDEN = 4
 ANDES_F_SLOW_PATH = 8
+ANDES_F_TRUNCATED = 16
+ANDES_E_INVAL = -1
+ANDES_E_RANGE = -2
+ANDES_E_CUDA = -3
+ANDES_E_CAPACITY = -5
 UINT32_MAX = 0xFFFFFFFF
 SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags", "k_star"]
 
@@ -56,7 +61,9 @@ STAGES = ["prep", "scan", "state", "cand", "select", "unused"]
 
 
 class AndesError(RuntimeError):
-    pass
+    def __init__(self, msg, rc=None):
+        super().__init__(msg)
+        self.rc = rc
 
 
 class Limits(C.Structure):
@@ -228,7 +235,7 @@ class Context:
 
     def _check(self, rc, what):
         if rc < 0:
-            raise AndesError(f"{what} failed rc={rc}: {lib().andes_last_error(self._h).decode()}")
+            raise AndesError(f"{what} failed rc={rc}: {lib().andes_last_error(self._h).decode()}", rc)
         return rc
 
     # -- profiling hooks

@@ -31,7 +31,7 @@ struct AndesCtx {
   Work w{};
   std::vector<void*> allocs;
   uint32_t* B_list_dev = nullptr;
-  uint32_t* err_pinned = nullptr;  // mapped/pinned copy of the device error word (debug checks)
+  uint32_t* err_pinned = nullptr;  // mapped pinned sticky error word (kernels raise bits into it)
   // device mirrors for andes_schedule_host
   struct Mirror {
     int64_t* arrival;
@@ -119,14 +119,19 @@ int check_requests(AndesCtx* c, const AndesRequests* r, bool need_sched_fields) 
   return ANDES_OK;
 }
 
+// The sticky error word: kernels of earlier calls raise bits into mapped pinned host memory
+// (raise_err); the first call that finds it non-zero reports it and clears it.  A failing call
+// is reported by the next call once the failing kernel has run (no synchronisation is added).
 int pending_device_error(AndesCtx* c) {
-  if (c->err_pinned && *c->err_pinned) {
-    const uint32_t e = *c->err_pinned;
-    *c->err_pinned = 0;
-    char buf[128];
-    snprintf(buf, sizeof buf, "device precondition check failed (error word 0x%x)", e);
+  volatile uint32_t* h = c->err_pinned;
+  if (h && *h) {
+    const uint32_t e = *h;
+    *h = 0;
+    char buf[160];
+    snprintf(buf, sizeof buf, "%s (error word 0x%x)",
+             (e & kErrCapacity) ? "capacity exceeded on the device" : "device precondition check failed", e);
     c->err = buf;
-    return (e & (kErrRunning | 128u)) ? ANDES_E_CAPACITY : ANDES_E_RANGE;
+    return (e & kErrCapacity) ? ANDES_E_CAPACITY : ANDES_E_RANGE;
   }
   return ANDES_OK;
 }
@@ -201,10 +206,8 @@ inline void mark(AndesCtx* c, int i, cudaStream_t s) {
 }
 
 int finish_call(AndesCtx* c, cudaStream_t s, bool debug) {
-  if (debug) {
-    cudaError_t e = cudaMemcpyAsync(c->err_pinned, &c->w.g->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return cuda_check(c, e, "error word copy");
-  }
+  (void)s;
+  (void)debug;
   return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
 
@@ -281,6 +284,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.qnow, N)) != cudaSuccess || (e = ctx_alloc(c, &w.vmark, N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.rf_vend, kMaxB)) != cudaSuccess || (e = ctx_alloc(c, &w.rf_D, kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.rf_loss, kMaxB)) != cudaSuccess ||
+      (e = ctx_alloc(c, &w.rank_set, 2ull * N)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
@@ -292,8 +296,9 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
   cudaMemset(w.hist_lb, 0, sizeof(uint32_t) * kHistK);
   cudaMemset(w.hist_ub, 0, sizeof(uint32_t) * kHistK);
   cudaMemset(w.hist_zr, 0, sizeof(uint32_t) * kHistK);
-  if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocDefault)) != cudaSuccess) {
-    int rc = cuda_check(c, e, "pinned alloc");
+  if ((e = cudaHostAlloc((void**)&c->err_pinned, sizeof(uint32_t), cudaHostAllocMapped)) != cudaSuccess ||
+      (e = cudaHostGetDevicePointer((void**)&w.err_map, c->err_pinned, 0)) != cudaSuccess) {
+    int rc = cuda_check(c, e, "mapped pinned alloc");
     andes_destroy(c);
     return rc;
   }
@@ -517,6 +522,7 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   // words), then Q_now (and its minimum); the tile counter is reset for the main scan
   const bool dual = w.obj != kObjAndes && r.n;
   launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask, p->now_us, dual);
+  if (debug) launch_debug_checks(L, r, w, p->now_us);
   if (dual) {
     Work wn = w;
     wn.m = w.m_now;
@@ -600,6 +606,7 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
     case 0: {
       if ((rc = reset_call(c, s))) return rc;
       launch_prep(L, r, w, eval, false, true, p->kv_capacity, debug, out->serve_mask);
+      if (debug) launch_debug_checks(L, r, w, p->now_us);
       const CUtensorMap* tm = c->pool_map;
       if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
       launch_scan(L, r, w, eval, false, tm);
@@ -653,12 +660,17 @@ int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedPa
   if (!rq || !p || !out) return set_err(c, ANDES_E_INVAL, "NULL argument%s");
   if (rq->n > c->lim.max_requests) return set_err(c, ANDES_E_CAPACITY, "n exceeds limits.max_requests%s");
   if (!p->tau_us || p->B_cap == 0 || p->B_cap > c->lim.max_B) return set_err(c, ANDES_E_INVAL, "bad tau/B_cap%s");
+  if (p->horizon_us == 0 || p->kv_capacity == 0) return set_err(c, ANDES_E_INVAL, "horizon and M must be >= 1%s");
   const uint32_t n = rq->n;
+  // every required host array is checked before any copy: a NULL one would otherwise leave the
+  // device mirror holding an earlier call's data
+  if (n && (!rq->arrival_us || !rq->ttft_us || !rq->period_us || !rq->ctx_len || !rq->n_deliv ||
+            !rq->max_total || !rq->rank || !rq->running || !rq->tl_base || !rq->tl_pool))
+    return set_err(c, ANDES_E_INVAL, "a required request array is NULL%s");
+  if (!out->scalars || !out->V || !out->kstar || !out->admit_idx || (n && (!out->serve_mask || !out->preempt_idx)))
+    return set_err(c, ANDES_E_INVAL, "a decision output is NULL%s");
   uint64_t span = 0;
-  if (n) {
-    if (!rq->tl_base || !rq->n_deliv) return set_err(c, ANDES_E_INVAL, "tl_base/n_deliv NULL%s");
-    span = rq->tl_base[n - 1] + rq->n_deliv[n - 1];
-  }
+  if (n) span = rq->tl_base[n - 1] + rq->n_deliv[n - 1];
   if (span > c->lim.max_tokens) return set_err(c, ANDES_E_CAPACITY, "timestamp pool exceeds limits.max_tokens%s");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto& m = c->mir;

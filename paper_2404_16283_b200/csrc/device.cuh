@@ -37,9 +37,12 @@ constexpr unsigned long long kStPrefix = 2ull << 62;
 constexpr unsigned long long kStMask = 3ull << 62;
 constexpr unsigned long long kFlagBit = 1ull << 32;
 
-// device error word bits (ANDES_DEBUG_CHECKS)
+// device error word bits.  Data preconditions (set only under ANDES_DEBUG_CHECKS): period,
+// context length, tl_base order, timestamps, rank uniqueness, tokens due; capacity (always):
+// running set above the workspace limits, timestamp pool above limits.max_tokens.
 constexpr uint32_t kErrPeriod = 1u, kErrCtx = 2u, kErrBase = 4u, kErrTimes = 8u, kErrRank = 16u,
                    kErrRunning = 32u, kErrDue = 64u, kErrTokens = 128u;
+constexpr uint32_t kErrCapacity = kErrRunning | kErrTokens;
 
 // ---------------------------------------------------------------- views
 struct ReqView {
@@ -88,7 +91,7 @@ struct Globals {
   uint32_t done;                 // select CTAs finished (last-block pattern)
   uint32_t B_lo, B_hi;           // candidate range
   uint32_t triggered;
-  uint32_t err;                  // device error word (debug checks), copied out by the host
+  uint32_t err;                  // this call's error bits (kErr*); also raised to Work::err_map
   uint32_t slow;                 // slow-path flags
   uint32_t tile_ctr;             // dynamic tile counter of the timeline scan
   uint32_t prep_done;            // prep CTAs finished (last-block pattern)
@@ -209,7 +212,23 @@ struct Work {
   uint32_t* rf_vend;         // [kMaxB] victims consumed after pair k
   long long* rf_D;           // [kMaxB] stall of pair k (us)
   long long* rf_loss;        // [kMaxB] QoE loss of pair k in units of 2^-32
+  // error reporting: mapped pinned host word (the context's sticky error word, read and cleared
+  // by the host at the start of the next call; no copy node, no synchronisation)
+  uint32_t* err_map;
+  // debug checks: open-addressing set of ranks (2 N_cap slots, self-cleaning), rank uniqueness
+  unsigned long long* rank_set;
 };
+
+// ---------------------------------------------------------------- error reporting
+// Raise error bits: into this call's Globals word (read by the decision's own kernels, e.g. the
+// ANDES_F_TRUNCATED flag) and into the mapped host word the next call reports.  Error paths only.
+__device__ __forceinline__ void raise_err(const Work& w, uint32_t bits) {
+  atomicOr(&w.g->err, bits);
+  if (w.err_map) {
+    volatile uint32_t* h = w.err_map;
+    *h = *h | bits;
+  }
+}
 
 // ---------------------------------------------------------------- small helpers
 __host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }

@@ -61,7 +61,6 @@ void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, i
                           const uint32_t* tau, const uint32_t* B_list_dev, uint32_t nB, double* gain_out,
                           float* key_out, double* qwait_out);
 void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon);
-void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau);
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o,
                    XEntry* xsend = nullptr);
@@ -84,5 +83,6 @@ void launch_knapsack_dp(cudaStream_t s, const long long* q, const uint32_t* l, u
 void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o, int64_t now,
                    const uint32_t* tau, uint64_t M, uint32_t prefill, uint32_t swap);
 void init_kernels();
+void launch_debug_checks(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now);
 
 }  // namespace andes

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
       if (debug && (l == 0 || l > kv_cap)) local_err |= kErrCtx;
     }
   }
-  if (local_err) atomicOr(&w.g->err, local_err);
+  if (local_err) raise_err(w, local_err);
   if (__any_sync(0xffffffffu, local_unal) && (threadIdx.x & 31) == 0) atomicOr(&w.g->unal, 1u);
   if (!sched) return;
   for (int o = 16; o; o >>= 1) {

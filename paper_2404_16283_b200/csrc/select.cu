@@ -335,7 +335,7 @@ __device__ void finalize_decision(const SelectArgs& A, const FinSmem& F) {
   const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
   const uint32_t n_run_all = __ldcg(&w.g->n_run);
   const uint32_t n_run = min(n_run_all, (uint32_t)kMaxRunning);
-  if (n_run_all > (uint32_t)kMaxRunning && tid == 0) atomicOr(&w.g->err, kErrRunning);
+  if (n_run_all > (uint32_t)kMaxRunning && tid == 0) raise_err(w, kErrRunning);
   if (!trig) {
     if (tid == 0) {
       for (int q = 0; q < 8; ++q) sc[q] = 0u;
@@ -992,12 +992,6 @@ void launch_state(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t n
 void launch_compact(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* lb_src, uint32_t G) {
   const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count) : 1u;
   launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w, lb_src, G);
-}
-
-void launch_cand(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* tau) {
-  const uint32_t cblocks = r.n ? umin32((r.n + kCandThreads - 1) / kCandThreads, L.sm_count) : 1u;
-  launch_pdl(k_compact, cblocks, kCandThreads, 0, L.stream, r, w, (const uint32_t*)nullptr, 1u);
-  (void)tau;
 }
 
 // victims keys + indices + prefix sums (the fused S5/S6 tail needs all three)

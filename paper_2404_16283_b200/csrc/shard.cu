@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kSelThreads) k_shard_merge(MergeArgs A) {
   if (tid == 0) {
     A.send->count = s_nv;
     A.send->pad[0] = A.send->pad[1] = A.send->pad[2] = 0u;
-    if (__ldcg(&w.g->n_run) > (uint32_t)kStageRun) atomicOr(&w.g->err, kErrRunning);
+    if (__ldcg(&w.g->n_run) > (uint32_t)kStageRun) raise_err(w, kErrRunning);
   }
 }
 
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kSelThreads) k_shard_cap(ReqView r, Work w, co
   if (tid == 0) {
     uint32_t nv = 0;
     for (uint32_t g = 0; g < G; ++g) nv += __ldcg(&recv[g].count);
-    if (nv > (uint32_t)kVictCap) atomicOr(&w.g->err, kErrRunning);
+    if (nv > (uint32_t)kVictCap) raise_err(w, kErrRunning);
     s_nv = min(nv, (uint32_t)kVictCap);
     s_e = 0;
     s_a = 0;

@@ -1,12 +1,13 @@
 """Multi-GPU decision (andes_schedule_shard) on one GPU: G shard contexts run the
 five steps in lockstep and the round blocks are gathered exactly as an all-gather would (rank
-order).  Pin (SURVEY 8(c) "Multi-GPU"): the sharded decision equals the single-GPU decision on
-the concatenated population bit for bit, which itself equals the oracle (test_gpu_parity)."""
+order).  Pins (SURVEY 8(c) "Multi-GPU"): the sharded decision equals the CPU oracle's decision on
+the concatenated population bit for bit, and equals the single-GPU decision."""
 import numpy as np
 import pytest
 import torch
 
 import workloads as W
+from conftest import assert_decision_equal, oracle_decision_cached, snapshot_cached
 
 pytestmark = pytest.mark.gpu
 
@@ -81,9 +82,21 @@ def single(A, snap, cap=None, flags=1, cur_latency=0):
                 preempt=d.preempt.cpu().numpy().view(np.uint32)[:sc[3]], mask=d.serve_mask.cpu().numpy()[:snap.n])
 
 
-def check(A, snap, G, cuts=None, **kw):
+def check(A, orc, snap, G, cuts=None, name=None, **kw):
+    """Sharded decision == oracle decision (every output, lists in order) and == the single-GPU
+    decision.  name: a full-size snapshot whose oracle decision is cached across tests."""
     res = run_sharded(A, snap, G, cuts=cuts, **kw)
     ref = single(A, snap, **kw)
+    okw = dict(cap=kw.get("cap"), flags=kw.get("flags", 1), cur_latency=kw.get("cur_latency", 0))
+    if name is not None:
+        o = oracle_decision_cached(orc, name, snap, **okw)
+    else:
+        cap = snap.preempt_cap if okw["cap"] is None else okw["cap"]
+        o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity, preempt_cap=cap,
+                         cur_latency_us=okw["cur_latency"], flags=okw["flags"], threads=orc.nproc())
+    mask = np.concatenate([r["mask"] for r in res])
+    for r in res:
+        assert_decision_equal(dict(r, mask=mask), o)
     trig = bool(ref["sc"][6] & 1)
     np.testing.assert_array_equal(np.concatenate([r["mask"] for r in res]), ref["mask"])
     for r in res:
@@ -100,53 +113,53 @@ def check(A, snap, G, cuts=None, **kw):
 
 
 @pytest.mark.parametrize("seed", range(24))
-def test_shard_random_small(A, seed):
+def test_shard_random_small(A, orc, seed):
     rng = np.random.default_rng(seed)
     snap = W.random_small(seed, B_cap=int(rng.integers(1, 20)))
     G = int(rng.integers(1, 6))
-    check(A, snap, G, flags=[1, 3, 0, 2][seed % 4], cur_latency=[0, 400_000][seed % 2],
+    check(A, orc, snap, G, flags=[1, 3, 0, 2][seed % 4], cur_latency=[0, 400_000][seed % 2],
           cap=[W.UINT32_MAX, 0, 2][seed % 3])
 
 
-def test_shard_uneven_and_empty_shards(A):
+def test_shard_uneven_and_empty_shards(A, orc):
     snap = W.random_small(3, n=25, B_cap=12)
-    check(A, snap, 4, cuts=[0, 0, 3, 25, 25])
-    check(A, snap, 8, cuts=[0, 1, 2, 3, 4, 5, 6, 7, 25])
+    check(A, orc, snap, 4, cuts=[0, 0, 3, 25, 25])
+    check(A, orc, snap, 8, cuts=[0, 1, 2, 3, 4, 5, 6, 7, 25])
 
 
-def test_shard_golden_g1(A):
+def test_shard_golden_g1(A, orc):
     from test_oracle_pins import g1_snapshot
     for cap in (W.UINT32_MAX, 0, 1):
         snap, d = g1_snapshot(cap)
-        res, ref = check(A, snap, 2, cap=cap)
+        res, ref = check(A, orc, snap, 2, cap=cap)
         assert int(res[0]["sc"][0]) == d["expected"]["B_star"]
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_shard_config2(A, G):
-    snap = W.config2()
-    check(A, snap, G)
-    check(A, snap, G, cap=16, flags=3)
+def test_shard_config2(A, orc, G):
+    snap = snapshot_cached("config2")
+    check(A, orc, snap, G, name="config2")
+    check(A, orc, snap, G, cap=16, flags=3, name="config2")
 
 
-def test_shard_config3(A):
-    snap = W.config3()
+def test_shard_config3(A, orc):
+    snap = snapshot_cached("config3")
     for G in (1, 2, 8):
-        check(A, snap, G)
+        check(A, orc, snap, G, name="config3")
 
 
-def test_shard_long_contexts_reach_the_long_bucket(A):
+def test_shard_long_contexts_reach_the_long_bucket(A, orc):
     """Few short contexts: the B_max walk of step 1 needs the ranks' lists of their smallest
     contexts >= 4095 tokens (exact merge)."""
     snap = W.random_small(8, n=40, B_cap=16)
     rng = np.random.default_rng(2)
     snap.ctx_len[:] = rng.integers(4000, 9000, snap.n).astype(np.uint32)
     snap.kv_capacity = 60_000
-    check(A, snap, 3)
-    check(A, snap, 5, cap=1)
+    check(A, orc, snap, 3)
+    check(A, orc, snap, 5, cap=1)
 
 
-def test_shard_lqsf(A):
-    snap = W.config2()
-    check(A, snap, 3, flags=1 | 16, cap=16)
-    check(A, W.random_small(5, B_cap=9), 2, flags=1 | 16)
+def test_shard_lqsf(A, orc):
+    snap = snapshot_cached("config2")
+    check(A, orc, snap, 3, flags=1 | 16, cap=16, name="config2")
+    check(A, orc, W.random_small(5, B_cap=9), 2, flags=1 | 16)

@@ -539,3 +539,27 @@ def test_refiner_zero_overhead_is_identity(orc):
     z = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
                      flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=0)
     assert list(z.admit) == list(base.admit) and list(z.preempt) == list(base.preempt)
+
+
+def test_threaded_oracle_equals_single_thread(orc):
+    """The per-B walks (S3/S4) and the per-request walks (S1, gains) are independent; splitting
+    them over threads must leave every output unchanged."""
+    snap = W.config2()
+    kw = dict(preempt_cap=16)
+    o1 = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us[:40], snap.kv_capacity, B_cap=40, **kw)
+    for th in (2, 3, 8):
+        o = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us[:40], snap.kv_capacity, B_cap=40,
+                         threads=th, **kw)
+        for f in ("serve_mask", "admit", "preempt", "V", "kstar"):
+            np.testing.assert_array_equal(getattr(o, f), getattr(o1, f))
+        assert (o.B_star, o.realized, o.B_lo, o.B_hi, o.flags, o.k_star) == \
+            (o1.B_star, o1.realized, o1.B_lo, o1.B_hi, o1.flags, o1.k_star)
+    q1 = orc.qoe_eval(snap, snap.now_us)
+    q8 = orc.qoe_eval(snap, snap.now_us, threads=8)
+    for a, b in zip(q1, q8):
+        np.testing.assert_array_equal(a, b)
+    Bl = np.array([1, 7, 40])
+    g1 = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, Bl)
+    g8 = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, Bl, threads=5)
+    for a, b in zip(g1, g8):
+        np.testing.assert_array_equal(a, b)
