@@ -86,6 +86,8 @@ def lib():
         _lib.oracle_gain_estimate_mt.argtypes = [C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_uint32,
                                                  C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                                  C.c_int]
+        _lib.oracle_overhead_us.restype = C.c_int
+        _lib.oracle_overhead_us.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p, C.c_void_p]
         _lib.oracle_schedule_mt.restype = C.c_int
         _lib.oracle_schedule_mt.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     return _lib
@@ -169,6 +171,14 @@ def gain_estimate(req, now_us, horizon_us, tau_us, B_list, threads=1):
     if rc != 0:
         raise ValueError(f"oracle_gain_estimate rc={rc}")
     return gain, key, qw
+
+
+def overhead_us(prefill_tok_s, swap_tok_s, l, queued=False):
+    """Reading R24's (preempt, resume) cost in us of a request of context l."""
+    pre, res = C.c_int64(), C.c_int64()
+    lib().oracle_overhead_us(int(prefill_tok_s), int(swap_tok_s), int(l), int(bool(queued)), C.byref(pre),
+                             C.byref(res))
+    return pre.value, res.value
 
 
 @dataclass

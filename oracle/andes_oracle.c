@@ -529,6 +529,18 @@ static void overhead_us(const orc_params *p, uint32_t l, int queued, int64_t *pr
     }
 }
 
+/* The R24 overhead model itself, exported for the pins (SPEC preemption_overhead /
+ * select_mechanism examples): *pre / *res in microseconds. */
+int oracle_overhead_us(uint32_t prefill_tok_s, uint32_t swap_tok_s, uint32_t l, int queued, int64_t *pre, int64_t *res)
+{
+    orc_params p;
+    memset(&p, 0, sizeof p);
+    p.prefill_tok_s = prefill_tok_s;
+    p.swap_tok_s = swap_tok_s;
+    overhead_us(&p, l, queued, pre, res);
+    return ORC_OK;
+}
+
 /* R25-R27: walk the admits (greedy order); each takes the minimal prefix of the remaining
  * victims (victim order) that makes room in M; its stall D = the victims' preempt costs + its
  * own resume cost; loss = sum over the requests still running after the pair of

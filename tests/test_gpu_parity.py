@@ -578,3 +578,17 @@ def test_scan_unit_width_forced(tw):
     r = subprocess.run([sys.executable, "-c", _TW2_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "tw2 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_refiner_fig7_toy_on_gpu(A, ctx, orc):
+    """The constructed Fig. 7 scenario (test_oracle_pins.fig7_snapshot) through the
+    C ABI: admits {R9, R10}, preempts {R1, R2} after refinement, equal to the oracle, also with
+    swapping available and with cheap admissions (every pair kept)."""
+    from test_oracle_pins import fig7_snapshot
+    snap = fig7_snapshot()
+    g, o = _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=50)
+    assert (g["admit"] + 1).tolist() == [10, 9] and (g["preempt"] + 1).tolist() == [1, 2]
+    g, o = _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=200)
+    assert (g["admit"] + 1).tolist() == [10, 9, 8]
+    for prefill, swap in ((50, 100), (50, 1000), (25, 400)):
+        _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=prefill, swap=swap)

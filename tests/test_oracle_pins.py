@@ -563,3 +563,81 @@ def test_threaded_oracle_equals_single_thread(orc):
     g8 = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, Bl, threads=5)
     for a, b in zip(g1, g8):
         np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- refiner pins fixed by the paper / SPEC
+def test_overhead_model_spec_examples(orc):
+    """SPEC preemption_overhead / select_mechanism, the R24 model: recompute =
+    (0, one prefill of the context), swap = (l / bandwidth, l / bandwidth), the faster round trip,
+    ties to swap ("selects the faster one")."""
+    # recompute, context 5000 at 5000 tok/s -> (0, 1.0 s)  (no swapping available)
+    assert orc.overhead_us(5000, 0, 5000) == (0, 1_000_000)
+    # swap, context 4000 at 20000 tok/s -> (0.2, 0.2) s: recompute at 5000 tok/s would take 0.8 s
+    assert orc.overhead_us(5000, 20000, 4000) == (200_000, 200_000)
+    # equal totals (recompute 0.4 s = swap 0.2 + 0.2 s) -> swap
+    assert orc.overhead_us(10000, 20000, 4000) == (200_000, 200_000)
+    # recompute total below swap total -> recompute
+    assert orc.overhead_us(20000, 20000, 4000) == (0, 200_000)
+    # a queued request's admission is its prefill (nothing to swap in)
+    assert orc.overhead_us(5000, 20000, 4000, queued=True) == (0, 800_000)
+
+
+def fig7_snapshot():
+    """The refiner's motivating example (Fig. 7), constructed: ten requests of
+    context 100 in M = 700 (one victim frees room for one admit), B = 1..7, tau = 50 ms,
+    Delta t = 2 s, ttft 1 s, 5 tok/s.
+      R1-R3 running, far ahead of schedule (gain 0; R1 the lowest priority by the rank tie-break);
+      R4-R7 running, exactly on schedule with no buffer (gain 9/308 each; a 2 s stall costs each
+             exactly that QoE: Q_now = 1 -> Q(now + 2 s) = 1 - 9/308);
+      R8-R10 queued for 8 s / 1.5 s / 0.5 s (gains ~0.05 / ~0.62 / 1).
+    Recomputation at 50 tok/s: admitting a queued request stalls everyone for 2 s."""
+    S = 1_000_000
+    now = 20 * S
+    tls, arr, run = [], [], []
+    for _ in range(3):
+        arr.append(now - 10 * S)
+        tls.append((S + np.arange(80) * 50_000).astype(np.uint32))
+        run.append(1)
+    for _ in range(4):
+        arr.append(now - 10 * S)
+        tls.append((S + np.arange(46) * 200_000).astype(np.uint32))
+        run.append(1)
+    for x in (8 * S, 3 * S // 2, S // 2):
+        arr.append(now - x)
+        tls.append(np.zeros(0, np.uint32))
+        run.append(0)
+    n = 10
+    g, base, pool = W._pack(tls)
+    return W.Snapshot(arrival_us=np.array(arr, np.int64), ttft_us=np.full(n, S, np.uint32),
+                      period_us=np.full(n, 200_000, np.uint32), ctx_len=np.full(n, 100, np.uint32), n_deliv=g,
+                      max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=np.array([2, 1, 0, 3, 4, 5, 6, 7, 8, 9], np.uint32), running=np.array(run, np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=now, horizon_us=2 * S, tau_us=np.full(7, 50_000, np.uint32),
+                      kv_capacity=700)
+
+
+def test_refiner_fig7_toy(orc):
+    """Fig. 7 (SPEC refine example): the priority scheduler admits
+    {R8, R9, R10} and preempts {R1, R2, R3}; the refiner keeps (R10, R1) and (R9, R2) because each
+    admit's gain exceeds the QoE the ongoing requests lose to the stall, rejects (R8, R3) and
+    cancels the rest: it "admits only {R9, R10} and preempts {R1, R2}"."""
+    snap = fig7_snapshot()
+    gain, key, qw = orc.gain_estimate(snap, snap.now_us, snap.horizon_us, snap.tau_us, [7])
+    # hand values: R4-R7 on schedule with 10 tokens due in the horizon -> S_d = 9 s, S_w = 308 s
+    for i in range(3, 7):
+        assert abs(gain[0, i] - 9 / 308) < 1e-15
+    assert gain[0, 9] == 1.0 and list(gain[0, :3]) == [0.0, 0.0, 0.0]
+    loss = 4 * round(9 / 308 * 2 ** 32)  # four on-schedule requests each lose 9/308 under a 2 s stall
+    assert round(gain[0, 8] * 2 ** 32) > loss > round(gain[0, 7] * 2 ** 32) > 0
+    base = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity)
+    assert base.B_star == 7
+    assert (base.admit + 1).tolist() == [10, 9, 8] and (base.preempt + 1).tolist() == [1, 2, 3]
+    ref = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                       flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=50)
+    assert ref.flags & orc.ORC_FLAG_REFINED
+    assert (ref.admit + 1).tolist() == [10, 9] and (ref.preempt + 1).tolist() == [1, 2]
+    assert ref.serve_mask.tolist() == [0, 0, 1, 1, 1, 1, 1, 0, 1, 1]
+    # cheaper admissions (prefill 200 tok/s: 0.5 s stalls cost far less) keep all three pairs
+    cheap = orc.schedule(snap, snap.now_us, snap.horizon_us, snap.tau_us, snap.kv_capacity,
+                         flags=orc.ORC_FORCE | orc.ORC_REFINE, prefill_tok_s=200)
+    assert (cheap.admit + 1).tolist() == [10, 9, 8] and (cheap.preempt + 1).tolist() == [1, 2, 3]
