@@ -225,6 +225,32 @@ int andes_schedule(AndesCtx *ctx, const AndesRequests *req, const AndesSchedPara
 int andes_schedule_host(AndesCtx *ctx, const AndesRequests *req_host, const AndesSchedParams *p_host,
                         AndesDecision *out_host, void *stream);
 
+/* ---- Request Tracker update ---------------------------------------------------
+ * Device-resident tracker state: the mutable views of the AndesRequests arrays a serving loop
+ * updates between decisions (DEVICE memory owned by the caller).  Each timeline must have room
+ * to grow: request i may hold tl_base[i+1] - tl_base[i] tokens (the last one tl_len - tl_base).
+ * Timelines should start 16-byte aligned (the scan's fast path); appending keeps them so. */
+typedef struct {
+    uint32_t n;
+    const int64_t *arrival_us;
+    const uint64_t *tl_base;
+    uint32_t *tl_pool;
+    uint64_t tl_len;
+    uint32_t *n_deliv;
+    uint32_t *ctx_len;
+    uint8_t *running;
+} AndesTracker;
+
+/* One iteration's deliveries: token k (k < count) of request idx[k] reached its client at absolute
+ * time t_abs[k]; idx/t_abs are DEVICE arrays in which a request's tokens are consecutive and in
+ * time order.  Appends t_abs[k] - a_i to the request's timeline, n_deliv[i] += 1, ctx_len[i] += 1
+ * (a generated token extends the context l_i of Eq. 5).  serve_mask (DEVICE u8[n], optional, e.g.
+ * the decision's output) becomes the running set.  Asynchronous on stream, capture safe.  A token
+ * without room in its timeline is dropped and the next call returns ANDES_E_CAPACITY.
+ * Errors: ANDES_E_INVAL (NULL arrays). */
+int andes_tracker_append(AndesCtx *ctx, const AndesTracker *t, const uint32_t *idx, const int64_t *t_abs,
+                         uint32_t count, const uint8_t *serve_mask, void *stream);
+
 /* ---- Multi-GPU decision ------------------------------------------
  * One process per GPU; rank g holds a contiguous range of the population (its requests have
  * global indices base_g .. base_g + n_g - 1, base_g = n_0 + ... + n_{g-1}; the rank fields must

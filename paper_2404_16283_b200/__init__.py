@@ -52,7 +52,7 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
            "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean", "andes_knapsack_dp",
-           "andes_knapsack_dp_workspace"]
+           "andes_knapsack_dp_workspace", "andes_tracker_append"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -96,6 +96,11 @@ class Shard(C.Structure):
                 ("xbytes", C.c_uint64 * SHARD_ROUNDS)]
 
 
+class Tracker(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("arrival_us", C.c_void_p), ("tl_base", C.c_void_p), ("tl_pool", C.c_void_p),
+                ("tl_len", C.c_uint64), ("n_deliv", C.c_void_p), ("ctx_len", C.c_void_p), ("running", C.c_void_p)]
+
+
 class QoeOut(C.Structure):
     _fields_ = [("q", C.c_void_p), ("q64", C.c_void_p), ("s_delay", C.c_void_p), ("s_whole", C.c_void_p),
                 ("m", C.c_void_p)]
@@ -134,6 +139,8 @@ def lib() -> C.CDLL:
         L.andes_knapsack_dp_workspace.restype = C.c_uint64
         L.andes_knapsack_dp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64,
                                         C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.andes_tracker_append.argtypes = [C.c_void_p, C.POINTER(Tracker), C.c_void_p, C.c_void_p, C.c_uint32,
+                                           C.c_void_p, C.c_void_p]
         L.andes_shard_init.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Shard)]
         L.andes_schedule_shard.argtypes = [C.c_void_p, C.POINTER(Shard), C.c_uint32, C.POINTER(Requests),
                                            C.POINTER(SchedParams), C.POINTER(DecisionPtrs), C.c_void_p, C.c_void_p,
@@ -191,7 +198,7 @@ def requests_to(src, device="cuda", pin=False):
 
 
 def _req_struct(t: dict, n: int) -> Requests:
-    return Requests(n, *[_ptr(t[name]) for name, _ in _FIELDS], int(t["tl_pool"].numel()))
+    return Requests(n, *[_ptr(t[name]) for name, _ in _FIELDS], int(t["tl_pool"].numel()) if t["tl_pool"] is not None else 0)
 
 
 @dataclass
@@ -338,6 +345,18 @@ class Context:
         rc = self._check(lib().andes_schedule_host(self._h, C.byref(_req_struct(req_host, n)), C.byref(p),
                                                    C.byref(d), _stream_ptr(stream)), "andes_schedule_host")
         return out, rc
+
+    # -- andes_tracker_append (device-resident Request Tracker update between decisions)
+    def tracker_append(self, req: dict, n: int, idx, t_abs, serve_mask=None, stream=None):
+        """req: the device request tensors (updated in place: tl_pool, n_deliv, ctx_len, running);
+        idx: device int32 [count] request index of each delivered token (a request's tokens
+        consecutive, in time order); t_abs: device int64 [count] absolute delivery times;
+        serve_mask: device uint8 [n] (optional) -> the new running set."""
+        t = Tracker(int(n), _ptr(req["arrival_us"]), _ptr(req["tl_base"]), _ptr(req["tl_pool"]),
+                    int(req["tl_pool"].numel()), _ptr(req["n_deliv"]), _ptr(req["ctx_len"]), _ptr(req["running"]))
+        count = int(idx.numel()) if idx is not None else 0
+        self._check(lib().andes_tracker_append(self._h, C.byref(t), _ptr(idx), _ptr(t_abs), count, _ptr(serve_mask),
+                                               _stream_ptr(stream)), "andes_tracker_append")
 
     # -- multi-GPU decision (andes_shard_init / andes_schedule_shard)
     def shard_init(self, world: int, rank: int, B_cap: int) -> Shard:

@@ -191,7 +191,7 @@ int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap*
 // per-call reset of the small globals and the look-back status words
 int reset_call(AndesCtx* c, cudaStream_t s) {
   // (the look-back status words are zeroed by k_prep, tile by tile)
-  cudaError_t e = cudaMemsetAsync(c->w.g, 0, sizeof(Globals), s);
+  cudaError_t e = cudaMemsetAsync(c->w.g, 0, 2 * sizeof(Globals), s);  // + the fused kernel's barrier line
   return cuda_check(c, e, "memset");
 }
 
@@ -285,7 +285,7 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
       (e = ctx_alloc(c, &w.rf_vend, kMaxB)) != cudaSuccess || (e = ctx_alloc(c, &w.rf_D, kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.rf_loss, kMaxB)) != cudaSuccess ||
       (e = ctx_alloc(c, &w.rank_set, 2ull * N)) != cudaSuccess ||
-      (e = ctx_alloc(c, &w.g, 1)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
+      (e = ctx_alloc(c, &w.g, 2)) != cudaSuccess || (e = ctx_alloc(c, &c->B_list_dev, kMaxB)) != cudaSuccess) {
     int rc = cuda_check(c, e, "workspace allocation");
     andes_destroy(c);
     return rc;
@@ -544,11 +544,18 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
     launch_scan(L, r, w, eval, false, tm, true, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
   }
   mark(c, 2, s);
-  launch_state(L, r, w, p->now_us, p->horizon_us);
-  mark(c, 3, s);
-  launch_compact(L, r, w, nullptr, 1u);
-  mark(c, 4, s);
-  launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
+  // S3-S6: one fused cooperative kernel when its grid fits on the GPU, else three kernels
+  if (!launch_decide(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity,
+                                p->preempt_cap, o)) {
+    launch_state(L, r, w, p->now_us, p->horizon_us);
+    mark(c, 3, s);
+    launch_compact(L, r, w, nullptr, 1u);
+    mark(c, 4, s);
+    launch_select(L, r, w, p->now_us, p->horizon_us, p->tau_us, p->B_cap, p->kv_capacity, p->preempt_cap, o);
+  } else {
+    mark(c, 3, s);
+    mark(c, 4, s);
+  }
   if (p->flags & ANDES_REFINE)
     launch_refine(L, r, w, o, p->now_us, p->tau_us, p->kv_capacity, p->prefill_tok_s, p->swap_tok_s);
   mark(c, 5, s);
@@ -634,6 +641,20 @@ int andes_schedule_shard(AndesCtx* c, const AndesShard* sh, uint32_t step, const
       return finish_call(c, s, debug);
   }
   return finish_call(c, s, false);
+}
+
+int andes_tracker_append(AndesCtx* c, const AndesTracker* t, const uint32_t* idx, const int64_t* t_abs, uint32_t count,
+                         const uint8_t* serve_mask, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if (!t) return set_err(c, ANDES_E_INVAL, "tracker is NULL%s");
+  if (t->n && (!t->arrival_us || !t->tl_base || !t->tl_pool || !t->n_deliv || !t->ctx_len || !t->running))
+    return set_err(c, ANDES_E_INVAL, "a tracker array is NULL%s");
+  if (count && (!idx || !t_abs)) return set_err(c, ANDES_E_INVAL, "idx/t_abs is NULL%s");
+  TrackerView v{t->n, t->arrival_us, t->tl_base, t->tl_pool, t->tl_len, t->n_deliv, t->ctx_len, t->running};
+  launch_tracker_append(cfg_of(c, stream), v, idx, t_abs, count, serve_mask, c->w);
+  return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
 
 uint64_t andes_knapsack_dp_workspace(uint32_t n, uint32_t B, uint64_t M) {

@@ -61,6 +61,18 @@ struct ReqView {
   uint64_t tl_len;  // readable elements at tl_pool
 };
 
+// Mutable view of the tracker arrays (andes_tracker_append).
+struct TrackerView {
+  uint32_t n;
+  const int64_t* arrival;
+  const uint64_t* tl_base;
+  uint32_t* tl_pool;
+  uint64_t tl_len;
+  uint32_t* n_deliv;
+  uint32_t* ctx_len;
+  uint8_t* running;
+};
+
 // Per-tile descriptor of the timeline scan (written by prep): the request owning the tile's
 // first position and the source of its head-segment carry.
 struct alignas(16) TileMeta {

@@ -65,6 +65,8 @@ void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t 
                    const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o,
                    XEntry* xsend = nullptr);
 void launch_compact(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* lb_src, uint32_t G);
+bool launch_decide(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
+                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o);
 // multi-GPU decision steps (shard.cu)
 constexpr uint32_t kMaxWorld = 8;
 void launch_shard_summary(const LaunchCfg& L, const ReqView& r, const Work& w, uint32_t B_cap, ShardSummary* out);
@@ -83,6 +85,8 @@ void launch_knapsack_dp(cudaStream_t s, const long long* q, const uint32_t* l, u
 void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o, int64_t now,
                    const uint32_t* tau, uint64_t M, uint32_t prefill, uint32_t swap);
 void init_kernels();
+void launch_tracker_append(const LaunchCfg& L, const TrackerView& t, const uint32_t* idx, const int64_t* t_abs,
+                           uint32_t count, const uint8_t* serve_mask, const Work& w);
 void launch_debug_checks(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now);
 
 }  // namespace andes

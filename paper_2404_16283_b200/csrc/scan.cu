@@ -184,7 +184,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   const uint32_t n = r.n;
   uint32_t local_err = 0, local_unal = 0;
   pdl_wait();
-  pdl_trigger();
   if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x);
   if (sched) {
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
@@ -926,7 +925,6 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t n = r.n;
   pdl_wait();
-  pdl_trigger();
   if (blockIdx.x < 1000) ANDES_TRACE(w, 5000 + 2 * blockIdx.x);
   if (A.sched && blockIdx.x == 0) {
     bounds_block(r, w, A.tau, A.B_cap, A.M, A.cur_latency, A.flags);
@@ -1217,7 +1215,6 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
 __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode, float* q,
                             double* q64, int64_t* sdo, int64_t* swo, uint32_t* mo) {
   pdl_wait();
-  pdl_trigger();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     const uint32_t g = r.n_deliv[i], m = w.m[i];
     const int64_t P = r.period[i];
@@ -1252,7 +1249,6 @@ __global__ void k_qoe_final(ReqView r, Work w, int64_t eval_abs, uint32_t final_
 __global__ void __launch_bounds__(256) k_qnow(ReqView r, Work w, int64_t now) {
   __shared__ unsigned long long s_best;
   pdl_wait();
-  pdl_trigger();
   if (threadIdx.x == 0) s_best = 0ull;
   __syncthreads();
   unsigned long long best = 0ull;
@@ -1299,7 +1295,6 @@ __global__ void __launch_bounds__(kScenThreads) k_scenario_mean(ReqView r, Work 
   __shared__ double s_sum[kScenThreads];
   __shared__ uint32_t s_cnt[kScenThreads];
   pdl_wait();
-  pdl_trigger();
   for (uint32_t sc = blockIdx.x; sc < S; sc += gridDim.x) {
     const uint32_t lo = off[sc], hi = off[sc + 1];
     double acc = 0.0;

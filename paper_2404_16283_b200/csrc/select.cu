@@ -21,6 +21,8 @@
 #include "device.cuh"
 #include "launch.h"
 
+#include <cstdlib>
+
 namespace andes {
 
 // ---------------------------------------------------------------- gain_estimate (parity API)
@@ -28,7 +30,6 @@ __global__ void k_gain_estimate(ReqView r, Work w, int64_t now, uint32_t horizon
                                 const uint32_t* __restrict__ B_list, uint32_t nB, double* gain_out, float* key_out,
                                 double* qwait_out) {
   pdl_wait();
-  pdl_trigger();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     const GainState s = make_state(r, w, i, now, horizon);
     const uint32_t l = r.ctx_len[i];
@@ -52,23 +53,22 @@ __device__ __forceinline__ uint32_t zr_shift(uint32_t max_rank) {
   return bits > 12u ? bits - 12u : 0u;
 }
 
-__global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
-  __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
-  __shared__ Globals s_g;
-  pdl_wait();
-  pdl_trigger();
-  snap_globals(w.g, &s_g);
-  if (!s_g.triggered || s_g.B_hi == 0) return;
+// Per request: the B-independent state (k_state's output array st), the running requests'
+// contiguous copy, rigorous key bounds over the candidate tau range and the CTA's bound
+// histograms (s_hlb / s_hub: kHistK words each in shared memory), flushed to the global ones.
+// CTA `cta` of `ncta` handles requests cta*NT + tid, + ncta*NT, ...
+template <int NT>
+__device__ void state_phase(const ReqView& r, const Work& w, int64_t now, uint32_t horizon, const Globals& sg,
+                            uint32_t* s_hlb, uint32_t* s_hub, uint32_t cta, uint32_t ncta) {
   const uint32_t tid = threadIdx.x;
-  if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
-  const uint32_t tlo = s_g.tau_lo, thi = s_g.tau_hi;
-  const uint32_t zs = zr_shift(s_g.max_rank);
-  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
+  const uint32_t tlo = sg.tau_lo, thi = sg.tau_hi;
+  const uint32_t zs = zr_shift(sg.max_rank);
+  for (uint32_t q = tid; q < kHistK; q += NT) {
     s_hlb[q] = 0u;
     s_hub[q] = 0u;
   }
   __syncthreads();
-  for (uint32_t i = blockIdx.x * blockDim.x + tid; i < r.n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = cta * NT + tid; i < r.n; i += ncta * NT) {
     const GainState s = make_state(r, w, i, now, horizon);
     PackedState p;
     p.w0 = s.w0; p.c0 = s.c0; p.spre = s.spre; p.cw = s.cw; p.dto = s.dto; p.qw = s.qw;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
     }
     w.ub[i] = ub;
     // a key exactly 0 at every B of the range (reading R10: ties by rank): only the B_hi smallest
-    // ranks of these can ever be selected, so k_compact may prune the rest (rank histogram)
+    // ranks of these can ever be selected, so the compaction may prune the rest (rank histogram)
     const bool zero = lb == kOKey0 && ub == kOKey0;
     const uint32_t zb = zero ? p.rank >> zs : 0xFFFFFFFFu;
     w.zr[i] = zb;
@@ -116,10 +116,20 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
     atomicAdd(&s_hub[ub >> 20], 1u);
   }
   __syncthreads();
-  for (uint32_t q = tid; q < kHistK; q += kStateThreads) {
+  for (uint32_t q = tid; q < kHistK; q += NT) {
     if (s_hlb[q]) atomicAdd(&w.hist_lb[q], s_hlb[q]);
     if (s_hub[q]) atomicAdd(&w.hist_ub[q], s_hub[q]);
   }
+}
+
+__global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int64_t now, uint32_t horizon) {
+  __shared__ uint32_t s_hlb[kHistK], s_hub[kHistK];
+  __shared__ Globals s_g;
+  pdl_wait();
+  snap_globals(w.g, &s_g);
+  if (!s_g.triggered || s_g.B_hi == 0) return;
+  if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
+  state_phase<kStateThreads>(r, w, now, horizon, s_g, s_hlb, s_hub, blockIdx.x, gridDim.x);
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
 }
 
@@ -129,11 +139,12 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
 // survivor count #(UB bucket >= b*); computed redundantly by every CTA of k_compact from the
 // completed histograms (16 KB each, L2-resident), so no CTA waits on a last-block reduction.
 // lb_src: G lower-bound histograms (stride kHistK), summed (multi-GPU: one per rank).
+// s_h: kHistK words of shared scratch.
+template <uint32_t NT>
 __device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, uint32_t G, uint32_t need,
-                                         uint32_t& cut, uint32_t& nsurv) {
-  constexpr uint32_t NT = kCandThreads, kPer = kHistK / NT;  // 16 buckets per thread, descending
+                                         uint32_t& cut, uint32_t& nsurv, uint32_t* s_h) {
+  constexpr uint32_t kPer = kHistK / NT;  // buckets per thread, descending
   __shared__ uint32_t s_w[NT / 32], s_cut, s_sv[NT / 32];
-  __shared__ uint32_t s_h[kHistK];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // coalesced loads of both histograms; survivors partial sums by bucket later
   // kPer independent loads per histogram (one round trip each, not kPer in sequence)
@@ -194,8 +205,9 @@ __device__ __forceinline__ void theta_of(const Work& w, const uint32_t* lb_src, 
 // The exact-zero rank cut: the smallest bucket z* with #(exact zeros in buckets <= z*) >= need
 // (every exact zero beyond it is pruned; non-zeros carry zr = ~0 and are never pruned), and
 // the survivor count reduced by the pruned ones.  Computed redundantly by every CTA.
+template <uint32_t NT>
 __device__ __forceinline__ void zero_rank_cut(const Work& w, uint32_t need, uint32_t& zcut, uint32_t& nsurv) {
-  constexpr uint32_t NT = kCandThreads, kPer = kHistK / NT;  // 16 buckets per thread, ascending
+  constexpr uint32_t kPer = kHistK / NT;  // buckets per thread, ascending
   __shared__ uint32_t s_w[NT / 32], s_zc, s_kept;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t h[kPer], cnt = 0;
@@ -236,32 +248,28 @@ __device__ __forceinline__ void zero_rank_cut(const Work& w, uint32_t need, uint
   __syncthreads();
 }
 
-// Compaction of the survivors (UB >= theta) into cand_idx, warp-aggregated appends.
-__global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, const uint32_t* lb_src, uint32_t G) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ Globals s_g;
-  if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
-  snap_globals(w.g, &s_g);
-  if (!s_g.triggered || s_g.B_hi == 0) return;
-  uint32_t cut, ns;
-  theta_of(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, s_g.B_hi, cut, ns);
-  if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
-  const uint32_t theta = cut << 20;
+// theta, the exact-zero rank cut and the survivor count from the completed histograms (every
+// thread of the CTA gets them; s_h: kHistK words of shared scratch).  lb_src: G lower-bound
+// histograms (multi-GPU: one per rank), else the local one.
+template <uint32_t NT>
+__device__ __forceinline__ void survivor_cut(const Work& w, const uint32_t* lb_src, uint32_t G, uint32_t B_hi,
+                                             uint32_t& theta, uint32_t& zcut, uint32_t& ns, uint32_t* s_h) {
+  uint32_t cut;
+  theta_of<NT>(w, lb_src ? lb_src : w.hist_lb, lb_src ? G : 1u, B_hi, cut, ns, s_h);
+  theta = cut << 20;
   // exact zeros beyond the B_hi smallest ranks never make any top-B (single GPU only: the
   // multi-GPU path has no global rank histogram)
-  uint32_t zcut = 0xFFFFFFFFu;
-  if (!lb_src && theta <= kOKey0) zero_rank_cut(w, s_g.B_hi, zcut, ns);
-  const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    w.g->theta = theta;
-    w.g->n_surv = ns;
-    w.g->overflow = ovf ? 1u : 0u;
-    if (ovf) atomicOr(&w.g->slow, 2u);
-  }
-  if (ovf) return;
+  zcut = 0xFFFFFFFFu;
+  if (!lb_src && theta <= kOKey0) zero_rank_cut<NT>(w, B_hi, zcut, ns);
+}
+
+// Compaction of the survivors (UB >= theta, not pruned by the zero-rank cut) into cand_idx /
+// cand_st, warp-aggregated appends; CTA `cta` of `ncta` scans blocks of NT requests.
+template <uint32_t NT>
+__device__ void compact_phase(const ReqView& r, const Work& w, uint32_t theta, uint32_t zcut, uint32_t cta,
+                              uint32_t ncta) {
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < r.n; i0 += gridDim.x * blockDim.x) {
+  for (uint32_t i0 = cta * NT; i0 < r.n; i0 += ncta * NT) {
     const uint32_t i = i0 + threadIdx.x;
     const bool surv = (i < r.n) && (w.ub[i] >= theta) && (zcut == 0xFFFFFFFFu || w.zr[i] == 0xFFFFFFFFu || w.zr[i] <= zcut);
     const uint32_t bal = __ballot_sync(0xffffffffu, surv);
@@ -275,6 +283,27 @@ __global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, con
       w.cand_st[slot] = w.st[i];
     }
   }
+}
+
+__global__ void __launch_bounds__(kCandThreads) k_compact(ReqView r, Work w, const uint32_t* lb_src, uint32_t G) {
+  pdl_wait();
+  __shared__ Globals s_g;
+  __shared__ uint32_t s_h[kHistK];
+  if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
+  snap_globals(w.g, &s_g);
+  if (!s_g.triggered || s_g.B_hi == 0) return;
+  uint32_t theta, zcut, ns;
+  survivor_cut<kCandThreads>(w, lb_src, G, s_g.B_hi, theta, zcut, ns, s_h);
+  if (blockIdx.x == 0) ANDES_TRACE(w, 2210);
+  const bool ovf = ns > w.S_cap;  // S_cap <= kCandCap < kRankCap: survivors fit k_select's scratch
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w.g->theta = theta;
+    w.g->n_surv = ns;
+    w.g->overflow = ovf ? 1u : 0u;
+    if (ovf) atomicOr(&w.g->slow, 2u);
+  }
+  if (ovf) return;
+  compact_phase<kCandThreads>(r, w, theta, zcut, blockIdx.x, gridDim.x);
   if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x + 1);
 }
 
@@ -716,34 +745,34 @@ __device__ bool finalize_fast(const SelectArgs& A) {
 // (P:L514-529): take while the running sum of l stays <= M (count <= B by construction), break
 // at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken prefix; then B's cap result
 // is staged (stage_cap) and the last CTA to finish picks B* and writes the outputs.
-__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
+// k_select's shared scratch (file scope: allocated in the kernels that use it)
+__shared__ unsigned long long s_sel_ps[kSortCap];
+__shared__ long long s_sel_gf[kSortCap];
+__shared__ uint32_t s_sel_k, s_sel_last;
+__shared__ long long s_sel_red[32];
+__shared__ uint8_t s_sel_run8[kSortCap];  // running flag of the ordered survivors (pruned path)
+__shared__ uint32_t s_sel_lsel[kSortCap];  // l of the ordered candidates (the walk's loads)
+
+// S4 for one candidate B (CTA-wide): the top min(B, n) requests by (key desc, rank asc), then
+// Algorithm 1: take while the running sum of l stays <= M (count <= B by
+// construction), break at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken
+// prefix; then B's cap result is staged (stage_cap).  Multi-GPU step 2 (A.xsend): publishes this
+// rank's top list of B instead.  s_g: the snapshot of the call's globals after the compaction.
+__device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g) {
   extern __shared__ unsigned char s_dyn[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
   unsigned long long* s_vc = reinterpret_cast<unsigned long long*>(s_idx + kVictCap);
-  __shared__ unsigned long long s_ps[kSortCap];
-  __shared__ long long s_gf[kSortCap];
-  __shared__ uint32_t s_k, s_last;
-  __shared__ long long s_red[32];
-  __shared__ Globals s_g;
-  __shared__ uint8_t s_run8[kSortCap];  // running flag of the ordered survivors (pruned path)
-  __shared__ uint32_t s_lsel[kSortCap];  // l of the ordered candidates (the walk's loads)
-
+  unsigned long long* const s_ps = s_sel_ps;
+  long long* const s_gf = s_sel_gf;
+  uint32_t& s_k = s_sel_k;
+  long long* const s_red = s_sel_red;
+  uint8_t* const s_run8 = s_sel_run8;
+  uint32_t* const s_lsel = s_sel_lsel;
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x;
-  const uint32_t B = gridDim.x - blockIdx.x;  // largest B (the longest walk) scheduled first
   const uint32_t n = r.n;
-  ANDES_TRACE(A.w, 9200 + B - 1);
-  pdl_wait();
-  pdl_trigger();
-  // the key histograms were consumed by k_compact: self-clean them for the next call
-  for (uint32_t q = blockIdx.x * blockDim.x + tid; q < kHistK; q += gridDim.x * blockDim.x) {
-    w.hist_lb[q] = 0u;
-    w.hist_ub[q] = 0u;
-    w.hist_zr[q] = 0u;
-  }
-  snap_globals(w.g, &s_g);
   const bool trig = s_g.triggered != 0;
   const uint32_t B_lo = s_g.B_lo, B_hi = s_g.B_hi;
   const bool ovf = s_g.overflow != 0;
@@ -951,13 +980,24 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
     if (B == 256) ANDES_TRACE(w, 2405);
   }
   ANDES_TRACE(w, 2 * (B - 1) + 1);
-  if (A.xsend) return;
-  // the last CTA to finish runs S5 + S6 (last-block pattern)
+}
+
+// S5 + S6 by the last of `ncta` CTAs to finish (last-block pattern): B* = argmax V (ties to the
+// larger B) and its staged cap result copied into the outputs, or the general finalize.
+__device__ void select_finish(const SelectArgs& A, const Globals& s_g, uint32_t ncta) {
+  extern __shared__ unsigned char s_dyn[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_dyn);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_dyn + sizeof(unsigned long long) * kVictCap);
+  unsigned long long* s_vc = reinterpret_cast<unsigned long long*>(s_idx + kVictCap);
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x;
+  const bool trig = s_g.triggered != 0;
+  const uint32_t n_run = s_g.n_run;
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&w.g->done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  if (tid == 0) s_sel_last = (atomicAdd(&w.g->done, 1u) == ncta - 1) ? 1u : 0u;
   __syncthreads();
-  if (!s_last) return;
+  if (!s_sel_last) return;
   __threadfence();
   ANDES_TRACE(w, 2100);
   if (trig && n_run <= (uint32_t)kStageRun && finalize_fast(A)) {
@@ -968,10 +1008,128 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
   F.key = s_key;
   F.idx = s_idx;
   F.vcum = s_vc;
-  F.acum = s_ps;
-  F.adm = reinterpret_cast<uint32_t*>(s_gf);
-  F.aflag = reinterpret_cast<uint32_t*>(s_gf) + kSortCap;
+  F.acum = s_sel_ps;
+  F.adm = reinterpret_cast<uint32_t*>(s_sel_gf);
+  F.aflag = reinterpret_cast<uint32_t*>(s_sel_gf) + kSortCap;
   finalize_decision(A, F);
+}
+
+// the key histograms were consumed by the compaction: self-clean them for the next call
+__device__ __forceinline__ void clean_key_hists(const Work& w) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < kHistK; q += gridDim.x * blockDim.x) {
+    w.hist_lb[q] = 0u;
+    w.hist_ub[q] = 0u;
+    w.hist_zr[q] = 0u;
+  }
+}
+
+// CTA b handles B = B_cap - b (largest B, the longest walk, scheduled first); the last CTA to
+// finish picks B* and writes the outputs.
+__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
+  __shared__ Globals s_g;
+  const uint32_t B = gridDim.x - blockIdx.x;
+  ANDES_TRACE(A.w, 9200 + B - 1);
+  pdl_wait();
+  clean_key_hists(A.w);
+  snap_globals(A.w.g, &s_g);
+  select_one_B(A, B, s_g);
+  if (A.xsend) return;
+  select_finish(A, s_g, gridDim.x);
+}
+
+// ---------------------------------------------------------------- fused post-scan decision
+// S3-S6 of a single-GPU decision in ONE cooperative kernel (all CTAs co-resident): the phases of
+// k_state, k_compact and k_select separated by grid-wide barriers instead of kernel boundaries
+// (each boundary cost a ~3-4 us launch gap plus the next grid's ramp-up):
+//   A  per-request state and key bounds (state_phase), bound histograms
+//   -- barrier: the last CTA to arrive computes theta / the zero-rank cut / the survivor count
+//      once and releases the others
+//   B  survivor compaction (compact_phase)
+//   -- barrier
+//   C  one candidate B per CTA (B = B_cap - b, b + grid, ...): select_one_B; S5/S6 by the last
+//      CTA (select_finish)
+// Grid-barrier words live in the second 128-byte line of the per-call globals (zeroed with them).
+struct DecideSync {
+  uint32_t arrive_a, ready_a, arrive_b, ready_b;
+  uint32_t theta, zcut, n_surv, overflow;
+};
+__device__ __forceinline__ DecideSync* decide_sync(const Work& w) { return reinterpret_cast<DecideSync*>(w.g + 1); }
+
+__device__ __forceinline__ void spin_until_set(const uint32_t* flag) {
+  while (ld_acquire_u32(flag) == 0u) __nanosleep(20);
+}
+
+__global__ void __launch_bounds__(kSelThreads, 2) k_decide(SelectArgs A) {
+  extern __shared__ unsigned char s_dyn[];
+  __shared__ Globals s_g;
+  __shared__ uint32_t s_flag;
+  const ReqView& r = A.r;
+  const Work& w = A.w;
+  DecideSync* ds = decide_sync(w);
+  const uint32_t tid = threadIdx.x, G = gridDim.x;
+  pdl_wait();
+  snap_globals(w.g, &s_g);
+  if (s_g.triggered && s_g.B_hi != 0) {
+    // ---- phase A: state and key bounds (histograms in the dynamic shared buffer)
+    uint32_t* s_hlb = reinterpret_cast<uint32_t*>(s_dyn);
+    if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
+    state_phase<kSelThreads>(r, w, A.now, A.horizon, s_g, s_hlb, s_hlb + kHistK, blockIdx.x, G);
+    if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
+    // ---- barrier A; the last arriver computes the survivor cut
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_flag = (atomicAdd(&ds->arrive_a, 1u) == G - 1) ? 1u : 0u;
+    __syncthreads();
+    if (s_flag) {
+      __threadfence();
+      ANDES_TRACE(w, 2200);
+      uint32_t theta, zcut, ns;
+      survivor_cut<kSelThreads>(w, nullptr, 1u, s_g.B_hi, theta, zcut, ns, reinterpret_cast<uint32_t*>(s_dyn));
+      const bool ovf = ns > w.S_cap;
+      if (tid == 0) {
+        ds->theta = theta;
+        ds->zcut = zcut;
+        ds->n_surv = ns;
+        ds->overflow = ovf ? 1u : 0u;
+        w.g->theta = theta;
+        w.g->n_surv = ns;
+        w.g->overflow = ovf ? 1u : 0u;
+        if (ovf) atomicOr(&w.g->slow, 2u);
+        __threadfence();
+        st_release_u32(&ds->ready_a, 1u);
+      }
+      ANDES_TRACE(w, 2201);
+    } else if (tid == 0) {
+      spin_until_set(&ds->ready_a);
+    }
+    __syncthreads();
+    // ---- phase B: survivor compaction
+    const uint32_t theta = __ldcg(&ds->theta), zcut = __ldcg(&ds->zcut);
+    if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x);
+    if (!__ldcg(&ds->overflow)) compact_phase<kSelThreads>(r, w, theta, zcut, blockIdx.x, G);
+    if (blockIdx.x < 512) ANDES_TRACE(w, 8100 + 2 * blockIdx.x + 1);
+    // ---- barrier B
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      if (atomicAdd(&ds->arrive_b, 1u) == G - 1) {
+        __threadfence();
+        st_release_u32(&ds->ready_b, 1u);
+        ANDES_TRACE(w, 2210);
+      } else {
+        spin_until_set(&ds->ready_b);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- phase C: Algorithm 1 per B, S5/S6
+  clean_key_hists(w);
+  snap_globals(w.g, &s_g);
+  for (uint32_t b = blockIdx.x; b < A.B_cap; b += G) {
+    ANDES_TRACE(w, 9200 + A.B_cap - b - 1);
+    select_one_B(A, A.B_cap - b, s_g);
+  }
+  select_finish(A, s_g, G);
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -1001,8 +1159,46 @@ static size_t select_smem() {
          (sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * kSelThreads;
 }
 
+static int g_decide_per_sm = 0;  // co-resident k_decide CTAs per SM (cooperative grid limit)
+
 void init_kernels() {
   cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
+  cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem());
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_decide, kSelThreads, select_smem()) != cudaSuccess) nb = 0;
+  g_decide_per_sm = nb;
+}
+
+// The fused post-scan decision (k_decide) when every CTA can be co-resident: a grid of
+// max(B_cap, enough CTAs for the requests) up to the cooperative limit, one candidate B per CTA
+// when B_cap fits.  Returns false (nothing launched) when it cannot run; the caller then launches
+// k_state, k_compact and k_select.  Off by default (ANDES_FUSED=1 turns it on): on config 3 its two
+// grid barriers (~1.7 us each, plus the single-CTA survivor cut) cost as much as the two kernel
+// boundaries they replace (84 vs 78 us per decision, tools/time_decision.py).
+bool launch_decide(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
+                   const uint32_t* tau, uint32_t B_cap, uint64_t M, uint32_t preempt_cap, const SchedOut& o) {
+  static const bool off = [] {
+    const char* v = getenv("ANDES_FUSED");
+    return !(v && v[0] == '1');
+  }();
+  const uint32_t limit = (uint32_t)g_decide_per_sm * L.sm_count;
+  if (off || limit == 0) return false;
+  const uint32_t want = umin32(limit, (r.n + kSelThreads - 1) / kSelThreads);
+  const uint32_t grid = umin32(limit, B_cap > want ? B_cap : want);
+  SelectArgs A{r, w, now, horizon, tau, B_cap, M, preempt_cap, o, nullptr};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid ? grid : 1u);
+  cfg.blockDim = dim3(kSelThreads);
+  cfg.dynamicSmemBytes = select_smem();
+  cfg.stream = L.stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_decide, A) == cudaSuccess;
 }
 
 void launch_select(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,

@@ -25,7 +25,7 @@ def A():
 
 @pytest.fixture(scope="module")
 def ctx(A):
-    return A.Context(max_requests=1 << 14, max_B=64, max_tokens=1 << 22)
+    return A.Context(max_requests=1 << 14, max_B=256, max_tokens=1 << 22)
 
 
 def _tau(snap):

@@ -314,53 +314,27 @@ def test_schedule_degenerate_cases(A, ctx, orc):
 
 
 # ---------------------------------------------------------------- config 1: 200-iteration driver
-def _iterate(A, ctx, orc, iters=200, seed=1):
-    """BASELINE config 1: 8 requests, ttft 1 s, 4.8 tok/s, M = 2048; each iteration the GPU
-    decision must equal the oracle's; the clock advances by tau(realized) and every served
-    request receives one token; finished requests leave."""
-    rng = np.random.default_rng(seed)
-    n = 8
-    prompt = rng.integers(150, 601, n)
-    out_len = rng.integers(20, 121, n)
-    arr = rng.integers(0, 2_000_001, n).astype(np.int64)
-    order = np.argsort(arr, kind="stable")
-    prompt, out_len, arr = prompt[order], out_len[order], arr[order]
-    tau = W.tau_table(8)
-    now = int(arr.max())
-    toks = [[] for _ in range(n)]
-    running = np.zeros(n, np.uint8)
-    alive = np.ones(n, bool)
-    checked = 0
-    for it in range(iters):
-        idx = np.nonzero(alive & (arr <= now))[0]
-        if idx.size == 0:
-            now += 100_000
-            continue
-        g, base, pool = W._pack([np.asarray(toks[i], np.uint32) for i in idx])
-        snap = W.Snapshot(arrival_us=arr[idx], ttft_us=np.full(idx.size, 1_000_000, np.uint32),
-                          period_us=np.full(idx.size, 208_333, np.uint32),
-                          ctx_len=(prompt[idx] + g).astype(np.uint32), n_deliv=g,
-                          max_total=np.full(idx.size, W.UINT32_MAX, np.uint32),
-                          start_off_us=np.zeros(idx.size, np.uint32), rank=idx.astype(np.uint32),
-                          running=running[idx], tl_base=base, tl_pool=pool, now_us=now, horizon_us=2_000_000,
-                          tau_us=tau, kv_capacity=2048)
-        gd, od = _check_sched(A, ctx, orc, snap, flags=1)
-        checked += 1
-        served = idx[np.nonzero(od.serve_mask)[0]]
-        realized = max(1, served.size)
-        now += int(tau[min(realized, tau.size) - 1])
-        running[:] = 0
-        for i in served:
-            toks[i].append(now - int(arr[i]))
-            running[i] = 1
-            if len(toks[i]) >= out_len[i]:
-                alive[i] = False
-                running[i] = 0
-    return checked
-
-
 def test_config1_iteration_driver(A, ctx, orc):
-    assert _iterate(A, ctx, orc) >= 150
+    """BASELINE config 1 (tests/config1.py): on every iteration the GPU decision equals the
+    oracle's, and at every candidate B Algorithm 2 on the GPU (andes_knapsack_dp) equals brute
+    force and bounds Algorithm 1 from above (SPEC acceptance #2/#3)."""
+    from config1 import QualityTracker, run
+    NEG = -(1 << 63)
+
+    def gpu_dp(q, l, B, M):
+        x, best, Vb = ctx.knapsack_dp(torch.tensor(q, dtype=torch.int64, device="cuda"),
+                                      torch.tensor(l, dtype=torch.int32, device="cuda"), B, M)
+        torch.cuda.synchronize()
+        b = int(best.item())
+        return (None if b == NEG else b), [None if int(v) == NEG else int(v) for v in Vb.cpu().numpy()]
+
+    qt = QualityTracker(orc, exact_dp=gpu_dp)
+
+    def decide(snap):
+        return _check_sched(A, ctx, orc, snap, flags=1)[1]
+
+    assert run(decide, on_iter=qt) >= 150
+    assert qt.summary()["B_values_checked"] >= 150
 
 
 def test_schedule_survivor_overflow_fallback(A, ctx, orc):

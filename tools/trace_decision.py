@@ -46,11 +46,13 @@ sc = span(5000, 7000)
 print("scan CTAs", len(sc), "start min/max", us(sc[:, 0].min()), us(sc[:, 0].max()), "bounds end", us(tr[2300]),
       "end min/med/max", us(sc[:, 1].min()), us(np.median(sc[:, 1])), us(sc[:, 1].max()))
 st = span(3000, 4024)
-print("state CTAs", len(st), "start", us(st[:, 0].min()), "end", us(st[:, 1].max()), "last-block",
-      us(tr[2200]), us(tr[2201]))
+if len(st):
+    print("state CTAs", len(st), "start", us(st[:, 0].min()), us(st[:, 0].max()), "end min/max", us(st[:, 1].min()),
+          us(st[:, 1].max()), "(fused) cut leader start / release", us(tr[2200]), us(tr[2201]))
 cp = span(8100, 9124)
-print("compact CTAs", len(cp), "start", us(cp[:, 0].min()), us(cp[:, 0].max()), "theta(CTA0)", us(tr[2210]),
-      "end max", us(cp[:, 1].max()))
+if len(cp):
+    print("compact CTAs", len(cp), "start", us(cp[:, 0].min()), us(cp[:, 0].max()), "theta(CTA0) / (fused) barrier B",
+          us(tr[2210]), "end max", us(cp[:, 1].max()))
 print("select CTA255 phases", [us(tr[s]) for s in range(2400, 2409) if tr[s]], "(2400 keys, 2401 rank, 2402-3 l loads, 2406 walk, 2407 V loop, 2408 block sum, 2404 V out, 2405 cap)")
 sel = span(0, 512)
 print("select CTAs", len(sel), "start", us(sel[:, 0].min()), us(sel[:, 0].max()), "end min/med/max",

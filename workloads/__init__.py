@@ -105,6 +105,22 @@ def _pack(timelines, align: int = POOL_ALIGN):
     return g, base, pool
 
 
+def with_room(snap: Snapshot, extra: int, align: int = POOL_ALIGN) -> Snapshot:
+    """The same snapshot with `extra` free token slots after every timeline (a device-resident
+    tracker appends into them, andes_tracker_append); timelines stay `align`-aligned."""
+    g = snap.n_deliv.astype(np.int64)
+    span = (g + extra + align - 1) // align * align
+    base = np.zeros(snap.n, np.int64)
+    if snap.n:
+        base[1:] = np.cumsum(span[:-1])
+    pool = np.zeros(int(span.sum()) if snap.n else 0, np.uint32)
+    src = snap.tl_base.astype(np.int64)
+    for i in range(snap.n):
+        if g[i]:
+            pool[base[i]:base[i] + g[i]] = snap.tl_pool[src[i]:src[i] + g[i]]
+    return replace(snap, tl_base=base.astype(np.uint64), tl_pool=pool)
+
+
 def sample_lengths(rng, n, dataset="sharegpt", in_clamp=(1, 32768), out_clamp=(1, 8192)):
     mi, si, mo, so = LENGTH_FITS[dataset]
     inp = np.clip(np.rint(rng.lognormal(mi, si, n)), *in_clamp).astype(np.int64)
@@ -182,6 +198,31 @@ def snapshot(n, seed=1, dataset="sharegpt", listen_frac=0.0, window_s=1200.0, ar
                     rank=np.arange(n, dtype=np.uint32), running=running, tl_base=base, tl_pool=pool,
                     now_us=now_us, horizon_us=horizon_us, tau_us=tau, kv_capacity=kv_capacity,
                     preempt_cap=preempt_cap, name=name or f"{dataset}-{n}-s{seed}")
+
+
+def config1_population(seed=1):
+    """BASELINE config 1: 8 requests, prompts U[150, 600], outputs U[20, 120],
+    arrivals U[0, 2] s, in arrival order.  Returns (prompt, out_len, arrival_us)."""
+    rng = np.random.default_rng(seed)
+    n = 8
+    prompt = rng.integers(150, 601, n)
+    out_len = rng.integers(20, 121, n)
+    arr = rng.integers(0, 2_000_001, n).astype(np.int64)
+    order = np.argsort(arr, kind="stable")
+    return prompt[order], out_len[order], arr[order]
+
+
+def config1(seed=1) -> Snapshot:
+    """The first decision of the config-1 driver: every request arrived, no token delivered yet;
+    ttft 1 s, 4.8 tok/s, M = 2048, tau(B) for B = 1..8, Delta t = 2 s, cap off."""
+    prompt, out_len, arr = config1_population(seed)
+    n = prompt.size
+    g, base, pool = _pack([np.zeros(0, np.uint32)] * n)
+    return Snapshot(arrival_us=arr, ttft_us=np.full(n, 1_000_000, np.uint32), period_us=np.full(n, READ_PERIOD_US, np.uint32),
+                    ctx_len=prompt.astype(np.uint32), n_deliv=g, max_total=np.full(n, UINT32_MAX, np.uint32),
+                    start_off_us=np.zeros(n, np.uint32), rank=np.arange(n, dtype=np.uint32),
+                    running=np.zeros(n, np.uint8), tl_base=base, tl_pool=pool, now_us=int(arr.max()),
+                    horizon_us=HORIZON_US, tau_us=tau_table(8), kv_capacity=2048, name="config1")
 
 
 def config2(seed=1) -> Snapshot:
