@@ -533,15 +533,15 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
     const CUtensorMap* tmn = c->pool_map;
     if ((rc = pool_map(c, r.tl_pool, r.tl_len, &tmn))) return rc;
     launch_scan(L, r, wn, p->now_us, false, tmn);
-    launch_qnow(L, r, wn, p->now_us);
-    cudaError_t e = cudaMemsetAsync(&c->w.g->tile_ctr, 0, sizeof(uint32_t), s);
-    if (e != cudaSuccess) return cuda_check(c, e, "memset");
   }
   mark(c, 1, s);
   {
     const CUtensorMap* tm = c->pool_map;
     if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
-    launch_scan(L, r, w, eval, false, tm, true, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags);
+    // after a scan at now (objectives) the decision scan counts its chunks on its own counter, and
+    // its idle warps finish Q_now / Q_min from the first scan's sums (no k_qnow, no memset)
+    launch_scan(L, r, w, eval, false, tm, true, p->tau_us, p->B_cap, p->kv_capacity, p->cur_latency_us, p->flags,
+                dual, dual, p->now_us);
   }
   mark(c, 2, s);
   // S3-S6: one fused cooperative kernel when its grid fits on the GPU, else three kernels

@@ -29,7 +29,8 @@ constexpr int kMaxRunning = 4096;
 constexpr int kStageRun = kMaxRunning / 2;        // running requests handled by the per-B cap staging
 constexpr uint32_t kHistL = 4096;                 // exact histogram of l < 4095 (+ overflow bucket)
 constexpr uint32_t kHistK = 4096;                 // key histograms: top 12 bits of the ordered key
-constexpr uint32_t kCandCap = 3071;               // survivor capacity of the pruned path (k_select scratch)
+constexpr uint32_t kCandCap = 2559;               // survivor capacity of the pruned path (k_select scratch)
+constexpr uint32_t kRunOrdAt = 3584;              // k_select scratch: running order / prefix sums (512 slots)
 
 // tile status words (decoupled look-back), see k_qoe_scan
 constexpr unsigned long long kStAgg = 1ull << 62;
@@ -128,6 +129,17 @@ struct Globals {
 
 static_assert(sizeof(Globals) == 128, "Globals: one 128-byte line, one warp snapshot");
 
+// Second line of the per-call globals (zeroed with them): grid-barrier words of the fused
+// decision kernel and the counters of a call's second timeline scan.
+struct Globals2 {
+  uint32_t arrive_a, ready_a, arrive_b, ready_b;  // k_decide grid barriers
+  uint32_t theta, zcut, n_surv, overflow;         // k_decide: survivor cut published at barrier A
+  uint32_t tile_ctr_b;                            // the decision scan's chunk counter after a scan at now
+  uint32_t qnow_ctr;                              // Q_now chunks claimed by the decision scan's idle warps
+  uint32_t pad[22];
+};
+static_assert(sizeof(Globals2) == 128, "Globals2: one 128-byte line");
+
 // Block snapshot of the Globals line: warp 0 loads it (one request per CTA) and the block reads
 // shared memory.  Every thread of a many-CTA grid loading the same global words instead queues
 // on one L2 slice; in k_select that skewed the CTA starts by 6 us.  Ends with __syncthreads().
@@ -177,6 +189,9 @@ struct ShardVictims {
   VictimX v[kStageRun];
 };
 __host__ __device__ __forceinline__ size_t tri_off(uint32_t B) { return (size_t)B * (B - 1) / 2; }
+
+struct Work;
+__host__ __device__ inline Globals2* globals2(const Work& w);
 
 struct Work {
   uint32_t* m;               // [N] tokens due at the evaluation time
@@ -230,6 +245,8 @@ struct Work {
   // debug checks: open-addressing set of ranks (2 N_cap slots, self-cleaning), rank uniqueness
   unsigned long long* rank_set;
 };
+
+__host__ __device__ inline Globals2* globals2(const Work& w) { return reinterpret_cast<Globals2*>(w.g + 1); }
 
 // ---------------------------------------------------------------- error reporting
 // Raise error bits: into this call's Globals word (read by the decision's own kernels, e.g. the

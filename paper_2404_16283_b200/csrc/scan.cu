@@ -435,6 +435,36 @@ __device__ __forceinline__ uint32_t swz(uint32_t x) {
   return (row << 7) | ((chunk ^ (row & 7u)) << 4) | ((x & 3u) << 2);
 }
 
+// Q_now of request i (the Appendix-A objectives' QoE at the decision time, reading R3) from the
+// scan at now (m_now / spre_now / edge_now), stored in qnow; returns ~(fp64 bits) for the min.
+__device__ __forceinline__ unsigned long long qnow_of(const ReqView& r, const Work& w, uint32_t i, int64_t now) {
+  const uint32_t g = r.n_deliv[i], m = w.m_now[i];
+  const int64_t P = r.period[i];
+  const int64_t spre = (int64_t)w.spre_now[i];
+  const int64_t cw = P * (((int64_t)m * ((int64_t)m - 1)) >> 1);
+  int64_t sd = 0, sw = 0;
+  if (m == 0) {
+    sd = sw = 0;
+  } else if (g >= m) {
+    sd = spre;
+    sw = (int64_t)m * (int64_t)w.edge_now[i] + cw;
+  } else {
+    const int64_t t = now - r.arrival[i];
+    const int64_t K = m - g;
+    const int64_t w0 = t - (int64_t)r.ttft[i] - ((int64_t)g - 1) * P;
+    sd = spre + sum_down(0, K, w0, P);
+    sw = (int64_t)m * (w0 - K * P) + cw;
+  }
+  const double q = qoe_value(sd, sw);
+  w.qnow[i] = q;
+  return ~(unsigned long long)__double_as_longlong(q);
+}
+
+// raise the objective's Q_min (stored inverted, atomicMax) unless the word already holds it
+__device__ __forceinline__ void qmin_raise(const Work& w, unsigned long long best) {
+  if (best && best > __ldcg(&w.g->qmin_bits)) atomicMax(&w.g->qmin_bits, best);
+}
+
 struct ScanArgs {
   ReqView r;
   Work w;
@@ -445,6 +475,9 @@ struct ScanArgs {
   uint32_t B_cap;
   uint64_t M;
   uint32_t cur_latency, flags;
+  uint32_t* tile_ctr;  // the chunk counter of this scan (a call's second scan has its own)
+  uint32_t qnow;       // objectives: idle warps finish Q_now from the scan at now (k_qnow's work)
+  int64_t now_abs;
 };
 
 // One request of a tile's window in tile-local coordinates (x = position - p0).
@@ -978,7 +1011,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t t0 = (nchunks - 1u - g_nxt) * CH;
     gs[0] = t0;
     gs[1] = min(t0 + CH, nunits);
-    gs[2] = static_next ? g_nxt + KS : atomicAdd(&w.g->tile_ctr, 1u) + 2u * KS;
+    gs[2] = static_next ? g_nxt + KS : atomicAdd(A.tile_ctr, 1u) + 2u * KS;
     return t0 | kStart;
   };
   uint32_t cur = kNone, s1 = kNone;
@@ -990,7 +1023,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     // two TMA copies
     gs[0] = kNone;
     gs[1] = 0u;
-    gs[2] = cta0_dyn ? atomicAdd(&w.g->tile_ctr, 1u) + 2u * KS
+    gs[2] = cta0_dyn ? atomicAdd(A.tile_ctr, 1u) + 2u * KS
                      : (blockIdx.x - (A.sched ? 1u : 0u)) * (kScanThreads / 32) + wid;
     cur = gen(!cta0_dyn);
     if (cur != kNone) {
@@ -1206,6 +1239,22 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     tm1 = tm2;
     r_end1 = r_end2;
   }
+  if (A.qnow) {
+    // k_qnow's work by the warps that have run out of tiles (chunks of 32 requests from a
+    // counter): it overlaps the scan's tail instead of costing a kernel of its own
+    unsigned long long best = 0ull;
+    const uint32_t nq = (n + 31u) / 32u;
+    for (;;) {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(&globals2(w)->qnow_ctr, 1u);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nq) break;
+      const uint32_t i = c * 32u + lane;
+      if (i < n) best = max(best, qnow_of(r, w, i, A.now_abs));
+    }
+    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) qmin_raise(w, best);
+  }
   if (w.trace && blockIdx.x < 1000 && lane == 0) atomicMax(&w.trace[5000 + 2 * blockIdx.x + 1], gtimer());
 }
 
@@ -1252,32 +1301,12 @@ __global__ void __launch_bounds__(256) k_qnow(ReqView r, Work w, int64_t now) {
   if (threadIdx.x == 0) s_best = 0ull;
   __syncthreads();
   unsigned long long best = 0ull;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
-    const uint32_t g = r.n_deliv[i], m = w.m_now[i];
-    const int64_t P = r.period[i];
-    const int64_t spre = (int64_t)w.spre_now[i];
-    const int64_t cw = P * (((int64_t)m * ((int64_t)m - 1)) >> 1);
-    int64_t sd = 0, sw = 0;
-    if (m == 0) {
-      sd = sw = 0;
-    } else if (g >= m) {
-      sd = spre;
-      sw = (int64_t)m * (int64_t)w.edge_now[i] + cw;
-    } else {
-      const int64_t t = now - r.arrival[i];
-      const int64_t K = m - g;
-      const int64_t w0 = t - (int64_t)r.ttft[i] - ((int64_t)g - 1) * P;
-      sd = spre + sum_down(0, K, w0, P);
-      sw = (int64_t)m * (w0 - K * P) + cw;
-    }
-    const double q = qoe_value(sd, sw);
-    w.qnow[i] = q;
-    best = max(best, ~(unsigned long long)__double_as_longlong(q));
-  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x)
+    best = max(best, qnow_of(r, w, i, now));
   for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
   if ((threadIdx.x & 31) == 0 && best) atomicMax(&s_best, best);
   __syncthreads();
-  if (threadIdx.x == 0 && s_best) atomicMax(&w.g->qmin_bits, s_best);
+  if (threadIdx.x == 0) qmin_raise(w, s_best);
 }
 
 void launch_qnow(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now) {
@@ -1343,9 +1372,10 @@ void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                  const CUtensorMap* tmap, bool sched, const uint32_t* tau, uint32_t B_cap, uint64_t M,
-                 uint32_t cur_latency, uint32_t flags) {
+                 uint32_t cur_latency, uint32_t flags, bool second, bool qnow, int64_t now_abs) {
   if (r.n == 0 && !sched) return;
-  ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags};
+  ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags,
+             second ? &globals2(w)->tile_ctr_b : &w.g->tile_ctr, qnow ? 1u : 0u, now_abs};
   const uint32_t grid = r.n ? L.scan_grid : 1u;
   // two-tile units for large pools (>= 16 M tokens: enough units per warp for balance);
   // ANDES_SCAN_TW=1|2 forces one (tests)

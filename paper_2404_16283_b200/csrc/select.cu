@@ -664,6 +664,99 @@ __device__ void stage_cap(const SelectArgs& A, uint32_t B, uint32_t tB, uint32_t
   if (tid == 0) w.stage_sc[B - 1] = make_uint4(n_pre, n_adm, realized, flags);
 }
 
+// stage_cap for the common case (no survivor overflow, n_run <= kSelThreads): the running
+// requests were already put in ascending composite order at B (rord, with the prefix sums rcum of
+// their l) during the survivors' rank counting, so the victims R \ S_B -- the running requests
+// whose composite is below the k*-th selected one (composites are unique) -- are its first nv
+// entries, in victim order (key asc, rank desc), and every cap quantity is a prefix sum:
+//   W(after preempting the first p victims) = W_run - rcum[p - 1].
+// sel / run8 / lsel: S_B in greedy order (request index, running flag, l); rk / rx: the running
+// requests' composites / indices by running slot; aflag: 2 kSortCap words of scratch (admit
+// index, admit l); acum: kSortCap words of scratch (admit prefix sums).
+__device__ void stage_cap_fast(const SelectArgs& A, uint32_t B, uint32_t kstar, unsigned long long thr,
+                               const uint32_t* sel, const uint8_t* run8, const uint32_t* lsel,
+                               const unsigned long long* rk, const uint32_t* rx, const uint32_t* rord,
+                               const unsigned long long* rcum, uint32_t n_run, uint32_t* aflag,
+                               unsigned long long* acum) {
+  __shared__ uint32_t s_wadm[kSelThreads / 32];
+  __shared__ unsigned long long s_tmp2[kSelThreads / 32];
+  const Work& w = A.w;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // victims: count of running composites below thr (all of them when k* = 0)
+  const uint32_t nv =
+      (uint32_t)__syncthreads_count(tid < n_run && (kstar == 0 || rk[tid] < thr));
+  // admits S_B \ R in greedy order: positions q = 2 tid, 2 tid + 1 (k* <= kSortCap = 2 kSelThreads)
+  const uint32_t q0 = 2 * tid;
+  const bool a0 = q0 < kstar && !run8[q0], a1 = q0 + 1 < kstar && !run8[q0 + 1];
+  const uint32_t mine = (a0 ? 1u : 0u) + (a1 ? 1u : 0u);
+  uint32_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += v;
+  }
+  if (lane == 31) s_wadm[wid] = inc;
+  __syncthreads();
+  uint32_t wpre = 0, na = 0;
+  for (uint32_t k2 = 0; k2 < kSelThreads / 32; ++k2) {
+    wpre += k2 < wid ? s_wadm[k2] : 0u;
+    na += s_wadm[k2];
+  }
+  {
+    uint32_t a = wpre + inc - mine;
+    if (a0) {
+      aflag[a] = sel[q0];
+      aflag[kSortCap + a] = lsel[q0];
+      ++a;
+    }
+    if (a1) {
+      aflag[a] = sel[q0 + 1];
+      aflag[kSortCap + a] = lsel[q0 + 1];
+    }
+  }
+  const uint32_t cap = A.preempt_cap;
+  const bool cap_hit = !(cap == 0xFFFFFFFFu || nv <= cap);
+  uint32_t n_pre, n_adm, flags = 1u, realized;
+  if (!cap_hit) {
+    n_pre = nv;
+    n_adm = na;
+    realized = kstar;
+    __syncthreads();  // aflag complete
+  } else {
+    flags |= 2u;
+    const unsigned long long Wrun = rcum[n_run - 1];  // nv > cap >= 0 implies n_run >= 1
+    const unsigned long long W0 = Wrun - (cap ? rcum[cap - 1] : 0ull);
+    const uint32_t c0 = n_run - cap;
+    if (W0 > A.M) {
+      flags |= 4u;  // memory beats the cap: keep preempting in victim order (reading R18 step 5)
+      // the first p >= cap + 1 with Wrun - rcum[p - 1] <= M (rcum increases), else all nv
+      const uint32_t over =
+          (uint32_t)__syncthreads_count(tid + cap < nv && Wrun - rcum[tid + cap] > A.M) +
+          (uint32_t)__syncthreads_count(tid + cap + kSelThreads < nv && Wrun - rcum[tid + cap + kSelThreads] > A.M);
+      n_pre = umin32(nv, cap + over + 1u);
+      n_adm = 0;
+      realized = n_run - n_pre;
+    } else {
+      // admit in greedy order while W0 + l <= M and c0 + 1 <= B, break at the first misfit: the
+      // count of admit prefix sums that stay within both (prefix sums strictly increase)
+      __syncthreads();  // aflag complete
+      for (uint32_t q = tid; q < na; q += kSelThreads) acum[q] = aflag[kSortCap + q];
+      __syncthreads();
+      block_inclusive_scan(acum, na, s_tmp2);
+      n_adm = (uint32_t)__syncthreads_count(tid < na && W0 + acum[tid] <= A.M && c0 + tid + 1 <= B) +
+              (uint32_t)__syncthreads_count(tid + kSelThreads < na && W0 + acum[tid + kSelThreads] <= A.M &&
+                                            c0 + tid + kSelThreads + 1 <= B);
+      n_pre = cap;
+      realized = c0 + n_adm;
+    }
+  }
+  uint32_t* pre = w.stage_pre + (size_t)(B - 1) * kStageRun;
+  uint32_t* adm = w.stage_adm + (size_t)(B - 1) * kMaxB;
+  for (uint32_t q = tid; q < n_pre; q += kSelThreads) pre[q] = rx[rord[q]];
+  for (uint32_t q = tid; q < n_adm; q += kSelThreads) adm[q] = aflag[q];
+  if (tid == 0) w.stage_sc[B - 1] = make_uint4(n_pre, n_adm, realized, flags);
+}
+
 // S5 + copy of B*'s staged cap result into the outputs (last CTA of k_select).
 __device__ bool finalize_fast(const SelectArgs& A) {
   __shared__ long long s_bv[kSelThreads / 32];
@@ -896,6 +989,24 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
           s_gf[pos] = s_gall[e];
         }
       }
+      if (rpre) {
+        // the running requests in ascending composite order at B (the victim order, reading
+        // R18, is a prefix of it) with the prefix sums of their l, by rank counting on the
+        // threads from the top down (they overlap the survivors' counting above)
+        for (uint32_t t = kSelThreads - 1 - tid; t < n_run; t += kSelThreads) {
+          const unsigned long long c = s_rk[t];
+          uint32_t pos = 0;
+          unsigned long long cum = 0;
+#pragma unroll 4
+          for (uint32_t f = 0; f < n_run; ++f) {
+            const unsigned long long v = s_rk[f];
+            pos += v < c ? 1u : 0u;
+            cum += v <= c ? (unsigned long long)s_rl[f] : 0ull;
+          }
+          s_vc[kRunOrdAt + pos] = cum;
+          s_idx[kRunOrdAt + pos] = t;
+        }
+      }
       __syncthreads();
       if (B == 256) ANDES_TRACE(w, 2401);
       cnt = k;
@@ -972,7 +1083,10 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
       w.sel_thr[B - 1] = thr;
     }
     if (B == 256) ANDES_TRACE(w, 2404);
-    if (n_run <= (uint32_t)kStageRun) {
+    if (rpre) {
+      stage_cap_fast(A, B, kstar, thr, s_idx, s_run8, s_lsel, s_rk, s_rx, s_idx + kRunOrdAt, s_vc + kRunOrdAt,
+                     n_run, reinterpret_cast<uint32_t*>(s_gf), s_ps);
+    } else if (n_run <= (uint32_t)kStageRun) {
       // victims and their prefix sums live past the first kStageRun slots of s_key / s_idx
       stage_cap(A, B, tB, kstar, thr, s_idx, s_key + kStageRun, s_idx + kStageRun, s_vc,
                 s_ps, reinterpret_cast<uint32_t*>(s_gf), rpre, s_rk, s_rx, s_rl, n_run, s_lsel);
@@ -1048,12 +1162,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs A) {
 //   -- barrier
 //   C  one candidate B per CTA (B = B_cap - b, b + grid, ...): select_one_B; S5/S6 by the last
 //      CTA (select_finish)
-// Grid-barrier words live in the second 128-byte line of the per-call globals (zeroed with them).
-struct DecideSync {
-  uint32_t arrive_a, ready_a, arrive_b, ready_b;
-  uint32_t theta, zcut, n_surv, overflow;
-};
-__device__ __forceinline__ DecideSync* decide_sync(const Work& w) { return reinterpret_cast<DecideSync*>(w.g + 1); }
+// Grid-barrier words live in the second 128-byte line of the per-call globals (Globals2).
 
 __device__ __forceinline__ void spin_until_set(const uint32_t* flag) {
   while (ld_acquire_u32(flag) == 0u) __nanosleep(20);
@@ -1065,7 +1174,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_decide(SelectArgs A) {
   __shared__ uint32_t s_flag;
   const ReqView& r = A.r;
   const Work& w = A.w;
-  DecideSync* ds = decide_sync(w);
+  Globals2* ds = globals2(w);
   const uint32_t tid = threadIdx.x, G = gridDim.x;
   pdl_wait();
   snap_globals(w.g, &s_g);
