@@ -4,10 +4,9 @@
 //   k_refine_pairs  one CTA: the admits (greedy order) are paired with the minimal prefix of the
 //                   remaining victims (victim order) that makes room in M; each pair's stall
 //                   D_k = its victims' preempt costs + the admit's resume cost (R24 model);
-//   k_refine_loss   one warp per still-running request i, all pairs k at once (one walk of i's
-//                   timeline): the QoE drop of i under each stall, llrint((Q_now,i -
-//                   Q_i(now + D_k)) 2^32), summed per pair in int64 (deterministic); Q_i(t) is the
-//                   in-flight QoE at t with no new token;
+//   k_refine_loss   one warp per (still-running request i, pair k): the QoE drop of i under the
+//                   stall, llrint((Q_now,i - Q_i(now + D_k)) 2^32), summed per pair in int64
+//                   (deterministic); Q_i(t) is the in-flight QoE at t with no new token;
 //   k_refine_final  one CTA: the first pair whose admit's gain does not exceed its loss cancels
 //                   itself and every later pair; the outputs are rewritten.
 // The pairs' acceptance is a prefix (the refiner stops at the first rejection), so every pair's
@@ -135,31 +134,57 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_pairs(ReqView r, Work
   if (tid == 0) w.g->rf_npairs = np;
 }
 
-// Q of a request from its delivered-token sums at relative time t (Eq. 1-3, readings R1-R3): sp =
-// sum of the clamped delays of the delivered due tokens, dm = delta_m when token m was delivered.
-__device__ __forceinline__ double q_at(uint32_t g, uint32_t P, uint32_t ttft, uint32_t m, long long t, long long sp,
-                                       uint32_t dm) {
-  if (m == 0) return 1.0;
-  const long long Pl = P;
-  const long long cw = Pl * (((long long)m * ((long long)m - 1)) >> 1);
-  if (g >= m) {
-    const long long Im = (long long)ttft + ((long long)m - 1) * Pl;
-    const long long dtm = min((long long)dm, t - Im);
-    return qoe_value(sp, (long long)m * dtm + cw);
+// Q of request i at relative time t with its delivered timeline only (Eq. 1-3, readings R1-R3),
+// by one warp: lateness max-scan over the delivered tokens, clamped sums for the two times.
+__device__ void walk_two(const ReqView& r, uint32_t i, long long t1, long long t2, double& q1, double& q2) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t g = r.n_deliv[i], P = r.period[i], ttft = r.ttft[i], mt = r.max_total[i];
+  const unsigned long long base = r.tl_base[i];
+  const uint32_t m1 = due_count(t1, ttft, P, mt), m2 = due_count(t2, ttft, P, mt);
+  const uint32_t lim = min(g, max(m1, m2));
+  long long s1 = 0, s2 = 0;     // sums of min(delta_j, t - I_j) over delivered due tokens
+  uint32_t carry = 0, dm1 = 0, dm2 = 0;  // lateness carried; delta at m1 / m2 (when delivered)
+  for (uint32_t j0 = 0; j0 < lim; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    const uint32_t I = ttft + j * P;
+    const uint32_t d = j < lim ? r.tl_pool[base + j] : I;
+    uint32_t v = d > I ? d - I : 0u;  // lateness (>= 0)
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= (uint32_t)off) v = max(v, u);
+    }
+    const uint32_t dj = max(carry, v);  // delta_{j+1}
+    if (j < lim) {
+      if (j < m1) s1 += min((long long)dj, t1 - (long long)I);
+      if (j < m2) s2 += min((long long)dj, t2 - (long long)I);
+      if (j + 1 == m1) dm1 = dj;
+      if (j + 1 == m2) dm2 = dj;
+    }
+    carry = max(carry, __shfl_sync(0xffffffffu, v, 31));
   }
-  const long long K = m - g;
-  const long long w0 = t - (long long)ttft - ((long long)g - 1) * Pl;
-  return qoe_value(sp + sum_down(0, K, w0, Pl), (long long)m * (w0 - K * Pl) + cw);
+  for (int off = 16; off; off >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    dm1 = max(dm1, __shfl_xor_sync(0xffffffffu, dm1, off));
+    dm2 = max(dm2, __shfl_xor_sync(0xffffffffu, dm2, off));
+  }
+  auto finish = [&](uint32_t m, long long t, long long sp, uint32_t dm) -> double {
+    if (m == 0) return 1.0;
+    const long long Pl = P;
+    const long long cw = Pl * (((long long)m * ((long long)m - 1)) >> 1);
+    if (g >= m) {
+      const long long Im = (long long)ttft + ((long long)m - 1) * Pl;
+      const long long dtm = min((long long)dm, t - Im);
+      return qoe_value(sp, (long long)m * dtm + cw);
+    }
+    const long long K = m - g;
+    const long long w0 = t - (long long)ttft - ((long long)g - 1) * Pl;
+    return qoe_value(sp + sum_down(0, K, w0, Pl), (long long)m * (w0 - K * Pl) + cw);
+  };
+  q1 = finish(m1, t1, s1, dm1);
+  q2 = finish(m2, t2, s2, dm2);
 }
-
-// One warp per still-running request i: its QoE drop under EVERY pair's stall in one walk of its
-// timeline.  Lanes own pairs (k = kb + lane + 32 s, s < kRfPerLane); the tokens are read once per
-// 32 (coalesced) and broadcast by shuffles; per token the lateness max (delta, reading R2) and,
-// for each of the lane's pairs whose time t_k = now + D_k - a_i has the token due, the clamped
-// delay min(delta, t_k - I_j) (R3) are accumulated.  Request i counts for pair k only while it is
-// still running: victims consumed by pairs <= k (rf_vend is nondecreasing) are excluded.  Losses
-// are summed per pair in int64 units of 2^-32 (order-independent, deterministic).
-constexpr uint32_t kRfPerLane = 8;
 
 __global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work w, int64_t now) {
   __shared__ Globals s_g;
@@ -170,72 +195,17 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work 
   const uint32_t n_run = min(s_g.n_run, (uint32_t)kMaxRunning);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t q = gw; q < n_run; q += W) {
+  for (uint32_t pr = gw; pr < n_run * np; pr += W) {
+    const uint32_t q = pr / np, k = pr - q * np;
     const uint32_t i = __ldcg(w.run_list + q);
     const uint32_t vm = __ldcg(w.vmark + i);
-    // pairs for which i is still running: k < klim
-    uint32_t klim = np;
-    if (vm) {
-      uint32_t lo = 0, hi = np;  // first k with rf_vend[k] > vm - 1
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldcg(w.rf_vend + mid) > vm - 1u) hi = mid;
-        else lo = mid + 1;
-      }
-      klim = lo;
-    }
-    if (klim == 0) continue;
+    if (vm && vm - 1u < __ldcg(w.rf_vend + k)) continue;  // preempted by pairs <= k
     const long long a = r.arrival[i];
-    const uint32_t g = r.n_deliv[i], P = r.period[i], ttft = r.ttft[i], mt = r.max_total[i];
-    const unsigned long long base = r.tl_base[i];
-    const long long t0 = now - a;
-    const uint32_t m0 = due_count(t0, ttft, P, mt);
-    double qn = 0.0;
-    for (uint32_t kb = 0; kb < klim; kb += 32u * kRfPerLane) {
-      long long tk[kRfPerLane], acc[kRfPerLane];
-      uint32_t mk[kRfPerLane], dmk[kRfPerLane];
-      uint32_t Lmax = kb == 0 ? min(g, m0) : 0u;
-#pragma unroll
-      for (uint32_t s2 = 0; s2 < kRfPerLane; ++s2) {
-        const uint32_t k = kb + lane + 32u * s2;
-        tk[s2] = k < klim ? now + __ldcg(w.rf_D + k) - a : t0;
-        mk[s2] = k < klim ? due_count(tk[s2], ttft, P, mt) : 0u;
-        acc[s2] = 0;
-        dmk[s2] = 0;
-        Lmax = max(Lmax, min(g, mk[s2]));
-      }
-      for (int o = 16; o; o >>= 1) Lmax = max(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, o));
-      long long acc0 = 0;  // the decision time (Q_now), first pass only
-      uint32_t dm0 = 0, delta = 0;
-      for (uint32_t j0 = 0; j0 < Lmax; j0 += 32) {
-        const uint32_t dl = j0 + lane < Lmax ? r.tl_pool[base + j0 + lane] : 0u;
-        const uint32_t cnt = min(32u, Lmax - j0);
-        for (uint32_t jj = 0; jj < cnt; ++jj) {
-          const uint32_t j = j0 + jj;
-          const uint32_t d = __shfl_sync(0xffffffffu, dl, jj);
-          const uint32_t I = ttft + j * P;
-          delta = max(delta, d > I ? d - I : 0u);
-          if (kb == 0) {
-            if (j < m0) acc0 += min((long long)delta, t0 - (long long)I);
-            if (j + 1 == m0) dm0 = delta;
-          }
-#pragma unroll
-          for (uint32_t s2 = 0; s2 < kRfPerLane; ++s2) {
-            if (j < mk[s2] && j < g) acc[s2] += min((long long)delta, tk[s2] - (long long)I);
-            if (j + 1 == mk[s2]) dmk[s2] = delta;
-          }
-        }
-      }
-      if (kb == 0) qn = q_at(g, P, ttft, m0, t0, acc0, dm0);
-#pragma unroll
-      for (uint32_t s2 = 0; s2 < kRfPerLane; ++s2) {
-        const uint32_t k = kb + lane + 32u * s2;
-        if (k < klim) {
-          const double qd = q_at(g, P, ttft, mk[s2], tk[s2], acc[s2], dmk[s2]);
-          const long long lf = gain_fixed(__dsub_rn(qn, qd));
-          if (lf) atomicAdd(reinterpret_cast<unsigned long long*>(w.rf_loss + k), (unsigned long long)lf);
-        }
-      }
+    double qn, qd;
+    walk_two(r, i, now - a, now + __ldcg(w.rf_D + k) - a, qn, qd);
+    if (lane == 0) {
+      const long long lf = gain_fixed(__dsub_rn(qn, qd));
+      if (lf) atomicAdd(reinterpret_cast<unsigned long long*>(w.rf_loss + k), (unsigned long long)lf);
     }
   }
 }
