@@ -355,6 +355,53 @@ def _oracle_decision(oracle, snap, threads):
                            preempt_cap=snap.preempt_cap, threads=threads)
 
 
+def serving_sim(args, lr, stream):
+    """NEXT-3: the serving loop on the device (andes_simulate) over cyclic-burst traces at four
+    load factors, Andes' priority (gain / l, Eq. 6) vs LQSF (raw gain, reading R21), zero
+    preemption overhead; end-of-trace average QoE (FINAL mode, mean over requests with tokens,
+    P:L719) per load -- the fig:e2e-intensity analog without models (iteration latency = the
+    synthetic tau(B) table).  Wall time of the whole loop (one host read per iteration)."""
+    import numpy as np
+    import torch
+
+    import paper_2404_16283_b200 as A
+    import workloads as W
+
+    dev = torch.device("cuda", lr)
+    tau = torch.from_numpy(W.tau_table().view(np.int32)).to(dev)
+    rhos = (0.5, 1.0, 1.5, 2.0)
+    seeds = (1, 2)
+    res = {"andes": {}, "lqsf": {}}
+    iters = 0
+    t_all = 0.0
+    traces = [(sd, rho, W.sim_trace(sd, rho, window_s=120.0)) for rho in rhos for sd in seeds]
+    nmax = max(t["n"] for _, _, t in traces)
+    tmax = max(t["tl_len"] for _, _, t in traces)
+    ctx = A.Context(max_requests=nmax, max_B=256, max_tokens=tmax + 64, device=lr)
+    for pol, fl in (("andes", 0), ("lqsf", A.ANDES_LQSF)):
+        for sd, rho, tr in traces:
+            t0 = time.perf_counter()
+            g, pool, t, st = ctx.simulate(tr, tau, W.KV_CAPACITY, flags=fl, stream=stream)
+            stream.synchronize()
+            t_all += time.perf_counter() - t0
+            iters += st["iterations"]
+            n = tr["n"]
+            req = {"arrival_us": t["arrival_us"], "ttft_us": t["ttft_us"], "period_us": t["period_us"],
+                   "ctx_len": t["prompt_len"], "n_deliv": g, "max_total": torch.full((n,), -1, dtype=torch.int32, device=dev),
+                   "start_off_us": None, "rank": torch.arange(n, dtype=torch.int32, device=dev),
+                   "running": torch.zeros(n, dtype=torch.uint8, device=dev), "tl_base": t["tl_base"], "tl_pool": pool}
+            q, q64, sd_, sw_, m = ctx.qoe_eval(req, n, 0, A.ANDES_EVAL_FINAL, stream=stream)
+            qq = q64.cpu().numpy()[g.cpu().numpy() > 0]
+            res[pol].setdefault(f"{rho:.2f}", []).append(float(qq.mean()) if qq.size else 0.0)
+    out = {"workload": ("NEXT-3 serving loop on the device: cyclic-burst traces (120 s, intensity 2, 35% burst), "
+                        "2 seeds x rho 0.5..2.0 (2 req/s at rho 1), ShareGPT-shaped, 50/50 reading/listening, "
+                        "M=163840, B=1..256, tau(B)=20ms+0.8ms*B, zero preemption overhead"),
+           "avg_qoe_by_rho": {pol: {k: round(float(np.mean(v)), 4) for k, v in d.items()} for pol, d in res.items()},
+           "decisions": iters, "wall_s": round(t_all, 2), "decisions_per_s": iters / t_all if t_all else None}
+    del ctx
+    return out
+
+
 def e2e_incremental(args, dist, snap, ws, lr, stream):
     """The serving loop through the public API with a device-resident Request Tracker: every step
     (a) copies the previous iteration's delivered tokens (request index, delivery time) from
@@ -676,6 +723,9 @@ def run_ours(args):
     # ---- config 4: the 2^20-request population sharded over the ranks (multi-GPU decision)
     config4 = None if args.no_sharded else sharded_decision(args, dist, rank, ws, lr, stream, flush)
 
+    # ---- NEXT-3: the serving loop with the decision in the loop (rank 0; replicas would repeat it)
+    sim = None if (args.no_sim or rank != 0) else serving_sim(args, lr, stream)
+
     # ---- config 5: the 1024-scenario sweep (end-of-trace QoE per scenario)
     sweep = None if args.no_sweep else sweep_run(args, dist, rank, ws, lr, stream)
 
@@ -721,6 +771,7 @@ def run_ours(args):
         "objectives": objectives,
         "config4_sharded": config4,
         "config5_sweep": sweep,
+        "serving_sim": sim,
         "e2e": e2e,
         "e2e_full_upload": full_upload,
         "gpu_launches": KERNELS_PER_DECISION * args.steps,
@@ -756,6 +807,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 sharded decision")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 scenario sweep")
+    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-3 serving-loop simulation")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         _relaunch(args.gpus)

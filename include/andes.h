@@ -251,6 +251,56 @@ typedef struct {
 int andes_tracker_append(AndesCtx *ctx, const AndesTracker *t, const uint32_t *idx, const int64_t *t_abs,
                          uint32_t count, const uint8_t *serve_mask, void *stream);
 
+/* ---- Serving-loop simulator --------------------------------------
+ * A trace is served iteration by iteration with andes_schedule in the loop, on the device:
+ * at time now, the live requests (arrived, a_i <= now, and unfinished, g_i < out_i; rank = trace
+ * index; running = served in the previous iteration; l_i = prompt_i + g_i; the output length is
+ * unknown to the scheduler, max_total = UINT32_MAX, reading R7) are scheduled (S0-S6, forced);
+ * every served request receives one token at now' = now + tau(min(realized, B_cap)) (at least
+ * one; zero preemption overhead, as BASELINE config 1's driver), appended to its timeline; the
+ * served set becomes the running set; now = now'.  With no live request the clock jumps to the
+ * next arrival.  Runs until every request has its whole output or max_iters iterations.
+ * The end-of-trace QoE (reading R19) is then andes_qoe_eval(FINAL) on the trace table.
+ * All arrays DEVICE memory owned by the caller; the host loop reads a 32-byte control block once
+ * per iteration (the call is synchronous on `stream`).  The context must hold n requests,
+ * tl_len tokens and B_cap. */
+typedef struct {
+    uint32_t n;                    /* trace requests, arrival order (arrival_us nondecreasing)   */
+    const int64_t *arrival_us;
+    const uint32_t *ttft_us, *period_us;
+    const uint32_t *prompt_len;    /* prompt tokens (context before the first output token)      */
+    const uint32_t *output_len;    /* tokens the request will receive (>= 1)                     */
+    const uint64_t *tl_base;       /* timeline offsets: room for output_len[i] tokens each,
+                                      16-byte aligned starts recommended                          */
+    uint32_t *tl_pool;             /* out: delivery times (us since arrival)                      */
+    uint64_t tl_len;
+    uint32_t *n_deliv;             /* out: tokens delivered (zeroed by the call)                  */
+    uint8_t *served;               /* scratch [n]                                                 */
+    void *workspace;               /* scratch of andes_sim_workspace(n) bytes, 16-byte aligned   */
+} AndesSim;
+
+typedef struct {
+    const uint32_t *tau_us;  /* DEVICE u32[B_cap] */
+    uint32_t B_cap;
+    uint64_t kv_capacity;
+    uint32_t horizon_us;
+    uint32_t preempt_cap;
+    uint32_t flags;          /* andes_schedule flags (ANDES_LQSF, objectives, ...); FORCE implied */
+    uint32_t max_iters;
+} AndesSimParams;
+
+typedef struct {            /* HOST */
+    uint64_t iterations;    /* decisions taken                                  */
+    int64_t start_us, end_us;
+    uint32_t finished;      /* requests that received their whole output        */
+    uint32_t pad;
+} AndesSimStats;
+
+uint64_t andes_sim_workspace(uint32_t n);
+/* Errors: ANDES_E_INVAL, ANDES_E_CAPACITY (n, tokens or B_cap above the context limits), any
+ * error of andes_schedule, ANDES_E_CUDA. */
+int andes_simulate(AndesCtx *ctx, const AndesSim *sim, const AndesSimParams *p, AndesSimStats *stats, void *stream);
+
 /* ---- Multi-GPU decision ------------------------------------------
  * One process per GPU; rank g holds a contiguous range of the population (its requests have
  * global indices base_g .. base_g + n_g - 1, base_g = n_0 + ... + n_{g-1}; the rank fields must

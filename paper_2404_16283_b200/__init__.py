@@ -52,7 +52,7 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
            "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean", "andes_knapsack_dp",
-           "andes_knapsack_dp_workspace", "andes_tracker_append"]
+           "andes_knapsack_dp_workspace", "andes_tracker_append", "andes_simulate", "andes_sim_workspace"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -101,6 +101,23 @@ class Tracker(C.Structure):
                 ("tl_len", C.c_uint64), ("n_deliv", C.c_void_p), ("ctx_len", C.c_void_p), ("running", C.c_void_p)]
 
 
+class Sim(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("arrival_us", C.c_void_p), ("ttft_us", C.c_void_p), ("period_us", C.c_void_p),
+                ("prompt_len", C.c_void_p), ("output_len", C.c_void_p), ("tl_base", C.c_void_p),
+                ("tl_pool", C.c_void_p), ("tl_len", C.c_uint64), ("n_deliv", C.c_void_p), ("served", C.c_void_p),
+                ("workspace", C.c_void_p)]
+
+
+class SimParams(C.Structure):
+    _fields_ = [("tau_us", C.c_void_p), ("B_cap", C.c_uint32), ("kv_capacity", C.c_uint64), ("horizon_us", C.c_uint32),
+                ("preempt_cap", C.c_uint32), ("flags", C.c_uint32), ("max_iters", C.c_uint32)]
+
+
+class SimStats(C.Structure):
+    _fields_ = [("iterations", C.c_uint64), ("start_us", C.c_int64), ("end_us", C.c_int64), ("finished", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
 class QoeOut(C.Structure):
     _fields_ = [("q", C.c_void_p), ("q64", C.c_void_p), ("s_delay", C.c_void_p), ("s_whole", C.c_void_p),
                 ("m", C.c_void_p)]
@@ -141,6 +158,9 @@ def lib() -> C.CDLL:
                                         C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.andes_tracker_append.argtypes = [C.c_void_p, C.POINTER(Tracker), C.c_void_p, C.c_void_p, C.c_uint32,
                                            C.c_void_p, C.c_void_p]
+        L.andes_sim_workspace.argtypes = [C.c_uint32]
+        L.andes_sim_workspace.restype = C.c_uint64
+        L.andes_simulate.argtypes = [C.c_void_p, C.POINTER(Sim), C.POINTER(SimParams), C.POINTER(SimStats), C.c_void_p]
         L.andes_shard_init.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Shard)]
         L.andes_schedule_shard.argtypes = [C.c_void_p, C.POINTER(Shard), C.c_uint32, C.POINTER(Requests),
                                            C.POINTER(SchedParams), C.POINTER(DecisionPtrs), C.c_void_p, C.c_void_p,
@@ -357,6 +377,36 @@ class Context:
         count = int(idx.numel()) if idx is not None else 0
         self._check(lib().andes_tracker_append(self._h, C.byref(t), _ptr(idx), _ptr(t_abs), count, _ptr(serve_mask),
                                                _stream_ptr(stream)), "andes_tracker_append")
+
+    # -- andes_simulate (NEXT-3: the serving loop on the device, the decision in the loop)
+    def simulate(self, trace: dict, tau, kv_capacity: int, horizon_us=2_000_000, preempt_cap=UINT32_MAX, flags=0,
+                 max_iters=0, stream=None):
+        """trace: dict with n and numpy arrays arrival_us, ttft_us, period_us, prompt_len, output_len,
+        tl_base, and tl_len (workloads.sim_trace).  Returns (n_deliv i32[n], tl_pool i32[tl_len],
+        trace tensors dict, stats dict); everything stays on the device."""
+        torch = _torch()
+        import numpy as np
+        dev = self.device
+        n = int(trace["n"])
+        t = {k: torch.from_numpy(np.ascontiguousarray(trace[k]).view(
+            {8: np.int64, 4: np.int32}[np.asarray(trace[k]).dtype.itemsize])).to(dev)
+             for k in ("arrival_us", "ttft_us", "period_us", "prompt_len", "output_len", "tl_base")}
+        tl_len = int(trace["tl_len"])
+        pool = torch.zeros(max(tl_len, 4), dtype=torch.int32, device=dev)
+        g = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        served = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib().andes_sim_workspace(n)) + 16, dtype=torch.uint8, device=dev)
+        sim = Sim(n, _ptr(t["arrival_us"]), _ptr(t["ttft_us"]), _ptr(t["period_us"]), _ptr(t["prompt_len"]),
+                  _ptr(t["output_len"]), _ptr(t["tl_base"]), _ptr(pool), tl_len, _ptr(g), _ptr(served), _ptr(ws))
+        p = SimParams(_ptr(tau), int(tau.numel()), int(kv_capacity), int(horizon_us), int(preempt_cap), int(flags),
+                      int(max_iters))
+        st = SimStats()
+        self._check(lib().andes_simulate(self._h, C.byref(sim), C.byref(p), C.byref(st), _stream_ptr(stream)),
+                    "andes_simulate")
+        t["tl_pool"] = pool
+        t["n_deliv"] = g
+        return g[:n], pool, t, {"iterations": int(st.iterations), "start_us": int(st.start_us),
+                                 "end_us": int(st.end_us), "finished": int(st.finished)}
 
     # -- multi-GPU decision (andes_shard_init / andes_schedule_shard)
     def shard_init(self, world: int, rank: int, B_cap: int) -> Shard:

@@ -32,6 +32,7 @@ struct AndesCtx {
   std::vector<void*> allocs;
   uint32_t* B_list_dev = nullptr;
   uint32_t* err_pinned = nullptr;  // mapped pinned sticky error word (kernels raise bits into it)
+  SimCtl* sim_ctl = nullptr;       // pinned: the simulator's control block, read once per iteration
   // device mirrors for andes_schedule_host
   struct Mirror {
     int64_t* arrival;
@@ -303,6 +304,11 @@ int andes_create(AndesCtx** out, const AndesLimits* lim) {
     return rc;
   }
   *c->err_pinned = 0;
+  if ((e = cudaHostAlloc((void**)&c->sim_ctl, sizeof(SimCtl), cudaHostAllocDefault)) != cudaSuccess) {
+    int rc = cuda_check(c, e, "pinned alloc");
+    andes_destroy(c);
+    return rc;
+  }
   // host-path mirrors
   auto& m = c->mir;
   const size_t T = c->lim.max_tokens;
@@ -390,6 +396,7 @@ int andes_destroy(AndesCtx* c) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   for (void* p : c->allocs) cudaFree(p);
   if (c->err_pinned) cudaFreeHost(c->err_pinned);
+  if (c->sim_ctl) cudaFreeHost(c->sim_ctl);
   delete c;
   return ANDES_OK;
 }
@@ -654,6 +661,136 @@ int andes_tracker_append(AndesCtx* c, const AndesTracker* t, const uint32_t* idx
   if (count && (!idx || !t_abs)) return set_err(c, ANDES_E_INVAL, "idx/t_abs is NULL%s");
   TrackerView v{t->n, t->arrival_us, t->tl_base, t->tl_pool, t->tl_len, t->n_deliv, t->ctx_len, t->running};
   launch_tracker_append(cfg_of(c, stream), v, idx, t_abs, count, serve_mask, c->w);
+  return cuda_check(c, cudaGetLastError(), "kernel launch");
+}
+
+// ---- serving-loop simulator (sim.cu): workspace carving and the host loop
+namespace {
+struct SimCarve {
+  SimView v;
+  uint8_t* serve_mask;
+  uint32_t *admit, *preempt, *scalars, *kstar;
+  int64_t* V;
+  size_t bytes;
+};
+SimCarve sim_carve(void* ws, uint32_t n) {
+  SimCarve c{};
+  size_t off = 0;
+  char* b = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) -> void* {
+    void* p = b ? b + off : nullptr;
+    off += (bytes + 15) & ~size_t(15);
+    return p;
+  };
+  const size_t N = n ? n : 1;
+  c.v.l_arr = static_cast<int64_t*>(take(8 * N));
+  c.v.l_base = static_cast<uint64_t*>(take(8 * N));
+  c.v.l_ttft = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_period = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_ctx = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_g = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_rank = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_idx = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_maxtot = static_cast<uint32_t*>(take(4 * N));
+  c.v.l_run = static_cast<uint8_t*>(take(N));
+  c.serve_mask = static_cast<uint8_t*>(take(N));
+  c.preempt = static_cast<uint32_t*>(take(4 * N));
+  c.admit = static_cast<uint32_t*>(take(4 * kMaxB));
+  c.V = static_cast<int64_t*>(take(8 * kMaxB));
+  c.kstar = static_cast<uint32_t*>(take(4 * kMaxB));
+  c.scalars = static_cast<uint32_t*>(take(4 * ANDES_SC_COUNT));
+  c.v.ctl = static_cast<SimCtl*>(take(sizeof(SimCtl)));
+  c.bytes = off;
+  return c;
+}
+}  // namespace
+
+uint64_t andes_sim_workspace(uint32_t n) { return sim_carve(nullptr, n).bytes; }
+
+int andes_simulate(AndesCtx* c, const AndesSim* sim, const AndesSimParams* p, AndesSimStats* stats, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  if (!sim || !p || !stats) return set_err(c, ANDES_E_INVAL, "NULL argument%s");
+  const uint32_t n = sim->n;
+  if (n && (!sim->arrival_us || !sim->ttft_us || !sim->period_us || !sim->prompt_len || !sim->output_len ||
+            !sim->tl_base || !sim->tl_pool || !sim->n_deliv || !sim->served || !sim->workspace))
+    return set_err(c, ANDES_E_INVAL, "a simulator array is NULL%s");
+  if ((reinterpret_cast<uintptr_t>(sim->workspace) & 15u) != 0) return set_err(c, ANDES_E_INVAL, "workspace alignment%s");
+  if (n > c->lim.max_requests || sim->tl_len > c->lim.max_tokens || p->B_cap > c->lim.max_B)
+    return set_err(c, ANDES_E_CAPACITY, "simulator sizes exceed the context limits%s");
+  if (!p->tau_us || p->B_cap == 0 || p->horizon_us == 0 || p->kv_capacity == 0)
+    return set_err(c, ANDES_E_INVAL, "bad simulator parameters%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SimCarve k = sim_carve(sim->workspace, n);
+  SimView& v = k.v;
+  v.n = n;
+  v.arrival = sim->arrival_us;
+  v.ttft = sim->ttft_us;
+  v.period = sim->period_us;
+  v.prompt = sim->prompt_len;
+  v.out_len = sim->output_len;
+  v.tl_base = sim->tl_base;
+  v.tl_pool = sim->tl_pool;
+  v.tl_len = sim->tl_len;
+  v.g = sim->n_deliv;
+  v.served = sim->served;
+  memset(stats, 0, sizeof *stats);
+  if (n == 0) return ANDES_OK;
+  cudaError_t e = cudaMemsetAsync(sim->n_deliv, 0, 4ull * n, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(sim->served, 0, n, s);
+  if (e != cudaSuccess) return cuda_check(c, e, "simulator reset");
+  int64_t now = 0;
+  if ((e = cudaMemcpyAsync(&now, sim->arrival_us, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return cuda_check(c, e, "simulator start");
+  stats->start_us = now;
+  SimCtl* h = c->sim_ctl;
+  AndesRequests rq{};
+  rq.arrival_us = v.l_arr;
+  rq.ttft_us = v.l_ttft;
+  rq.period_us = v.l_period;
+  rq.ctx_len = v.l_ctx;
+  rq.n_deliv = v.l_g;
+  rq.max_total = v.l_maxtot;
+  rq.start_off_us = nullptr;
+  rq.rank = v.l_rank;
+  rq.running = v.l_run;
+  rq.tl_base = v.l_base;
+  rq.tl_pool = sim->tl_pool;
+  rq.tl_len = sim->tl_len;
+  AndesSchedParams sp{};
+  sp.horizon_us = p->horizon_us;
+  sp.B_cap = p->B_cap;
+  sp.tau_us = p->tau_us;
+  sp.kv_capacity = p->kv_capacity;
+  sp.preempt_cap = p->preempt_cap;
+  sp.flags = p->flags | ANDES_FORCE;
+  sp.prefill_tok_s = 5000;
+  AndesDecision dd{k.serve_mask, k.admit, k.preempt, k.scalars, k.V, k.kstar};
+  const uint32_t max_iters = p->max_iters ? p->max_iters : 0xFFFFFFFFu;
+  const int64_t kFromCtl = (int64_t)0x8000000000000000ll;
+  int64_t pending = now;  // the next k_sim_live's time (kFromCtl: the one k_sim_step computed)
+  for (uint64_t it = 0;;) {
+    launch_sim_live(s, v, pending);
+    if ((e = cudaMemcpyAsync(h, v.ctl, sizeof(SimCtl), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return cuda_check(c, e, "simulator iteration");
+    now = h->now;
+    stats->finished = h->finished;
+    if (h->finished == n || it >= max_iters) break;
+    if (h->n_live == 0) {
+      pending = h->next_arrival;
+      continue;
+    }
+    rq.n = h->n_live;
+    sp.now_us = now;
+    int rc = andes_schedule(c, &rq, &sp, &dd, stream);
+    if (rc) return rc;
+    launch_sim_step(s, c->sm_count, v, h->n_live, now, p->tau_us, p->B_cap, k.serve_mask, k.scalars);
+    pending = kFromCtl;
+    ++it;
+    stats->iterations = it;
+  }
+  stats->end_us = now;
   return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
 

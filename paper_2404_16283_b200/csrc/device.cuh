@@ -74,6 +74,32 @@ struct TrackerView {
   uint8_t* running;
 };
 
+// Serving-loop simulator (sim.cu): the control block read by the host once per iteration, and
+// the trace + live-table view.
+struct SimCtl {
+  int64_t now;           // the iteration's time (after k_sim_step: the next one)
+  int64_t next_arrival;  // first request not yet arrived (INT64_MAX if none)
+  uint32_t n_live;       // live requests (k_sim_live)
+  uint32_t finished;     // arrived requests that have received their whole output
+  uint32_t pad[2];
+};
+struct SimView {
+  uint32_t n;
+  const int64_t* arrival;
+  const uint32_t *ttft, *period, *prompt, *out_len;
+  const uint64_t* tl_base;
+  uint32_t* tl_pool;
+  uint64_t tl_len;
+  uint32_t* g;
+  uint8_t* served;
+  // live table (k_sim_live), in trace order
+  int64_t* l_arr;
+  uint32_t *l_ttft, *l_period, *l_ctx, *l_g, *l_rank, *l_idx, *l_maxtot;
+  uint8_t* l_run;
+  uint64_t* l_base;
+  SimCtl* ctl;
+};
+
 // Per-tile descriptor of the timeline scan (written by prep): the request owning the tile's
 // first position and the source of its head-segment carry.
 struct alignas(16) TileMeta {

@@ -88,6 +88,9 @@ void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const Sc
 void init_kernels();
 void launch_tracker_append(const LaunchCfg& L, const TrackerView& t, const uint32_t* idx, const int64_t* t_abs,
                            uint32_t count, const uint8_t* serve_mask, const Work& w);
+void launch_sim_live(cudaStream_t s, const SimView& v, int64_t now);
+void launch_sim_step(cudaStream_t s, uint32_t sm_count, const SimView& v, uint32_t n_live, int64_t now,
+                     const uint32_t* tau, uint32_t B_cap, const uint8_t* serve_mask, const uint32_t* scalars);
 void launch_debug_checks(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now);
 
 }  // namespace andes

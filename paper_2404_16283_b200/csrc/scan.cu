@@ -825,10 +825,19 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
     t1 = ntail > 1 ? v.y : 0u;
     t2 = ntail > 2 ? v.z : 0u;
   }
-  // ---- pass 1: zero-carry lateness at the sub-range's end
+  // ---- pass 1: zero-carry lateness at the sub-range's end.  The groups every active lane has
+  // (gi < nmin, warp-uniform) run unpredicated; the few that only some lanes have, predicated.
+  const uint32_t nmin = min(gmax, __reduce_min_sync(0xffffffffu, active ? nfull : 0xFFFFFFFFu));
   uint32_t a = Is - P;
 #pragma unroll kTokUnroll
-  for (uint32_t gi = 0; gi < gmax; ++gi) {
+  for (uint32_t gi = 0; gi < nmin; ++gi) {
+    const uint4 v = ld_shared_v4(a0 + (gi << 4));
+    a = max(a + P, v.x);
+    a = max(a + P, v.y);
+    a = max(a + P, v.z);
+    a = max(a + P, v.w);
+  }
+  for (uint32_t gi = nmin; gi < gmax; ++gi) {
     if (gi < nfull) {
       const uint4 v = ld_shared_v4(a0 + (gi << 4));
       a = max(a + P, v.x);
@@ -873,15 +882,59 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   prefix = seg_combine(acc, tile_agg);
   if (pub && last_batch && lane < (uint32_t)TW) st_relaxed(&w.tile_status[t + lane], kStPrefix | prefix);
   const uint32_t carry = flag ? 0u : excl_flag ? excl_v : max((uint32_t)acc, excl_v);
-  // ---- pass 2: consumption times from the carry, sums, edge
+  // ---- pass 2: consumption times from the carry, sums, edge.
+  // Sum of T~ = min(A, t) over the sub-range.  Only S = sum(T~ - I) is needed, and every term is
+  // at most the lateness at the sub-range's last token, max(dz, carry) (the lateness max is
+  // nondecreasing): when nn * max(dz, carry) < 2^32 for every lane (warp-uniform), the sums run
+  // in 32-bit arithmetic modulo 2^32 and S = (sum T~ - sum I) mod 2^32 is exact; else 64-bit.
   uint32_t Ac = Is - P + carry;
-  unsigned long long sumT = 0ull;
+  const uint32_t nn_all = active ? (uint32_t)max(xe - xs, 0) : 0u;
+  const bool fits32 = __all_sync(0xffffffffu, (unsigned long long)nn_all * max(dz, carry) < (1ull << 32));
 #ifndef ANDES_NO_NOCLAMP
   // consumption times are nondecreasing, so the clamp min(A, t) is void for the whole warp when
   // every lane's last one, I_last + max(L_end, carry), is <= t (warp-uniform loop choice)
   const uint32_t A_hi = Is + (uint32_t)max(xe - xs - 1, 0) * P + max(dz, carry);
   const bool noclamp = kFinal || __all_sync(0xffffffffu, !active || A_hi <= tcl);
-  if (noclamp) {
+#else
+  const bool noclamp = kFinal;
+#endif
+  unsigned long long sumT = 0ull;
+  uint32_t sum32 = 0u;
+  if (fits32) {
+    if (noclamp) {
+#pragma unroll kTokUnroll
+      for (uint32_t gi = 0; gi < nmin; ++gi) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+        Ac = A3;
+        sum32 += A0 + A1 + A2 + A3;
+      }
+      for (uint32_t gi = nmin; gi < gmax; ++gi) {
+        if (gi < nfull) {
+          const uint4 v = ld_shared_v4(a0 + (gi << 4));
+          const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+          Ac = A3;
+          sum32 += A0 + A1 + A2 + A3;
+        }
+      }
+    } else {
+#pragma unroll kTokUnroll
+      for (uint32_t gi = 0; gi < nmin; ++gi) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+        Ac = A3;
+        sum32 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+      }
+      for (uint32_t gi = nmin; gi < gmax; ++gi) {
+        if (gi < nfull) {
+          const uint4 v = ld_shared_v4(a0 + (gi << 4));
+          const uint32_t A0 = max(Ac + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+          Ac = A3;
+          sum32 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+        }
+      }
+    }
+  } else if (noclamp) {
 #pragma unroll kTokUnroll
     for (uint32_t gi = 0; gi < gmax; ++gi) {
       if (gi < nfull) {
@@ -891,9 +944,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
         sumT += (unsigned long long)A0 + A1 + A2 + A3;
       }
     }
-  } else
-#endif
-  {
+  } else {
 #pragma unroll kTokUnroll
     for (uint32_t gi = 0; gi < gmax; ++gi) {
       if (gi < nfull) {
@@ -907,9 +958,9 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   uint32_t A_last = Ac;  // consumption time of the last valid token
   if (ntail) {
     const uint32_t A0 = max(Ac + P, t0), A1 = max(A0 + P, t1), A2 = max(A1 + P, t2);
-    sumT += min(A0, tcl);
-    if (ntail > 1) sumT += min(A1, tcl);
-    if (ntail > 2) sumT += min(A2, tcl);
+    const uint32_t c0 = min(A0, tcl), c1 = ntail > 1 ? min(A1, tcl) : 0u, c2 = ntail > 2 ? min(A2, tcl) : 0u;
+    sum32 += c0 + c1 + c2;
+    sumT += (unsigned long long)c0 + c1 + c2;
     A_last = ntail == 1 ? A0 : ntail == 2 ? A1 : A2;
   }
   const int32_t xl = xe - 1;  // the sub-range's last valid token
@@ -917,7 +968,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
     const uint32_t nn = (uint32_t)(xe - xs);
     const unsigned long long sumI =
         (unsigned long long)nn * Is + (unsigned long long)P * (((unsigned long long)nn * (nn - 1)) >> 1);
-    const unsigned long long dsum = sumT - sumI;
+    const unsigned long long dsum = fits32 ? (unsigned long long)(sum32 - (uint32_t)sumI) : sumT - sumI;
     if (dsum) atomicAdd(&w.spre[qridx], dsum);
     if (qek && xe == qvend) {
       const uint32_t Il = qA + (uint32_t)xl * P;

@@ -338,6 +338,27 @@ def sweep(scenarios, n_base: int = 2000) -> tuple[Snapshot, np.ndarray]:
     return snap, off
 
 
+def sim_trace(seed: int, rho: float, window_s: float = 120.0, rate_at_rho1: float = 2.0, listen_frac: float = 0.5,
+              dataset: str = "sharegpt", max_prompt: int = 32768, max_out: int = 8192) -> dict:
+    """A request trace for the serving-loop simulator (NEXT-3, andes_simulate): cyclic-burst
+    arrivals (intensity 2, 35% burst; the cycle shortened to the window) at
+    rho * rate_at_rho1 requests/s on average (rate_at_rho1 ~ the synthetic tau(B) model's service
+    rate at M = 163,840 for ShareGPT-shaped requests), Table-2 lengths (clamped), TTFT target
+    max(input/5000, 1) s, reading / listening speeds.  Timelines get room for the
+    whole output (16-byte aligned starts).  Arrival order = rank."""
+    rng = np.random.default_rng([int(seed), int(round(rho * 100)), 7])
+    n = max(1, int(round(rate_at_rho1 * rho * window_s)))
+    inp, out = sample_lengths(rng, n, dataset, in_clamp=(1, max_prompt), out_clamp=(1, max_out))
+    arr_s = cyclic_burst_arrivals(rng, n, n / window_s, cycle_s=window_s)
+    arr = np.rint(arr_s * 1e6).astype(np.int64)
+    span = (out.astype(np.int64) + POOL_ALIGN - 1) // POOL_ALIGN * POOL_ALIGN
+    base = np.concatenate([[0], np.cumsum(span)[:-1]]).astype(np.uint64)
+    return dict(n=n, arrival_us=arr, ttft_us=np.maximum(200 * inp, 1_000_000).astype(np.uint32),
+                period_us=np.where(rng.random(n) < listen_frac, LISTEN_PERIOD_US, READ_PERIOD_US).astype(np.uint32),
+                prompt_len=inp.astype(np.uint32), output_len=out.astype(np.uint32), tl_base=base,
+                tl_len=int(span.sum()), name=f"sim-s{seed}-rho{rho:.2f}")
+
+
 def config5_scenarios(seeds: int = 32, rhos=SWEEP_RHOS):
     """BASELINE config 5: 1024 scenarios = 32 trace seeds x 32 load factors."""
     return [(sd, rho) for sd in range(1, seeds + 1) for rho in rhos]
