@@ -355,6 +355,55 @@ def _oracle_decision(oracle, snap, threads):
                            preempt_cap=snap.preempt_cap, threads=threads)
 
 
+def decision_trace(ctx, req, n, snap, tau, out, stream):
+    """Stage breakdown of one decision from the kernels' own %globaltimer stamps (one store per
+    CTA start and end by thread 0: the graph's launches and overlaps are not perturbed the way
+    event records between kernels perturb them).  Internal hooks andes_debug_trace/_read."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2404_16283_b200 as A
+    L = A.lib()
+    L.andes_debug_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]
+    L.andes_debug_trace.argtypes = [C.c_void_p, C.c_int]
+    L.andes_debug_trace(ctx._h, 1)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream,
+                         preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
+        stream.synchronize()
+        L.andes_debug_trace(ctx._h, 0)
+        L.andes_debug_trace(ctx._h, 1)  # fresh stamps for one decision
+        ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream,
+                     preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
+        stream.synchronize()
+    tr = np.zeros(1 << 16, np.uint64)
+    L.andes_debug_read(ctx._h, 7, tr.ctypes.data, tr.nbytes)
+    L.andes_debug_trace(ctx._h, 0)
+    tr = tr.astype(np.int64)
+
+    def span(lo, hi):
+        x = tr[lo:hi].reshape(-1, 2)
+        return x[x[:, 0] > 0]
+    pr, sc, st, cp, sel = span(7000, 8024), span(5000, 7000), span(3000, 4024), span(8100, 9124), span(0, 512)
+    if not (len(pr) and len(sc) and len(st) and len(cp) and len(sel)):
+        return None
+    t0 = pr[:, 0].min()
+    us = lambda v: round((int(v) - t0) / 1e3, 2)  # noqa: E731
+    fin = [us(tr[k]) for k in (2100, 2105) if tr[k]]
+    stages = {"prep": [0.0, us(pr[:, 1].max())], "scan": [us(sc[:, 0].min()), us(sc[:, 1].max())],
+              "state": [us(st[:, 0].min()), us(st[:, 1].max())], "compact": [us(cp[:, 0].min()), us(cp[:, 1].max())],
+              "select": [us(sel[:, 0].min()), us(sel[:, 1].max())], "finalize": fin}
+    return {"source": "in-kernel %globaltimer stamps (CTA start/end), one config-3 decision, L2 warm",
+            "stages_us_from_prep_start": stages,
+            "gaps_us": {"prep->scan": round(stages["scan"][0] - stages["prep"][1], 2),
+                        "scan->state": round(stages["state"][0] - stages["scan"][1], 2),
+                        "state->compact": round(stages["compact"][0] - stages["state"][1], 2),
+                        "compact->select": round(stages["select"][0] - stages["compact"][1], 2)}}
+
+
 def serving_sim(args, lr, stream):
     """NEXT-3: the serving loop on the device (andes_simulate) over cyclic-burst traces at four
     load factors, Andes' priority (gain / l, Eq. 6) vs LQSF (raw gain, reading R21), zero
@@ -370,11 +419,11 @@ def serving_sim(args, lr, stream):
     dev = torch.device("cuda", lr)
     tau = torch.from_numpy(W.tau_table().view(np.int32)).to(dev)
     rhos = (0.5, 1.0, 1.5, 2.0)
-    seeds = (1, 2)
+    seeds = (1,)
     res = {"andes": {}, "lqsf": {}}
     iters = 0
     t_all = 0.0
-    traces = [(sd, rho, W.sim_trace(sd, rho, window_s=120.0)) for rho in rhos for sd in seeds]
+    traces = [(sd, rho, W.sim_trace(sd, rho, window_s=60.0, rate_at_rho1=8.0)) for rho in rhos for sd in seeds]
     nmax = max(t["n"] for _, _, t in traces)
     tmax = max(t["tl_len"] for _, _, t in traces)
     ctx = A.Context(max_requests=nmax, max_B=256, max_tokens=tmax + 64, device=lr)
@@ -393,8 +442,8 @@ def serving_sim(args, lr, stream):
             q, q64, sd_, sw_, m = ctx.qoe_eval(req, n, 0, A.ANDES_EVAL_FINAL, stream=stream)
             qq = q64.cpu().numpy()[g.cpu().numpy() > 0]
             res[pol].setdefault(f"{rho:.2f}", []).append(float(qq.mean()) if qq.size else 0.0)
-    out = {"workload": ("NEXT-3 serving loop on the device: cyclic-burst traces (120 s, intensity 2, 35% burst), "
-                        "2 seeds x rho 0.5..2.0 (2 req/s at rho 1), ShareGPT-shaped, 50/50 reading/listening, "
+    out = {"workload": ("NEXT-3 serving loop on the device: cyclic-burst traces (60 s, intensity 2, 35% burst), "
+                        "rho 0.5..2.0 x 8 req/s, ShareGPT-shaped, 50/50 reading/listening, "
                         "M=163840, B=1..256, tau(B)=20ms+0.8ms*B, zero preemption overhead"),
            "avg_qoe_by_rho": {pol: {k: round(float(np.mean(v)), 4) for k, v in d.items()} for pol, d in res.items()},
            "decisions": iters, "wall_s": round(t_all, 2), "decisions_per_s": iters / t_all if t_all else None}
@@ -643,6 +692,10 @@ def run_ours(args):
 
     sc = out.scalars.cpu().numpy().view(np.uint32)
     stage_ms = [x / args.steps for x in stage_sum]
+    try:
+        trace = decision_trace(ctx, req, n, snap, tau, out, stream)
+    except Exception as ex:  # noqa: BLE001 -- the breakdown is context, the line must still print
+        trace = {"error": f"{type(ex).__name__}: {ex}"}
     ms_per_step = total_ms / args.steps
     value = ws * args.steps / (total_ms / 1e3)
 
@@ -663,8 +716,10 @@ def run_ours(args):
                      "HBM-bound kernel. At 64K requests (38 MB) its launch is latency-bound (ramp-up and "
                      "tail of ~2.4 tiles per warp); its throughput roofline is qoe_eval.roofline (2^20 "
                      "requests, the same kernel)")}
-    roof["stage_ms"] = dict(zip(names, stage_ms))
-    roof["stage_share"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
+    roof["stage_ms_event_graph"] = dict(zip(names, stage_ms))
+    roof["stage_trace"] = trace
+    roof["ib_evaluations_per_s"] = n * 256 / (ms_per_step / 1e3)
+    roof["stage_share_event_graph"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
 
     # ---- S1 alone at scale: QoE-eval token-events/s on a 1M-request population (config-4 size)
     big = _tile(snap, 16)
