@@ -1,4 +1,6 @@
-"""Small decisions and QoE evaluations for compute-sanitizer (memcheck / racecheck runs)."""
+"""Small decisions and QoE evaluations for compute-sanitizer (memcheck / racecheck runs): every
+decision flavour, debug checks, the sharded steps at world 1, the tracker update, the serving-loop
+simulator and the fused cooperative kernel (ANDES_FUSED=1 when set in the environment)."""
 import os
 import sys
 
@@ -18,8 +20,25 @@ for seed in range(6):
     for fl in (1, 1 | 16, 1 | 32, 1 | 64, 1 | 128):
         ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=2, flags=fl)
     ctx.qoe_eval(req, snap.n, snap.now_us, A.ANDES_EVAL_FINAL)
+    ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=2,
+                 flags=1 | A.ANDES_DEBUG_CHECKS)
+    # sharded entry point, world 1 (the exchange is a device copy)
+    sh = ctx.shard_init(1, 0, int(tau.numel()))
+    out = ctx.alloc_shard_decision(snap.n, int(tau.numel()))
+    A.schedule_sharded(ctx, sh, req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity,
+                       lambda a, b: b.copy_(a), out=out, preempt_cap=2)
+    # tracker update with room
+    sr = W.with_room(snap, 4)
+    rq2 = A.requests_to(sr)
+    d = ctx.schedule(rq2, sr.n, sr.now_us, sr.horizon_us, tau, sr.kv_capacity)
+    idx = torch.nonzero(d.serve_mask[:sr.n]).flatten().to(torch.int32)
+    ts = torch.full((idx.numel(),), sr.now_us + 1000, dtype=torch.int64, device="cuda")
+    ctx.tracker_append(rq2, sr.n, idx if idx.numel() else None, ts if idx.numel() else None, serve_mask=d.serve_mask)
 snap = W.long_requests(3, n=60, lo=5000, hi=9000)
 req = A.requests_to(snap)
 ctx.qoe_eval(req, snap.n, snap.now_us, A.ANDES_EVAL_INFLIGHT)
+tr = W.sim_trace(2, 1.5, window_s=8.0, rate_at_rho1=2.5, max_prompt=3000, max_out=30)
+sc = A.Context(max_requests=tr["n"], max_B=16, max_tokens=tr["tl_len"] + 64)
+sc.simulate(tr, torch.from_numpy(W.tau_table(16).view(np.int32)).cuda(), 12_000, flags=16)
 torch.cuda.synchronize()
 print("sanitize run ok")
