@@ -162,7 +162,8 @@ struct Globals2 {
   uint32_t theta, zcut, n_surv, overflow;         // k_decide: survivor cut published at barrier A
   uint32_t tile_ctr_b;                            // the decision scan's chunk counter after a scan at now
   uint32_t qnow_ctr;                              // Q_now chunks claimed by the decision scan's idle warps
-  uint32_t pad[22];
+  uint32_t rf_done;                               // refiner: k_refine_loss CTAs finished (last block)
+  uint32_t pad[21];
 };
 static_assert(sizeof(Globals2) == 128, "Globals2: one 128-byte line");
 

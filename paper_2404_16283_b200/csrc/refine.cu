@@ -7,8 +7,8 @@
 //   k_refine_loss   one warp per (still-running request i, pair k): the QoE drop of i under the
 //                   stall, llrint((Q_now,i - Q_i(now + D_k)) 2^32), summed per pair in int64
 //                   (deterministic); Q_i(t) is the in-flight QoE at t with no new token;
-//   k_refine_final  one CTA: the first pair whose admit's gain does not exceed its loss cancels
-//                   itself and every later pair; the outputs are rewritten.
+//   refine_final    the last CTA of k_refine_loss: the first pair whose admit's gain does not
+//                   exceed its loss cancels itself and every later pair; the outputs are rewritten.
 // The pairs' acceptance is a prefix (the refiner stops at the first rejection), so every pair's
 // loss can be evaluated in parallel assuming its predecessors were accepted.
 #include "block.cuh"
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_pairs(ReqView r, Work
     overhead_us(lv, false, prefill, swap, pre, res);
     s_LV[v + 1] = lv;
     s_PV[v + 1] = pre;
-    w.vmark[i] = v + 1u;  // 1 + victim position of request i (cleared by k_refine_final)
+    w.vmark[i] = v + 1u;  // 1 + victim position of request i (cleared by refine_final)
   }
   if (tid == 0) {
     s_LV[0] = 0ull;
@@ -186,34 +186,10 @@ __device__ void walk_two(const ReqView& r, uint32_t i, long long t1, long long t
   q2 = finish(m2, t2, s2, dm2);
 }
 
-__global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work w, int64_t now) {
-  __shared__ Globals s_g;
-  pdl_wait();
-  snap_globals(w.g, &s_g);
-  const uint32_t np = s_g.rf_npairs;
-  if (np == 0) return;
-  const uint32_t n_run = min(s_g.n_run, (uint32_t)kMaxRunning);
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t pr = gw; pr < n_run * np; pr += W) {
-    const uint32_t q = pr / np, k = pr - q * np;
-    const uint32_t i = __ldcg(w.run_list + q);
-    const uint32_t vm = __ldcg(w.vmark + i);
-    if (vm && vm - 1u < __ldcg(w.rf_vend + k)) continue;  // preempted by pairs <= k
-    const long long a = r.arrival[i];
-    double qn, qd;
-    walk_two(r, i, now - a, now + __ldcg(w.rf_D + k) - a, qn, qd);
-    if (lane == 0) {
-      const long long lf = gain_fixed(__dsub_rn(qn, qd));
-      if (lf) atomicAdd(reinterpret_cast<unsigned long long*>(w.rf_loss + k), (unsigned long long)lf);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kRefineThreads) k_refine_final(ReqView r, Work w, SchedOut o, const uint32_t* tau,
-                                                                 uint64_t M) {
+// The first pair whose admit's gain does not exceed its loss cancels itself and every later pair
+// (R27); the outputs are rewritten.  One CTA: the last CTA of k_refine_loss.
+__device__ void refine_final(const ReqView& r, const Work& w, const SchedOut& o, const uint32_t* tau, uint64_t M) {
   __shared__ uint32_t s_na;
-  pdl_wait();
   const uint32_t tid = threadIdx.x;
   const bool trig = __ldcg(&w.g->triggered) != 0;
   const uint32_t Bs = o.scalars[0];
@@ -241,6 +217,39 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_final(ReqView r, Work
   }
 }
 
+__global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work w, int64_t now, SchedOut o,
+                                                                const uint32_t* tau, uint64_t M) {
+  __shared__ Globals s_g;
+  pdl_wait();
+  snap_globals(w.g, &s_g);
+  const uint32_t np = s_g.rf_npairs;
+  const uint32_t n_run = min(s_g.n_run, (uint32_t)kMaxRunning);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t pr = gw; np && pr < n_run * np; pr += W) {
+    const uint32_t q = pr / np, k = pr - q * np;
+    const uint32_t i = __ldcg(w.run_list + q);
+    const uint32_t vm = __ldcg(w.vmark + i);
+    if (vm && vm - 1u < __ldcg(w.rf_vend + k)) continue;  // preempted by pairs <= k
+    const long long a = r.arrival[i];
+    double qn, qd;
+    walk_two(r, i, now - a, now + __ldcg(w.rf_D + k) - a, qn, qd);
+    if (lane == 0) {
+      const long long lf = gain_fixed(__dsub_rn(qn, qd));
+      if (lf) atomicAdd(reinterpret_cast<unsigned long long*>(w.rf_loss + k), (unsigned long long)lf);
+    }
+  }
+  // the last CTA to finish takes the acceptance decision (k_refine_final's work, last-block)
+  __shared__ uint32_t s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&globals2(w)->rf_done, 1u) == gridDim.x - 1 ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  refine_final(r, w, o, tau, M);
+}
+
 static size_t refine_pairs_smem() { return 2 * sizeof(unsigned long long) * (kMaxRunning + 1); }
 
 void init_refine_kernels() {
@@ -250,8 +259,7 @@ void init_refine_kernels() {
 void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const SchedOut& o, int64_t now,
                    const uint32_t* tau, uint64_t M, uint32_t prefill, uint32_t swap) {
   launch_pdl(k_refine_pairs, 1, kRefineThreads, refine_pairs_smem(), L.stream, r, w, o, M, prefill, swap);
-  launch_pdl(k_refine_loss, L.sm_count * 4, kRefineThreads, 0, L.stream, r, w, now);
-  launch_pdl(k_refine_final, 1, kRefineThreads, 0, L.stream, r, w, o, tau, M);
+  launch_pdl(k_refine_loss, L.sm_count * 4, kRefineThreads, 0, L.stream, r, w, now, o, tau, M);
 }
 
 }  // namespace andes
