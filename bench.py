@@ -388,20 +388,20 @@ def decision_trace(ctx, req, n, snap, tau, out, stream):
         x = tr[lo:hi].reshape(-1, 2)
         return x[x[:, 0] > 0]
     pr, sc, st, cp, sel = span(7000, 8024), span(5000, 7000), span(3000, 4024), span(8100, 9124), span(0, 512)
-    if not (len(pr) and len(sc) and len(st) and len(cp) and len(sel)):
+    if not (len(pr) and len(sc) and len(cp) and len(sel)):
         return None
     t0 = pr[:, 0].min()
     us = lambda v: round((int(v) - t0) / 1e3, 2)  # noqa: E731
     fin = [us(tr[k]) for k in (2100, 2105) if tr[k]]
-    stages = {"prep": [0.0, us(pr[:, 1].max())], "scan": [us(sc[:, 0].min()), us(sc[:, 1].max())],
-              "state": [us(st[:, 0].min()), us(st[:, 1].max())], "compact": [us(cp[:, 0].min()), us(cp[:, 1].max())],
-              "select": [us(sel[:, 0].min()), us(sel[:, 1].max())], "finalize": fin}
+    stages = {"prep": [0.0, us(pr[:, 1].max())], "scan": [us(sc[:, 0].min()), us(sc[:, 1].max())]}
+    if len(st):  # k_state (absent when the state is fused into the scan)
+        stages["state"] = [us(st[:, 0].min()), us(st[:, 1].max())]
+    stages.update({"compact": [us(cp[:, 0].min()), us(cp[:, 1].max())],
+                   "select": [us(sel[:, 0].min()), us(sel[:, 1].max())], "finalize": fin})
+    names = list(stages)[:-1]
+    gaps = {f"{a}->{b}": round(stages[b][0] - stages[a][1], 2) for a, b in zip(names, names[1:])}
     return {"source": "in-kernel %globaltimer stamps (CTA start/end), one config-3 decision, L2 warm",
-            "stages_us_from_prep_start": stages,
-            "gaps_us": {"prep->scan": round(stages["scan"][0] - stages["prep"][1], 2),
-                        "scan->state": round(stages["state"][0] - stages["scan"][1], 2),
-                        "state->compact": round(stages["compact"][0] - stages["state"][1], 2),
-                        "compact->select": round(stages["select"][0] - stages["compact"][1], 2)}}
+            "stages_us_from_prep_start": stages, "gaps_us": gaps}
 
 
 def serving_sim(args, lr, stream):

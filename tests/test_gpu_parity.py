@@ -566,3 +566,4 @@ def test_refiner_fig7_toy_on_gpu(A, ctx, orc):
     assert (g["admit"] + 1).tolist() == [10, 9, 8]
     for prefill, swap in ((50, 100), (50, 1000), (25, 400)):
         _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=prefill, swap=swap)
+
