@@ -567,3 +567,42 @@ def test_refiner_fig7_toy_on_gpu(A, ctx, orc):
     for prefill, swap in ((50, 100), (50, 1000), (25, 400)):
         _check_sched(A, ctx, orc, snap, flags=1 | 128, prefill=prefill, swap=swap)
 
+
+# ---------------------------------------------------------------- maximum sizes
+def _many_short(n, seed, run_frac, l_lo, l_hi, M):
+    """n requests with short, partly late timelines and small contexts (B_hi reaches B_cap)."""
+    rng = np.random.default_rng(seed)
+    tl = []
+    for i in range(n):
+        g = int(rng.integers(0, 12))
+        d = 1_000_000 + np.arange(g) * 200_000 + rng.integers(0, 900_000)
+        tl.append(np.maximum.accumulate(np.minimum(d, 4_900_000)).astype(np.uint32))
+    g, base, pool = W._pack(tl)
+    return W.Snapshot(arrival_us=np.zeros(n, np.int64), ttft_us=np.full(n, 1_000_000, np.uint32),
+                      period_us=rng.choice([208_333, 303_030], n).astype(np.uint32),
+                      ctx_len=rng.integers(l_lo, l_hi, n).astype(np.uint32), n_deliv=g,
+                      max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=rng.permutation(n).astype(np.uint32), running=(rng.random(n) < run_frac).astype(np.uint8),
+                      tl_base=base, tl_pool=pool, now_us=5_000_000, horizon_us=2_000_000, kv_capacity=M)
+
+
+def test_schedule_max_B_cap_1024(A, orc):
+    """B_cap at the library's maximum (1024 candidate batch sizes, 1024 k_select CTAs, Algorithm 1
+    prefixes up to 1024 long): every output equal to the oracle's, with and without the cap."""
+    import dataclasses
+    c = A.Context(max_requests=8192, max_B=1024, max_tokens=1 << 20)
+    snap = dataclasses.replace(_many_short(3000, 4, 0.1, 20, 200, 120_000), tau_us=W.tau_table(1024))
+    for cap, flags in ((W.UINT32_MAX, 1), (16, 1), (16, 1 | 16)):
+        g, o = _check_sched(A, c, orc, snap, flags=flags, cap=cap)
+        assert o.B_hi == 1024 and int(o.kstar.max()) > 512
+
+
+def test_schedule_large_running_sets(A, orc):
+    """Running sets past the per-B cap staging (n_run > 512: the general staging; > 2048: the
+    last CTA's general finalize) up to the 4096 maximum, against the oracle."""
+    c = A.Context(max_requests=8192, max_B=256, max_tokens=1 << 20)
+    for n, frac, cap in ((1500, 0.6, 16), (5000, 0.55, 40), (5000, 0.8, W.UINT32_MAX)):
+        snap = _many_short(n, n + int(frac * 100), frac, 1, 40, 200_000)
+        assert int(snap.running.sum()) <= 4096
+        g, o = _check_sched(A, c, orc, snap, cap=cap)
+        assert not int(g["sc"][6]) & A.ANDES_F_TRUNCATED
