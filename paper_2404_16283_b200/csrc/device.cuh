@@ -163,9 +163,18 @@ struct Globals2 {
   uint32_t tile_ctr_b;                            // the decision scan's chunk counter after a scan at now
   uint32_t qnow_ctr;                              // Q_now chunks claimed by the decision scan's idle warps
   uint32_t rf_done;                               // refiner: k_refine_loss CTAs finished (last block)
-  uint32_t pad[21];
+  uint32_t pad0;
+  unsigned long long best_vb;                     // S5: max over B of pack_vb(V(B), B) (select CTAs)
+  uint32_t pad[18];
 };
 static_assert(sizeof(Globals2) == 128, "Globals2: one 128-byte line");
+
+// S5 (ties to the larger B, reading R13) as one 64-bit atomicMax: V(B) (|V| < 2^43: a sum
+// of at most 1024 values llrint(gain 2^32) with |gain| <= 1) offset to be positive, then B in the
+// low 11 bits, so the larger packed value is the larger V, or on equal V the larger B; 0 = none.
+__host__ __device__ __forceinline__ unsigned long long pack_vb(long long V, uint32_t B) {
+  return ((unsigned long long)(V + (1ll << 43)) << 11) | (unsigned long long)B;
+}
 
 // Block snapshot of the Globals line: warp 0 loads it (one request per CTA) and the block reads
 // shared memory.  Every thread of a many-CTA grid loading the same global words instead queues

@@ -759,48 +759,14 @@ __device__ void stage_cap_fast(const SelectArgs& A, uint32_t B, uint32_t kstar, 
 
 // S5 + copy of B*'s staged cap result into the outputs (last CTA of k_select).
 __device__ bool finalize_fast(const SelectArgs& A) {
-  __shared__ long long s_bv[kSelThreads / 32];
-  __shared__ uint32_t s_bb[kSelThreads / 32];
   __shared__ uint32_t s_Bstar;
   const ReqView& r = A.r;
   const Work& w = A.w;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tid = threadIdx.x;
   const uint32_t B_lo = __ldcg(&w.g->B_lo), B_hi = __ldcg(&w.g->B_hi);
-  {
-    long long bv = (long long)0x8000000000000000ull;
-    uint32_t bb = 0;
-    for (uint32_t B = B_lo + tid; B <= B_hi; B += kSelThreads) {
-      const long long v = __ldcg(A.o.V + (B - 1));
-      if (bb == 0 || v > bv || (v == bv && B > bb)) {
-        bv = v;
-        bb = B;
-      }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const long long v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      const uint32_t b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-      if (b2 != 0 && (bb == 0 || v2 > bv || (v2 == bv && b2 > bb))) {
-        bv = v2;
-        bb = b2;
-      }
-    }
-    if (lane == 0) {
-      s_bv[wid] = bv;
-      s_bb[wid] = bb;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      bv = s_bv[0];
-      bb = s_bb[0];
-      for (uint32_t q = 1; q < kSelThreads / 32; ++q)
-        if (s_bb[q] != 0 && (bb == 0 || s_bv[q] > bv || (s_bv[q] == bv && s_bb[q] > bb))) {
-          bv = s_bv[q];
-          bb = s_bb[q];
-        }
-      s_Bstar = bb;
-    }
-    __syncthreads();
-  }
+  // B* from the select CTAs' packed atomicMax (no reduction over V here)
+  if (tid == 0) s_Bstar = (uint32_t)(__ldcg(&globals2(w)->best_vb) & 2047ull);
+  __syncthreads();
   const uint32_t Bs = s_Bstar;
   if (Bs == 0) return false;  // no candidate B: general path
   const uint4 sc4 = __ldcg(w.stage_sc + (Bs - 1));
@@ -1079,6 +1045,7 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
     const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
     if (tid == 0) {
       A.o.V[B - 1] = v;
+      if (!A.xsend) atomicMax(&globals2(w)->best_vb, pack_vb(v, B));
       A.o.kstar[B - 1] = kstar;
       w.sel_thr[B - 1] = thr;
     }
