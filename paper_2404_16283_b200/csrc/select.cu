@@ -811,6 +811,7 @@ __shared__ uint32_t s_sel_k, s_sel_last;
 __shared__ long long s_sel_red[32];
 __shared__ uint8_t s_sel_run8[kSortCap];  // running flag of the ordered survivors (pruned path)
 __shared__ uint32_t s_sel_lsel[kSortCap];  // l of the ordered candidates (the walk's loads)
+__shared__ long long s_sel_vsum;           // V(B) accumulator
 
 // S4 for one candidate B (CTA-wide): the top min(B, n) requests by (key desc, rank asc), then
 // Algorithm 1: take while the running sum of l stays <= M (count <= B by
@@ -828,6 +829,7 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
   long long* const s_red = s_sel_red;
   uint8_t* const s_run8 = s_sel_run8;
   uint32_t* const s_lsel = s_sel_lsel;
+  long long& s_vsum = s_sel_vsum;
   const ReqView& r = A.r;
   const Work& w = A.w;
   const uint32_t tid = threadIdx.x;
@@ -942,6 +944,7 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
       const uint32_t np = (ns + 1) >> 1;
       for (uint32_t e = tid; e < ns; e += kSelThreads) {
         const unsigned long long c = s_all[e];
+        const uint32_t le = __ldcg(&w.cand_st[e].l);  // its l for the walk (latency under the count)
         uint32_t pos = 0;
 #pragma unroll 8
         for (uint32_t f = 0; f < np; ++f) {
@@ -953,6 +956,7 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
           s_idx[pos] = s_ri[e] & 0x7FFFFFFFu;
           s_run8[pos] = (uint8_t)(s_ri[e] >> 31);
           s_gf[pos] = s_gall[e];
+          s_lsel[pos] = le;
         }
       }
       if (rpre) {
@@ -1010,10 +1014,18 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
     uint32_t kstar;
     {
       const uint32_t lane = tid & 31, wid = tid >> 5, q0 = 2 * tid;
-      const unsigned long long l0 = q0 < cnt ? r.ctx_len[s_idx[q0]] : 0ull;
-      const unsigned long long l1 = q0 + 1 < cnt ? r.ctx_len[s_idx[q0 + 1]] : 0ull;
-      if (q0 < cnt) s_lsel[q0] = (uint32_t)l0;
-      if (q0 + 1 < cnt) s_lsel[q0 + 1] = (uint32_t)l1;
+      // l of the ordered candidates: placed by the pruned path's rank count, else loaded here
+      unsigned long long l0 = 0, l1 = 0;
+      if (ovf) {
+        l0 = q0 < cnt ? r.ctx_len[s_idx[q0]] : 0ull;
+        l1 = q0 + 1 < cnt ? r.ctx_len[s_idx[q0 + 1]] : 0ull;
+        if (q0 < cnt) s_lsel[q0] = (uint32_t)l0;
+        if (q0 + 1 < cnt) s_lsel[q0 + 1] = (uint32_t)l1;
+      } else {
+        l0 = q0 < cnt ? s_lsel[q0] : 0u;
+        l1 = q0 + 1 < cnt ? s_lsel[q0 + 1] : 0u;
+      }
+      if (tid == 0) s_vsum = 0;
       unsigned long long inc = l0 + l1;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1040,7 +1052,11 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
       s_ps[q] = (ovf ? r.running[i] != 0 : s_run8[q] != 0) ? 0ull : 1ull;
     }
     if (B == 256) ANDES_TRACE(w, 2407);
-    v = block_sum_ll<kSelThreads>(v, s_red);
+    // V(B): warp sums, one shared 64-bit atomic per warp, one barrier
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&s_vsum), (unsigned long long)v);
+    __syncthreads();
+    v = s_vsum;
     if (B == 256) ANDES_TRACE(w, 2408);
     const unsigned long long thr = kstar ? s_key[kstar - 1] : ~0ull;  // k*-th composite
     if (tid == 0) {
