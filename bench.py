@@ -746,7 +746,29 @@ def run_ours(args):
                              "unit": "GB/s", "frac": q_ach / hbm_peak,
                              "traffic": _ncu_traffic().get("k_qoe_scan_2p20"),
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
-    del qctx, breq
+    # the same population with unaligned timelines (packed back to back, align 1): the scan's
+    # row-per-lane event path (128B-swizzled tiles) instead of the aligned piece-parallel path
+    import workloads as W
+    ubig = _tile(W.config3().subset(np.arange(snap.n), align=1), 16)
+    ureq = A.requests_to(ubig, device=dev)
+    u_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(max(args.warmup, 3) + 10):
+            flush.zero_()
+            qctx.qoe_eval(ureq, ubig.n, ubig.now_us + ubig.horizon_us, A.ANDES_EVAL_INFLIGHT, stream=stream)
+            st = qctx.profile_read()
+            if k >= max(args.warmup, 3):
+                u_ms.append(st)
+    u_scan = statistics.median([s_[1] for s_ in u_ms])
+    ubytes = 4 * ubig.n_tokens + 44 * ubig.n
+    qoe_eval["unaligned_pool"] = {
+        "path": "row-per-lane event path (timelines packed back to back, 128B-swizzled TMA tiles)",
+        "pool_tokens": ubig.n_tokens, "scan_ms": u_scan,
+        "ms_per_eval": statistics.median([s_[0] + s_[1] + s_[2] for s_ in u_ms]),
+        "roofline": {"kernel": "k_qoe_scan (row path)", "bound": "hbm", "achieved": ubytes / (u_scan / 1e3) / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": ubytes / (u_scan / 1e3) / 1e9 / hbm_peak,
+                     "algorithmic_bytes_per_launch": ubytes}}
+    del qctx, breq, ureq
 
     # ---- the same decision under the LQSF priority, the Appendix-A objectives (NEXT-2) and with
     # the overhead-aware refiner (NEXT-1; prefill 5000 tok/s, no swapping)

@@ -314,7 +314,10 @@ __device__ __forceinline__ unsigned long long composite(uint32_t okey, uint32_t 
 // capped by max_total (reading R7).
 __device__ __forceinline__ uint32_t due_count(int64_t t, uint32_t ttft, uint32_t P, uint32_t max_total) {
   if (t < (int64_t)ttft) return 0;
-  unsigned long long q = (unsigned long long)(t - (int64_t)ttft) / P + 1ull;
+  const unsigned long long d = (unsigned long long)(t - (int64_t)ttft);
+  // 32-bit division when the span fits (always, for times below 2^32 us): the 64-bit one is a
+  // called subroutine
+  unsigned long long q = ((d >> 32) == 0ull ? (unsigned long long)((uint32_t)d / P) : d / P) + 1ull;
   if (q > max_total) q = max_total;
   return (uint32_t)q;
 }
