@@ -132,8 +132,12 @@ def _dist():
         import torch
         import torch.distributed as dist
         lr = int(os.environ.get("LOCAL_RANK", "0"))
+        # test hooks for the N > 1 code path on a one-GPU box: every rank on cuda:0, gloo instead
+        # of NCCL (NCCL refuses two ranks on one GPU); the driver's runs use neither
+        if os.environ.get("ANDES_BENCH_ONE_GPU") == "1":
+            lr = 0
         torch.cuda.set_device(lr)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("ANDES_DIST_BACKEND", "nccl"))
         return dist, dist.get_rank(), ws, lr
     return None, 0, 1, 0
 

@@ -765,7 +765,7 @@ __constant__ SubRangeTab kSubRange2 = make_subrange_tab(2 * kWTile);  // two-til
 static_assert(make_subrange_tab(2 * kWTile).sr[31] <= 4 * kWTile, "SR table (2 tiles)");
 static_assert(make_subrange_tab().sr[31] <= 2 * kWTile && make_subrange_tab().sr[0] == 4u * 9u, "SR table");
 
-template <bool kFinal, int TW = 1>
+template <bool kFinal, int TW = 1, bool kHead = false>
 __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry& e, uint32_t tile_s, uint32_t t,
                                                   uint32_t mode, uint32_t cdirect, unsigned long long& prefix,
                                                   bool first_batch, bool last_batch, bool pub) {
@@ -810,13 +810,28 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   const int32_t xe = active ? min(xs + (int32_t)SR, q_pe) : 0;
   const uint32_t P = active ? qP : 0u;
   const uint32_t tcl = kFinal ? 0xFFFFFFFFu : qtrel;
+  // kHead (unaligned timelines: a piece may start inside a 4-token group): the sub-range's first
+  // hn <= 3 tokens, up to the next 16-byte boundary, form a head group processed first
+  uint32_t hn = 0, h0 = 0, h1 = 0, h2 = 0;
+  int32_t xa = xs;
+  if constexpr (kHead) {
+    const uint32_t mis = (uint32_t)xs & 3u;
+    hn = (active && mis) ? min(4u - mis, (uint32_t)(xe - xs)) : 0u;
+    if (hn) {
+      const uint4 v = ld_shared_v4(tile_s + (((uint32_t)xs >> 2) << 4));
+      h0 = mis == 1u ? v.y : mis == 2u ? v.z : v.w;
+      h1 = mis == 1u ? v.z : v.w;
+      h2 = v.w;
+    }
+    xa = xs + (int32_t)hn;
+  }
   // full 4-token groups of the sub-range, then at most one partial group (the valid end)
-  const uint32_t nfull = active ? (uint32_t)(xe - xs) >> 2 : 0u;
-  const uint32_t ntail = active ? (uint32_t)(xe - xs) & 3u : 0u;
+  const uint32_t nfull = active ? (uint32_t)(xe - xa) >> 2 : 0u;
+  const uint32_t ntail = active ? (uint32_t)(xe - xa) & 3u : 0u;
   const uint32_t gmax = __reduce_max_sync(0xffffffffu, nfull);
   const uint32_t Is = qA + (uint32_t)xs * P;  // ideal time of the sub-range's first token
   // the tile is in plain row-major layout here (no swizzle): chunk c at tile_s + 16 c
-  const uint32_t a0 = tile_s + (((uint32_t)xs >> 2) << 4);
+  const uint32_t a0 = tile_s + (((uint32_t)xa >> 2) << 4);
   // the tail group's tokens (loaded once, used by both passes); missing tokens read as 0
   uint32_t t0 = 0, t1 = 0, t2 = 0;
   if (ntail) {
@@ -829,6 +844,11 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   // (gi < nmin, warp-uniform) run unpredicated; the few that only some lanes have, predicated.
   const uint32_t nmin = min(gmax, __reduce_min_sync(0xffffffffu, active ? nfull : 0xFFFFFFFFu));
   uint32_t a = Is - P;
+  if (kHead && hn) {
+    a = max(a + P, h0);
+    if (hn > 1u) a = max(a + P, h1);
+    if (hn > 2u) a = max(a + P, h2);
+  }
 #pragma unroll kTokUnroll
   for (uint32_t gi = 0; gi < nmin; ++gi) {
     const uint4 v = ld_shared_v4(a0 + (gi << 4));
@@ -851,7 +871,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
     a = max(a + P, t1);
     a = max(a + P, t2);
   }
-  const uint32_t nslots = 4u * nfull + (ntail ? 3u : 0u);  // processed token slots
+  const uint32_t nslots = hn + 4u * nfull + (ntail ? 3u : 0u);  // processed token slots
   const uint32_t dz = nslots ? a - (Is + (nslots - 1u) * P) : 0u;
   // a request starts in this sub-range; idle lanes (after every sub-range) are the identity
   const bool flag = active && k == 0 && qls >= 0;
@@ -900,6 +920,20 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
 #endif
   unsigned long long sumT = 0ull;
   uint32_t sum32 = 0u;
+  if (kHead && hn) {  // the head group (clamped: min(A, t) = A whenever the clamp is void)
+    Ac = max(Ac + P, h0);
+    unsigned long long hs = min(Ac, tcl);
+    if (hn > 1u) {
+      Ac = max(Ac + P, h1);
+      hs += min(Ac, tcl);
+    }
+    if (hn > 2u) {
+      Ac = max(Ac + P, h2);
+      hs += min(Ac, tcl);
+    }
+    sumT = hs;
+    sum32 = (uint32_t)hs;
+  }
   if (fits32) {
     if (noclamp) {
 #pragma unroll kTokUnroll
@@ -1021,7 +1055,16 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   const unsigned long long full_rows_end = (r.tl_len / 32ull) * 32ull;  // tokens covered by the TMA view
   // 16-byte aligned timelines (every request): plain tiles and the piece-parallel path; else
   // 128B-swizzled tiles and the row-per-lane event path
-  const uint32_t swz_on = w.g->unal ? 1u : 0u;  // (L1: one L2 request per SM, not per warp)
+  // Unaligned timelines (a request starting inside a 16-byte group): plain tiles and the
+  // piece-parallel path with head groups (round 2; before, 128B-swizzled tiles and the row-per-lane
+  // event path at about a third of the speed, kept under ANDES_UNAL_ROWPATH).  The row path then
+  // serves only the tiles that look back, on plain tiles.
+  const uint32_t unal = w.g->unal;  // (L1: one L2 request per SM, not per warp)
+#ifdef ANDES_UNAL_ROWPATH
+  const uint32_t swz_on = unal ? 1u : 0u;
+#else
+  const uint32_t swz_on = 0u;
+#endif
   const CUtensorMap* pmap = swz_on ? &tmap_swz : &tmap_plain;
   const uint32_t wbase = smem_u32(s_base) + wid * kWarpSmem;  // [2][kWTile*4] tiles (shared address)
   uint64_t* bar = s_bar[wid];
@@ -1216,7 +1259,8 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
         // the status words are read only by look-backs, i.e. from inside a request longer than
         // kCarryDirect: publish when the request crossing the tile's end (the last one) is such
         const bool pub = __shfl_sync(0xffffffffu, rb.lim, nb_req - 1u) > (uint32_t)kCarryDirect;
-        warp_tile_aligned<kFinal, TW>(A, e, tile, tcur * TW, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
+        if (unal) warp_tile_aligned<kFinal, TW, true>(A, e, tile, tcur * TW, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
+        else warp_tile_aligned<kFinal, TW, false>(A, e, tile, tcur * TW, mb, cb, pref, b == 0, b + 1 == nbatch, pub);
         mb = 1u;
         cb = (uint32_t)pref;
       }

@@ -126,6 +126,22 @@ def test_qoe_config3_full(A, ctx, orc):
     _check_qoe(A, ctx, orc, snap, snap.now_us, True)
 
 
+def test_qoe_config3_unaligned(A, ctx, orc):
+    """Config 3 with its timelines packed back to back (a tracker that does not pad): every
+    request starts at an arbitrary token, so the scan's piece-parallel path runs with head groups
+    (and the row path on the tiles that look back)."""
+    snap = W.config3().subset(np.arange(65536), align=1)
+    assert np.any(snap.tl_base.astype(np.int64) % 4 != 0)
+    _check_qoe(A, ctx, orc, snap, snap.now_us + snap.horizon_us, False)
+    _check_qoe(A, ctx, orc, snap, snap.now_us, True)
+
+
+def test_schedule_config2_unaligned(A, ctx, orc):
+    snap = W.config2().subset(np.arange(W.config2().n), align=1)
+    _check_sched(A, ctx, orc, snap)
+    _check_sched(A, ctx, orc, snap, cap=16)
+
+
 # ---------------------------------------------------------------- S3 gains
 def _check_gains(A, ctx, orc, snap, B_list, sub=None):
     gain, key, qw = ctx.gain_estimate(_dev(A, snap), snap.n, snap.now_us, snap.horizon_us, _tau(snap), B_list)
