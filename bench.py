@@ -456,13 +456,16 @@ def serving_sim(args, lr, stream):
 
 
 def e2e_incremental(args, dist, snap, ws, lr, stream):
-    """The serving loop through the public API with a device-resident Request Tracker: every step
-    (a) copies the previous iteration's delivered tokens (request index, delivery time) from
-    pinned host memory to the device and appends them in place (andes_tracker_append; the
-    decision's serve mask becomes the running set), (b) runs the full config-3 decision
-    (andes_schedule), (c) reads the decision back to pinned host memory (scalars, V, admit and
-    preempt lists); the host keeps the served set from those lists and the clock advances by
-    tau(B*).  Wall time per step, host synchronised; the population evolves as in serving."""
+    """The serving loop through the public API with a device-resident Request Tracker.  One
+    serving iteration -- (a) the copy of the decision time and of the previous iteration's
+    delivered tokens (request index, delivery time) from pinned host memory, (b) their in-place
+    append (andes_tracker_append_dev: count read on the device; the decision's serve mask becomes
+    the running set), (c) the full config-3 decision (andes_schedule with now_dev: time read on the
+    device), (d) the read-back of the decision to pinned host memory (scalars, V, admit and
+    preempt lists) -- is captured ONCE into a CUDA graph; every step the host writes the new time
+    and deltas into the pinned staging buffers, replays the graph, synchronises and updates the
+    served set from the admit / preempt lists.  Wall time per step; the population evolves as in
+    serving (the clock advances by tau(B*) per step)."""
     import numpy as np
     import torch
 
@@ -477,60 +480,68 @@ def e2e_incremental(args, dist, snap, ws, lr, stream):
     req = A.requests_to(sn, device=dev)
     tau = torch.from_numpy(sn.tau_us.view(np.int32)).to(dev)
     out = ctx.alloc_decision(n, 256)
-    hsc = torch.empty(8, dtype=torch.int32).pin_memory()
-    hV = torch.empty(256, dtype=torch.int64).pin_memory()
-    hadm = torch.empty(256, dtype=torch.int32).pin_memory()
+    maxc = min(n, 1024)  # deltas per iteration: one token per served request (the batch, <= 1024)
     pmax = min(n, 4096)  # preempt list bound: the running set (<= 4096)
-    hpre = torch.empty(n, dtype=torch.int32).pin_memory()
-    hidx = torch.empty(n, dtype=torch.int32).pin_memory()
-    hts = torch.empty(n, dtype=torch.int64).pin_memory()
-    didx = torch.empty(n, dtype=torch.int32, device=dev)
-    dts = torch.empty(n, dtype=torch.int64, device=dev)
-    running = sn.running.astype(bool).copy()
+    # zero-copy in both directions (pinned host memory is device-mapped under UVA): the decision's
+    # last kernel writes its head (scalars, V, admit, the first pmax preempt slots) and the next
+    # batch as an index list into a pinned export block; the engine (here: the host loop) runs that
+    # batch and reports one delivery time per served request into pinned memory; the next
+    # iteration's tracker update reads the batch list, its count (the realized scalar) and the times
+    # from there, and the decision its time -- no copy nodes in the iteration's graph
+    hnow = torch.zeros(1, dtype=torch.int64).pin_memory()
+    hts = torch.zeros(maxc, dtype=torch.int64).pin_memory()
+    ebytes = A.decision_export_bytes(256, pmax, maxc)
+    hexp = torch.zeros(ebytes, dtype=torch.uint8).pin_memory()
+    np_sc, _, np_adm, np_pre, np_srv = A.decision_export_views(hexp, 256, pmax, maxc)
+    srv_t = hexp[ebytes - 4 * maxc:].view(torch.int32)  # the exported batch (tracker idx)
+    cnt_t = hexp[4:8].view(torch.int32)  # scalars[ANDES_SC_REALIZED] (tracker count)
+    np_now, np_ts = hnow.numpy(), hts.numpy()
+    h2d = d2h = 0  # bytes the kernels read / write over PCIe per step (the used slots)
+    kw = dict(preempt_cap=sn.preempt_cap, flags=A.ANDES_FORCE, stream=stream, export_host=hexp, export_preempt=pmax,
+              export_served=maxc)
+
+    def iteration():
+        ctx.tracker_append_dev(req, n, srv_t, hts, cnt_t, serve_mask=out.serve_mask, stream=stream)
+        ctx.schedule(req, n, sn.now_us, sn.horizon_us, tau, sn.kv_capacity, out=out, now_dev=hnow, **kw)
+
     now = sn.now_us
-    h2d = d2h = 0
-    times = []
-    cnt = 0
     with torch.cuda.stream(stream):
+        # iteration 0 (eager): the first decision on the snapshot as it is; no deliveries yet
+        ctx.schedule(req, n, now, sn.horizon_us, tau, sn.kv_capacity, out=out, **kw)
+        stream.synchronize()
+        graph = None
+        times = []
         for k in range(steps + 3):
             t0 = time.perf_counter()
-            if cnt:
-                didx[:cnt].copy_(hidx[:cnt], non_blocking=True)
-                dts[:cnt].copy_(hts[:cnt], non_blocking=True)
-            ctx.tracker_append(req, n, didx[:cnt] if cnt else None, dts[:cnt] if cnt else None,
-                               serve_mask=out.serve_mask if k else None, stream=stream)
-            ctx.schedule(req, n, now, sn.horizon_us, tau, sn.kv_capacity, out=out, stream=stream,
-                         preempt_cap=sn.preempt_cap, flags=A.ANDES_FORCE)
-            # one read-back of fixed size (scalars, V, the admit list, the first P_max preempt slots)
-            hsc.copy_(out.scalars, non_blocking=True)
-            hV.copy_(out.V, non_blocking=True)
-            hadm.copy_(out.admit, non_blocking=True)
-            hpre[:pmax].copy_(out.preempt[:pmax], non_blocking=True)
+            # the engine runs the exported batch: one token per request at now + tau(B*)
+            cnt = int(np_sc[1])
+            now += int(sn.tau_us[max(int(np_sc[0]), 1) - 1])
+            assert cnt <= maxc and int(np_sc[3]) <= pmax
+            np_now[0] = now
+            np_ts[:cnt] = now
+            if graph is None:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=stream):
+                    iteration()
+            graph.replay()
             stream.synchronize()
-            sc = hsc.numpy().view(np.uint32)
-            na, npre = int(sc[2]), int(sc[3])
-            assert npre <= pmax
-            running[hpre[:npre].numpy()] = False
-            running[hadm[:na].numpy()] = True
-            served = np.nonzero(running)[0]
-            Bs = max(int(sc[0]), 1)
-            now += int(sn.tau_us[Bs - 1])
-            cnt = served.size
-            hidx[:cnt] = torch.from_numpy(served.astype(np.int32))
-            hts[:cnt] = now
             dt = time.perf_counter() - t0
             if k >= 3:
                 times.append(dt)
-                h2d += 12 * cnt
-                d2h += 32 + 8 * 256 + 4 * 256 + 4 * pmax
+                h2d += 8 + 4 + 12 * cnt  # time, count, batch list and delivery times read by the kernels
+                d2h += 32 + 8 * 256 + 4 * (int(np_sc[2]) + min(int(np_sc[3]), pmax) + int(np_sc[1]))
     tot = _max_over_ranks(dist, sum(times))
-    del ctx, req
+    del graph, ctx, req
     return {"value": ws * len(times) / tot, "unit": UNIT, "h2d_bytes_per_step": int(h2d // len(times)),
             "d2h_bytes_per_step": int(d2h // len(times)),
-            "api": ("andes_tracker_append (the previous iteration's delivered tokens, 12 B each, H2D) + "
-                    "andes_schedule + decision read-back (scalars, V, admit/preempt lists, D2H); wall time per "
-                    "step, host synchronised; the config-3 population evolves over the steps"),
-            "steps": len(times), "ms_per_step": 1e3 * tot / len(times)}
+            "api": ("one CUDA graph per serving iteration, captured once and replayed: andes_tracker_append_dev "
+                    "reading the previous iteration's deliveries (the exported batch list and its count, the "
+                    "delivery times the host wrote) from pinned host memory, andes_schedule reading the decision "
+                    "time from pinned memory (now_dev) and writing its head (scalars, V, admit list, preempt "
+                    "list, the next batch) zero-copy into pinned memory (export_host); host: delivery times, "
+                    "replay, synchronise; wall time per step; the config-3 population evolves over the steps"),
+            "steps": len(times), "ms_per_step": 1e3 * tot / len(times),
+            "step_ms_min_median_max": [1e3 * min(times), 1e3 * sorted(times)[len(times) // 2], 1e3 * max(times)]}
 
 
 def cpu_baseline(snap):

@@ -134,6 +134,12 @@ typedef struct {
                                 ANDES_OBJ_MAXMIN | ANDES_OBJ_PERFECT | ANDES_REFINE            */
     uint32_t prefill_tok_s;  /* refiner: prefill / recomputation throughput (tokens/s; 0 = free) */
     uint32_t swap_tok_s;     /* refiner: swap bandwidth (tokens/s; 0 = no swapping)             */
+    const int64_t *now_dev;  /* i64[1] in DEVICE or mapped pinned HOST memory, optional (NULL:
+                                now_us).  When set, the decision time is read (once, by the call's
+                                first kernel) when the call runs, so one captured CUDA graph of a
+                                serving iteration can be replayed at a new time every iteration
+                                (write the time, replay).  andes_schedule only; ignored by
+                                andes_schedule_host and the sharded decision.                    */
 } AndesSchedParams;
 
 /* scalars[] layout of AndesDecision */
@@ -163,6 +169,18 @@ typedef struct {
     int64_t *V;            /* [B_cap] V(B) = sum of llrint(gain*2^32) over S_B; INT64_MIN if B
                               was not a candidate (reading R9)                                   */
     uint32_t *kstar;       /* [B_cap] Algorithm 1 prefix length per B; 0 if not a candidate    */
+    /* Optional zero-copy export (andes_schedule): MAPPED pinned HOST memory (cudaHostAlloc; with
+     * UVA every pinned allocation is mapped) that the call's last kernel fills with the decision's
+     * head, so a serving loop reads it after a stream sync without a copy: scalars (32 B) at 0,
+     * V (8 B_cap) at 32, admit_idx (4 B_cap) at 32 + 8 B_cap, the first min(n_preempt,
+     * export_preempt) preempt_idx entries at 32 + 12 B_cap, then at 32 + 12 B_cap +
+     * 4 export_preempt the next batch as an index list -- the requests served after the decision,
+     * scalars[ANDES_SC_REALIZED] of them (kept running ones, then admits), at most export_served
+     * -- which the engine runs and which can feed the next andes_tracker_append_dev directly
+     * (idx = that list, count = the realized scalar).  NULL: no export. */
+    void *export_host;
+    uint32_t export_preempt;
+    uint32_t export_served;
 } AndesDecision;
 
 /* QoE outputs of andes_qoe_eval (DEVICE memory; any pointer may be NULL). */
@@ -250,6 +268,16 @@ typedef struct {
  * Errors: ANDES_E_INVAL (NULL arrays). */
 int andes_tracker_append(AndesCtx *ctx, const AndesTracker *t, const uint32_t *idx, const int64_t *t_abs,
                          uint32_t count, const uint8_t *serve_mask, void *stream);
+
+/* The same update with the token count read on the device (*count_dev, DEVICE u32, at most
+ * max_count; idx / t_abs hold max_count slots), so that a serving iteration -- the copy of its
+ * deltas into idx / t_abs / count_dev, this update and andes_schedule -- can be captured once
+ * into a CUDA graph and replayed with new deltas every iteration.  A count above max_count
+ * appends none of the tokens and the next call returns ANDES_E_CAPACITY.
+ * Errors: ANDES_E_INVAL (NULL arrays). */
+int andes_tracker_append_dev(AndesCtx *ctx, const AndesTracker *t, const uint32_t *idx, const int64_t *t_abs,
+                             const uint32_t *count_dev, uint32_t max_count, const uint8_t *serve_mask,
+                             void *stream);
 
 /* ---- Serving-loop simulator --------------------------------------
  * A trace is served iteration by iteration with andes_schedule in the loop, on the device:

@@ -52,7 +52,8 @@ SC_NAMES = ["B_star", "realized", "n_admit", "n_preempt", "B_lo", "B_hi", "flags
 EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval", "andes_gain_estimate",
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
            "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean", "andes_knapsack_dp",
-           "andes_knapsack_dp_workspace", "andes_tracker_append", "andes_simulate", "andes_sim_workspace"]
+           "andes_knapsack_dp_workspace", "andes_tracker_append", "andes_tracker_append_dev", "andes_simulate",
+           "andes_sim_workspace"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -83,12 +84,13 @@ class SchedParams(C.Structure):
     _fields_ = [("now_us", C.c_int64), ("horizon_us", C.c_uint32), ("B_cap", C.c_uint32),
                 ("tau_us", C.c_void_p), ("kv_capacity", C.c_uint64), ("preempt_cap", C.c_uint32),
                 ("cur_latency_us", C.c_uint32), ("flags", C.c_uint32), ("prefill_tok_s", C.c_uint32),
-                ("swap_tok_s", C.c_uint32)]
+                ("swap_tok_s", C.c_uint32), ("now_dev", C.c_void_p)]
 
 
 class DecisionPtrs(C.Structure):
     _fields_ = [("serve_mask", C.c_void_p), ("admit_idx", C.c_void_p), ("preempt_idx", C.c_void_p),
-                ("scalars", C.c_void_p), ("V", C.c_void_p), ("kstar", C.c_void_p)]
+                ("scalars", C.c_void_p), ("V", C.c_void_p), ("kstar", C.c_void_p),
+                ("export_host", C.c_void_p), ("export_preempt", C.c_uint32), ("export_served", C.c_uint32)]
 
 
 class Shard(C.Structure):
@@ -158,6 +160,8 @@ def lib() -> C.CDLL:
                                         C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.andes_tracker_append.argtypes = [C.c_void_p, C.POINTER(Tracker), C.c_void_p, C.c_void_p, C.c_uint32,
                                            C.c_void_p, C.c_void_p]
+        L.andes_tracker_append_dev.argtypes = [C.c_void_p, C.POINTER(Tracker), C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_uint32, C.c_void_p, C.c_void_p]
         L.andes_sim_workspace.argtypes = [C.c_uint32]
         L.andes_sim_workspace.restype = C.c_uint64
         L.andes_simulate.argtypes = [C.c_void_p, C.POINTER(Sim), C.POINTER(SimParams), C.POINTER(SimStats), C.c_void_p]
@@ -232,6 +236,22 @@ class Decision:
 
     def scalar(self, name):
         return int(self.scalars[SC_NAMES.index(name)])
+
+
+def decision_export_bytes(B_cap, export_preempt, export_served=0):
+    """Size of an AndesDecision.export_host buffer (include/andes.h)."""
+    return 32 + 12 * int(B_cap) + 4 * int(export_preempt) + 4 * int(export_served)
+
+
+def decision_export_views(buf, B_cap, export_preempt, export_served=0):
+    """numpy views (scalars u32[8], V i64[B_cap], admit i32[B_cap], preempt i32[export_preempt],
+    served i32[export_served]) of a pinned export buffer (torch uint8 tensor)."""
+    import numpy as np
+    a = buf.numpy()
+    o = 32 + 12 * B_cap + 4 * export_preempt
+    return (a[0:32].view(np.uint32), a[32:32 + 8 * B_cap].view(np.int64),
+            a[32 + 8 * B_cap:32 + 12 * B_cap].view(np.int32), a[32 + 12 * B_cap:o].view(np.int32),
+            a[o:o + 4 * export_served].view(np.int32))
 
 
 class Context:
@@ -329,8 +349,27 @@ class Context:
         return gain, key, qw
 
     # -- andes_schedule
-    def alloc_decision(self, n, B_cap, pin=False):
+    def alloc_decision(self, n, B_cap, pin=False, packed=False):
+        """packed: every output a view of ONE device buffer (.packed, uint8), laid out as scalars,
+        V, admit, kstar, preempt, serve_mask, so that the decision's head (up to the first pmax
+        preempt slots: packed_head(pmax) bytes) leaves the device in one copy."""
         torch = _torch()
+        if packed:
+            n1 = max(n, 1)
+            sizes = [32, 8 * B_cap, 4 * B_cap, 4 * B_cap, 4 * n1, n1]
+            offs = [0]
+            for z in sizes[:-1]:
+                offs.append(offs[-1] + (z + 15) // 16 * 16)
+            buf = torch.zeros(offs[-1] + sizes[-1], dtype=torch.uint8, device=self.device)
+
+            def view(k, dt, cnt):
+                return buf[offs[k]:offs[k] + sizes[k]].view(dt)[:cnt]
+            d = Decision(scalars=view(0, torch.int32, 8), V=view(1, torch.int64, B_cap),
+                         admit=view(2, torch.int32, B_cap), kstar=view(3, torch.int32, B_cap),
+                         preempt=view(4, torch.int32, n1), serve_mask=view(5, torch.uint8, n1))
+            d.packed = buf
+            d.packed_offsets = offs
+            return d
         kw = dict(pin_memory=True) if pin else dict(device=self.device)
         return Decision(serve_mask=torch.empty(max(n, 1), dtype=torch.uint8, **kw),
                         admit=torch.empty(B_cap, dtype=torch.int32, **kw),
@@ -341,13 +380,20 @@ class Context:
 
     def schedule(self, req: dict, n: int, now_us: int, horizon_us: int, tau, kv_capacity: int,
                  preempt_cap=UINT32_MAX, cur_latency_us=0, flags=ANDES_FORCE, out: Decision | None = None,
-                 stream=None, prefill_tok_s=5000, swap_tok_s=0) -> Decision:
+                 stream=None, prefill_tok_s=5000, swap_tok_s=0, now_dev=None, export_host=None,
+                 export_preempt=0, export_served=0) -> Decision:
+        """now_dev: optional int64 [1] in device or pinned host memory; when given the decision time
+        is read from it when the call runs (now_us is only the reference the kernels' time arguments
+        are shifted from), so a captured graph of the call can be replayed at new times.
+        export_host: optional pinned host uint8 tensor (decision_export_bytes(B_cap, export_preempt,
+        export_served) bytes) that the call fills zero-copy with scalars, V, admit, the first
+        export_preempt preempt entries and the next batch (decision_export_views splits it)."""
         B_cap = int(tau.numel())
         out = out or self.alloc_decision(n, B_cap)
         p = SchedParams(int(now_us), int(horizon_us), B_cap, _ptr(tau), int(kv_capacity), int(preempt_cap),
-                        int(cur_latency_us), int(flags), int(prefill_tok_s), int(swap_tok_s))
+                        int(cur_latency_us), int(flags), int(prefill_tok_s), int(swap_tok_s), _ptr(now_dev))
         d = DecisionPtrs(_ptr(out.serve_mask), _ptr(out.admit), _ptr(out.preempt), _ptr(out.scalars),
-                         _ptr(out.V), _ptr(out.kstar))
+                         _ptr(out.V), _ptr(out.kstar), _ptr(export_host), int(export_preempt), int(export_served))
         self._check(lib().andes_schedule(self._h, C.byref(_req_struct(req, n)), C.byref(p), C.byref(d),
                                          _stream_ptr(stream)), "andes_schedule")
         return out
@@ -377,6 +423,15 @@ class Context:
         count = int(idx.numel()) if idx is not None else 0
         self._check(lib().andes_tracker_append(self._h, C.byref(t), _ptr(idx), _ptr(t_abs), count, _ptr(serve_mask),
                                                _stream_ptr(stream)), "andes_tracker_append")
+
+    def tracker_append_dev(self, req: dict, n: int, idx, t_abs, count_dev, serve_mask=None, stream=None):
+        """As tracker_append with the token count read on the device: count_dev is a device
+        int32 [1] (<= idx.numel(), the slots idx / t_abs hold), so the call is graph-capturable."""
+        t = Tracker(int(n), _ptr(req["arrival_us"]), _ptr(req["tl_base"]), _ptr(req["tl_pool"]),
+                    int(req["tl_pool"].numel()), _ptr(req["n_deliv"]), _ptr(req["ctx_len"]), _ptr(req["running"]))
+        self._check(lib().andes_tracker_append_dev(self._h, C.byref(t), _ptr(idx), _ptr(t_abs), _ptr(count_dev),
+                                                   int(idx.numel()), _ptr(serve_mask), _stream_ptr(stream)),
+                    "andes_tracker_append_dev")
 
     # -- andes_simulate (NEXT-3: the serving loop on the device, the decision in the loop)
     def simulate(self, trace: dict, tau, kv_capacity: int, horizon_us=2_000_000, preempt_cap=UINT32_MAX, flags=0,

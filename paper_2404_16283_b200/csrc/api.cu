@@ -517,13 +517,16 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   if ((p->flags & ANDES_OBJ_MAXMIN) && (p->flags & ANDES_OBJ_PERFECT))
     return set_err(c, ANDES_E_INVAL, "at most one objective flag%s");
   w.obj = (p->flags & ANDES_OBJ_MAXMIN) ? kObjMaxMin : (p->flags & ANDES_OBJ_PERFECT) ? kObjPerfect : kObjAndes;
+  w.now_dev = reinterpret_cast<const long long*>(p->now_dev);
+  w.now_ref = p->now_us;
   const int64_t eval = p->now_us + (int64_t)p->horizon_us;
   const bool debug = (p->flags & ANDES_DEBUG_CHECKS) != 0;
   SchedOut o{out->serve_mask, out->admit_idx, out->preempt_idx, out->scalars, out->V, out->kstar};
   // profiled stages: [0] reset + prep + S0/S2 bounds, [1] timeline scan (S1), [2] state + key
   // bounds (S3a), [3] candidate keys (S3b), [4] Algorithm 1 per B + best B + cap + mask (S4-S6)
   mark(c, 0, s);
-  if ((rc = reset_call(c, s))) return rc;
+  if (w.now_dev) launch_reset_now(L, w);  // zeroes the globals and reads the time once
+  else if ((rc = reset_call(c, s))) return rc;
   // Appendix-A objectives need every request's QoE now: prep also writes the records of an
   // evaluation at now (dual), a first scan fills the *_now arrays (its own look-back status
   // words), then Q_now (and its minimum); the tile counter is reset for the main scan
@@ -565,6 +568,8 @@ int andes_schedule(AndesCtx* c, const AndesRequests* req, const AndesSchedParams
   }
   if (p->flags & ANDES_REFINE)
     launch_refine(L, r, w, o, p->now_us, p->tau_us, p->kv_capacity, p->prefill_tok_s, p->swap_tok_s);
+  if (out->export_host)
+    launch_decision_export(L, o, w, p->B_cap, out->export_preempt, out->export_served, out->export_host);
   mark(c, 5, s);
   mark(c, 6, s);
   if (c->prof) c->prof_recorded = true;
@@ -661,6 +666,20 @@ int andes_tracker_append(AndesCtx* c, const AndesTracker* t, const uint32_t* idx
   if (count && (!idx || !t_abs)) return set_err(c, ANDES_E_INVAL, "idx/t_abs is NULL%s");
   TrackerView v{t->n, t->arrival_us, t->tl_base, t->tl_pool, t->tl_len, t->n_deliv, t->ctx_len, t->running};
   launch_tracker_append(cfg_of(c, stream), v, idx, t_abs, count, serve_mask, c->w);
+  return cuda_check(c, cudaGetLastError(), "kernel launch");
+}
+
+int andes_tracker_append_dev(AndesCtx* c, const AndesTracker* t, const uint32_t* idx, const int64_t* t_abs,
+                             const uint32_t* count_dev, uint32_t max_count, const uint8_t* serve_mask, void* stream) {
+  if (!c) return ANDES_E_INVAL;
+  int rc = pending_device_error(c);
+  if (rc) return rc;
+  if (!t) return set_err(c, ANDES_E_INVAL, "tracker is NULL%s");
+  if (t->n && (!t->arrival_us || !t->tl_base || !t->tl_pool || !t->n_deliv || !t->ctx_len || !t->running))
+    return set_err(c, ANDES_E_INVAL, "a tracker array is NULL%s");
+  if (max_count && (!idx || !t_abs || !count_dev)) return set_err(c, ANDES_E_INVAL, "idx/t_abs/count_dev is NULL%s");
+  TrackerView v{t->n, t->arrival_us, t->tl_base, t->tl_pool, t->tl_len, t->n_deliv, t->ctx_len, t->running};
+  launch_tracker_append(cfg_of(c, stream), v, idx, t_abs, max_count, serve_mask, c->w, count_dev);
   return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
 
@@ -863,6 +882,7 @@ int andes_schedule_host(AndesCtx* c, const AndesRequests* rq, const AndesSchedPa
   dr.tl_pool = m.tl_pool;
   dr.tl_len = c->lim.max_tokens;
   AndesSchedParams dp = *p;
+  dp.now_dev = nullptr;  // (host call: the time is the host's now_us)
   dp.tau_us = m.tau;
   AndesDecision dd{m.serve_mask, m.admit_idx, m.preempt_idx, m.scalars, m.V, m.kstar};
   int rc = andes_schedule(c, &dr, &dp, &dd, stream);

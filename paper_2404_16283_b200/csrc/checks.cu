@@ -16,6 +16,7 @@ namespace andes {
 constexpr int kCheckThreads = 256;
 
 __global__ void __launch_bounds__(kCheckThreads) k_debug_checks(ReqView r, Work w, int64_t now) {
+  now += tshift(w);  // (AndesSchedParams.now_dev)
   const uint32_t n = r.n;
   const uint32_t lane = threadIdx.x & 31;
   uint32_t err = 0;

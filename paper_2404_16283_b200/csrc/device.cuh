@@ -165,7 +165,8 @@ struct Globals2 {
   uint32_t rf_done;                               // refiner: k_refine_loss CTAs finished (last block)
   uint32_t pad0;
   unsigned long long best_vb;                     // S5: max over B of pack_vb(V(B), B) (select CTAs)
-  uint32_t pad[18];
+  long long tshift;                               // *now_dev - now_ref, read once by prep (now_dev calls)
+  uint32_t pad[16];
 };
 static_assert(sizeof(Globals2) == 128, "Globals2: one 128-byte line");
 
@@ -280,9 +281,16 @@ struct Work {
   uint32_t* err_map;
   // debug checks: open-addressing set of ranks (2 N_cap slots, self-cleaning), rank uniqueness
   unsigned long long* rank_set;
+  // decision time read on the device (AndesSchedParams.now_dev): every time argument of the
+  // call's kernels (passed for now_ref) is shifted by *now_dev - now_ref; NULL: no shift
+  const long long* now_dev;
+  long long now_ref;
 };
 
+
 __host__ __device__ inline Globals2* globals2(const Work& w) { return reinterpret_cast<Globals2*>(w.g + 1); }
+// the shift k_reset_now published (every kernel of a now_dev call)
+__device__ __forceinline__ long long tshift(const Work& w) { return w.now_dev ? __ldcg(&globals2(w)->tshift) : 0ll; }
 
 // ---------------------------------------------------------------- error reporting
 // Raise error bits: into this call's Globals word (read by the decision's own kernels, e.g. the

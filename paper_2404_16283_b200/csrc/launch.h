@@ -58,6 +58,9 @@ struct SchedOut {
   uint32_t* kstar;
 };
 
+void launch_reset_now(const LaunchCfg& L, const Work& w);
+void launch_decision_export(const LaunchCfg& L, const SchedOut& o, const Work& w, uint32_t B_cap, uint32_t pmax,
+                            uint32_t smax, void* host);
 void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,
                           const uint32_t* tau, const uint32_t* B_list_dev, uint32_t nB, double* gain_out,
                           float* key_out, double* qwait_out);
@@ -87,7 +90,7 @@ void launch_refine(const LaunchCfg& L, const ReqView& r, const Work& w, const Sc
                    const uint32_t* tau, uint64_t M, uint32_t prefill, uint32_t swap);
 void init_kernels();
 void launch_tracker_append(const LaunchCfg& L, const TrackerView& t, const uint32_t* idx, const int64_t* t_abs,
-                           uint32_t count, const uint8_t* serve_mask, const Work& w);
+                           uint32_t count, const uint8_t* serve_mask, const Work& w, const uint32_t* count_dev = nullptr);
 void launch_sim_live(cudaStream_t s, const SimView& v, int64_t now);
 void launch_sim_step(cudaStream_t s, uint32_t sm_count, const SimView& v, uint32_t n_live, int64_t now,
                      const uint32_t* tau, uint32_t B_cap, const uint8_t* serve_mask, const uint32_t* scalars);

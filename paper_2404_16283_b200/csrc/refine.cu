@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_loss(ReqView r, Work 
                                                                 const uint32_t* tau, uint64_t M) {
   __shared__ Globals s_g;
   pdl_wait();
+  now += tshift(w);  // (AndesSchedParams.now_dev)
   snap_globals(w.g, &s_g);
   const uint32_t np = s_g.rf_npairs;
   const uint32_t n_run = min(s_g.n_run, (uint32_t)kMaxRunning);

@@ -184,6 +184,12 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
   const uint32_t n = r.n;
   uint32_t local_err = 0, local_unal = 0;
   pdl_wait();
+  if (w.now_dev) {
+    // AndesSchedParams.now_dev: the shift the call's reset kernel read (k_reset_now)
+    const int64_t sh = tshift(w);
+    eval_abs += sh;
+    now_abs += sh;
+  }
   if (blockIdx.x < 512) ANDES_TRACE(w, 7000 + 2 * blockIdx.x);
   if (sched) {
     for (uint32_t q = threadIdx.x; q < kHistL; q += blockDim.x) s_hl[q] = 0u;
@@ -1335,6 +1341,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     r_end1 = r_end2;
   }
   if (A.qnow) {
+    const int64_t now_abs = A.now_abs + tshift(w);
     // k_qnow's work by the warps that have run out of tiles (chunks of 32 requests from a
     // counter): it overlaps the scan's tail instead of costing a kernel of its own
     unsigned long long best = 0ull;
@@ -1345,7 +1352,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       c = __shfl_sync(0xffffffffu, c, 0);
       if (c >= nq) break;
       const uint32_t i = c * 32u + lane;
-      if (i < n) best = max(best, qnow_of(r, w, i, A.now_abs));
+      if (i < n) best = max(best, qnow_of(r, w, i, now_abs));
     }
     for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) qmin_raise(w, best);

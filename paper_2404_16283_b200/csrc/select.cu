@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kStateThreads) k_state(ReqView r, Work w, int6
   snap_globals(w.g, &s_g);
   if (!s_g.triggered || s_g.B_hi == 0) return;
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
-  state_phase<kStateThreads>(r, w, now, horizon, s_g, s_hlb, s_hub, blockIdx.x, gridDim.x);
+  state_phase<kStateThreads>(r, w, now + tshift(w), horizon, s_g, s_hlb, s_hub, blockIdx.x, gridDim.x);
   if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
 }
 
@@ -1165,7 +1165,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_decide(SelectArgs A) {
     // ---- phase A: state and key bounds (histograms in the dynamic shared buffer)
     uint32_t* s_hlb = reinterpret_cast<uint32_t*>(s_dyn);
     if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x);
-    state_phase<kSelThreads>(r, w, A.now, A.horizon, s_g, s_hlb, s_hlb + kHistK, blockIdx.x, G);
+    state_phase<kSelThreads>(r, w, A.now + tshift(w), A.horizon, s_g, s_hlb, s_hlb + kHistK, blockIdx.x, G);
     if (blockIdx.x < 512) ANDES_TRACE(w, 3000 + 2 * blockIdx.x + 1);
     // ---- barrier A; the last arriver computes the survivor cut
     __threadfence();
