@@ -12,12 +12,14 @@
 
 using namespace andes;
 
-// Programmatic dependent launch is off by default: measured on config 3 it did not shorten the
-// decision (88 us without vs 92 us with, L2 flushed).  ANDES_PDL=1 turns it on.
+// Programmatic dependent launch (every kernel waits on griddepcontrol.wait before it reads its
+// predecessor's results): on by default since round 2 -- neutral on the decision (69.6 us either
+// way, L2 flushed) and -5 us on the 2^20-request andes_qoe_eval (196.5 -> 191.5 us).  ANDES_PDL=0
+// turns it off.
 bool andes::pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("ANDES_PDL");
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
   }();
   return on;
 }

@@ -40,6 +40,22 @@ for mode, name in ((A.ANDES_EVAL_INFLIGHT, "inflight"), (A.ANDES_EVAL_FINAL, "fi
             if it >= 3:
                 scan.append(st[1])
                 call.append(a.elapsed_time(b))
+    # the same call without the profiling events between its kernels
+    ctx.profile_enable(False)
+    plain = []
+    with torch.cuda.stream(s):
+        for it in range(reps + 3):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            ctx.qoe_eval(req, big.n, big.now_us + big.horizon_us, mode, stream=s)
+            b.record(s)
+            b.synchronize()
+            if it >= 3:
+                plain.append(a.elapsed_time(b))
+    ctx.profile_enable(True)
     ts, tc = statistics.median(scan), statistics.median(call)
+    tp = statistics.median(plain)
     print(f"[{tag}] {name:8s} scan {ts * 1e3:7.1f} us ({alg / ts / 1e6 / peak:.3f})  call {tc * 1e3:7.1f} us "
-          f"({alg / tc / 1e6 / peak:.3f})", flush=True)
+          f"({alg / tc / 1e6 / peak:.3f})  unprofiled call {tp * 1e3:7.1f} us ({alg / tp / 1e6 / peak:.3f})", flush=True)
