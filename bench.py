@@ -264,55 +264,75 @@ def sharded_decision(args, dist, rank, ws, lr, stream, flush):
             if s_ < A.SHARD_ROUNDS:
                 ag(send[s_], recv[s_])
 
-    with torch.cuda.stream(stream):
-        for _ in range(3):
-            eager()
-        stream.synchronize()
-        # the whole sharded decision -- five steps and the four all-gathers between them -- in one
-        # CUDA graph (NCCL collectives are capturable); if this runtime cannot capture the
-        # collective, per-step graphs with the all-gathers issued between their replays
-        launch = "one CUDA graph: 5 steps + 4 all-gathers (NCCL at world > 1, a device copy at world 1)"
-        try:
-            g1 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g1, stream=stream):
+    def timed(ag_fn, tag):
+        """Capture the decision (five steps + four all-gathers with ag_fn) in one graph (per-step
+        graphs with eager all-gathers if the collective cannot be captured), replay, time."""
+        nonlocal ag
+        ag = ag_fn
+        with torch.cuda.stream(stream):
+            for _ in range(3):
                 eager()
-            g1.replay()
             stream.synchronize()
-
-            def decide():
+            launch = f"one CUDA graph: 5 steps + 4 all-gathers ({tag})"
+            try:
+                g1 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g1, stream=stream):
+                    eager()
                 g1.replay()
-        except Exception as ex:  # noqa: BLE001 -- reported in the line
-            launch = f"5 step CUDA graphs + 4 eager all-gathers (capture failed: {type(ex).__name__})"
-            stream.synchronize()
-            graphs = []
-            for s_ in range(A.SHARD_STEPS):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    step(s_)
-                graphs.append(g)
+                stream.synchronize()
 
-            def decide():
+                def decide():
+                    g1.replay()
+            except Exception as ex:  # noqa: BLE001 -- reported in the line
+                launch = f"5 step CUDA graphs + 4 eager all-gathers ({tag}; capture failed: {type(ex).__name__})"
+                stream.synchronize()
+                graphs = []
                 for s_ in range(A.SHARD_STEPS):
-                    graphs[s_].replay()
-                    if s_ < A.SHARD_ROUNDS:
-                        ag(send[s_], recv[s_])
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        step(s_)
+                    graphs.append(g)
 
-        for _ in range(max(args.warmup, 3)):
-            flush.zero_()
-            decide()
-        stream.synchronize()
-        ms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            if dist is not None:
-                dist.barrier()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            decide()
-            b.record(stream)
-            b.synchronize()
-            ms.append(a.elapsed_time(b))
+                def decide():
+                    for s_ in range(A.SHARD_STEPS):
+                        graphs[s_].replay()
+                        if s_ < A.SHARD_ROUNDS:
+                            ag(send[s_], recv[s_])
+
+            for _ in range(max(args.warmup, 3)):
+                flush.zero_()
+                decide()
+            stream.synchronize()
+            ms = []
+            for _ in range(args.steps):
+                flush.zero_()
+                if dist is not None:
+                    dist.barrier()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                decide()
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+        return ms, launch
+
+    ms, launch = timed(ag, "NCCL at world > 1, a device copy at world 1")
+    collectives = {}
+    if dist is not None:
+        # the same decision with the exchanges as device collectives over peer memory (andes_comm:
+        # CUDA IPC mappings of each rank's arena, P2P stores over NVLink; no NCCL)
+        collectives[f"{dist.get_backend()}_ms_per_decision"] = _max_over_ranks(dist, sum(ms)) / args.steps
+        try:
+            comm = A.Comm(ws, rank, max(int(x) for x in sh.xbytes), device=lr)
+            hs = [None] * ws
+            dist.all_gather_object(hs, comm.handle)
+            comm.connect(hs)
+            ms_c, launch_c = timed(comm.allgather, "andes_comm peer-memory all-gathers")
+            collectives["peer_memory_ms_per_decision"] = _max_over_ranks(dist, sum(ms_c)) / args.steps
+            collectives["peer_memory_launch"] = launch_c
+        except Exception as ex:  # noqa: BLE001 -- reported in the line
+            collectives["peer_memory_error"] = f"{type(ex).__name__}: {ex}"[:200]
     total = _max_over_ranks(dist, sum(ms))
     sc = out.scalars.cpu().numpy().view(np.uint32).copy()
     res = {"workload": "config4: 2^20 live requests (config 3 x16, running batch in the first copy), "
@@ -320,6 +340,7 @@ def sharded_decision(args, dist, rank, ws, lr, stream, flush):
            "n_requests": int(big.n), "world": ws, "requests_per_rank": int(mine.n),
            "ms_per_decision": total / args.steps, "decisions_per_s": args.steps / (total / 1e3),
            "launch": launch,
+           "collectives": collectives or None,
            "xbytes_per_round": [int(x) for x in sh.xbytes],
            "decision": {k: int(v) for k, v in zip(A.SC_NAMES, sc)}}
     if dist is not None:

@@ -57,7 +57,7 @@ typedef enum {
     ANDES_E_INVAL = -1,    /* bad argument (null pointer, zero period, B out of range, ...) */
     ANDES_E_RANGE = -2,    /* a device-side data precondition failed (debug checks)        */
     ANDES_E_CUDA = -3,     /* a CUDA runtime error; see andes_last_error                   */
-    ANDES_E_NCCL = -4,     /* reserved for the multi-GPU entry points                      */
+    ANDES_E_NCCL = -4,     /* the peer-memory all-gather timed out waiting for a peer       */
     ANDES_E_CAPACITY = -5, /* n, B_cap, token count or running-set size above the limits   */
     ANDES_NOT_TRIGGERED = 1 /* _host entry points only: the trigger did not fire           */
 } AndesStatus;
@@ -373,6 +373,26 @@ int andes_shard_init(AndesCtx *ctx, uint32_t world, uint32_t rank, uint32_t B_ca
 int andes_schedule_shard(AndesCtx *ctx, const AndesShard *shard, uint32_t step, const AndesRequests *local,
                          const AndesSchedParams *p, AndesDecision *out, const void *recv, void *send,
                          void *stream);
+
+/* ---- Peer-memory all-gather for the sharded decision (no NCCL) ---------------------------
+ * The four exchanges of andes_schedule_shard as device collectives over CUDA IPC mappings: each
+ * rank's arena (G flags, two parities of G slots of max_block bytes) lives in its own device
+ * memory and is written by every peer directly (P2P stores over NVLink between the GPUs of a node;
+ * on one GPU, processes sharing the device).  Setup: andes_comm_create returns this rank's IPC
+ * handle (ANDES_COMM_HANDLE_BYTES); the caller exchanges the handles (any host channel, e.g.
+ * torch.distributed.all_gather_object) and passes all of them, in rank order, to
+ * andes_comm_connect.  andes_comm_allgather(send, recv, bytes): every rank's send block (DEVICE,
+ * bytes <= max_block, the same bytes on every rank) into recv (DEVICE, world * bytes, rank order);
+ * two kernels on the stream (push + publish, wait + pull), capture safe; all ranks must issue the
+ * same all-gathers in the same order.  A wait longer than 10 s for a peer is flagged and the next
+ * call returns ANDES_E_NCCL.  Errors: ANDES_E_INVAL, ANDES_E_CUDA. */
+#define ANDES_COMM_HANDLE_BYTES 64
+typedef struct AndesComm AndesComm;
+int andes_comm_create(AndesComm **out, int device, uint32_t world, uint32_t rank, uint64_t max_block,
+                      void *handle_out);
+int andes_comm_connect(AndesComm *comm, const void *handles);
+int andes_comm_allgather(AndesComm *comm, const void *send, void *recv, uint64_t bytes, void *stream);
+int andes_comm_destroy(AndesComm *comm);
 
 /* ---- Exact reference solver (NEXT-4; Algorithm 2) --------------------------
  * The 3D dynamic program for Eq. 5 at target batch size B over n items with integer values

@@ -53,7 +53,8 @@ EXPORTS = ["andes_create", "andes_destroy", "andes_last_error", "andes_qoe_eval"
            "andes_schedule", "andes_schedule_host", "andes_version", "andes_profile_enable", "andes_profile_read",
            "andes_shard_init", "andes_schedule_shard", "andes_qoe_scenario_mean", "andes_knapsack_dp",
            "andes_knapsack_dp_workspace", "andes_tracker_append", "andes_tracker_append_dev", "andes_simulate",
-           "andes_sim_workspace"]
+           "andes_sim_workspace", "andes_comm_create", "andes_comm_connect", "andes_comm_allgather",
+           "andes_comm_destroy"]
 SHARD_ROUNDS = 4
 SHARD_STEPS = 5
 MAX_WORLD = 8
@@ -162,6 +163,10 @@ def lib() -> C.CDLL:
                                            C.c_void_p, C.c_void_p]
         L.andes_tracker_append_dev.argtypes = [C.c_void_p, C.POINTER(Tracker), C.c_void_p, C.c_void_p, C.c_void_p,
                                                C.c_uint32, C.c_void_p, C.c_void_p]
+        L.andes_comm_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p]
+        L.andes_comm_connect.argtypes = [C.c_void_p, C.c_void_p]
+        L.andes_comm_allgather.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
+        L.andes_comm_destroy.argtypes = [C.c_void_p]
         L.andes_sim_workspace.argtypes = [C.c_uint32]
         L.andes_sim_workspace.restype = C.c_uint64
         L.andes_simulate.argtypes = [C.c_void_p, C.POINTER(Sim), C.POINTER(SimParams), C.POINTER(SimStats), C.c_void_p]
@@ -523,6 +528,37 @@ def run_shard_steps(step_fn, allgather, send, recv, steps=SHARD_STEPS):
             allgather(cur, recv[s])
             prev = recv[s]
     return prev
+
+
+class Comm:
+    """The peer-memory all-gather (andes_comm_*): create on every rank, exchange .handle over any
+    host channel, connect(handles in rank order); allgather(send, recv) is a device collective."""
+
+    def __init__(self, world: int, rank: int, max_block: int, device: int = 0):
+        self._h = C.c_void_p()
+        h = (C.c_char * 64)()
+        rc = lib().andes_comm_create(C.byref(self._h), int(device), int(world), int(rank), int(max_block), h)
+        if rc < 0:
+            raise AndesError(f"andes_comm_create failed rc={rc}", rc)
+        self.handle = bytes(h)
+        self.world = world
+
+    def connect(self, handles):
+        buf = C.create_string_buffer(b"".join(handles), 64 * self.world)
+        rc = lib().andes_comm_connect(self._h, buf)
+        if rc < 0:
+            raise AndesError(f"andes_comm_connect failed rc={rc}", rc)
+
+    def allgather(self, send, recv, stream=None):
+        rc = lib().andes_comm_allgather(self._h, _ptr(send), _ptr(recv), int(send.numel() * send.element_size()),
+                                        _stream_ptr(stream))
+        if rc < 0:
+            raise AndesError(f"andes_comm_allgather failed rc={rc}", rc)
+
+    def close(self):
+        if self._h:
+            lib().andes_comm_destroy(self._h)
+            self._h = C.c_void_p()
 
 
 def schedule_sharded(ctx: Context, sh: Shard, req: dict, n: int, now_us: int, horizon_us: int, tau,

@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libandes.so")
-SOURCES = ["api.cu", "scan.cu", "select.cu", "shard.cu", "refine.cu", "dp.cu", "checks.cu", "tracker.cu", "sim.cu"]
+SOURCES = ["api.cu", "scan.cu", "select.cu", "shard.cu", "refine.cu", "dp.cu", "checks.cu", "tracker.cu", "sim.cu",
+           "comm.cu"]
 HEADERS = ["device.cuh", "block.cuh", "launch.h", os.path.join("..", "..", "include", "andes.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

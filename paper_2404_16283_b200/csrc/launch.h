@@ -59,6 +59,9 @@ struct SchedOut {
 };
 
 void launch_reset_now(const LaunchCfg& L, const Work& w);
+struct CommView;
+void launch_comm_allgather(cudaStream_t s, const CommView& v, const void* send, void* recv, uint64_t bytes,
+                           uint32_t sm_count);
 void launch_decision_export(const LaunchCfg& L, const SchedOut& o, const Work& w, uint32_t B_cap, uint32_t pmax,
                             uint32_t smax, void* host);
 void launch_gain_estimate(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t now, uint32_t horizon,

@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, cap, flags, q):
+def _worker(rank, world, port, name, cap, flags, q, comm=False):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -53,8 +53,24 @@ def _worker(rank, world, port, name, cap, flags, q):
             dist.all_gather(list(hr.chunk(world)), h)
             recv.copy_(hr)
 
+        ag = host_allgather
+        if comm:
+            # the exchanges as device collectives over peer memory (andes_comm: CUDA IPC mappings of
+            # each rank's arena); only the 64-byte handles travel over the host channel, once
+            c = A.Comm(world, rank, max(int(x) for x in sh.xbytes), device=0)
+            hs = [None] * world
+            dist.all_gather_object(hs, c.handle)
+            c.connect(hs)
+            ag = c.allgather
         out = A.schedule_sharded(ctx, sh, req, mine.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity,
-                                 host_allgather, bufs=bufs, preempt_cap=cap, flags=flags)
+                                 ag, bufs=bufs, preempt_cap=cap, flags=flags)
+        if comm:
+            # a second decision through the same communicator (sequence numbers and arena parities
+            # carry over) must give the same result
+            out2 = A.schedule_sharded(ctx, sh, req, mine.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity,
+                                      ag, bufs=bufs, preempt_cap=cap, flags=flags)
+            torch.cuda.synchronize()
+            assert torch.equal(out.scalars, out2.scalars) and torch.equal(out.V, out2.V)
         torch.cuda.synchronize()
         sc = out.scalars.cpu().numpy().view(np.uint32).copy()
         q.put((rank, dict(sc=sc, V=out.V.cpu().numpy(), kstar=out.kstar.cpu().numpy().view(np.uint32),
@@ -74,6 +90,30 @@ def test_sharded_decision_two_processes(orc, name, cap, flags):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     ps = [ctx.Process(target=_worker, args=(r, world, port, name, cap, flags, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    snap = snapshot_cached(name)
+    o = oracle_decision_cached(orc, name, snap, cap=cap, flags=flags)
+    mask = np.concatenate([got[r]["mask"] for r in range(world)])
+    for r in range(world):
+        assert_decision_equal(dict(got[r], mask=mask), o)
+
+
+@pytest.mark.parametrize("name,cap,flags", [("config2", 16, 1), ("config3", 16, 1)])
+def test_sharded_decision_two_processes_peer_memory(orc, name, cap, flags):
+    """The same two-process decision with the four exchanges done on the device by andes_comm (CUDA
+    IPC: every rank stores its block into every peer's arena and publishes a flag; no host
+    staging, no NCCL), compared with the oracle."""
+    import torch.multiprocessing as mp
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, name, cap, flags, q, True)) for r in range(world)]
     for p in ps:
         p.start()
     got = dict(q.get(timeout=600) for _ in range(world))
