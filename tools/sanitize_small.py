@@ -1,6 +1,8 @@
 """Small decisions and QoE evaluations for compute-sanitizer (memcheck / racecheck runs): every
-decision flavour, debug checks, the sharded steps at world 1, the tracker update, the serving-loop
-simulator and the fused cooperative kernel (ANDES_FUSED=1 when set in the environment)."""
+decision flavour, debug checks, the sharded steps at world 1, the tracker update (host count and
+device count with pinned inputs), the decision with now_dev and the zero-copy export, the
+peer-memory all-gather at world 1, the serving-loop simulator and the fused cooperative kernel
+(ANDES_FUSED=1 when set in the environment)."""
 import os
 import sys
 
@@ -34,6 +36,27 @@ for seed in range(6):
     idx = torch.nonzero(d.serve_mask[:sr.n]).flatten().to(torch.int32)
     ts = torch.full((idx.numel(),), sr.now_us + 1000, dtype=torch.int64, device="cuda")
     ctx.tracker_append(rq2, sr.n, idx if idx.numel() else None, ts if idx.numel() else None, serve_mask=d.serve_mask)
+    # round 2: the replayable serving step -- the tracker update reading pinned host inputs with
+    # the count on the device, the decision time from pinned memory, the zero-copy export
+    hts = torch.full((64,), sr.now_us + 2000, dtype=torch.int64).pin_memory()
+    hexp = torch.zeros(A.decision_export_bytes(int(tau.numel()), 64, 64), dtype=torch.uint8).pin_memory()
+    hnow = torch.tensor([sr.now_us + 2000], dtype=torch.int64).pin_memory()
+    d = ctx.schedule(rq2, sr.n, sr.now_us, sr.horizon_us, tau, sr.kv_capacity, preempt_cap=2, export_host=hexp,
+                     export_preempt=64, export_served=64, now_dev=hnow)
+    torch.cuda.synchronize()
+    srv = hexp[hexp.numel() - 4 * 64:].view(torch.int32)
+    cnt = hexp[4:8].view(torch.int32)
+    ctx.tracker_append_dev(rq2, sr.n, srv, hts, cnt, serve_mask=d.serve_mask)
+# the peer-memory all-gather at world 1 (arena slot copies, flag publish and wait)
+cm = A.Comm(1, 0, 4096)
+cm.connect([cm.handle])
+src = torch.arange(1000, dtype=torch.int32, device="cuda")
+dstb = torch.zeros(1000, dtype=torch.int32, device="cuda")
+for _ in range(3):
+    cm.allgather(src, dstb)
+torch.cuda.synchronize()
+assert torch.equal(src, dstb)
+cm.close()
 snap = W.long_requests(3, n=60, lo=5000, hi=9000)
 req = A.requests_to(snap)
 ctx.qoe_eval(req, snap.n, snap.now_us, A.ANDES_EVAL_INFLIGHT)
