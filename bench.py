@@ -755,6 +755,11 @@ def run_ours(args):
     roof["stage_ms_event_graph"] = dict(zip(names, stage_ms))
     roof["stage_trace"] = trace
     roof["ib_evaluations_per_s"] = n * 256 / (ms_per_step / 1e3)
+    try:  # issue-slot utilisation of every decision kernel, from the committed ncu capture
+        roof["issue_active_pct_ncu"] = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                                   "profiles", "ncu_issue.json")))
+    except (OSError, ValueError):
+        roof["issue_active_pct_ncu"] = None
     roof["stage_share_event_graph"] = {k: v / sum(stage_ms) for k, v in zip(names, stage_ms)}
 
     # ---- S1 alone at scale: QoE-eval token-events/s on a 1M-request population (config-4 size)
