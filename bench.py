@@ -400,10 +400,17 @@ def decision_trace(ctx, req, n, snap, tau, out, stream):
                          preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
         stream.synchronize()
         L.andes_debug_trace(ctx._h, 0)
-        L.andes_debug_trace(ctx._h, 1)  # fresh stamps for one decision
-        ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream,
-                     preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
+        L.andes_debug_trace(ctx._h, 1)  # fresh stamps
+        # the decision captured into a CUDA graph and replayed, as the timed steps run it; every
+        # replay overwrites the stamps (later times), so they describe the last replay
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            ctx.schedule(req, n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, out=out, stream=stream,
+                         preempt_cap=snap.preempt_cap, flags=A.ANDES_FORCE)
+        for _ in range(3):
+            g.replay()
         stream.synchronize()
+        del g
     tr = np.zeros(1 << 16, np.uint64)
     L.andes_debug_read(ctx._h, 7, tr.ctypes.data, tr.nbytes)
     L.andes_debug_trace(ctx._h, 0)
@@ -425,7 +432,7 @@ def decision_trace(ctx, req, n, snap, tau, out, stream):
                    "select": [us(sel[:, 0].min()), us(sel[:, 1].max())], "finalize": fin})
     names = list(stages)[:-1]
     gaps = {f"{a}->{b}": round(stages[b][0] - stages[a][1], 2) for a, b in zip(names, names[1:])}
-    return {"source": "in-kernel %globaltimer stamps (CTA start/end), one config-3 decision, L2 warm",
+    return {"source": "in-kernel %globaltimer stamps (CTA start/end), one config-3 decision replayed from a CUDA graph as in the timed steps (the last of three replays), L2 warm",
             "stages_us_from_prep_start": stages, "gaps_us": gaps}
 
 
