@@ -27,6 +27,18 @@ for it in range(int(os.environ.get("ITERS", "4"))):
         L.andes_debug_trace(ctx._h, 1)
     d = ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=16)
 torch.cuda.synchronize()
+if os.environ.get("GRAPH", "1") == "1":
+    # as the bench times it: the decision captured in a CUDA graph, replayed (stamps of the last replay)
+    s = torch.cuda.Stream()
+    out = ctx.alloc_decision(snap.n, 256)
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=16, out=out,
+                         stream=s)
+        for _ in range(3):
+            g.replay()
+    s.synchronize()
 tr = np.zeros(1 << 16, np.uint64)
 print("read rc", L.andes_debug_read(ctx._h, 7, tr.ctypes.data, tr.nbytes))
 tr = tr.astype(np.int64)
