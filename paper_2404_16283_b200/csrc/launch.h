@@ -36,11 +36,11 @@ struct LaunchCfg {
 
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                  bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask = nullptr, int64_t now_abs = 0,
-                 bool dual = false);
+                 bool dual = false, bool eval = false);
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                  const CUtensorMap* tmap, bool sched = false, const uint32_t* tau = nullptr, uint32_t B_cap = 0,
                  uint64_t M = 0, uint32_t cur_latency = 0, uint32_t flags = 0, bool second = false,
-                 bool qnow = false, int64_t now_abs = 0);
+                 bool qnow = false, int64_t now_abs = 0, bool eval = false);
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                       float* q, double* q64, int64_t* sd, int64_t* sw, uint32_t* m);
 void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, const uint32_t* off, uint32_t S,

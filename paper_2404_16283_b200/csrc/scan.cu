@@ -177,7 +177,7 @@ __device__ void bounds_block(const ReqView& r, const Work& w, const uint32_t* __
 __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_t eval_abs, uint32_t final_mode,
                                                       uint32_t sched, uint64_t kv_cap, uint32_t debug,
                                                       uint8_t* __restrict__ serve_mask, int64_t now_abs,
-                                                      uint32_t dual) {
+                                                      uint32_t dual, uint32_t eval) {
   __shared__ uint32_t s_hl[kHistL];
   __shared__ uint32_t s_minP, s_maxR;
   __shared__ unsigned long long s_runl;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(ReqView r, Work w, int64_
     w.m[i] = m;
     w.spre[i] = 0ull;
     w.edge[i] = 0u;
-    {
+    if (!eval) {  // (andes_qoe_eval: the scan builds its records from the request table)
       ScanRec sr;
       sr.base = r.tl_base[i];
       sr.lim = min(g, m);
@@ -486,6 +486,61 @@ struct ScanArgs {
   int64_t now_abs;
 };
 
+// kEval (andes_qoe_eval): the scan builds request i's record from the request table instead of
+// reading prep's copy (srec): the request-table fields are loaded one unit ahead (RawRec) and
+// converted when the unit is processed, so the prefetch never waits for its loads.
+struct RawRec {
+  unsigned long long base;
+  long long arr;
+  uint32_t g, P, ttft, mt;
+};
+template <bool kFinal>
+__device__ __forceinline__ RawRec raw_of(const ReqView& r, uint32_t i) {
+  RawRec x;
+  x.base = r.tl_base[i];
+  x.g = r.n_deliv[i];
+  x.P = r.period[i];
+  x.ttft = r.ttft[i];
+  x.arr = kFinal ? 0ll : r.arrival[i];
+  x.mt = kFinal ? 0u : r.max_total[i];
+  return x;
+}
+// prep's record (k_prep, the same arithmetic)
+template <bool kFinal>
+__device__ __forceinline__ ScanRec rec_from_raw(int64_t eval_abs, const RawRec& x) {
+  ScanRec s;
+  s.base = x.base;
+  s.P = x.P;
+  s.ttft = x.ttft;
+  s.pad = 0u;
+  uint32_t m;
+  if (kFinal) {
+    m = x.g;
+    s.trel = 0u;
+    s.ek = 2u;
+  } else {
+    const int64_t t = eval_abs - x.arr;
+    m = due_count(t, x.ttft, x.P ? x.P : 1u, x.mt);
+    s.trel = (uint32_t)t;
+    s.ek = x.g < m ? 1u : 2u;
+  }
+  s.lim = min(x.g, m);
+  return s;
+}
+template <bool kEval, bool kFinal>
+__device__ __forceinline__ ScanRec rec_of(const ScanArgs& A, uint32_t i) {
+  if constexpr (kEval) return rec_from_raw<kFinal>(A.eval_abs, raw_of<kFinal>(A.r, i));
+  else return A.w.srec[i];
+}
+template <bool kEval>
+struct PipeRec {
+  using T = ScanRec;
+};
+template <>
+struct PipeRec<true> {
+  using T = RawRec;
+};
+
 // One request of a tile's window in tile-local coordinates (x = position - p0).
 struct Entry {
   int32_t ls;     // local start (base - p0), clamped to [-1, kWTile + 1]
@@ -526,19 +581,21 @@ __device__ __forceinline__ Entry null_entry(bool sentinel) {
 // Window = requests r0 .. r0+wn-1-dummy overlapping the tile (entry 0 is a dummy when a gap
 // precedes r0), from their raw scan records (warp-staged in shared memory, or global memory
 // when the tile overlaps more than kWWinCap requests).
+template <bool kEval, bool kFinal>
 struct RawWin {
-  const ScanRec* rec;
+  const ScanArgs* A;
   unsigned long long p0;
   uint32_t r0, dummy, wn;
   __device__ __forceinline__ int32_t start(uint32_t q) const {
     if (q >= wn) return kWTile + 1;
     if (dummy && q == 0) return -1;
-    const long long ls = (long long)rec[q - dummy].base - (long long)p0;
+    const unsigned long long base = kEval ? A->r.tl_base[r0 + q - dummy] : A->w.srec[r0 + q - dummy].base;
+    const long long ls = (long long)base - (long long)p0;
     return (int32_t)max(-1ll, min(ls, (long long)kWTile + 1));
   }
   __device__ __forceinline__ Entry get(uint32_t q) const {
     if (q >= wn || (dummy && q == 0)) return null_entry(q >= wn);
-    return entry_of(rec[q - dummy], r0 + q - dummy, p0);
+    return entry_of(rec_of<kEval, kFinal>(*A, r0 + q - dummy), r0 + q - dummy, p0);
   }
 };
 
@@ -1017,11 +1074,11 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   }
 }
 
-template <bool kFinal>
+template <bool kFinal, bool kEval>
 __device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, uint32_t tile_s, unsigned long long p0,
                                                             uint32_t r0, uint32_t dummy, uint32_t wn, uint32_t t,
                                                             uint32_t mode, uint32_t cdirect, uint32_t swz_on) {
-  RawWin win{A.w.srec + r0, p0, r0, dummy, wn};
+  RawWin<kEval, kFinal> win{&A, p0, r0, dummy, wn};
   return warp_tile<kFinal>(A, win, tile_s, wn, t, mode, cdirect, swz_on);
 }
 
@@ -1035,7 +1092,7 @@ __device__ __noinline__ unsigned long long warp_tile_global(const ScanArgs& A, u
 // request's earlier tokens are read directly when it started <= kCarryDirect tokens before the
 // unit (else a bounded decoupled look-back on per-tile status words, on the row path); the
 // scan itself uses warp shuffles only: no CTA-wide barriers on the hot path.
-template <bool kFinal, int TW>
+template <bool kFinal, int TW, bool kEval = false>
 __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_constant__ ScanArgs A,
                                                            const __grid_constant__ CUtensorMap tmap_swz,
                                                            const __grid_constant__ CUtensorMap tmap_plain) {
@@ -1150,8 +1207,10 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   };
   MetaLite tm{0u, 0u, 0u};
   uint32_t r_end = 0;
-  ScanRec rec;
-  rec.lim = 0;
+  using PR = typename PipeRec<kEval>::T;
+  PR rec;
+  if constexpr (kEval) rec.g = 0u;
+  else rec.lim = 0u;
   auto load_meta = [&](uint32_t tt, MetaLite& m, uint32_t& re) {  // tt: unit index
     if (lane == 0) {
       const TileMeta* tmp = w.tile_meta + tt * TW;
@@ -1161,9 +1220,14 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       re = (tt * TW + TW < ntiles) ? w.tile_meta[tt * TW + TW].r0 : n - 1;
     }
   };
-  auto load_rec = [&](uint32_t rr, ScanRec& sr) {
-    sr.lim = 0;
-    if (rr + lane < n) sr = w.srec[rr + lane];
+  auto load_rec = [&](uint32_t rr, PR& sr) {
+    if constexpr (kEval) {
+      sr.g = 0u;
+      if (rr + lane < n) sr = raw_of<kFinal>(r, rr + lane);
+    } else {
+      sr.lim = 0u;
+      if (rr + lane < n) sr = w.srec[rr + lane];
+    }
   };
   // three-stage pipeline: the descriptor of the tile after next is requested when that tile is
   // generated (end of an iteration), the records of the next tile once the current tile's data
@@ -1194,8 +1258,9 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t re = __shfl_sync(0xffffffffu, r_end, 0);
     // ---- the next tile (its descriptor is in tm1)
     const uint32_t nxt = __shfl_sync(0xffffffffu, s1, 0);
-    ScanRec recn;
-    recn.lim = 0;
+    PR recn;
+    if constexpr (kEval) recn.g = 0u;
+    else recn.lim = 0u;
     const bool seq = nxt != kNone && (nxt & ~kStart) == tcur + 1u;
     if (seq) load_rec(re, recn);
     const uint32_t dummy = flags & 1u;
@@ -1259,8 +1324,10 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       uint32_t mb = mode, cb = cm;
       for (uint32_t b = 0; b < nbatch; ++b) {
         const uint32_t nb_req = min(31u, nrec - 31u * b);
-        ScanRec rb = rec;
-        if (b && lane < nb_req) rb = w.srec[r0 + 31u * b + lane];
+        ScanRec rb;
+        if constexpr (kEval) rb = rec_from_raw<kFinal>(A.eval_abs, rec);
+        else rb = rec;
+        if (b && lane < nb_req) rb = rec_of<kEval, kFinal>(A, r0 + 31u * b + lane);
         const Entry e = lane < nb_req ? entry_of<TW * kWTile>(rb, r0 + 31u * b + lane, p0) : null_entry(true);
         // the status words are read only by look-backs, i.e. from inside a request longer than
         // kCarryDirect: publish when the request crossing the tile's end (the last one) is such
@@ -1275,7 +1342,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
       // row-per-lane event path (unaligned pools, or a dense tile that must look back); the
       // window's records are read from global memory
       if (TW == 1) {
-        acc_reg = warp_tile_global<kFinal>(A, tile, p0, r0, dummy, wn, tcur, mode, cm, swz_on);
+        acc_reg = warp_tile_global<kFinal, kEval>(A, tile, p0, r0, dummy, wn, tcur, mode, cm, swz_on);
       } else {
         // a unit's warp-tiles one by one, each with its own descriptor; the second continues
         // from the first's carry (the in-chunk rule)
@@ -1296,7 +1363,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
           fh = __shfl_sync(0xffffffffu, fh, 0);
           reh = __shfl_sync(0xffffffffu, reh, 0);
           const uint32_t dh = fh & 1u;
-          a = warp_tile_global<kFinal>(A, tile + h * (kWTile * 4), p0 + h * kWTile, r0h, dh, reh - r0h + 1 + dh, t,
+          a = warp_tile_global<kFinal, kEval>(A, tile + h * (kWTile * 4), p0 + h * kWTile, r0h, dh, reh - r0h + 1 + dh, t,
                                        h ? 1u : mode, (uint32_t)a, swz_on);
         }
         acc_reg = a;
@@ -1465,16 +1532,17 @@ void launch_scenario_mean(const LaunchCfg& L, const ReqView& r, const Work& w, c
 }
 
 void launch_prep(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
-                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask, int64_t now_abs, bool dual) {
+                 bool sched, uint64_t kv_cap, bool debug, uint8_t* serve_mask, int64_t now_abs, bool dual,
+                 bool eval) {
   if (r.n == 0) return;
   const uint32_t blocks = umin32((r.n + kPrepThreads - 1) / kPrepThreads, L.sm_count * 8);
   launch_pdl(k_prep, blocks, kPrepThreads, 0, L.stream, r, w, eval_abs, final_mode ? 1u : 0u, sched ? 1u : 0u,
-             kv_cap, debug ? 1u : 0u, serve_mask, now_abs, dual ? 1u : 0u);
+             kv_cap, debug ? 1u : 0u, serve_mask, now_abs, dual ? 1u : 0u, eval ? 1u : 0u);
 }
 
 void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
                  const CUtensorMap* tmap, bool sched, const uint32_t* tau, uint32_t B_cap, uint64_t M,
-                 uint32_t cur_latency, uint32_t flags, bool second, bool qnow, int64_t now_abs) {
+                 uint32_t cur_latency, uint32_t flags, bool second, bool qnow, int64_t now_abs, bool eval) {
   if (r.n == 0 && !sched) return;
   ScanArgs A{r, w, eval_abs, sched ? 1u : 0u, tau, B_cap, M, cur_latency, flags,
              second ? &globals2(w)->tile_ctr_b : &w.g->tile_ctr, qnow ? 1u : 0u, now_abs};
@@ -1486,13 +1554,12 @@ void launch_scan(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t ev
     return v ? atoi(v) : 0;
   }();
   const bool tw2 = tw_env ? tw_env == 2 : r.tl_len >= (1ull << 24);
-  if (final_mode) {
-    if (tw2) launch_pdl(k_qoe_scan<true, 2>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
-    else launch_pdl(k_qoe_scan<true, 1>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
-  } else {
-    if (tw2) launch_pdl(k_qoe_scan<false, 2>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
-    else launch_pdl(k_qoe_scan<false, 1>, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
-  }
+  // eval: records from the request table (prep wrote none); else prep's records
+  auto* k = eval ? (final_mode ? (tw2 ? &k_qoe_scan<true, 2, true> : &k_qoe_scan<true, 1, true>)
+                               : (tw2 ? &k_qoe_scan<false, 2, true> : &k_qoe_scan<false, 1, true>))
+                 : (final_mode ? (tw2 ? &k_qoe_scan<true, 2> : &k_qoe_scan<true, 1>)
+                               : (tw2 ? &k_qoe_scan<false, 2> : &k_qoe_scan<false, 1>));
+  launch_pdl(k, grid, kScanThreads, kScanDynSmem, L.stream, A, tmap[0], tmap[1]);
 }
 
 void launch_qoe_final(const LaunchCfg& L, const ReqView& r, const Work& w, int64_t eval_abs, bool final_mode,
@@ -1507,14 +1574,20 @@ void init_scan_kernels() {
   cudaFuncSetAttribute(k_qoe_scan<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
   cudaFuncSetAttribute(k_qoe_scan<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
   cudaFuncSetAttribute(k_qoe_scan<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
+  cudaFuncSetAttribute(k_qoe_scan<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanDynSmem);
 }
 
 int scan_blocks_per_sm() {
   int b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_qoe_scan<false, 1>, kScanThreads, kScanDynSmem);
-  int b2 = 0;
+  int b2 = 0, b3 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_qoe_scan<true, 2>, kScanThreads, kScanDynSmem);
-  return b < b2 ? b : b2;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_qoe_scan<false, 2, true>, kScanThreads, kScanDynSmem);
+  b = b < b2 ? b : b2;
+  return b < b3 ? b : b3;
 }
 
 }  // namespace andes
