@@ -324,10 +324,18 @@ def sharded_decision(args, dist, rank, ws, lr, stream, flush):
         # CUDA IPC mappings of each rank's arena, P2P stores over NVLink; no NCCL)
         collectives[f"{dist.get_backend()}_ms_per_decision"] = _max_over_ranks(dist, sum(ms)) / args.steps
         try:
-            comm = A.Comm(ws, rank, max(int(x) for x in sh.xbytes), device=lr)
-            hs = [None] * ws
-            dist.all_gather_object(hs, comm.handle)
-            comm.connect(hs)
+            comm, ok = None, 1
+            try:
+                comm = A.Comm(ws, rank, max(int(x) for x in sh.xbytes), device=lr)
+                hs = [None] * ws
+                dist.all_gather_object(hs, comm.handle)
+                comm.connect(hs)
+            except Exception:  # noqa: BLE001 -- every rank must agree before any waits on a peer
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                raise RuntimeError("andes_comm setup failed on some rank (CUDA IPC / peer access)")
             ms_c, launch_c = timed(comm.allgather, "andes_comm peer-memory all-gathers")
             collectives["peer_memory_ms_per_decision"] = _max_over_ranks(dist, sum(ms_c)) / args.steps
             collectives["peer_memory_launch"] = launch_c
