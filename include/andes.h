@@ -382,9 +382,10 @@ int andes_schedule_shard(AndesCtx *ctx, const AndesShard *shard, uint32_t step, 
  * handle (ANDES_COMM_HANDLE_BYTES); the caller exchanges the handles (any host channel, e.g.
  * torch.distributed.all_gather_object) and passes all of them, in rank order, to
  * andes_comm_connect.  andes_comm_allgather(send, recv, bytes): every rank's send block (DEVICE,
- * bytes <= max_block, the same bytes on every rank) into recv (DEVICE, world * bytes, rank order);
- * two kernels on the stream (push + publish, wait + pull), capture safe; all ranks must issue the
- * same all-gathers in the same order.  A wait longer than 10 s for a peer is flagged and the next
+ * bytes <= max_block, a multiple of 16, the same bytes on every rank; send and recv 16-byte
+ * aligned) into recv (DEVICE, world * bytes, rank order); two kernels on the stream (push +
+ * publish, wait + pull), capture safe; all ranks must issue the same all-gathers in the same
+ * order, and one communicator's all-gathers must be ordered on one stream.  A wait longer than 10 s for a peer is flagged and the next
  * call returns ANDES_E_NCCL.  Errors: ANDES_E_INVAL, ANDES_E_CUDA. */
 #define ANDES_COMM_HANDLE_BYTES 64
 typedef struct AndesComm AndesComm;

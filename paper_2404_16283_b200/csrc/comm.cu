@@ -200,6 +200,9 @@ extern "C" int andes_comm_connect(AndesComm* c, const void* handles) {
 
 extern "C" int andes_comm_allgather(AndesComm* c, const void* send, void* recv, uint64_t bytes, void* stream) {
   if (!c || !c->connected || !send || !recv || bytes > c->max_block) return ANDES_E_INVAL;
+  // 16-byte vector copies: blocks, send and recv 16-byte aligned
+  if ((bytes & 15u) || ((reinterpret_cast<uintptr_t>(send) | reinterpret_cast<uintptr_t>(recv)) & 15u))
+    return ANDES_E_INVAL;
   if (c->err && *reinterpret_cast<volatile uint32_t*>(c->err)) {
     *c->err = 0u;
     return ANDES_E_NCCL;  // an earlier all-gather waited past its bound for a peer
