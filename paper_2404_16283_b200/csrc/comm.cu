@@ -76,7 +76,6 @@ __global__ void __launch_bounds__(kCommThreads) k_comm_push(CommView v, const ui
 }
 
 __global__ void __launch_bounds__(kCommThreads) k_comm_pull(CommView v, uint8_t* __restrict__ recv, uint64_t bytes) {
-  __shared__ uint32_t s_ok;
   const unsigned long long q = *reinterpret_cast<volatile unsigned long long*>(v.seq);
   const uint32_t par = (uint32_t)(q & 1ull);
   uint8_t* own = v.arena[v.rank];
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(kCommThreads) k_comm_pull(CommView v, uint8_t*
       }
     }
     if (!ok) atomicOr(v.err, 1u);
-    s_ok = ok;
   }
   __syncthreads();
   __threadfence_system();
@@ -110,7 +108,6 @@ __global__ void __launch_bounds__(kCommThreads) k_comm_pull(CommView v, uint8_t*
     for (uint64_t b = n16 * 16 + threadIdx.x; b < bytes; b += blockDim.x)
       for (uint32_t g = 0; g < v.world; ++g)
         recv[(size_t)g * bytes + b] = *reinterpret_cast<const volatile uint8_t*>(slot_of(v, own, par, g) + b);
-  (void)s_ok;
 }
 
 void launch_comm_allgather(cudaStream_t s, const CommView& v, const void* send, void* recv, uint64_t bytes,

@@ -804,6 +804,29 @@ __device__ bool finalize_fast(const SelectArgs& A) {
 // (P:L514-529): take while the running sum of l stays <= M (count <= B by construction), break
 // at the first misfit; V(B) = sum of llrint(gain 2^32) over the taken prefix; then B's cap result
 // is staged (stage_cap) and the last CTA to finish picks B* and writes the outputs.
+// descending bitonic sort of one 64-bit value per lane across the warp (shuffles only)
+__device__ __forceinline__ unsigned long long warp_sort_desc(unsigned long long v) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll 1
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool keep_max = ((lane & k) == 0) == ((lane & j) == 0);
+      v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
+    }
+  }
+  return v;
+}
+// number of entries > c in a 32-entry chunk sorted descending (0-padded: never larger)
+__device__ __forceinline__ uint32_t count_gt32(const unsigned long long* ch, unsigned long long c) {
+  uint32_t p = 0;
+#pragma unroll
+  for (uint32_t st = 16; st; st >>= 1)
+    if (ch[p + st - 1] > c) p += st;
+  return p + (ch[p] > c ? 1u : 0u);
+}
+
 // k_select's shared scratch (file scope: allocated in the kernels that use it)
 __shared__ unsigned long long s_sel_ps[kSortCap];
 __shared__ long long s_sel_gf[kSortCap];
@@ -940,41 +963,76 @@ __device__ void select_one_B(const SelectArgs& A, uint32_t B, const Globals& s_g
       __syncthreads();
       if (B == 256) ANDES_TRACE(w, 2400);
       if (B == 256 && w.trace && tid == 0) w.trace[2410] = ns;
-      const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(s_all);
-      const uint32_t np = (ns + 1) >> 1;
-      for (uint32_t e = tid; e < ns; e += kSelThreads) {
-        const unsigned long long c = s_all[e];
-        const uint32_t le = __ldcg(&w.cand_st[e].l);  // its l for the walk (latency under the count)
-        uint32_t pos = 0;
-#pragma unroll 8
-        for (uint32_t f = 0; f < np; ++f) {
-          const ulonglong2 v = a2[f];
-          pos += (v.x > c ? 1u : 0u) + (v.y > c ? 1u : 0u);
+      // positions from sorted 32-entry chunks (round 2): every thread keeps its elements'
+      // composites in registers, every warp sorts 32-entry chunks of the survivors' and of the
+      // running requests' composites in place (bitonic, shuffles), and an element's position is
+      // the number of larger composites, summed over the chunks by binary searches: O(n log 32)
+      // per element instead of the O(n) count (4 us per CTA)
+      {
+        const uint32_t lane = tid & 31, wid = tid >> 5;
+        constexpr uint32_t kPer = (kCandCap + kSelThreads - 1) / kSelThreads;  // survivors per thread
+        unsigned long long cs[kPer];
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+          const uint32_t e = tid + u * kSelThreads;
+          cs[u] = e < ns ? s_all[e] : 0ull;
         }
-        if (pos < k) {
-          s_key[pos] = c;
-          s_idx[pos] = s_ri[e] & 0x7FFFFFFFu;
-          s_run8[pos] = (uint8_t)(s_ri[e] >> 31);
-          s_gf[pos] = s_gall[e];
-          s_lsel[pos] = le;
+        const uint32_t tr = kSelThreads - 1 - tid;  // this thread's running request (top down)
+        const unsigned long long cr = (rpre && tr < n_run) ? s_rk[tr] : 0ull;
+        __syncthreads();
+        const uint32_t nch_s = (ns + 31) >> 5, nch_r = rpre ? (n_run + 31) >> 5 : 0u;
+#pragma unroll 1
+        for (uint32_t ch = wid; ch < nch_s + nch_r; ch += kSelThreads / 32) {
+          const bool sv = ch < nch_s;
+          const uint32_t e = (sv ? ch : ch - nch_s) * 32 + lane;
+          unsigned long long* const arr = sv ? s_all : s_rk;
+          const unsigned long long c = e < (sv ? ns : n_run) ? arr[e] : 0ull;
+          arr[e] = warp_sort_desc(c);  // (chunk padding 0: never larger)
         }
-      }
-      if (rpre) {
-        // the running requests in ascending composite order at B (the victim order, reading
-        // R18, is a prefix of it) with the prefix sums of their l, by rank counting on the
-        // threads from the top down (they overlap the survivors' counting above)
-        for (uint32_t t = kSelThreads - 1 - tid; t < n_run; t += kSelThreads) {
-          const unsigned long long c = s_rk[t];
+        __syncthreads();
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+          const uint32_t e = tid + u * kSelThreads;
+          if (e >= ns) break;
+          const unsigned long long c = cs[u];
+          const uint32_t le = __ldcg(&w.cand_st[e].l);  // its l for the walk
           uint32_t pos = 0;
-          unsigned long long cum = 0;
-#pragma unroll 4
-          for (uint32_t f = 0; f < n_run; ++f) {
-            const unsigned long long v = s_rk[f];
-            pos += v < c ? 1u : 0u;
-            cum += v <= c ? (unsigned long long)s_rl[f] : 0ull;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < nch_s; ++ch) pos += count_gt32(s_all + 32 * ch, c);
+          if (pos < k) {
+            s_key[pos] = c;
+            s_idx[pos] = s_ri[e] & 0x7FFFFFFFu;
+            s_run8[pos] = (uint8_t)(s_ri[e] >> 31);
+            s_gf[pos] = s_gall[e];
+            s_lsel[pos] = le;
           }
-          s_vc[kRunOrdAt + pos] = cum;
-          s_idx[kRunOrdAt + pos] = t;
+        }
+        if (rpre) {
+          // ascending position = n_run - 1 - (number of larger composites); l placed by position
+          if (tr < n_run) {
+            uint32_t gt = 0;
+#pragma unroll 1
+            for (uint32_t ch = 0; ch < nch_r; ++ch) gt += count_gt32(s_rk + 32 * ch, cr);
+            const uint32_t pos = n_run - 1u - gt;
+            s_idx[kRunOrdAt + pos] = tr;
+            s_vc[kRunOrdAt + pos] = s_rl[tr];
+          }
+          __syncthreads();
+          if (wid == 0) {  // inclusive prefix sums of l in ascending order (per lane, then a warp scan)
+            const uint32_t per = (n_run + 31) >> 5, q0 = lane * per, q1 = min(q0 + per, n_run);
+            unsigned long long part = 0;
+            for (uint32_t q = q0; q < q1; ++q) part += s_vc[kRunOrdAt + q];
+            unsigned long long inc = part;
+            for (int o = 1; o < 32; o <<= 1) {
+              const unsigned long long u2 = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= (uint32_t)o) inc += u2;
+            }
+            unsigned long long run = inc - part;
+            for (uint32_t q = q0; q < q1; ++q) {
+              run += s_vc[kRunOrdAt + q];
+              s_vc[kRunOrdAt + q] = run;
+            }
+          }
         }
       }
       __syncthreads();
