@@ -177,7 +177,9 @@ typedef struct {
      * 4 export_preempt the next batch as an index list -- the requests served after the decision,
      * scalars[ANDES_SC_REALIZED] of them (kept running ones, then admits), at most export_served
      * -- which the engine runs and which can feed the next andes_tracker_append_dev directly
-     * (idx = that list, count = the realized scalar).  NULL: no export. */
+     * (idx = that list, count = the realized scalar), and last, 8-byte aligned after the list,
+     * a completion word set to 1 behind a system-scope fence: a host that clears it before the
+     * call may poll it instead of synchronising the stream.  NULL: no export. */
     void *export_host;
     uint32_t export_preempt;
     uint32_t export_served;

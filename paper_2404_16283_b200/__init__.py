@@ -244,8 +244,20 @@ class Decision:
 
 
 def decision_export_bytes(B_cap, export_preempt, export_served=0):
-    """Size of an AndesDecision.export_host buffer (include/andes.h)."""
-    return 32 + 12 * int(B_cap) + 4 * int(export_preempt) + 4 * int(export_served)
+    """Size of an AndesDecision.export_host buffer (include/andes.h), completion word included."""
+    return _export_done_offset(B_cap, export_preempt, export_served) + 8
+
+
+def _export_done_offset(B_cap, export_preempt, export_served):
+    return (32 + 12 * int(B_cap) + 4 * int(export_preempt) + 4 * int(export_served) + 7) // 8 * 8
+
+
+def decision_export_done(buf, B_cap, export_preempt, export_served=0):
+    """numpy view (u64[1]) of the export's completion word: clear it before the call, poll it
+    instead of a stream sync."""
+    import numpy as np
+    o = _export_done_offset(B_cap, export_preempt, export_served)
+    return buf.numpy()[o:o + 8].view(np.uint64)
 
 
 def decision_export_views(buf, B_cap, export_preempt, export_served=0):

@@ -150,10 +150,20 @@ __global__ void k_decision_export(const uint32_t* __restrict__ scalars, const in
     if (nk + q < smax) h_srv[nk + q] = __ldcg(admit + q);
 }
 
+// the export's completion word (after every section): the kernel's last store, behind a
+// system-scope fence, so a host that polls it may read the block without a stream sync
+__global__ void k_decision_export_done(unsigned long long* flag, unsigned long long v) {
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(flag) = v;
+}
+
 void launch_decision_export(const LaunchCfg& L, const SchedOut& o, const Work& w, uint32_t B_cap, uint32_t pmax,
                             uint32_t smax, void* host) {
   k_decision_export<<<1, 256, 0, L.stream>>>(o.scalars, o.V, o.admit_idx, o.preempt_idx, o.serve_mask, w, B_cap, pmax,
                                              smax, static_cast<unsigned char*>(host));
+  const size_t off = 32 + 12 * (size_t)B_cap + 4 * (size_t)pmax + 4 * (size_t)smax;
+  k_decision_export_done<<<1, 1, 0, L.stream>>>(
+      reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(host) + ((off + 7) & ~size_t(7))), 1ull);
 }
 
 }  // namespace andes

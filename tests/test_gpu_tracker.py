@@ -219,6 +219,9 @@ def test_decision_export_zero_copy(A):
                            flags=flags, export_host=buf, export_preempt=pmax, export_served=smax, now_dev=hnow)
         torch.cuda.synchronize()
         sc, V, adm, pre, srv = A.decision_export_views(buf, 256, pmax, smax)
+        done = A.decision_export_done(buf, 256, pmax, smax)
+        assert int(done[0]) == 1
+        done[0] = 0
         dsc = out.scalars.cpu().numpy().view(np.uint32)
         np.testing.assert_array_equal(sc, dsc)
         np.testing.assert_array_equal(V, out.V.cpu().numpy())
