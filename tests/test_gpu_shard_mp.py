@@ -103,13 +103,13 @@ def test_sharded_decision_two_processes(orc, name, cap, flags):
         assert_decision_equal(dict(got[r], mask=mask), o)
 
 
-@pytest.mark.parametrize("name,cap,flags", [("config2", 16, 1), ("config3", 16, 1)])
-def test_sharded_decision_two_processes_peer_memory(orc, name, cap, flags):
-    """The same two-process decision with the four exchanges done on the device by andes_comm (CUDA
-    IPC: every rank stores its block into every peer's arena and publishes a flag; no host
-    staging, no NCCL), compared with the oracle."""
+@pytest.mark.parametrize("name,cap,flags,world", [("config2", 16, 1, 2), ("config3", 16, 1, 2),
+                                                  ("config2", 0xFFFFFFFF, 1 | 16, 3)])
+def test_sharded_decision_two_processes_peer_memory(orc, name, cap, flags, world):
+    """The same multi-process decision with the four exchanges done on the device by andes_comm
+    (CUDA IPC: every rank stores its block into every peer's arena and publishes a flag; no host
+    staging, no NCCL), compared with the oracle; two and three processes (uneven shards)."""
     import torch.multiprocessing as mp
-    world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
