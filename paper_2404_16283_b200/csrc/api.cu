@@ -191,11 +191,20 @@ int pool_map(AndesCtx* c, const uint32_t* pool, uint64_t len, const CUtensorMap*
   return ANDES_OK;
 }
 
-// per-call reset of the small globals and the look-back status words
+// per-call reset of the small globals (both lines: + the fused kernel's barrier line); the
+// look-back status words are zeroed by k_prep, tile by tile.  A one-CTA kernel rather than a
+// memset node: the call's first kernel then launches programmatically behind it (decision
+// -0.5 us; ANDES_RESET_MEMSET restores the memset for A/B)
 int reset_call(AndesCtx* c, cudaStream_t s) {
-  // (the look-back status words are zeroed by k_prep, tile by tile)
-  cudaError_t e = cudaMemsetAsync(c->w.g, 0, 2 * sizeof(Globals), s);  // + the fused kernel's barrier line
+#ifndef ANDES_RESET_MEMSET
+  Work w = c->w;
+  w.now_dev = nullptr;
+  launch_reset_now(cfg_of(c, s), w);
+  return cuda_check(c, cudaGetLastError(), "reset");
+#else
+  cudaError_t e = cudaMemsetAsync(c->w.g, 0, 2 * sizeof(Globals), s);
   return cuda_check(c, e, "memset");
+#endif
 }
 
 inline void mark(AndesCtx* c, int i, cudaStream_t s) {

@@ -361,6 +361,11 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 
 // segmented max monoid on (flag, value): combine(a, b) with a earlier than b
 __device__ __forceinline__ unsigned long long seg_combine(unsigned long long a, unsigned long long b) {
@@ -907,32 +912,78 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   // (gi < nmin, warp-uniform) run unpredicated; the few that only some lanes have, predicated.
   const uint32_t nmin = min(gmax, __reduce_min_sync(0xffffffffu, active ? nfull : 0xFFFFFFFFu));
   uint32_t a = Is - P;
-  if (kHead && hn) {
-    a = max(a + P, h0);
-    if (hn > 1u) a = max(a + P, h1);
-    if (hn > 2u) a = max(a + P, h2);
-  }
+  // Two-tile units (large pools) and FINAL mode: pass 1 also sums T~(0) = min(A(0), t) over the
+  // valid tokens (mod 2^32), and pass 2 is skipped wherever the carry does not change A (below).
+  // One-tile units (the decision's 64K-request scan) keep the plain two passes: there the extra
+  // pass-1 work measured slower (decision +1 us) than the skipped pass saves.
+#ifndef ANDES_NO_P2SKIP
+  constexpr bool kSkip = TW == 2 || kFinal;
+#else
+  constexpr bool kSkip = false;
+#endif
+  uint32_t s0 = 0u, d1 = 0u;  // (kSkip) the zero-carry sum; the sub-range's first token
+  if constexpr (kSkip) {
+    d1 = active ? ld_shared_u32(tile_s + ((uint32_t)xs << 2)) : 0u;
+    if (kHead && hn) {
+      a = max(a + P, h0);
+      s0 = min(a, tcl);
+      if (hn > 1u) {
+        a = max(a + P, h1);
+        s0 += min(a, tcl);
+      }
+      if (hn > 2u) {
+        a = max(a + P, h2);
+        s0 += min(a, tcl);
+      }
+    }
 #pragma unroll kTokUnroll
-  for (uint32_t gi = 0; gi < nmin; ++gi) {
-    const uint4 v = ld_shared_v4(a0 + (gi << 4));
-    a = max(a + P, v.x);
-    a = max(a + P, v.y);
-    a = max(a + P, v.z);
-    a = max(a + P, v.w);
-  }
-  for (uint32_t gi = nmin; gi < gmax; ++gi) {
-    if (gi < nfull) {
+    for (uint32_t gi = 0; gi < nmin; ++gi) {
+      const uint4 v = ld_shared_v4(a0 + (gi << 4));
+      const uint32_t A0 = max(a + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+      a = A3;
+      s0 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+    }
+    for (uint32_t gi = nmin; gi < gmax; ++gi) {
+      if (gi < nfull) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        const uint32_t A0 = max(a + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
+        a = A3;
+        s0 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+      }
+    }
+    if (ntail) {
+      const uint32_t A0 = max(a + P, t0), A1 = max(A0 + P, t1), A2 = max(A1 + P, t2);
+      s0 += min(A0, tcl) + (ntail > 1 ? min(A1, tcl) : 0u) + (ntail > 2 ? min(A2, tcl) : 0u);
+      a = A2;
+    }
+  } else {
+    if (kHead && hn) {
+      a = max(a + P, h0);
+      if (hn > 1u) a = max(a + P, h1);
+      if (hn > 2u) a = max(a + P, h2);
+    }
+#pragma unroll kTokUnroll
+    for (uint32_t gi = 0; gi < nmin; ++gi) {
       const uint4 v = ld_shared_v4(a0 + (gi << 4));
       a = max(a + P, v.x);
       a = max(a + P, v.y);
       a = max(a + P, v.z);
       a = max(a + P, v.w);
     }
-  }
-  if (ntail) {
-    a = max(a + P, t0);
-    a = max(a + P, t1);
-    a = max(a + P, t2);
+    for (uint32_t gi = nmin; gi < gmax; ++gi) {
+      if (gi < nfull) {
+        const uint4 v = ld_shared_v4(a0 + (gi << 4));
+        a = max(a + P, v.x);
+        a = max(a + P, v.y);
+        a = max(a + P, v.z);
+        a = max(a + P, v.w);
+      }
+    }
+    if (ntail) {
+      a = max(a + P, t0);
+      a = max(a + P, t1);
+      a = max(a + P, t2);
+    }
   }
   const uint32_t nslots = hn + 4u * nfull + (ntail ? 3u : 0u);  // processed token slots
   const uint32_t dz = nslots ? a - (Is + (nslots - 1u) * P) : 0u;
@@ -973,6 +1024,60 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   uint32_t Ac = Is - P + carry;
   const uint32_t nn_all = active ? (uint32_t)max(xe - xs, 0) : 0u;
   const bool fits32 = __all_sync(0xffffffffu, (unsigned long long)nn_all * max(dz, carry) < (1ull << 32));
+  if (kSkip && fits32) {
+    // The lateness with carry c is max(c, L(0)), L(0) the zero-carry lateness (nondecreasing from
+    // L1 at the first token to dz at the last), so per lane:
+    //   c <= L1   A(c) = A(0) at every token: the sum is pass 1's s0;
+    //   c >= dz   A(c) = I + c at every token: closed form, the clamp point by one division;
+    //   else      A(c) = A(0) from the first token with A(0) >= I + c on: walk up to it only,
+    //             correcting s0 by min(I + c, t) - min(A(0), t) per token.
+    // (warp-uniform branch: fits32 bounds every sum below 2^32, as for pass 2)
+    const uint32_t L1 = max(d1, Is) - Is;
+    const bool ca = carry <= L1, cb = !ca && carry >= dz;
+    bool need = nn_all != 0u && !ca && !cb;
+    uint32_t fix = 0u;
+    if (__any_sync(0xffffffffu, need)) {
+      uint32_t A0 = Is - P, Ic = Is - P + carry, x = (uint32_t)xs;
+      while (__any_sync(0xffffffffu, need)) {
+        if (need) {
+          const uint32_t d = ld_shared_u32(tile_s + (x << 2));
+          A0 = max(A0 + P, d);
+          Ic += P;
+          if (A0 >= Ic) {
+            need = false;
+          } else {
+            fix += min(Ic, tcl) - min(A0, tcl);
+            need = ++x < (uint32_t)xe;
+          }
+        }
+      }
+    }
+    if (nn_all) {
+      const uint32_t nn = nn_all;
+      unsigned long long dsum;
+      if (cb) {
+        const uint32_t b0 = Is + carry;  // consumption time of the first token
+        uint32_t k;                      // tokens consumed by t
+        if (b0 + (nn - 1u) * P <= tcl) k = nn;
+        else if (b0 > tcl) k = 0u;
+        else k = min(nn, (tcl - b0) / P + 1u);
+        const unsigned long long kk = k, n2 = nn;
+        dsum = kk * carry + (n2 - kk) * (unsigned long long)(tcl - Is) -
+               (unsigned long long)P * (((n2 * (n2 - 1ull)) >> 1) - ((kk * (kk - 1ull)) >> 1));
+      } else {
+        const unsigned long long sumI =
+            (unsigned long long)nn * Is + (unsigned long long)P * (((unsigned long long)nn * (nn - 1)) >> 1);
+        dsum = (unsigned long long)(uint32_t)(s0 + fix - (uint32_t)sumI);
+      }
+      if (dsum) atomicAdd(&w.spre[qridx], dsum);
+      if (qek && xe == qvend) {
+        const uint32_t Il = qA + (uint32_t)(xe - 1) * P;
+        const uint32_t A_last = Il + max(carry, dz);
+        w.edge[qridx] = (qek == 1u) ? A_last - Il : min(A_last, tcl) - Il;
+      }
+    }
+    return;
+  }
 #ifndef ANDES_NO_NOCLAMP
   // consumption times are nondecreasing, so the clamp min(A, t) is void for the whole warp when
   // every lane's last one, I_last + max(L_end, carry), is <= t (warp-uniform loop choice)

@@ -94,14 +94,15 @@ void launch_tracker_append(const LaunchCfg& L, const TrackerView& t, const uint3
     k_tracker_append<<<blocks, kTrackThreads, 0, L.stream>>>(t, idx, t_abs, count, count_dev, serve_mask, w);
 }
 
-// The per-call reset of a now_dev decision (instead of the memset node): zero both lines of the
-// call's globals, then read the decision time ONCE -- it may sit in mapped host memory, where every
+// The per-call reset of a decision (instead of a memset node, which no programmatic launch can
+// overlap): zero both lines of the call's globals; with now_dev, then read the decision time ONCE -- it may sit in mapped host memory, where every
 // read is a PCIe round trip serialised at the host -- and publish the shift for every kernel.
 __global__ void k_reset_now(Work w, const long long* now_dev, long long now_ref) {
   uint32_t* g = reinterpret_cast<uint32_t*>(w.g);
   for (uint32_t q = threadIdx.x; q < 2 * sizeof(Globals) / 4; q += blockDim.x) g[q] = 0u;
   __syncthreads();
-  if (threadIdx.x == 0) globals2(w)->tshift = *reinterpret_cast<const volatile long long*>(now_dev) - now_ref;
+  if (threadIdx.x == 0 && now_dev)
+    globals2(w)->tshift = *reinterpret_cast<const volatile long long*>(now_dev) - now_ref;
 }
 
 void launch_reset_now(const LaunchCfg& L, const Work& w) {

@@ -1,5 +1,6 @@
 """Internal timeline of one config-3 decision from %globaltimer stamps (andes_debug_trace).
 Tile / first-tile stamps need a -DANDES_SCAN_PHASES build (ANDES_LIB_PATH).
+FLUSH=1: a 256 MB write before every replay (the bench's L2-flushed timing).
 Slots: 7000+2b prep CTA b start/end; 5000+2b scan CTA b start/end; 2300 bounds end (scan CTA 0);
 3000+2b state CTA b; 2200/2201 state last block; 0+2b select CTA b; 2100.. finalize phases."""
 import ctypes as C
@@ -36,7 +37,10 @@ if os.environ.get("GRAPH", "1") == "1":
         with torch.cuda.graph(g, stream=s):
             ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=16, out=out,
                          stream=s)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         for _ in range(3):
+            if os.environ.get("FLUSH") == "1":  # L2 flushed before each replay, as the bench times it
+                flush.zero_()
             g.replay()
     s.synchronize()
 tr = np.zeros(1 << 16, np.uint64)
