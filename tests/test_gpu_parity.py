@@ -551,6 +551,41 @@ for align in (4, 1):
 snap = W.config3()
 _check_qoe(A, ctx, oracle, snap, snap.now_us + snap.horizon_us, False)
 _check_sched(A, ctx, oracle, W.config2(), cap=16)
+# the three carry cases of the two-tile pass-2 skip (scan.cu, warp_tile_aligned): timelines
+# delivered ahead of consumption (clamped at t), late then faster than the period (the carry
+# dominates: closed form), lateness oscillating by +-P (the zero-carry lateness catches up inside
+# a sub-range: partial walk), slowly growing lateness with jitter
+rng = np.random.default_rng(7)
+n = 96
+P = rng.choice([20_000, 50_000, 208_333], n).astype(np.int64)
+ttft = rng.choice([0, 1_000_000], n).astype(np.int64)
+tls = []
+for i in range(n):
+    g = int(rng.integers(1, 6000))
+    j = np.arange(g, dtype=np.int64)
+    kind = i % 4
+    if kind == 0:
+        d = ttft[i] + j * (P[i] // 4)
+    elif kind == 1:
+        d = ttft[i] + 5 * P[i] + j * (P[i] * 3 // 4)
+    elif kind == 2:
+        d = ttft[i] + j * P[i] + rng.integers(-P[i], P[i] + 1, g)
+    else:
+        d = ttft[i] + j * (P[i] * 11 // 10) + rng.integers(-P[i] // 3, P[i] // 3 + 1, g)
+    tls.append(np.maximum.accumulate(np.maximum(d, 0)).astype(np.uint32))
+# each request evaluated shortly after its last delivery (its late tokens then clamp at t)
+now = 1 << 31
+arr = np.array([now - int(t[-1]) - int(rng.integers(0, 2 * P[i])) for i, t in enumerate(tls)], np.int64)
+for align in (4, 1):
+    g, base, pool = W._pack(tls, align)
+    snap = W.Snapshot(arrival_us=arr, ttft_us=ttft.astype(np.uint32), period_us=P.astype(np.uint32),
+                      ctx_len=rng.integers(1, 4096, n).astype(np.uint32), n_deliv=g,
+                      max_total=np.full(n, W.UINT32_MAX, np.uint32), start_off_us=np.zeros(n, np.uint32),
+                      rank=np.arange(n, dtype=np.uint32), running=np.zeros(n, np.uint8), tl_base=base, tl_pool=pool,
+                      now_us=now, horizon_us=2_000_000)
+    for ev in (snap.now_us, snap.now_us + snap.horizon_us):
+        _check_qoe(A, ctx, oracle, snap, ev, False)
+    _check_qoe(A, ctx, oracle, snap, snap.now_us, True)
 print("tw2 ok")
 """
 
@@ -559,7 +594,8 @@ print("tw2 ok")
 def test_scan_unit_width_forced(tw):
     """The scan's work unit is two warp-tiles (2048 tokens) on large pools and one on small ones;
     ANDES_SCAN_TW forces either, so both are checked against the oracle on the same inputs
-    (aligned and unaligned pools, long requests, config 3, a config-2 decision)."""
+    (aligned and unaligned pools, long requests, config 3, a config-2 decision, and timelines
+    built for the three carry cases of the two-tile pass-2 skip)."""
     import os
     import subprocess
     import sys
