@@ -25,6 +25,10 @@ constexpr int kPrepThreads = 256;
 #define ANDES_TOK_UNROLL 4
 #endif
 constexpr int kTokUnroll = ANDES_TOK_UNROLL;  // unroll of the aligned path's token loops
+#ifndef ANDES_STATIC_PCT
+#define ANDES_STATIC_PCT 95
+#endif
+constexpr uint32_t kStaticPct = ANDES_STATIC_PCT;  // share of the scan's chunks assigned statically
 
 __device__ __forceinline__ void bounds_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kScanThreads) : "memory"); }
 
@@ -1253,15 +1257,20 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   const uint32_t nchunks = (nunits + CH - 1) / CH;
   // lane 0's generator state (position, chunk end, claimed chunk) lives in shared memory: it is
   // touched once per tile and would otherwise hold registers across the whole tile body
-  __shared__ uint32_t s_gen[kScanThreads / 32][3];
+  __shared__ uint32_t s_gen[kScanThreads / 32][4];
   uint32_t* const gs = s_gen[wid];
-  // claims: chunk sw then chunk KS + sw are static (sw: the warp's index among the KS static
-  // warps), later ones come from the counter (+ 2 KS); the counter's result is first needed a
-  // whole tile after it is asked.  CTA 0 of a decision computes the bounds first: its warps
-  // claim from the counter only (static chunks there would start last and form the tail).
+  // claims: a warp's first R chunks are static (chunk sw + r KS, r < R; sw: the warp's index
+  // among the KS static warps), later ones come from the counter (+ R KS); the counter's result
+  // is first needed a whole tile after it is asked.  R = 2 on small pools; on large ones the
+  // static rounds cover ~kStaticPct % of the chunks, 95 (the counter's same-address round trips
+  // held ~10% of the 2^20 scan's stall samples; the dynamic rest still balances the tail).
+  // CTA 0 of a decision computes the bounds first: its warps claim from the counter only
+  // (static chunks there would start last and form the tail).
   const uint32_t cta0_dyn = (A.sched && blockIdx.x == 0) ? 1u : 0u;
   const uint32_t KS = KW - (A.sched ? (kScanThreads / 32) : 0u);
-  auto gen = [&](bool static_next) -> uint32_t {
+  const uint32_t R = max(2u, (uint32_t)(((unsigned long long)nchunks * kStaticPct / 100u) / KS));
+  const uint32_t Rw = cta0_dyn ? 0u : R;
+  auto gen = [&]() -> uint32_t {
     const uint32_t g_t = gs[0], g_hi = gs[1], g_nxt = gs[2];
     if (g_t + 1 < g_hi) {
       gs[0] = g_t + 1;
@@ -1273,7 +1282,9 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     const uint32_t t0 = (nchunks - 1u - g_nxt) * CH;
     gs[0] = t0;
     gs[1] = min(t0 + CH, nunits);
-    gs[2] = static_next ? g_nxt + KS : atomicAdd(A.tile_ctr, 1u) + 2u * KS;
+    const uint32_t c = gs[3] + 1u;  // chunks this warp has started
+    gs[3] = c;
+    gs[2] = c < Rw ? g_nxt + KS : atomicAdd(A.tile_ctr, 1u) + R * KS;
     return t0 | kStart;
   };
   uint32_t cur = kNone, s1 = kNone;
@@ -1285,16 +1296,17 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     // two TMA copies
     gs[0] = kNone;
     gs[1] = 0u;
-    gs[2] = cta0_dyn ? atomicAdd(A.tile_ctr, 1u) + 2u * KS
+    gs[3] = 0u;
+    gs[2] = cta0_dyn ? atomicAdd(A.tile_ctr, 1u) + R * KS
                      : (blockIdx.x - (A.sched ? 1u : 0u)) * (kScanThreads / 32) + wid;
-    cur = gen(!cta0_dyn);
+    cur = gen();
     if (cur != kNone) {
       mbar_expect_tx_s(bar_s, TW * kWTile * 4u);
 #pragma unroll
       for (int h = 0; h < TW; ++h)
         tma_tile(pmap, wbase + h * kWTile * 4, ((cur & ~kStart) * TW + h) * (kWTile / 32), bar_s);
     }
-    s1 = gen(false);
+    s1 = gen();
     if (TW == 1 && s1 != kNone) {
       mbar_expect_tx_s(bar_s + 8u, kWTile * 4u);
       tma_tile(pmap, wbase + kWTile * 4, (s1 & ~kStart) * (kWTile / 32), bar_s + 8u);
@@ -1486,7 +1498,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
     MetaLite tm2{0u, 0u, 0u};
     uint32_t r_end2 = 0;
     if (lane == 0) {
-      const uint32_t s2 = gen(false);
+      const uint32_t s2 = gen();
       if (TW == 1 && s2 != kNone) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx_s(bar_s + 8u * buf, kWTile * 4u);
