@@ -428,15 +428,21 @@ int andes_qoe_eval(AndesCtx* c, const AndesRequests* req, int64_t eval_time_us, 
   // profiled stages: [0] prep, [1] timeline scan, [2] QoE finalize (others empty)
   mark(c, 0, s);
   if ((rc = reset_call(c, s))) return rc;
-  // FINAL mode: the scan builds its records from the request table (no prep copy; measured
-  // -5 us on 2^20 requests); INFLIGHT keeps prep's records (the due-token division at use time
-  // made the scan slower there, 149.5 -> 155.6 us)
-  launch_prep(L, r, w, eval_time_us, fin, false, 0, false, nullptr, 0, false, fin);
+  // the scan builds its records from the request table (no prep copy): FINAL -5 us on 2^20
+  // requests; INFLIGHT since the static chunk claims too (whole call 194.6 -> 186.7 us; before
+  // them the due-token division at use time had made the scan slower, 149.5 -> 155.6 us).
+  // ANDES_SREC_INFLIGHT restores prep's records for A/B
+#ifdef ANDES_SREC_INFLIGHT
+  const bool raw = fin;
+#else
+  const bool raw = true;
+#endif
+  launch_prep(L, r, w, eval_time_us, fin, false, 0, false, nullptr, 0, false, raw);
   mark(c, 1, s);
   {
     const CUtensorMap* tm = nullptr;
     if (r.n && (rc = pool_map(c, r.tl_pool, r.tl_len, &tm))) return rc;
-    launch_scan(L, r, w, eval_time_us, fin, tm, false, nullptr, 0, 0, 0, 0, false, false, 0, fin);
+    launch_scan(L, r, w, eval_time_us, fin, tm, false, nullptr, 0, 0, 0, 0, false, false, 0, raw);
   }
   mark(c, 2, s);
   launch_qoe_final(L, r, w, eval_time_us, fin, out->q, out->q64, out->s_delay, out->s_whole, out->m);
