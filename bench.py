@@ -823,6 +823,24 @@ def run_ours(args):
             b.synchronize()
             if k >= max(args.warmup, 3):
                 c_ms.append(a.elapsed_time(b))
+    # the same call asking for the QoE only (AndesQoeOut.q; the other outputs NULL), and the
+    # FINAL-mode evaluation (whole timelines, no clamp: the config-5 sweep's mode)
+    def _whole_call(mode, outputs):
+        ms = []
+        with torch.cuda.stream(stream):
+            for k in range(max(args.warmup, 3) + 10):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                qctx.qoe_eval(breq, big.n, big.now_us + big.horizon_us, mode, stream=stream, outputs=outputs)
+                b.record(stream)
+                b.synchronize()
+                if k >= max(args.warmup, 3):
+                    ms.append(a.elapsed_time(b))
+        return statistics.median(ms)
+    q_only_ms = _whole_call(A.ANDES_EVAL_INFLIGHT, ("q",))
+    final_ms = _whole_call(A.ANDES_EVAL_FINAL, None)
     qctx.profile_enable(True)
     qoe_ms = statistics.median(c_ms)
     qbytes = 4 * big.n_tokens + 44 * big.n
@@ -832,12 +850,18 @@ def run_ours(args):
                 "pool_tokens": big.n_tokens, "ms_per_eval": qoe_ms, "scan_ms": scan_ms,
                 "stage_sum_ms_profiled": stage_sum_ms,
                 "whole_call_frac": qbytes / (qoe_ms / 1e3) / 1e9 / hbm_peak,
+                "whole_call_q_only": {"ms_per_eval": q_only_ms, "frac": qbytes / (q_only_ms / 1e3) / 1e9 / hbm_peak,
+                                      "note": "the same call with only AndesQoeOut.q requested (q64, S_delay, "
+                                              "S_whole, m NULL)"},
+                "whole_call_final_mode": {"ms_per_eval": final_ms,
+                                          "frac": qbytes / (final_ms / 1e3) / 1e9 / hbm_peak,
+                                          "note": "ANDES_EVAL_FINAL (every delivered token, no clamp), all outputs"},
                 "roofline": {"kernel": "k_qoe_scan", "bound": "hbm", "achieved": q_ach, "peak": hbm_peak,
                              "unit": "GB/s", "frac": q_ach / hbm_peak,
                              "traffic": _ncu_traffic().get("k_qoe_scan_2p20"),
                              "algorithmic_bytes_per_launch": qbytes, "peak_source": hbm_src}}
     # the same population with unaligned timelines (packed back to back, align 1): the scan's
-    # row-per-lane event path (128B-swizzled tiles) instead of the aligned piece-parallel path
+    # piece-parallel path with head groups (a sub-range's first <= 3 tokens up to a 16-byte boundary)
     import workloads as W
     ubig = _tile(W.config3().subset(np.arange(snap.n), align=1), 16)
     ureq = A.requests_to(ubig, device=dev)
@@ -852,10 +876,10 @@ def run_ours(args):
     u_scan = statistics.median([s_[1] for s_ in u_ms])
     ubytes = 4 * ubig.n_tokens + 44 * ubig.n
     qoe_eval["unaligned_pool"] = {
-        "path": "row-per-lane event path (timelines packed back to back, 128B-swizzled TMA tiles)",
+        "path": "timelines packed back to back (align 1): the piece-parallel path with head groups on plain TMA tiles",
         "pool_tokens": ubig.n_tokens, "scan_ms": u_scan,
         "ms_per_eval": statistics.median([s_[0] + s_[1] + s_[2] for s_ in u_ms]),
-        "roofline": {"kernel": "k_qoe_scan (row path)", "bound": "hbm", "achieved": ubytes / (u_scan / 1e3) / 1e9,
+        "roofline": {"kernel": "k_qoe_scan (head groups)", "bound": "hbm", "achieved": ubytes / (u_scan / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s", "frac": ubytes / (u_scan / 1e3) / 1e9 / hbm_peak,
                      "algorithmic_bytes_per_launch": ubytes}}
     del qctx, breq, ureq

@@ -312,15 +312,21 @@ class Context:
         return list(buf)
 
     # -- andes_qoe_eval
-    def qoe_eval(self, req: dict, n: int, eval_time_us: int, mode=ANDES_EVAL_INFLIGHT, stream=None):
+    _QOE_OUTPUTS = ("q", "q64", "s_delay", "s_whole", "m")
+
+    def qoe_eval(self, req: dict, n: int, eval_time_us: int, mode=ANDES_EVAL_INFLIGHT, stream=None, outputs=None):
+        """(q f32, q64 f64, s_delay i64, s_whole i64, m i32) per request; `outputs` (a subset of
+        _QOE_OUTPUTS, default all) selects which the call writes -- the others are NULL in
+        AndesQoeOut and come back as None."""
         torch = _torch()
         dev = self.device
-        q = torch.empty(n, dtype=torch.float32, device=dev)
-        q64 = torch.empty(n, dtype=torch.float64, device=dev)
-        sd = torch.empty(n, dtype=torch.int64, device=dev)
-        sw = torch.empty(n, dtype=torch.int64, device=dev)
-        m = torch.empty(n, dtype=torch.int32, device=dev)
-        out = QoeOut(_ptr(q), _ptr(q64), _ptr(sd), _ptr(sw), _ptr(m))
+        want = set(self._QOE_OUTPUTS if outputs is None else outputs)
+        if not want <= set(self._QOE_OUTPUTS):
+            raise ValueError(f"unknown qoe_eval outputs {sorted(want - set(self._QOE_OUTPUTS))}")
+        dt = {"q": torch.float32, "q64": torch.float64, "s_delay": torch.int64, "s_whole": torch.int64, "m": torch.int32}
+        t = {k: (torch.empty(n, dtype=dt[k], device=dev) if k in want else None) for k in self._QOE_OUTPUTS}
+        q, q64, sd, sw, m = (t[k] for k in self._QOE_OUTPUTS)
+        out = QoeOut(*[(_ptr(x) if x is not None else None) for x in (q, q64, sd, sw, m)])
         self._check(lib().andes_qoe_eval(self._h, C.byref(_req_struct(req, n)), int(eval_time_us), int(mode),
                                          C.byref(out), _stream_ptr(stream)), "andes_qoe_eval")
         return q, q64, sd, sw, m
