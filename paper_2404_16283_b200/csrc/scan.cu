@@ -926,18 +926,26 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   constexpr bool kSkip = false;
 #endif
   uint32_t s0 = 0u, d1 = 0u;  // (kSkip) the zero-carry sum; the sub-range's first token
+  // kUnc: pass 1 sums A(0) unclamped (two adds per four tokens instead of four mins more); the
+  // sum is then used only where no token of the sub-range reaches past t (below)
+#ifndef ANDES_CLAMPED_S0
+  constexpr bool kUnc = true;
+#else
+  constexpr bool kUnc = false;
+#endif
+  auto cl = [&](uint32_t x) -> uint32_t { return kUnc ? x : min(x, tcl); };
   if constexpr (kSkip) {
     d1 = active ? ld_shared_u32(tile_s + ((uint32_t)xs << 2)) : 0u;
     if (kHead && hn) {
       a = max(a + P, h0);
-      s0 = min(a, tcl);
+      s0 = cl(a);
       if (hn > 1u) {
         a = max(a + P, h1);
-        s0 += min(a, tcl);
+        s0 += cl(a);
       }
       if (hn > 2u) {
         a = max(a + P, h2);
-        s0 += min(a, tcl);
+        s0 += cl(a);
       }
     }
 #pragma unroll kTokUnroll
@@ -945,19 +953,19 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
       const uint4 v = ld_shared_v4(a0 + (gi << 4));
       const uint32_t A0 = max(a + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
       a = A3;
-      s0 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+      s0 += cl(A0) + cl(A1) + cl(A2) + cl(A3);
     }
     for (uint32_t gi = nmin; gi < gmax; ++gi) {
       if (gi < nfull) {
         const uint4 v = ld_shared_v4(a0 + (gi << 4));
         const uint32_t A0 = max(a + P, v.x), A1 = max(A0 + P, v.y), A2 = max(A1 + P, v.z), A3 = max(A2 + P, v.w);
         a = A3;
-        s0 += min(A0, tcl) + min(A1, tcl) + min(A2, tcl) + min(A3, tcl);
+        s0 += cl(A0) + cl(A1) + cl(A2) + cl(A3);
       }
     }
     if (ntail) {
       const uint32_t A0 = max(a + P, t0), A1 = max(A0 + P, t1), A2 = max(A1 + P, t2);
-      s0 += min(A0, tcl) + (ntail > 1 ? min(A1, tcl) : 0u) + (ntail > 2 ? min(A2, tcl) : 0u);
+      s0 += cl(A0) + (ntail > 1 ? cl(A1) : 0u) + (ntail > 2 ? cl(A2) : 0u);
       a = A2;
     }
   } else {
@@ -1031,15 +1039,23 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   if (kSkip && fits32) {
     // The lateness with carry c is max(c, L(0)), L(0) the zero-carry lateness (nondecreasing from
     // L1 at the first token to dz at the last), so per lane:
-    //   c <= L1   A(c) = A(0) at every token: the sum is pass 1's s0;
     //   c >= dz   A(c) = I + c at every token: closed form, the clamp point by one division;
+    //   c <= L1   A(c) = A(0) at every token: the sum is pass 1's s0;
     //   else      A(c) = A(0) from the first token with A(0) >= I + c on: walk up to it only,
     //             correcting s0 by min(I + c, t) - min(A(0), t) per token.
+    // With the unclamped s0 (kUnc) the last two need every token consumed by t (the last one's
+    // consumption I_last + max(c, dz) <= t); a lane where some token clamps walks its sub-range
+    // with the carry instead (pass 2 for that lane only).
     // (warp-uniform branch: fits32 bounds every sum below 2^32, as for pass 2)
     const uint32_t L1 = max(d1, Is) - Is;
-    const bool ca = carry <= L1, cb = !ca && carry >= dz;
-    bool need = nn_all != 0u && !ca && !cb;
-    uint32_t fix = 0u;
+    const uint32_t Ilast = Is + (nn_all ? nn_all - 1u : 0u) * P;
+    const bool cb = carry >= dz;
+    const bool clampfree = !kUnc || kFinal || Ilast + max(carry, dz) <= tcl;
+    const bool ca = !cb && carry <= L1;
+    bool need = nn_all != 0u && !cb && !ca && clampfree;
+    bool full = kUnc && !kFinal && nn_all != 0u && !cb && !clampfree;
+    const bool fw = full;
+    uint32_t fix = 0u, sumc = 0u;
     if (__any_sync(0xffffffffu, need)) {
       uint32_t A0 = Is - P, Ic = Is - P + carry, x = (uint32_t)xs;
       while (__any_sync(0xffffffffu, need)) {
@@ -1050,9 +1066,19 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
           if (A0 >= Ic) {
             need = false;
           } else {
-            fix += min(Ic, tcl) - min(A0, tcl);
+            fix += cl(Ic) - cl(A0);
             need = ++x < (uint32_t)xe;
           }
+        }
+      }
+    }
+    if (kUnc && !kFinal && __any_sync(0xffffffffu, full)) {
+      uint32_t Ac = Is - P + carry, x = (uint32_t)xs;
+      while (__any_sync(0xffffffffu, full)) {
+        if (full) {
+          Ac = max(Ac + P, ld_shared_u32(tile_s + (x << 2)));
+          sumc += min(Ac, tcl);
+          full = ++x < (uint32_t)xe;
         }
       }
     }
@@ -1071,7 +1097,7 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
       } else {
         const unsigned long long sumI =
             (unsigned long long)nn * Is + (unsigned long long)P * (((unsigned long long)nn * (nn - 1)) >> 1);
-        dsum = (unsigned long long)(uint32_t)(s0 + fix - (uint32_t)sumI);
+        dsum = (unsigned long long)(uint32_t)((fw ? sumc : s0 + fix) - (uint32_t)sumI);
       }
       if (dsum) atomicAdd(&w.spre[qridx], dsum);
       if (qek && xe == qvend) {
@@ -1268,7 +1294,10 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // (static chunks there would start last and form the tail).
   const uint32_t cta0_dyn = (A.sched && blockIdx.x == 0) ? 1u : 0u;
   const uint32_t KS = KW - (A.sched ? (kScanThreads / 32) : 0u);
-  const uint32_t R = max(2u, (uint32_t)(((unsigned long long)nchunks * kStaticPct / 100u) / KS));
+  // (unaligned pools in INFLIGHT mode keep R = 2: their units vary more in cost, and the static
+  // share measured 161 -> 170 us there; FINAL mode gains on both layouts)
+  const uint32_t spct = (unal && !kFinal) ? 0u : kStaticPct;
+  const uint32_t R = max(2u, (uint32_t)(((unsigned long long)nchunks * spct / 100u) / KS));
   const uint32_t Rw = cta0_dyn ? 0u : R;
   auto gen = [&]() -> uint32_t {
     const uint32_t g_t = gs[0], g_hi = gs[1], g_nxt = gs[2];
