@@ -60,6 +60,27 @@ def test_qoe_random_small(A, ctx, orc, seed):
         _check_qoe(A, ctx, orc, snap, snap.now_us, final)
 
 
+def test_qoe_outputs_subset(A, ctx, orc):
+    """qoe_eval(outputs=...): only the requested outputs are written (the others NULL in
+    AndesQoeOut, None in Python), equal to the full call's and to the oracle's."""
+    snap = W.random_small(5, n=40, max_tokens=300)
+    ev = snap.now_us + snap.horizon_us
+    full = ctx.qoe_eval(_dev(A, snap), snap.n, ev, A.ANDES_EVAL_INFLIGHT)
+    oq, osd, osw, om = orc.qoe_eval(snap, ev, final=False)
+    for outs in (("q",), ("q64", "m"), ("s_delay", "s_whole")):
+        part = ctx.qoe_eval(_dev(A, snap), snap.n, ev, A.ANDES_EVAL_INFLIGHT, outputs=outs)
+        torch.cuda.synchronize()
+        for k, (a, b) in enumerate(zip(part, full)):
+            if A.Context._QOE_OUTPUTS[k] in outs:
+                np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+            else:
+                assert a is None
+    np.testing.assert_array_equal(full[1].cpu().numpy(), oq)
+    np.testing.assert_array_equal(full[2].cpu().numpy(), osd)
+    with pytest.raises(ValueError):
+        ctx.qoe_eval(_dev(A, snap), snap.n, ev, outputs=("qoe",))
+
+
 def test_qoe_many_tiles_ragged(A, ctx, orc):
     # ~4.7 tiles of tokens, a 100k-token request spanning many tiles, empty requests, a ragged tail
     rng = np.random.default_rng(99)

@@ -22,6 +22,8 @@ for seed in range(6):
     for fl in (1, 1 | 16, 1 | 32, 1 | 64, 1 | 128):
         ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=2, flags=fl)
     ctx.qoe_eval(req, snap.n, snap.now_us, A.ANDES_EVAL_FINAL)
+    ctx.qoe_eval(req, snap.n, snap.now_us + snap.horizon_us, A.ANDES_EVAL_INFLIGHT)
+    ctx.qoe_eval(req, snap.n, snap.now_us, A.ANDES_EVAL_INFLIGHT, outputs=("q",))
     ctx.schedule(req, snap.n, snap.now_us, snap.horizon_us, tau, snap.kv_capacity, preempt_cap=2,
                  flags=1 | A.ANDES_DEBUG_CHECKS)
     # sharded entry point, world 1 (the exchange is a device copy)
