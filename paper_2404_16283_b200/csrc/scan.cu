@@ -1039,7 +1039,8 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   if (kSkip && fits32) {
     // The lateness with carry c is max(c, L(0)), L(0) the zero-carry lateness (nondecreasing from
     // L1 at the first token to dz at the last), so per lane:
-    //   c >= dz   A(c) = I + c at every token: closed form, the clamp point by one division;
+    //   c >= dz   A(c) = I + c at every token: closed form, the clamp point by one division
+    //             (with c replaced by dz when L(0) is constant);
     //   c <= L1   A(c) = A(0) at every token: the sum is pass 1's s0;
     //   else      A(c) = A(0) from the first token with A(0) >= I + c on: walk up to it only,
     //             correcting s0 by min(I + c, t) - min(A(0), t) per token.
@@ -1049,7 +1050,10 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
     // (warp-uniform branch: fits32 bounds every sum below 2^32, as for pass 2)
     const uint32_t L1 = max(d1, Is) - Is;
     const uint32_t Ilast = Is + (nn_all ? nn_all - 1u : 0u) * P;
-    const bool cb = carry >= dz;
+    // (also when the zero-carry lateness is constant, L1 == dz: then A(c) = I + max(c, dz) at
+    // every token -- e.g. a request's first sub-range with its later tokens delivered ahead)
+    const bool cb = carry >= dz || L1 >= dz;
+    const uint32_t Lc = max(carry, dz);
     const bool clampfree = !kUnc || kFinal || Ilast + max(carry, dz) <= tcl;
     const bool ca = !cb && carry <= L1;
     bool need = nn_all != 0u && !cb && !ca && clampfree;
@@ -1086,13 +1090,13 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
       const uint32_t nn = nn_all;
       unsigned long long dsum;
       if (cb) {
-        const uint32_t b0 = Is + carry;  // consumption time of the first token
+        const uint32_t b0 = Is + Lc;  // consumption time of the first token
         uint32_t k;                      // tokens consumed by t
         if (b0 + (nn - 1u) * P <= tcl) k = nn;
         else if (b0 > tcl) k = 0u;
         else k = min(nn, (tcl - b0) / P + 1u);
         const unsigned long long kk = k, n2 = nn;
-        dsum = kk * carry + (n2 - kk) * (unsigned long long)(tcl - Is) -
+        dsum = kk * Lc + (n2 - kk) * (unsigned long long)(tcl - Is) -
                (unsigned long long)P * (((n2 * (n2 - 1ull)) >> 1) - ((kk * (kk - 1ull)) >> 1));
       } else {
         const unsigned long long sumI =
