@@ -916,8 +916,9 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
   // (gi < nmin, warp-uniform) run unpredicated; the few that only some lanes have, predicated.
   const uint32_t nmin = min(gmax, __reduce_min_sync(0xffffffffu, active ? nfull : 0xFFFFFFFFu));
   uint32_t a = Is - P;
-  // Two-tile units (large pools) and FINAL mode: pass 1 also sums T~(0) = min(A(0), t) over the
-  // valid tokens (mod 2^32), and pass 2 is skipped wherever the carry does not change A (below).
+  // Two-tile units (large pools) and FINAL mode: pass 1 also sums the zero-carry consumption
+  // times A(0) over the valid tokens (mod 2^32), and pass 2 is skipped wherever the carry and the
+  // clamp at t allow a closed form or that sum (below).
   // One-tile units (the decision's 64K-request scan) keep the plain two passes: there the extra
   // pass-1 work measured slower (decision +1 us) than the skipped pass saves.
 #ifndef ANDES_NO_P2SKIP
@@ -927,7 +928,8 @@ __device__ __forceinline__ void warp_tile_aligned(const ScanArgs& A, const Entry
 #endif
   uint32_t s0 = 0u, d1 = 0u;  // (kSkip) the zero-carry sum; the sub-range's first token
   // kUnc: pass 1 sums A(0) unclamped (two adds per four tokens instead of four mins more); the
-  // sum is then used only where no token of the sub-range reaches past t (below)
+  // sum is then used only where no token of the sub-range reaches past t (below).
+  // ANDES_CLAMPED_S0: the clamped sum min(A(0), t) instead (A/B)
 #ifndef ANDES_CLAMPED_S0
   constexpr bool kUnc = true;
 #else
