@@ -1300,10 +1300,7 @@ __global__ void __launch_bounds__(kScanThreads, 6) k_qoe_scan(const __grid_const
   // (static chunks there would start last and form the tail).
   const uint32_t cta0_dyn = (A.sched && blockIdx.x == 0) ? 1u : 0u;
   const uint32_t KS = KW - (A.sched ? (kScanThreads / 32) : 0u);
-  // (unaligned pools in INFLIGHT mode keep R = 2: their units vary more in cost, and the static
-  // share measured 161 -> 170 us there; FINAL mode gains on both layouts)
-  const uint32_t spct = (unal && !kFinal) ? 0u : kStaticPct;
-  const uint32_t R = max(2u, (uint32_t)(((unsigned long long)nchunks * spct / 100u) / KS));
+  const uint32_t R = max(2u, (uint32_t)(((unsigned long long)nchunks * kStaticPct / 100u) / KS));
   const uint32_t Rw = cta0_dyn ? 0u : R;
   auto gen = [&]() -> uint32_t {
     const uint32_t g_t = gs[0], g_hi = gs[1], g_nxt = gs[2];
